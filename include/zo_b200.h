@@ -1,0 +1,181 @@
+/*
+ * zo_b200.h -- C ABI of the B200 (sm_100a) zeroth-order training-step kernels.
+ *
+ * Drop-in boundary for the hot path of the DistZO2 reference package
+ * `zosim` (/root/reference/pkg/src/zosim).  The reference has no FFI: its
+ * boundary is a Python function API.  Each entry below replaces one
+ * numpy call site of that API (file:line cited per entry); the Python
+ * package paper_2507_03211_b200 mirrors the reference's function names and
+ * binds these symbols with ctypes.
+ *
+ * Conventions
+ *  - every entry returns an int status: ZO_OK or one of the ZO_ERR_* codes
+ *    below, which map 1:1 onto the reference's exception hierarchy
+ *    (src/zosim/errors.py:8-56); zo_last_error() returns the message.
+ *  - all device pointers are plain CUDA device addresses; `stream` is a
+ *    cudaStream_t passed as void* (NULL = legacy default stream); every
+ *    compute entry is asynchronous on that stream.
+ *  - element offsets ("keys") are GLOBAL parameter indices in the
+ *    reference's (block, tensor, element) order (src/zosim/model.py:81-101);
+ *    they key the counter-based direction z, so z never depends on how a
+ *    block is sliced or which rank computes it.
+ *  - bf16 buffers are passed as void* (bit pattern of __nv_bfloat16).
+ */
+#ifndef ZO_B200_H_
+#define ZO_B200_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes <-> src/zosim/errors.py (CLI exit codes src/zosim/cli.py:176-192) */
+#define ZO_OK 0
+#define ZO_ERR_PROTOCOL 1 /* ProtocolError       (errors.py:47-51)  */
+#define ZO_ERR_CONFIG 2   /* ConfigurationError / DimensionError (errors.py:13-20) */
+#define ZO_ERR_NUMERIC 3  /* NumericError        (errors.py:31-34)  */
+#define ZO_ERR_FABRIC 4   /* FabricFault         (errors.py:37-40)  */
+#define ZO_ERR_CUDA 5     /* CUDA runtime failure (no reference analogue) */
+
+/* direction source */
+#define ZO_Z_PHILOX 0 /* z = Philox4x32-10(seed, key) + Box-Muller, in-register   */
+#define ZO_Z_ORACLE 1 /* z = injected f64 array (the reference's PCG64 stream)   */
+
+/* shadow kinds of a segment */
+#define ZO_SHADOW_BF16 0 /* perturbed copy rounded to bf16 (GEMM operand)        */
+#define ZO_SHADOW_F32 1  /* perturbed copy kept in fp32 (LN gains, biases)       */
+#define ZO_SHADOW_NONE 2 /* update only; consumer perturbs on read (embedding)  */
+
+/* zo_perturb_update flags */
+#define ZO_PU_UPDATE 1u  /* apply the pending update theta -= (lr g_prev) z_prev  */
+#define ZO_PU_SHADOW_A 2u /* write shadow A = theta' + scale_a z_cur             */
+#define ZO_PU_SHADOW_B 4u /* write shadow B = theta' + scale_b z_cur             */
+
+/* zo_gemm_bf16 epilogues */
+#define ZO_EPI_F32 0          /* out f32  = acc                                   */
+#define ZO_EPI_BIAS_BF16 1    /* out bf16 = acc + bias            (QKV)           */
+#define ZO_EPI_BIAS_GELU_BF16 2 /* out bf16 = gelu_tanh(acc + bias) (FFN up)      */
+#define ZO_EPI_BIAS_RESID_F32 3 /* out f32 += (acc + bias)        (O-proj, FFN down) */
+#define ZO_EPI_CE 4           /* LM head: per-row partial max/sum-exp + target logit */
+
+/* One tensor of a parameter block, as the perturb/update kernel sees it. */
+typedef struct ZoSegment {
+  int64_t src;    /* global element offset (z key) of the tensor's element 0  */
+  int64_t rows;   /* rows x cols elements, row-major in the master buffer     */
+  int64_t cols;
+  int64_t dst;    /* element offset of the tensor inside its shadow buffer    */
+  int64_t dst_ld; /* shadow row stride in elements (>= cols)                  */
+  int32_t kind;   /* ZO_SHADOW_*                                              */
+  int32_t reserved;
+} ZoSegment;
+
+/* Per-iteration scalars, device-resident so a captured CUDA graph can replay
+ * steps: the host writes seed_cur; zo_grad_finalize writes the rest. */
+typedef struct ZoStepScalars {
+  uint64_t seed_cur;  /* key of this iteration's direction z_j              */
+  uint64_t seed_prev; /* key of the pending update's direction z_{j-1}      */
+  double lr_g_prev;   /* lr * g_{j-1}; formed as (lr*g) like zo.py:125      */
+  int64_t pending;    /* 1 when an update is pending (zo.py:267-271 flag)    */
+} ZoStepScalars;
+
+const char* zo_version(void);
+const char* zo_last_error(void);
+/* 0 when device `dev` is an sm_100 part the library was built for. */
+int zo_device_check(int dev);
+
+/*
+ * Fused perturb / update over a set of tensors (one block or a whole model).
+ * Replaces perturb_block / perturb_params (src/zosim/zo.py:90-113) and
+ * update_block / update_params (src/zosim/zo.py:116-130), and the per-block
+ * deferred update of dual_forward (src/zosim/zo.py:204-211).
+ *   theta        fp32 master; element with key e lives at theta[e - theta_key0]
+ *   segs/prefix  device table: prefix[i] = first tile of segs[i], prefix[n]=total
+ *   flags        ZO_PU_*; the update is applied only when scal->pending != 0
+ *   zmode        ZO_Z_PHILOX (keys scal->seed_cur/seed_prev) or ZO_Z_ORACLE
+ *                (z_cur/z_prev f64 arrays indexed by key - z_key0; exact f64
+ *                arithmetic, bit-identical to the reference's f32 results)
+ *   scale_a/b    cumulative perturbation of shadows A/B (e.g. +eps, -eps)
+ */
+int zo_perturb_update(float* theta, int64_t theta_key0, const ZoSegment* segs,
+                      const int64_t* tile_prefix, int32_t n_segs, int64_t n_tiles,
+                      void* wsh_a, float* vsh_a, void* wsh_b, float* vsh_b,
+                      double scale_a, double scale_b, uint32_t flags,
+                      const ZoStepScalars* scal, int32_t zmode,
+                      const double* z_cur, const double* z_prev, int64_t z_key0,
+                      void* stream);
+/* Tile granularity (elements) the host must use to build tile_prefix. */
+int64_t zo_perturb_tile_elems(void);
+
+/*
+ * Embedding forward with perturb-on-gather (src/zosim/model.py:300-310):
+ * x[b,t,:] = f32(tok[ids[b,t]] + s z) + f32(pos[t] + s z), z keyed by the
+ * gathered element's global key.  Only gathered rows are perturbed.
+ */
+int zo_embed_fwd(const float* tok, int64_t tok_key0, const float* pos, int64_t pos_key0,
+                 const int32_t* ids, int64_t batch, int64_t seq, int64_t d, int64_t vocab,
+                 double scale, const ZoStepScalars* scal, int32_t zmode,
+                 const double* z, int64_t z_key0, float* x, int64_t ldx,
+                 int32_t* err_flag, void* stream);
+
+/* LayerNorm over the last dim, eps 1e-5, biased variance, fp32 statistics,
+ * bf16 output (src/zosim/model.py:280-283). */
+int zo_layernorm_fwd(const float* x, int64_t ldx, const float* gamma, const float* beta,
+                     int64_t rows, int64_t d, void* out_bf16, int64_t ldo, void* stream);
+
+/*
+ * C[M,N] = A[M,K] (bf16, K-major) x B[K,N] (bf16, N-major = the reference's
+ * (d_in, d_out) weight layout, src/zosim/model.py:325) on tcgen05 tensor
+ * cores with TMA-fed shared memory and fp32 TMEM accumulators, plus a fused
+ * epilogue.  Replaces h @ W + b, the residual adds and GELU of
+ * src/zosim/model.py:325-344, and (ZO_EPI_CE) the logits half of loss
+ * (src/zosim/model.py:357-372): ce_part[m, tile] = (max, sum exp(l-max)) over
+ * the tile's columns and ce_tgt[m] = logit of targets[m].
+ * Leading dimensions are in elements and must be multiples of 8.
+ */
+int zo_gemm_bf16(const void* A, int64_t lda, const void* B, int64_t ldb,
+                 int64_t M, int64_t N, int64_t K, int32_t epilogue,
+                 const float* bias, void* out, int64_t ldo,
+                 const int32_t* targets, float* ce_part, float* ce_tgt,
+                 int32_t* err_flag, void* stream);
+/* number of N tiles the ZO_EPI_CE epilogue writes per row for a given N */
+int64_t zo_gemm_ce_tiles(int64_t N);
+
+/* Causal exact-softmax attention (src/zosim/model.py:325-332): qkv rows are
+ * [q | k | v] (each H*hd wide), out ctx[B*T, H*hd] bf16. */
+int zo_attn_causal_fwd(const void* qkv, int64_t ldqkv, int64_t batch, int64_t seq,
+                       int64_t heads, int64_t head_dim, void* ctx, int64_t ldc, void* stream);
+
+/* Mean cross-entropy over rows from the ZO_EPI_CE partials, combined and
+ * summed in f64 in a fixed order (src/zosim/model.py:366-372). Sets
+ * err_flag bit 1 on non-finite logits (-> NumericError). */
+int zo_ce_finalize(const float* ce_part, const float* ce_tgt, int64_t rows, int64_t n_tiles,
+                   double* loss_out, double* row_scratch /* >= rows */, int32_t* err_flag,
+                   void* stream);
+
+/* g = (loss_pos - loss_neg) / (2 eps) (src/zosim/zo.py:80-84); record =
+ * {loss_pos, loss_neg, g}; then scal->{seed_prev, lr_g_prev, pending} =
+ * {seed_cur, lr*g, 1} so the next zo_perturb_update folds the update in. */
+int zo_grad_finalize(const double* loss_pos, const double* loss_neg, double eps, double lr,
+                     ZoStepScalars* scal, double* record, void* stream);
+
+/* g from n gathered per-group central differences: ordered ascending sum of
+ * (lp_i - ln_i)/(2 eps) / n -- the 2D / DDP reduction of
+ * src/zosim/strategies.py:197-216 and src/zosim/fabric.py:105-113. losses is
+ * [n][2] = (loss_pos, loss_neg) per group. record gets {lp_k, ln_k, g} of group
+ * `mine`. */
+int zo_grad_finalize_groups(const double* losses, int32_t n_groups, int32_t mine, double eps,
+                            double lr, ZoStepScalars* scal, double* record, void* stream);
+
+/* 64-bit FNV-style hash of a device buffer (replica-divergence guard that
+ * replaces the SHA-256 all_gather of src/zosim/strategies.py:86-89). */
+int zo_hash_u64(const void* data, int64_t nbytes, uint64_t* out_dev,
+                uint64_t* scratch_dev /* >= 256 words */, void* stream);
+
+/* Debug/test: the Philox direction itself, z[i] for keys e0 .. e0+n-1. */
+int zo_philox_normals(uint64_t seed, int64_t e0, int64_t n, float* out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ZO_B200_H_ */

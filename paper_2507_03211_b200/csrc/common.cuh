@@ -1,0 +1,142 @@
+// Shared device/host helpers for the sm_100a ZO-step kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+#include <stdio.h>
+
+#include "../../include/zo_b200.h"
+
+namespace zo {
+
+// ---------------------------------------------------------------------------
+// status / last error (thread-local, read through zo_last_error())
+// ---------------------------------------------------------------------------
+void set_error(const char* fmt, ...);
+
+#define ZO_CHECK_ARG(cond, code, ...)     \
+  do {                                    \
+    if (!(cond)) {                        \
+      ::zo::set_error(__VA_ARGS__);       \
+      return (code);                      \
+    }                                     \
+  } while (0)
+
+#define ZO_CUDA_TRY(expr)                                                        \
+  do {                                                                           \
+    cudaError_t _e = (expr);                                                     \
+    if (_e != cudaSuccess) {                                                     \
+      ::zo::set_error("%s failed: %s", #expr, cudaGetErrorString(_e));           \
+      return ZO_ERR_CUDA;                                                        \
+    }                                                                            \
+  } while (0)
+
+inline int launch_status(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error("%s launch failed: %s", what, cudaGetErrorString(e));
+    return ZO_ERR_CUDA;
+  }
+  return ZO_OK;
+}
+
+int num_sms();
+
+// ---------------------------------------------------------------------------
+// Philox4x32-10 (Salmon et al., SC'11): counter-based, so z for global
+// element e is a pure function of (seed, e) -- identical on every rank and
+// for every slicing of a block.  counter = (e/4 lo, e/4 hi, 0, 0),
+// key = (seed lo, seed hi); the 4 outputs become z[4q .. 4q+3].
+// ---------------------------------------------------------------------------
+struct u32x4 { uint32_t x, y, z, w; };
+
+__host__ __device__ __forceinline__ uint32_t mulhi32(uint32_t a, uint32_t b) {
+#ifdef __CUDA_ARCH__
+  return __umulhi(a, b);
+#else
+  return (uint32_t)(((uint64_t)a * (uint64_t)b) >> 32);
+#endif
+}
+
+__host__ __device__ __forceinline__ u32x4 philox4x32_10(uint64_t ctr, uint64_t seed) {
+  uint32_t c0 = (uint32_t)ctr, c1 = (uint32_t)(ctr >> 32), c2 = 0u, c3 = 0u;
+  uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint32_t hi0 = mulhi32(0xD2511F53u, c0), lo0 = 0xD2511F53u * c0;
+    const uint32_t hi1 = mulhi32(0xCD9E8D57u, c2), lo1 = 0xCD9E8D57u * c2;
+    const uint32_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
+    c0 = n0; c1 = lo1; c2 = n2; c3 = lo0;
+    k0 += 0x9E3779B9u; k1 += 0xBB67AE85u;
+  }
+  return {c0, c1, c2, c3};
+}
+
+// Box-Muller on 24-bit uniforms: u1 in (0,1) (never 0), angle in [-pi, pi).
+// Fast MUFU intrinsics; outputs are a deterministic function of the bits.
+__device__ __forceinline__ void box_muller(uint32_t a, uint32_t b, float& z0, float& z1) {
+  const float u1 = (float)(a >> 8) * 5.9604644775390625e-08f + 2.98023223876953125e-08f;
+  const float ang = (float)(b >> 8) * 3.7450702706353989e-07f - 3.14159265358979f;  // 2pi/2^24
+  const float r = sqrtf(-1.3862943611198906f * __log2f(u1));                      // -2 ln2 log2(u)
+  float s, c;
+  __sincosf(ang, &s, &c);
+  z0 = r * c;
+  z1 = r * s;
+}
+
+struct f32x4 { float x, y, z, w; };
+
+__device__ __forceinline__ f32x4 philox_normal4(uint64_t seed, uint64_t q) {
+  const u32x4 r = philox4x32_10(q, seed);
+  f32x4 o;
+  box_muller(r.x, r.y, o.x, o.y);
+  box_muller(r.z, r.w, o.z, o.w);
+  return o;
+}
+
+__device__ __forceinline__ float philox_normal1(uint64_t seed, uint64_t e) {
+  const f32x4 v = philox_normal4(seed, e >> 2);
+  switch (e & 3) { case 0: return v.x; case 1: return v.y; case 2: return v.z; default: return v.w; }
+}
+
+__device__ __forceinline__ float f4get(const f32x4& v, int i) {
+  return i == 0 ? v.x : (i == 1 ? v.y : (i == 2 ? v.z : v.w));
+}
+
+// Direction source shared by every kernel that perturbs on the fly.
+// mode ZO_Z_PHILOX: z = philox(seed, e).  mode ZO_Z_ORACLE: z = zsrc[e - zbase]
+// (the reference's f64 z, injected), with exact f64 arithmetic.
+struct ZSource {
+  int mode;
+  uint64_t seed;
+  const double* zsrc;
+  int64_t zbase;
+};
+
+// Parameter block of the perturb/update kernel (perturb.cu; filled by api.cu).
+struct PuParams {
+  float* theta;
+  int64_t theta_key0;
+  const ZoSegment* segs;
+  const int64_t* prefix;
+  int32_t n_segs;
+  int64_t n_tiles;
+  __nv_bfloat16* wsh[2];
+  float* vsh[2];
+  double scale[2];
+  uint32_t flags;
+  const ZoStepScalars* scal;
+  const double* z_cur;
+  const double* z_prev;
+  int64_t z_key0;
+};
+
+// ---------------------------------------------------------------------------
+// small PTX wrappers (mbarrier / TMA / tcgen05) for the GEMM
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+}  // namespace zo

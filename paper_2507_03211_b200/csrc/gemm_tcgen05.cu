@@ -1,0 +1,487 @@
+// bf16 GEMM on the 5th-generation tensor cores (tcgen05) with TMA-fed shared
+// memory, fp32 accumulators in TMEM and a fused epilogue.
+//
+//   C[M,N] = A[M,K] . B[K,N]
+//   A: activations, row-major, K contiguous          -> UMMA K-major operand
+//   B: weights in the reference's (d_in, d_out) layout, N contiguous
+//      (src/zosim/model.py:325 `h @ W`)                 -> UMMA MN-major operand
+//
+// Persistent, warp-specialised CTA (192 threads, 1 CTA per SM):
+//   warp 0      TMA producer (one lane): A 128x64 box + B 64x64 boxes per stage
+//   warp 1      TMEM allocator + MMA issuer (one lane issues tcgen05.mma)
+//   warps 2..5  epilogue: tcgen05.ld 32x32b -> registers -> fused op -> global
+// Pipelines: smem ring full/empty mbarriers (TMA <-> MMA) and a 2-deep TMEM
+// accumulator ring tfull/tempty (MMA <-> epilogue), so the epilogue of tile i
+// overlaps the MMAs of tile i+1.
+//
+// Epilogues (the ops that follow each GEMM in model.py:325-344):
+//   ZO_EPI_BIAS_BF16       qkv  = h @ Wqkv + b                 (bf16 out)
+//   ZO_EPI_BIAS_GELU_BF16  f    = gelu_tanh(h2 @ W1 + b1)      (bf16 out)
+//   ZO_EPI_BIAS_RESID_F32  x   += ctx @ Wo + bo / f @ W2 + b2  (fp32 residual)
+//   ZO_EPI_CE              per-row (max, sum exp) of logits + target logit;
+//                          the [M, V] logits never reach HBM
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <mutex>
+#include <unordered_map>
+
+#include "common.cuh"
+
+namespace zo {
+
+constexpr int kBM = 128;
+constexpr int kBK = 64;
+constexpr int kGemmThreads = 192;
+
+template <int BN>
+struct GemmCfg {
+  static constexpr int kStages = BN == 256 ? 4 : 6;
+  static constexpr int kABytes = kBM * kBK * 2;   // 16 KB
+  static constexpr int kBBytes = kBK * BN * 2;    // 32 KB / 16 KB
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kTmemCols = 2 * BN;        // double-buffered accumulator
+  static constexpr int kSmem = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+};
+
+struct GemmArgs {
+  int64_t M, N, K;
+  const float* bias;
+  void* out;
+  int64_t ldo;
+  const int32_t* targets;
+  float* ce_part;
+  float* ce_tgt;
+  int32_t* err;
+  int64_t ce_tiles;
+};
+
+// ----------------------------- PTX wrappers ---------------------------------
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n.reg .pred p;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      "selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok) : "r"(bar), "r"(parity) : "memory");
+  return ok != 0;
+}
+// Bounded wait: a protocol bug traps (kernel error) instead of hanging the GPU.
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  if (mbar_try_wait(bar, parity)) return;
+  const long long t0 = clock64();
+  while (!mbar_try_wait(bar, parity)) {
+    if (clock64() - t0 > 8000000000ll) __trap();
+  }
+}
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, uint32_t bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n"
+      ::"r"(dst), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ void tc_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void tc_mma_f16(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                           uint32_t accumulate) {
+  asm volatile(
+      "{\n.reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n"
+      ::"r"(d_tmem), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void tmem_ld_32x32b_x32(uint32_t taddr, float (&v)[32]) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// UMMA shared-memory descriptors (SWIZZLE_128B, Blackwell version bit 46).
+//  K-major A: 8-row x 128 B swizzle atoms stacked along M; SBO = 1024 B.
+//  MN-major B: atoms of 64 N x 8 K; LBO = stride between 64-wide N chunks
+//  (one TMA box = kBK rows x 128 B = 8 KB), SBO = 1024 B between 8-row K groups.
+__device__ __forceinline__ uint64_t desc_sw128(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  return (uint64_t)((saddr & 0x3FFFFu) >> 4) | ((uint64_t)(lbo >> 4) << 16) | ((uint64_t)(sbo >> 4) << 32) |
+         (1ull << 46) | (2ull << 61);
+}
+
+template <int BN>
+__device__ __forceinline__ uint32_t make_idesc() {
+  // c_format F32 [4,6)=1, a_format BF16 [7,10)=1, b_format BF16 [10,13)=1,
+  // a_major K (bit 15 = 0), b_major MN (bit 16 = 1), N>>3 at [17,23), M>>4 at [24,29)
+  return (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) | ((uint32_t)(BN >> 3) << 17) |
+         ((uint32_t)(kBM >> 4) << 24);
+}
+
+__device__ __forceinline__ float gelu_tanh(float x) {
+  const float c = 0.7978845608028654f;  // sqrt(2/pi)
+  return 0.5f * x * (1.0f + tanhf(c * (x + 0.044715f * x * x * x)));
+}
+
+template <int BN, int EPI>
+__global__ void __launch_bounds__(kGemmThreads, 1)
+    gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                        const GemmArgs args) {
+  using C = GemmCfg<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  const uint32_t base = (raw + 1023u) & ~1023u;
+  uint8_t* gbase = smem_raw + (base - raw);
+  const uint32_t sA = base;
+  const uint32_t sB = base + C::kStages * C::kABytes;
+  const uint32_t bars = base + C::kStages * C::kStageBytes;
+  // barrier layout: full[S], empty[S], tfull[2], tempty[2], then tmem ptr
+  auto full_bar = [&](int s) { return bars + 8u * s; };
+  auto empty_bar = [&](int s) { return bars + 8u * (C::kStages + s); };
+  auto tfull_bar = [&](int a) { return bars + 8u * (2 * C::kStages + a); };
+  auto tempty_bar = [&](int a) { return bars + 8u * (2 * C::kStages + 2 + a); };
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + C::kStages * C::kStageBytes + 8 * (2 * C::kStages + 4));
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t num_m = (args.M + kBM - 1) / kBM;
+  const int64_t num_n = (args.N + BN - 1) / BN;
+  const int64_t tiles = num_m * num_n;
+  const int nk = (int)((args.K + kBK - 1) / kBK);
+
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&tmA);
+    prefetch_tmap(&tmB);
+    for (int s = 0; s < C::kStages; ++s) { mbar_init(full_bar(s), 1); mbar_init(empty_bar(s), 1); }
+    for (int a = 0; a < 2; ++a) { mbar_init(tfull_bar(a), 1); mbar_init(tempty_bar(a), 128); }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tmem_slot)),
+                 "r"((uint32_t)C::kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ============================ TMA producer ============================
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+        const int m0 = (int)((tile % num_m) * kBM);
+        const int n0 = (int)((tile / num_m) * BN);
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_wait(empty_bar(stage), phase ^ 1u);
+          mbar_expect_tx(full_bar(stage), (uint32_t)C::kStageBytes);
+          tma_load_2d(sA + stage * C::kABytes, &tmA, full_bar(stage), kb * kBK, m0);
+#pragma unroll
+          for (int j = 0; j < BN / 64; ++j)
+            tma_load_2d(sB + stage * C::kBBytes + j * (kBK * 128), &tmB, full_bar(stage), n0 + 64 * j, kb * kBK);
+          if (++stage == C::kStages) { stage = 0; phase ^= 1u; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ============================ MMA issuer ==============================
+    const uint32_t idesc = make_idesc<BN>();
+    int stage = 0;
+    uint32_t phase = 0;
+    int64_t local = 0;
+    for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++local) {
+      const int acc = (int)(local & 1);
+      const uint32_t acc_phase = (uint32_t)((local >> 1) & 1);
+      mbar_wait(tempty_bar(acc), acc_phase ^ 1u);
+      tc_fence_after();
+      const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
+      for (int kb = 0; kb < nk; ++kb) {
+        mbar_wait(full_bar(stage), phase);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t a0 = sA + stage * C::kABytes;
+          const uint32_t b0 = sB + stage * C::kBBytes;
+#pragma unroll
+          for (int kk = 0; kk < kBK / 16; ++kk) {
+            const uint64_t ad = desc_sw128(a0 + kk * 32, 16, 1024);
+            const uint64_t bd = desc_sw128(b0 + kk * 2048, kBK * 128, 1024);
+            tc_mma_f16(d_tmem, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
+          }
+          tc_commit(empty_bar(stage));   // frees the smem slot once these MMAs retire
+        }
+        __syncwarp();
+        if (++stage == C::kStages) { stage = 0; phase ^= 1u; }
+      }
+      if (lane == 0) tc_commit(tfull_bar(acc));  // accumulator ready for the epilogue
+      __syncwarp();
+    }
+  } else {
+    // ============================ epilogue ================================
+    const int quarter = warp & 3;   // TMEM lanes 32*quarter .. +31
+    int64_t local = 0;
+    for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++local) {
+      const int acc = (int)(local & 1);
+      const uint32_t acc_phase = (uint32_t)((local >> 1) & 1);
+      const int64_t m0 = (tile % num_m) * kBM;
+      const int64_t tn = tile / num_m;
+      const int64_t n0 = tn * BN;
+      mbar_wait(tfull_bar(acc), acc_phase);
+      tc_fence_after();
+      const int64_t row = m0 + quarter * 32 + lane;
+      const bool row_ok = row < args.M;
+      float ce_m = -INFINITY, ce_s = 0.f;
+      int32_t tgt = -1;
+      bool bad = false;
+      if constexpr (EPI == ZO_EPI_CE) {
+        if (row_ok) tgt = args.targets[row];
+      }
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        float v[32];
+        tmem_ld_32x32b_x32(tmem_base + (uint32_t)(acc * BN + c * 32) + ((uint32_t)(quarter * 32) << 16), v);
+        const int64_t col0 = n0 + c * 32;
+        if (!row_ok || col0 >= args.N) continue;
+        const bool full = col0 + 32 <= args.N;
+        if constexpr (EPI == ZO_EPI_F32) {
+          float* o = static_cast<float*>(args.out) + row * args.ldo + col0;
+          if (full && ((reinterpret_cast<uintptr_t>(o) & 15) == 0)) {
+#pragma unroll
+            for (int i = 0; i < 32; i += 4) *reinterpret_cast<float4*>(o + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+          } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              if (col0 + i < args.N) o[i] = v[i];
+          }
+        } else if constexpr (EPI == ZO_EPI_BIAS_BF16 || EPI == ZO_EPI_BIAS_GELU_BF16) {
+          __nv_bfloat16* o = static_cast<__nv_bfloat16*>(args.out) + row * args.ldo + col0;
+          const float* bb = args.bias + col0;
+          if (full && ((reinterpret_cast<uintptr_t>(o) & 15) == 0)) {
+#pragma unroll
+            for (int i = 0; i < 32; i += 8) {
+              uint32_t pk[4];
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                float a = v[i + 2 * j] + bb[i + 2 * j], b = v[i + 2 * j + 1] + bb[i + 2 * j + 1];
+                if constexpr (EPI == ZO_EPI_BIAS_GELU_BF16) { a = gelu_tanh(a); b = gelu_tanh(b); }
+                __nv_bfloat162 h2 = __floats2bfloat162_rn(a, b);
+                pk[j] = *reinterpret_cast<uint32_t*>(&h2);
+              }
+              *reinterpret_cast<uint4*>(o + i) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              if (col0 + i < args.N) {
+                float a = v[i] + bb[i];
+                if constexpr (EPI == ZO_EPI_BIAS_GELU_BF16) a = gelu_tanh(a);
+                o[i] = __float2bfloat16_rn(a);
+              }
+            }
+          }
+        } else if constexpr (EPI == ZO_EPI_BIAS_RESID_F32) {
+          float* o = static_cast<float*>(args.out) + row * args.ldo + col0;
+          const float* bb = args.bias + col0;
+          if (full && ((reinterpret_cast<uintptr_t>(o) & 15) == 0)) {
+#pragma unroll
+            for (int i = 0; i < 32; i += 4) {
+              float4 x = *reinterpret_cast<float4*>(o + i);
+              x.x += v[i] + bb[i]; x.y += v[i + 1] + bb[i + 1];
+              x.z += v[i + 2] + bb[i + 2]; x.w += v[i + 3] + bb[i + 3];
+              *reinterpret_cast<float4*>(o + i) = x;
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              if (col0 + i < args.N) o[i] += v[i] + bb[i];
+          }
+        } else {  // ZO_EPI_CE
+          const float* bb = args.bias + col0;
+          const int lim = full ? 32 : (int)(args.N - col0);
+          float cm = -INFINITY;
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            if (i < lim) {
+              v[i] += bb[i];
+              bad |= !isfinite(v[i]);
+              cm = fmaxf(cm, v[i]);
+            }
+          }
+          const float nm = fmaxf(ce_m, cm);
+          float s = ce_s * __expf(ce_m - nm);
+          if (ce_m == -INFINITY) s = 0.f;
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            if (i < lim) s += __expf(v[i] - nm);
+          ce_m = nm;
+          ce_s = s;
+          if (tgt >= col0 && tgt < col0 + lim) {
+            const int ti = (int)(tgt - col0);
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              if (i == ti) args.ce_tgt[row] = v[i];
+          }
+        }
+      }
+      if constexpr (EPI == ZO_EPI_CE) {
+        if (row_ok) {
+          args.ce_part[(row * args.ce_tiles + tn) * 2] = ce_m;
+          args.ce_part[(row * args.ce_tiles + tn) * 2 + 1] = ce_s;
+          if (bad) atomicOr(args.err, 2);
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(tempty_bar(acc));
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem_base),
+                 "r"((uint32_t)C::kTmemCols));
+  }
+}
+
+// ------------------------------ host side -----------------------------------
+namespace {
+
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+struct MapKey {
+  uint64_t ptr, inner, outer, ld, box_in, box_out;
+  bool operator==(const MapKey& o) const {
+    return ptr == o.ptr && inner == o.inner && outer == o.outer && ld == o.ld && box_in == o.box_in &&
+           box_out == o.box_out;
+  }
+};
+struct MapKeyHash {
+  size_t operator()(const MapKey& k) const {
+    uint64_t h = k.ptr * 0x9E3779B97F4A7C15ull;
+    h ^= k.inner + 0x7F4A7C15ull + (h << 6) + (h >> 2);
+    h ^= k.outer + (h << 6) + (h >> 2);
+    h ^= k.ld + (h << 6) + (h >> 2);
+    h ^= (k.box_in << 20) ^ k.box_out;
+    return (size_t)h;
+  }
+};
+
+std::mutex g_map_mu;
+std::unordered_map<MapKey, CUtensorMap, MapKeyHash> g_maps;
+
+// 2-D bf16 tensor map, inner dim contiguous, 128B swizzle, zero OOB fill.
+int get_map(const void* ptr, int64_t inner, int64_t outer, int64_t ld, int box_in, int box_out, CUtensorMap* out) {
+  MapKey key{(uint64_t)ptr, (uint64_t)inner, (uint64_t)outer, (uint64_t)ld, (uint64_t)box_in, (uint64_t)box_out};
+  std::lock_guard<std::mutex> lk(g_map_mu);
+  auto it = g_maps.find(key);
+  if (it != g_maps.end()) { *out = it->second; return ZO_OK; }
+  auto enc = get_encode();
+  if (!enc) { set_error("cuTensorMapEncodeTiled unavailable (driver too old?)"); return ZO_ERR_CUDA; }
+  CUtensorMap m;
+  cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
+  cuuint32_t box[2] = {(cuuint32_t)box_in, (cuuint32_t)box_out};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled failed (%d): ptr=%p inner=%lld outer=%lld ld=%lld", (int)r, ptr,
+              (long long)inner, (long long)outer, (long long)ld);
+    return ZO_ERR_CONFIG;
+  }
+  if (g_maps.size() > 4096) g_maps.clear();
+  g_maps.emplace(key, m);
+  *out = m;
+  return ZO_OK;
+}
+
+template <int BN, int EPI>
+int launch_t(const CUtensorMap& ma, const CUtensorMap& mb, const GemmArgs& a, cudaStream_t st) {
+  using C = GemmCfg<BN>;
+  static bool attr_done = false;   // per-instantiation (benign race: idempotent)
+  if (!attr_done) {
+    cudaError_t e = cudaFuncSetAttribute(gemm_tcgen05_kernel<BN, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         C::kSmem);
+    if (e != cudaSuccess) { set_error("gemm smem attribute: %s", cudaGetErrorString(e)); return ZO_ERR_CUDA; }
+    attr_done = true;
+  }
+  const int64_t tiles = ((a.M + kBM - 1) / kBM) * ((a.N + BN - 1) / BN);
+  const int grid = (int)(tiles < num_sms() ? tiles : num_sms());
+  gemm_tcgen05_kernel<BN, EPI><<<grid, kGemmThreads, C::kSmem, st>>>(ma, mb, a);
+  return launch_status("gemm_tcgen05_kernel");
+}
+
+template <int BN>
+int launch_bn(int epi, const CUtensorMap& ma, const CUtensorMap& mb, const GemmArgs& a, cudaStream_t st) {
+  switch (epi) {
+    case ZO_EPI_F32: return launch_t<BN, ZO_EPI_F32>(ma, mb, a, st);
+    case ZO_EPI_BIAS_BF16: return launch_t<BN, ZO_EPI_BIAS_BF16>(ma, mb, a, st);
+    case ZO_EPI_BIAS_GELU_BF16: return launch_t<BN, ZO_EPI_BIAS_GELU_BF16>(ma, mb, a, st);
+    case ZO_EPI_BIAS_RESID_F32: return launch_t<BN, ZO_EPI_BIAS_RESID_F32>(ma, mb, a, st);
+    case ZO_EPI_CE: return launch_t<BN, ZO_EPI_CE>(ma, mb, a, st);
+  }
+  set_error("zo_gemm_bf16: unknown epilogue %d", epi);
+  return ZO_ERR_CONFIG;
+}
+
+}  // namespace
+
+int64_t gemm_ce_tiles(int64_t N) { return (N + 255) / 256; }
+
+int gemm_launch(const void* A, int64_t lda, const void* B, int64_t ldb, int64_t M, int64_t N, int64_t K, int epi,
+                const float* bias, void* out, int64_t ldo, const int32_t* targets, float* ce_part, float* ce_tgt,
+                int32_t* err, cudaStream_t st) {
+  if (M == 0 || N == 0) return ZO_OK;
+  if (K <= 0) { set_error("zo_gemm_bf16: K must be positive"); return ZO_ERR_CONFIG; }
+  if (lda % 8 || ldb % 8 || lda < K || ldb < N) {
+    set_error("zo_gemm_bf16: lda/ldb must be multiples of 8 and >= K/N (lda=%lld ldb=%lld)", (long long)lda,
+              (long long)ldb);
+    return ZO_ERR_CONFIG;
+  }
+  if ((reinterpret_cast<uintptr_t>(A) & 15) || (reinterpret_cast<uintptr_t>(B) & 15)) {
+    set_error("zo_gemm_bf16: operands must be 16-byte aligned");
+    return ZO_ERR_CONFIG;
+  }
+  int bn = 128;
+  const int64_t tiles256 = ((M + kBM - 1) / kBM) * ((N + 255) / 256);
+  if (epi == ZO_EPI_CE || tiles256 >= num_sms()) bn = 256;
+  CUtensorMap ma, mb;
+  int rc = get_map(A, K, M, lda, kBK, kBM, &ma);
+  if (rc) return rc;
+  rc = get_map(B, N, K, ldb, 64, kBK, &mb);
+  if (rc) return rc;
+  GemmArgs a{M, N, K, bias, out, ldo, targets, ce_part, ce_tgt, err, gemm_ce_tiles(N)};
+  return bn == 256 ? launch_bn<256>(epi, ma, mb, a, st) : launch_bn<128>(epi, ma, mb, a, st);
+}
+
+}  // namespace zo

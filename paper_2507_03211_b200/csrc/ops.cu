@@ -1,0 +1,246 @@
+// Row-wise forward ops of the zosim decoder block and the step's scalar tail.
+//   embedding gather (model.py:300-310) with perturb-on-gather
+//   LayerNorm (model.py:280-283)
+//   cross-entropy finalize (model.py:357-372), projected gradient (zo.py:80-84)
+//   replica hash (strategies.py:86-89 guard)
+#include "common.cuh"
+
+namespace zo {
+
+// ---------------------------------------------------------------------------
+// embedding: x = f32(tok[id] + s z) + f32(pos[t] + s z)
+// ---------------------------------------------------------------------------
+template <int ZMODE>
+__global__ void embed_kernel(const float* __restrict__ tok, int64_t tok_key0,
+                             const float* __restrict__ pos, int64_t pos_key0,
+                             const int32_t* __restrict__ ids, int64_t seq, int64_t d, int64_t vocab,
+                             double scale, const ZoStepScalars* scal, const double* z, int64_t z_key0,
+                             float* __restrict__ x, int64_t ldx, int32_t* err) {
+  const int64_t m = blockIdx.x;
+  const int64_t t = m % seq;
+  int64_t id = ids[m];
+  if (id < 0 || id >= vocab) {
+    if (threadIdx.x == 0) atomicOr(err, 4);
+    id = 0;
+  }
+  const uint64_t seed = scal ? scal->seed_cur : 0ull;
+  const float s32 = (float)scale;
+  for (int64_t c = threadIdx.x; c < d; c += blockDim.x) {
+    const int64_t kt = tok_key0 + id * d + c, kp = pos_key0 + t * d + c;
+    float a = tok[id * d + c], b = pos[t * d + c];
+    if (scale != 0.0) {
+      if constexpr (ZMODE == ZO_Z_PHILOX) {
+        a = fmaf(s32, philox_normal1(seed, (uint64_t)kt), a);
+        b = fmaf(s32, philox_normal1(seed, (uint64_t)kp), b);
+      } else {
+        a = __double2float_rn(__dadd_rn((double)a, __dmul_rn(scale, z[kt - z_key0])));
+        b = __double2float_rn(__dadd_rn((double)b, __dmul_rn(scale, z[kp - z_key0])));
+      }
+    }
+    x[m * ldx + c] = __fadd_rn(a, b);
+  }
+}
+
+int embed_launch(const float* tok, int64_t tok_key0, const float* pos, int64_t pos_key0,
+                 const int32_t* ids, int64_t batch, int64_t seq, int64_t d, int64_t vocab,
+                 double scale, const ZoStepScalars* scal, int32_t zmode, const double* z,
+                 int64_t z_key0, float* x, int64_t ldx, int32_t* err, cudaStream_t st) {
+  const int64_t rows = batch * seq;
+  if (rows == 0) return ZO_OK;
+  const int threads = d >= 256 ? 256 : (int)((d + 31) / 32 * 32);
+  if (zmode == ZO_Z_PHILOX)
+    embed_kernel<ZO_Z_PHILOX><<<(unsigned)rows, threads, 0, st>>>(tok, tok_key0, pos, pos_key0, ids, seq, d, vocab,
+                                                                  scale, scal, z, z_key0, x, ldx, err);
+  else
+    embed_kernel<ZO_Z_ORACLE><<<(unsigned)rows, threads, 0, st>>>(tok, tok_key0, pos, pos_key0, ids, seq, d, vocab,
+                                                                  scale, scal, z, z_key0, x, ldx, err);
+  return launch_status("embed_kernel");
+}
+
+// ---------------------------------------------------------------------------
+// LayerNorm: one CTA per row, row cached in shared memory, fp32 two-pass stats
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ float block_sum(float v, float* red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31, nw = blockDim.x >> 5;
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  float tot = 0.f;
+  for (int i = 0; i < nw; ++i) tot += red[i];   // fixed order: deterministic
+  return tot;
+}
+
+__global__ void layernorm_kernel(const float* __restrict__ x, int64_t ldx, const float* __restrict__ g,
+                                 const float* __restrict__ b, int64_t d, __nv_bfloat16* __restrict__ out,
+                                 int64_t ldo) {
+  extern __shared__ float srow[];
+  __shared__ float red[32];
+  const float* xr = x + blockIdx.x * ldx;
+  float s = 0.f;
+  for (int64_t c = threadIdx.x; c < d; c += blockDim.x) {
+    const float v = xr[c];
+    srow[c] = v;
+    s += v;
+  }
+  const float mu = block_sum(s, red) / (float)d;
+  float q = 0.f;
+  for (int64_t c = threadIdx.x; c < d; c += blockDim.x) {
+    const float dv = srow[c] - mu;
+    q += dv * dv;
+  }
+  const float var = block_sum(q, red) / (float)d;
+  const float rstd = 1.0f / sqrtf(var + 1e-5f);
+  __nv_bfloat16* orow = out + blockIdx.x * ldo;
+  for (int64_t c = threadIdx.x; c < d; c += blockDim.x)
+    orow[c] = __float2bfloat16_rn(fmaf((srow[c] - mu) * rstd, g[c], b[c]));
+}
+
+int layernorm_launch(const float* x, int64_t ldx, const float* g, const float* b, int64_t rows, int64_t d,
+                     __nv_bfloat16* out, int64_t ldo, cudaStream_t st) {
+  if (rows == 0) return ZO_OK;
+  const size_t smem = (size_t)d * sizeof(float);
+  static bool big_smem = false;
+  if (smem + 256 > 48 * 1024 && !big_smem) {
+    cudaFuncSetAttribute(layernorm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    big_smem = true;
+  }
+  const int threads = d >= 1024 ? 512 : (d >= 256 ? 256 : 64);
+  layernorm_kernel<<<(unsigned)rows, threads, smem, st>>>(x, ldx, g, b, d, out, ldo);
+  return launch_status("layernorm_kernel");
+}
+
+// ---------------------------------------------------------------------------
+// cross-entropy finalize: per row combine the N-tile partials (fixed order),
+// then a single-CTA fixed-order f64 mean -- bit-stable run to run.
+// ---------------------------------------------------------------------------
+__global__ void ce_rows_kernel(const float* __restrict__ part, const float* __restrict__ tgt, int64_t rows,
+                               int64_t n_tiles, double* __restrict__ row_loss, int32_t* err) {
+  const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r >= rows) return;
+  const float* p = part + r * n_tiles * 2;
+  double m = -INFINITY;
+  bool bad = false;
+  for (int64_t i = 0; i < n_tiles; ++i) {
+    const float v = p[2 * i];
+    if (!isfinite(v)) bad = true;
+    m = fmax(m, (double)v);
+  }
+  double s = 0.0;
+  for (int64_t i = 0; i < n_tiles; ++i) {
+    const float ps = p[2 * i + 1];
+    if (!isfinite(ps)) bad = true;
+    s += (double)ps * exp((double)p[2 * i] - m);
+  }
+  const float tl = tgt[r];
+  if (!isfinite(tl)) bad = true;
+  if (bad) atomicOr(err, 2);
+  row_loss[r] = m + log(s) - (double)tl;
+}
+
+__global__ void mean_f64_kernel(const double* __restrict__ v, int64_t n, double* out) {
+  __shared__ double red[1024];
+  double s = 0.0;
+  // contiguous chunk per thread, then a fixed-shape tree: deterministic
+  const int64_t per = (n + blockDim.x - 1) / blockDim.x;
+  const int64_t lo = threadIdx.x * per, hi = min(lo + per, n);
+  for (int64_t i = lo; i < hi; ++i) s += v[i];
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int st = blockDim.x / 2; st > 0; st >>= 1) {
+    if ((int)threadIdx.x < st) red[threadIdx.x] += red[threadIdx.x + st];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[0] = red[0] / (double)n;
+}
+
+int ce_finalize_launch(const float* part, const float* tgt, int64_t rows, int64_t n_tiles, double* loss,
+                       double* row_scratch, int32_t* err, cudaStream_t st) {
+  if (rows == 0) return ZO_OK;
+  ce_rows_kernel<<<(unsigned)((rows + 127) / 128), 128, 0, st>>>(part, tgt, rows, n_tiles, row_scratch, err);
+  mean_f64_kernel<<<1, 1024, 0, st>>>(row_scratch, rows, loss);
+  return launch_status("ce_finalize");
+}
+
+// ---------------------------------------------------------------------------
+// projected gradient + scalar state for the folded update
+// ---------------------------------------------------------------------------
+__global__ void grad_finalize_kernel(const double* lp, const double* ln, double eps, double lr,
+                                     ZoStepScalars* scal, double* rec) {
+  const double a = *lp, b = *ln;
+  const double g = (a - b) / (2.0 * eps);
+  rec[0] = a; rec[1] = b; rec[2] = g;
+  scal->seed_prev = scal->seed_cur;
+  scal->lr_g_prev = lr * g;
+  scal->pending = 1;
+}
+
+__global__ void grad_groups_kernel(const double* losses, int n, int mine, double eps, double lr,
+                                   ZoStepScalars* scal, double* rec) {
+  double tot = 0.0;
+  for (int i = 0; i < n; ++i) tot += (losses[2 * i] - losses[2 * i + 1]) / (2.0 * eps);
+  const double g = tot / (double)n;
+  rec[0] = losses[2 * mine]; rec[1] = losses[2 * mine + 1]; rec[2] = g;
+  scal->seed_prev = scal->seed_cur;
+  scal->lr_g_prev = lr * g;
+  scal->pending = 1;
+}
+
+int grad_finalize_launch(const double* lp, const double* ln, double eps, double lr, ZoStepScalars* scal,
+                         double* rec, cudaStream_t st) {
+  grad_finalize_kernel<<<1, 1, 0, st>>>(lp, ln, eps, lr, scal, rec);
+  return launch_status("grad_finalize_kernel");
+}
+
+int grad_groups_launch(const double* losses, int n, int mine, double eps, double lr, ZoStepScalars* scal,
+                       double* rec, cudaStream_t st) {
+  grad_groups_kernel<<<1, 1, 0, st>>>(losses, n, mine, eps, lr, scal, rec);
+  return launch_status("grad_groups_kernel");
+}
+
+// ---------------------------------------------------------------------------
+// replica hash: per-CTA FNV-1a-style mix of 8-byte words, combined in order
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t mix64(uint64_t h, uint64_t v) {
+  h ^= v + 0x9E3779B97F4A7C15ull + (h << 6) + (h >> 2);
+  h *= 0x100000001B3ull;
+  return h;
+}
+
+__global__ void hash_partial_kernel(const uint8_t* __restrict__ p, int64_t nbytes, uint64_t* partial) {
+  __shared__ uint64_t red[256];
+  const int64_t nblk = gridDim.x;
+  const int64_t chunk = ((nbytes + nblk - 1) / nblk + 7) & ~int64_t(7);
+  const int64_t lo = blockIdx.x * chunk, hi = min(lo + chunk, nbytes);
+  uint64_t h = 0xcbf29ce484222325ull ^ (uint64_t)threadIdx.x;
+  for (int64_t i = lo + threadIdx.x * 8; i < hi; i += blockDim.x * 8) {
+    uint64_t w = 0;
+    if (i + 8 <= hi) w = *reinterpret_cast<const uint64_t*>(p + i);
+    else for (int64_t j = i; j < hi; ++j) w |= (uint64_t)p[j] << (8 * (j - i));
+    h = mix64(h, w ^ (uint64_t)i);
+  }
+  red[threadIdx.x] = h;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint64_t acc = 0x84222325cbf29ce4ull;
+    for (int i = 0; i < (int)blockDim.x; ++i) acc = mix64(acc, red[i]);
+    partial[blockIdx.x] = acc;
+  }
+}
+
+__global__ void hash_final_kernel(const uint64_t* partial, int n, uint64_t* out) {
+  uint64_t acc = 0x1234567887654321ull;
+  for (int i = 0; i < n; ++i) acc = mix64(acc, partial[i]);
+  *out = acc;
+}
+
+int hash_launch(const void* data, int64_t nbytes, uint64_t* out, uint64_t* scratch, int nblk, cudaStream_t st) {
+  const bool aligned = (reinterpret_cast<uintptr_t>(data) & 7) == 0;
+  if (!aligned) { set_error("zo_hash_u64: buffer must be 8-byte aligned"); return ZO_ERR_CONFIG; }
+  hash_partial_kernel<<<nblk, 256, 0, st>>>(static_cast<const uint8_t*>(data), nbytes, scratch);
+  hash_final_kernel<<<1, 1, 0, st>>>(scratch, nblk, out);
+  return launch_status("hash");
+}
+
+}  // namespace zo

@@ -1,0 +1,359 @@
+"""Device-resident ZO engine: parameter master, shadow layout, workspaces and
+the launch plans of the perturb / dual-forward / projected-gradient step.
+
+HBM layout (one GPU, resident model):
+  theta       fp32 [P]  master in the reference's (block, tensor, element)
+              order; element index == global key of the direction z
+  wsh[s]      bf16      perturbed GEMM operands for direction s (s=0: +eps,
+              s=1: -eps); each weight keeps the reference's (d_in, d_out)
+              row-major layout, wq|wk|wv are interleaved into one
+              [d, 3d] operand so QKV is a single GEMM
+  vsh[s]      fp32      perturbed LN gains/biases and GEMM biases
+  (embedding) no shadow: the gather kernel perturbs the rows it reads
+  scal        ZoStepScalars (device) - seeds, lr*g_prev, pending flag
+Per-direction workspace: x fp32 [M,d] residual stream, h/ctx bf16 [M,d],
+qkv bf16 [M,3d], ff bf16 [M,4d], CE partials [M, V/256, 2].
+
+Every launch is a ctypes call into libzo_b200.so with precomputed integer
+arguments ("launch plans"), so a step costs ~one Python call per kernel and
+can be captured into a CUDA graph.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+import torch
+
+from . import _lib as L
+from .errors import ConfigurationError, DimensionError, NumericError
+from .model import EMBEDDING, HEAD, TRANSFORMER, ModelConfig, init_block_host, model_layout
+
+PLUS, MINUS = 0, 1
+
+
+def _r8(x: int) -> int:
+    return (x + 7) // 8 * 8
+
+
+def _a64(x: int) -> int:
+    return (x + 63) // 64 * 64
+
+
+class ShadowPlan:
+    """Where each tensor's perturbed copy lives, and the perturb kernel's
+    segment tables (per block and for the whole model)."""
+
+    def __init__(self, config: ModelConfig, layouts):
+        d, v = config.d_model, config.vocab_size
+        self.config = config
+        self.w_elems = 0
+        self.v_elems = 0
+        self.views = {}       # bid -> name -> (buffer 'w'|'v', offset, rows, cols, ld)
+        self.segments = {}    # bid -> [ZoSegment fields]
+
+        def walloc(rows, cols):
+            ld = _r8(cols)
+            off = _a64(self.w_elems)
+            self.w_elems = off + rows * ld
+            return off, ld
+
+        def valloc(n):
+            off = (self.v_elems + 3) // 4 * 4
+            self.v_elems = off + n
+            return off
+
+        for bl in layouts:
+            vw, segs = {}, []
+            if bl.kind == EMBEDDING:
+                for name in bl.names:
+                    segs.append((bl.key(name), 1, bl.size(name), 0, bl.size(name), L.ZO_SHADOW_NONE))
+            elif bl.kind == TRANSFORMER:
+                qo, qld = walloc(d, 3 * d)
+                vw["qkv"] = ("w", qo, d, 3 * d, qld)
+                for name, (r, c) in (("wo", (d, d)), ("w1", (d, 4 * d)), ("w2", (4 * d, d))):
+                    o, ld = walloc(r, c)
+                    vw[name] = ("w", o, r, c, ld)
+                for name, n in (("ln1_g", d), ("ln1_b", d), ("bqkv", 3 * d), ("bo", d), ("ln2_g", d),
+                                ("ln2_b", d), ("b1", 4 * d), ("b2", d)):
+                    vw[name] = ("v", valloc(n), 1, n, n)
+                for name in bl.names:
+                    k, n = bl.key(name), bl.size(name)
+                    if name in ("wq", "wk", "wv"):
+                        j = "qkv".index(name[1])
+                        segs.append((k, d, d, qo + j * d, qld, L.ZO_SHADOW_BF16))
+                    elif name in ("bq", "bk", "bv"):
+                        j = "qkv".index(name[1])
+                        segs.append((k, 1, d, vw["bqkv"][1] + j * d, d, L.ZO_SHADOW_F32))
+                    elif name in ("wo", "w1", "w2"):
+                        _, o, r, c, ld = vw[name]
+                        if ld == c:
+                            segs.append((k, 1, r * c, o, r * c, L.ZO_SHADOW_BF16))
+                        else:
+                            segs.append((k, r, c, o, ld, L.ZO_SHADOW_BF16))
+                    else:
+                        segs.append((k, 1, n, vw[name][1], n, L.ZO_SHADOW_F32))
+            else:  # head
+                wo_, wld = walloc(d, v)
+                vw["w_out"] = ("w", wo_, d, v, wld)
+                for name, n in (("lnf_g", d), ("lnf_b", d), ("b_out", v)):
+                    vw[name] = ("v", valloc(n), 1, n, n)
+                for name in bl.names:
+                    k, n = bl.key(name), bl.size(name)
+                    if name == "w_out":
+                        if wld == v:
+                            segs.append((k, 1, d * v, wo_, d * v, L.ZO_SHADOW_BF16))
+                        else:
+                            segs.append((k, d, v, wo_, wld, L.ZO_SHADOW_BF16))
+                    else:
+                        segs.append((k, 1, n, vw[name][1], n, L.ZO_SHADOW_F32))
+            self.views[bl.block_id] = vw
+            self.segments[bl.block_id] = segs
+        self.w_elems = _a64(self.w_elems) + 64
+        self.v_elems = self.v_elems + 4
+
+
+class SegTable:
+    """Device copy of a segment list + its tile prefix."""
+
+    def __init__(self, segs, device):
+        tile = int(L.lib().zo_perturb_tile_elems())
+        arr = (L.ZoSegment * max(1, len(segs)))()
+        prefix = np.zeros(len(segs) + 1, dtype=np.int64)
+        for i, (src, rows, cols, dst, ld, kind) in enumerate(segs):
+            arr[i] = L.ZoSegment(src, rows, cols, dst, ld, kind, 0)
+            prefix[i + 1] = prefix[i] + rows * ((cols + tile - 1) // tile)
+        raw = np.frombuffer(bytes(arr), dtype=np.uint8).copy()
+        self.segs = torch.from_numpy(raw).to(device)
+        self.prefix = torch.from_numpy(prefix).to(device)
+        self.n_segs = len(segs)
+        self.n_tiles = int(prefix[-1])
+        self.elems = int(sum(r * c for _, r, c, _, _, _ in segs))
+
+
+class Workspace:
+    """Activations of one directional forward at batch shape (B, T)."""
+
+    def __init__(self, config: ModelConfig, batch: int, seq: int, device):
+        d, v = config.d_model, config.vocab_size
+        self.batch, self.seq, self.M = batch, seq, batch * seq
+        M = self.M
+        ld = _r8(d)
+        self.x = torch.zeros(M, ld, dtype=torch.float32, device=device)
+        self.h = torch.zeros(M, ld, dtype=torch.bfloat16, device=device)
+        self.ctx = torch.zeros(M, ld, dtype=torch.bfloat16, device=device)
+        self.qkv = torch.zeros(M, _r8(3 * d), dtype=torch.bfloat16, device=device)
+        self.ff = torch.zeros(M, _r8(4 * d), dtype=torch.bfloat16, device=device)
+        self.n_ce = int(L.lib().zo_gemm_ce_tiles(v))
+        self.ce_part = torch.zeros(M, self.n_ce, 2, dtype=torch.float32, device=device)
+        self.ce_tgt = torch.zeros(M, dtype=torch.float32, device=device)
+        self.row_scratch = torch.zeros(M, dtype=torch.float64, device=device)
+        self.loss = torch.zeros(1, dtype=torch.float64, device=device)
+        self.ids = torch.zeros(M, dtype=torch.int32, device=device)
+        self.tgt = torch.zeros(M, dtype=torch.int32, device=device)
+        self.err = torch.zeros(1, dtype=torch.int32, device=device)
+
+
+def _ptr(t):
+    return 0 if t is None else t.data_ptr()
+
+
+class DeviceStore:
+    """The model's parameters on one GPU plus everything the ZO step needs.
+
+    ``theta`` is the fp32 master (the reference's ParamStore buffers,
+    src/zosim/model.py:160-200, concatenated in block order).
+    """
+
+    def __init__(self, config: ModelConfig, init_seed: int = 7, device=None, init: str = "host",
+                 directions=(PLUS, MINUS)):
+        config.validate()
+        self.config = config
+        self.init_seed = init_seed
+        self.device = torch.device(device or f"cuda:{torch.cuda.current_device()}")
+        L.lib()
+        self.layouts = model_layout(config)
+        self.total_params = sum(b.elem_count for b in self.layouts)
+        self.theta = torch.empty(self.total_params, dtype=torch.float32, device=self.device)
+        if init == "host":
+            for bl in self.layouts:
+                buf = init_block_host(config, bl, init_seed)
+                self.theta[bl.key0:bl.key0 + bl.elem_count].copy_(torch.from_numpy(buf))
+        elif init == "philox":
+            self._init_philox(init_seed)
+        elif init != "none":
+            raise ConfigurationError(f"unknown init {init!r}")
+        self.plan = ShadowPlan(config, self.layouts)
+        self.directions = tuple(directions)
+        self.wsh = [None, None]
+        self.vsh = [None, None]
+        for s in self.directions:
+            self.wsh[s] = torch.zeros(self.plan.w_elems, dtype=torch.bfloat16, device=self.device)
+            self.vsh[s] = torch.zeros(self.plan.v_elems, dtype=torch.float32, device=self.device)
+        self.block_tables = {bid: SegTable(segs, self.device) for bid, segs in self.plan.segments.items()}
+        self.model_table = SegTable([s for bid in sorted(self.plan.segments) for s in self.plan.segments[bid]],
+                                    self.device)
+        self.scal = torch.zeros(4, dtype=torch.int64, device=self.device)   # ZoStepScalars
+        self.record = torch.zeros(3, dtype=torch.float64, device=self.device)
+        self._ws = {}
+
+    # -- initialisation at scale -----------------------------------------------
+    def _init_philox(self, init_seed: int):
+        """Random init on the GPU for models too large for a host numpy draw
+        (configs #3-#5 are 'random-init'): weights 0.02 * z(init_seed, key),
+        LN gains 1, biases 0 -- same distribution as model.py:203-229."""
+        seed = (0x1A2B3C4D << 32) ^ int(init_seed)
+        chunk = 1 << 26
+        for bl in self.layouts:
+            for name in bl.names:
+                k, n = bl.key(name), bl.size(name)
+                dst = self.theta[k:k + n]
+                if name.endswith("_g"):
+                    dst.fill_(1.0)
+                elif name.startswith("b") or name.endswith("_b"):
+                    dst.zero_()
+                else:
+                    for o in range(0, n, chunk):
+                        m = min(chunk, n - o)
+                        z = torch.empty(m, dtype=torch.float32, device=self.device)
+                        L.call("zo_philox_normals", seed, k + o, m, z.data_ptr(), L.stream_ptr())
+                        dst[o:o + m].copy_(z.mul_(0.02))
+
+    # -- views -----------------------------------------------------------------
+    def block_buf(self, bid: int) -> torch.Tensor:
+        bl = self.layouts[bid]
+        return self.theta[bl.key0:bl.key0 + bl.elem_count]
+
+    def wview(self, s: int, bid: int, name: str):
+        buf, off, rows, cols, ld = self.plan.views[bid][name]
+        assert buf == "w"
+        return self.wsh[s][off:off + rows * ld].view(rows, ld), rows, cols
+
+    def vview(self, s: int, bid: int, name: str) -> torch.Tensor:
+        buf, off, rows, cols, ld = self.plan.views[bid][name]
+        assert buf == "v"
+        return self.vsh[s][off:off + cols]
+
+    def workspace(self, s: int, batch: int, seq: int) -> Workspace:
+        key = (s, batch, seq)
+        if key not in self._ws:
+            self._ws[key] = Workspace(self.config, batch, seq, self.device)
+        return self._ws[key]
+
+    # -- scalar state ----------------------------------------------------------
+    def set_seed(self, seed: int, stream=None):
+        self.scal[0:1].fill_(int(seed))
+
+    def set_pending(self, g_lr: float, seed_prev: int, pending: bool):
+        host = np.zeros(4, dtype=np.int64)
+        host[0] = int(self.scal[0].item())
+        host[1] = np.int64(np.uint64(seed_prev & ((1 << 64) - 1)).view(np.int64))
+        host[2] = np.float64(g_lr).view(np.int64)
+        host[3] = 1 if pending else 0
+        self.scal.copy_(torch.from_numpy(host))
+
+    def scalars(self) -> dict:
+        h = self.scal.cpu().numpy()
+        return {"seed_cur": int(h[0]), "seed_prev": int(h[1]), "lr_g_prev": float(h[2:3].view(np.float64)[0]),
+                "pending": int(h[3])}
+
+    # -- launch plans ----------------------------------------------------------
+    def perturb_call(self, table: SegTable, flags: int, scale_a: float, scale_b: float, sa=PLUS, sb=MINUS,
+                     zmode=L.ZO_Z_PHILOX, z_cur=None, z_prev=None, stream=None):
+        fn = L.lib().zo_perturb_update
+        args = (_ptr(self.theta), 0, _ptr(table.segs), _ptr(table.prefix), table.n_segs, table.n_tiles,
+                _ptr(self.wsh[sa]) if sa is not None else 0, _ptr(self.vsh[sa]) if sa is not None else 0,
+                _ptr(self.wsh[sb]) if sb is not None else 0, _ptr(self.vsh[sb]) if sb is not None else 0,
+                float(scale_a), float(scale_b), flags, _ptr(self.scal), zmode, _ptr(z_cur), _ptr(z_prev), 0,
+                L.stream_ptr(stream))
+        return [(fn, args)]
+
+    def forward_calls(self, s: int, ws: Workspace, scale: float, zmode=L.ZO_Z_PHILOX, z_cur=None, stream=None,
+                      blocks=None, head_mode="ce", logits=None):
+        """Launch plan of one directional forward through blocks [0..N+1]
+        (embedding -> N decoder blocks -> LN_f + LM head + CE)."""
+        cfg, lib = self.config, L.lib()
+        d, H, hd, V = cfg.d_model, cfg.n_heads, cfg.head_dim, cfg.vocab_size
+        M, B, T = ws.M, ws.batch, ws.seq
+        st = L.stream_ptr(stream)
+        calls = []
+        blocks = range(len(self.layouts)) if blocks is None else blocks
+        for bid in blocks:
+            bl = self.layouts[bid]
+            if bl.kind == EMBEDDING:
+                calls.append((lib.zo_embed_fwd, (
+                    _ptr(self.theta) + 4 * bl.key("tok_emb"), bl.key("tok_emb"),
+                    _ptr(self.theta) + 4 * bl.key("pos_emb"), bl.key("pos_emb"),
+                    _ptr(ws.ids), B, T, d, V, float(scale), _ptr(self.scal), zmode, _ptr(z_cur), 0,
+                    _ptr(ws.x), ws.x.stride(0), _ptr(ws.err), st)))
+            elif bl.kind == TRANSFORMER:
+                v = lambda n: _ptr(self.vview(s, bid, n))  # noqa: E731
+                wq, _, _ = self.wview(s, bid, "qkv")
+                wo, _, _ = self.wview(s, bid, "wo")
+                w1, _, _ = self.wview(s, bid, "w1")
+                w2, _, _ = self.wview(s, bid, "w2")
+                ldx, ldh = ws.x.stride(0), ws.h.stride(0)
+                calls += [
+                    (lib.zo_layernorm_fwd, (_ptr(ws.x), ldx, v("ln1_g"), v("ln1_b"), M, d, _ptr(ws.h), ldh, st)),
+                    (lib.zo_gemm_bf16, (_ptr(ws.h), ldh, _ptr(wq), wq.stride(0), M, 3 * d, d, L.ZO_EPI_BIAS_BF16,
+                                        v("bqkv"), _ptr(ws.qkv), ws.qkv.stride(0), 0, 0, 0, 0, st)),
+                    (lib.zo_attn_causal_fwd, (_ptr(ws.qkv), ws.qkv.stride(0), B, T, H, hd, _ptr(ws.ctx),
+                                              ws.ctx.stride(0), st)),
+                    (lib.zo_gemm_bf16, (_ptr(ws.ctx), ws.ctx.stride(0), _ptr(wo), wo.stride(0), M, d, d,
+                                        L.ZO_EPI_BIAS_RESID_F32, v("bo"), _ptr(ws.x), ldx, 0, 0, 0, 0, st)),
+                    (lib.zo_layernorm_fwd, (_ptr(ws.x), ldx, v("ln2_g"), v("ln2_b"), M, d, _ptr(ws.h), ldh, st)),
+                    (lib.zo_gemm_bf16, (_ptr(ws.h), ldh, _ptr(w1), w1.stride(0), M, 4 * d, d,
+                                        L.ZO_EPI_BIAS_GELU_BF16, v("b1"), _ptr(ws.ff), ws.ff.stride(0), 0, 0, 0, 0,
+                                        st)),
+                    (lib.zo_gemm_bf16, (_ptr(ws.ff), ws.ff.stride(0), _ptr(w2), w2.stride(0), M, d, 4 * d,
+                                        L.ZO_EPI_BIAS_RESID_F32, v("b2"), _ptr(ws.x), ldx, 0, 0, 0, 0, st)),
+                ]
+            else:
+                wout, _, _ = self.wview(s, bid, "w_out")
+                calls.append((lib.zo_layernorm_fwd, (_ptr(ws.x), ws.x.stride(0), _ptr(self.vview(s, bid, "lnf_g")),
+                                                     _ptr(self.vview(s, bid, "lnf_b")), M, d, _ptr(ws.h),
+                                                     ws.h.stride(0), st)))
+                bout = _ptr(self.vview(s, bid, "b_out"))
+                if head_mode == "ce":
+                    calls.append((lib.zo_gemm_bf16, (_ptr(ws.h), ws.h.stride(0), _ptr(wout), wout.stride(0), M, V, d,
+                                                     L.ZO_EPI_CE, bout, 0, 0, _ptr(ws.tgt), _ptr(ws.ce_part),
+                                                     _ptr(ws.ce_tgt), _ptr(ws.err), st)))
+                    calls.append((lib.zo_ce_finalize, (_ptr(ws.ce_part), _ptr(ws.ce_tgt), M, ws.n_ce, _ptr(ws.loss),
+                                                       _ptr(ws.row_scratch), _ptr(ws.err), st)))
+                else:   # materialise logits (API forward(); not on the step)
+                    calls.append((lib.zo_gemm_bf16, (_ptr(ws.h), ws.h.stride(0), _ptr(wout), wout.stride(0), M, V, d,
+                                                     L.ZO_EPI_F32, 0, _ptr(logits), logits.stride(0), 0, 0, 0, 0,
+                                                     st)))
+        return calls
+
+    def grad_call(self, ws_pos: Workspace, ws_neg: Workspace, eps: float, lr: float, stream=None):
+        return [(L.lib().zo_grad_finalize, (_ptr(ws_pos.loss), _ptr(ws_neg.loss), float(eps), float(lr),
+                                            _ptr(self.scal), _ptr(self.record), L.stream_ptr(stream)))]
+
+    @staticmethod
+    def run(calls):
+        for fn, args in calls:
+            rc = fn(*args)
+            if rc:
+                L.check(rc)
+
+    # -- host <-> device batch staging -----------------------------------------
+    def load_batch(self, ws: Workspace, token_ids, targets):
+        ids = np.asarray(token_ids)
+        tg = np.asarray(targets)
+        if ids.shape != (ws.batch, ws.seq) or tg.shape != ids.shape:
+            raise DimensionError(f"batch shape {ids.shape} does not match workspace ({ws.batch}, {ws.seq})")
+        if ids.size and (ids.min() < 0 or ids.max() >= self.config.vocab_size):
+            raise DimensionError("token id out of embedding range")
+        ws.ids.copy_(torch.from_numpy(ids.reshape(-1).astype(np.int32)), non_blocking=False)
+        ws.tgt.copy_(torch.from_numpy(tg.reshape(-1).astype(np.int32)), non_blocking=False)
+
+    def check_errors(self, *wss):
+        for ws in wss:
+            e = int(ws.err.item())
+            if e:
+                ws.err.zero_()
+                if e & 4:
+                    raise DimensionError("token id out of embedding range")
+                raise NumericError("non-finite logits")

@@ -1,0 +1,124 @@
+"""Kernel-level parity of the sm_100a library against plain torch fp32
+references of the same op (bf16 operands where the kernel consumes bf16)."""
+
+import math
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+from paper_2507_03211_b200 import _lib as L  # noqa: E402
+from paper_2507_03211_b200 import ops  # noqa: E402
+
+DEV = "cuda"
+
+
+def _rand(*shape, scale=1.0, dtype=torch.bfloat16, seed=0):
+    g = torch.Generator(device="cpu").manual_seed(seed)
+    return (torch.randn(*shape, generator=g) * scale).to(DEV, dtype)
+
+
+GEMM_SHAPES = [(128, 256, 64), (128, 128, 128), (256, 512, 512), (200, 304, 136), (64, 96, 32),
+               (16, 16, 16), (1000, 1000, 1000), (2048, 2048, 2048), (512, 6144, 2048), (64, 50272, 768)]
+
+
+@pytest.mark.parametrize("M,N,K", GEMM_SHAPES)
+def test_gemm_f32_matches_torch(M, N, K):
+    a, b = _rand(M, K, seed=1), _rand(K, N, seed=2)
+    out = torch.full((M, N), float("nan"), device=DEV)
+    ops.gemm(a, b, L.ZO_EPI_F32, out=out)
+    torch.cuda.synchronize()
+    ref = a.float() @ b.float()
+    torch.testing.assert_close(out, ref, rtol=2e-3, atol=2e-3 * math.sqrt(K / 64))
+
+
+@pytest.mark.parametrize("M,N,K", [(256, 768, 256), (200, 304, 136), (2048, 8192, 2048)])
+def test_gemm_bias_and_gelu_epilogues(M, N, K):
+    a, b = _rand(M, K, seed=3, scale=0.5), _rand(K, N, seed=4, scale=0.1)
+    bias = _rand(N, dtype=torch.float32, seed=5)
+    out = torch.empty(M, N, device=DEV, dtype=torch.bfloat16)
+    ops.gemm(a, b, L.ZO_EPI_BIAS_BF16, out=out, bias=bias)
+    ref = a.float() @ b.float() + bias
+    torch.testing.assert_close(out.float(), ref, rtol=1e-2, atol=1e-2)
+    ops.gemm(a, b, L.ZO_EPI_BIAS_GELU_BF16, out=out, bias=bias)
+    refg = torch.nn.functional.gelu(ref, approximate="tanh")
+    torch.testing.assert_close(out.float(), refg, rtol=1e-2, atol=1e-2)
+
+
+@pytest.mark.parametrize("M,N,K", [(256, 768, 3072), (200, 304, 136), (2048, 2048, 8192)])
+def test_gemm_residual_epilogue(M, N, K):
+    a, b = _rand(M, K, seed=6, scale=0.5), _rand(K, N, seed=7, scale=0.05)
+    bias = _rand(N, dtype=torch.float32, seed=8)
+    x = _rand(M, N, dtype=torch.float32, seed=9)
+    ref = x + (a.float() @ b.float() + bias)
+    ops.gemm(a, b, L.ZO_EPI_BIAS_RESID_F32, out=x, bias=bias)
+    torch.testing.assert_close(x, ref, rtol=1e-4, atol=2e-3)
+
+
+@pytest.mark.parametrize("M,V,K", [(64, 50272, 768), (130, 1000, 64), (32, 16, 16)])
+def test_gemm_ce_epilogue_and_finalize(M, V, K):
+    a, b = _rand(M, K, seed=10, scale=0.5), _rand(K, V, seed=11, scale=0.1)
+    bias = _rand(V, dtype=torch.float32, seed=12, scale=0.1)
+    tg = torch.randint(0, V, (M,), generator=torch.Generator().manual_seed(3)).to(DEV, torch.int32)
+    nt = ops.ce_tiles(V)
+    part = torch.empty(M, nt, 2, device=DEV)
+    tl = torch.empty(M, device=DEV)
+    err = torch.zeros(1, dtype=torch.int32, device=DEV)
+    ops.gemm(a, b, L.ZO_EPI_CE, bias=bias, targets=tg, ce_part=part, ce_tgt=tl, err=err)
+    loss = torch.empty(1, dtype=torch.float64, device=DEV)
+    scratch = torch.empty(M, dtype=torch.float64, device=DEV)
+    ops.ce_finalize(part, tl, M, nt, loss, scratch, err)
+    logits = (a.float() @ b.float() + bias).double()
+    ref = torch.nn.functional.cross_entropy(logits, tg.long())
+    assert err.item() == 0
+    assert abs(loss.item() - ref.item()) < 1e-4
+    torch.testing.assert_close(tl.double(), logits.gather(1, tg.long()[:, None])[:, 0], rtol=1e-4, atol=1e-3)
+
+
+@pytest.mark.parametrize("rows,d", [(64, 768), (513, 2048), (7, 6), (3, 12288)])
+def test_layernorm(rows, d):
+    x = _rand(rows, d, dtype=torch.float32, seed=13) * 3 + 1
+    g = _rand(d, dtype=torch.float32, seed=14)
+    b = _rand(d, dtype=torch.float32, seed=15)
+    out = torch.empty(rows, d, dtype=torch.bfloat16, device=DEV)
+    ops.layernorm(x, g, b, out)
+    ref = torch.nn.functional.layer_norm(x, (d,), g, b, eps=1e-5)
+    torch.testing.assert_close(out.float(), ref, rtol=1e-2, atol=2e-2)
+
+
+def _attn_ref(qkv, B, T, H, hd):
+    d = H * hd
+    q, k, v = qkv[:, :d].float(), qkv[:, d:2 * d].float(), qkv[:, 2 * d:3 * d].float()
+    q = q.view(B, T, H, hd).transpose(1, 2)
+    k = k.view(B, T, H, hd).transpose(1, 2)
+    v = v.view(B, T, H, hd).transpose(1, 2)
+    o = torch.nn.functional.scaled_dot_product_attention(q, k, v, is_causal=True)
+    return o.transpose(1, 2).reshape(B * T, d)
+
+
+@pytest.mark.parametrize("B,T,H,hd", [(1, 64, 12, 64), (2, 512, 4, 64), (1, 100, 2, 64), (2, 256, 2, 128),
+                                      (4, 8, 2, 8), (2, 6, 2, 3), (1, 33, 3, 32)])
+def test_attention(B, T, H, hd):
+    qkv = _rand(B * T, 3 * H * hd, seed=16)
+    out = torch.empty(B * T, H * hd, dtype=torch.bfloat16, device=DEV)
+    ops.attention(qkv, B, T, H, hd, out)
+    ref = _attn_ref(qkv, B, T, H, hd)
+    torch.testing.assert_close(out.float(), ref, rtol=2e-2, atol=2e-2)
+
+
+def test_philox_distribution_and_slice_invariance():
+    z = ops.philox_normals(1234567, 0, 1 << 22)
+    zc = z.double().cpu().numpy()
+    assert abs(zc.mean()) < 3e-3 and abs(zc.var() - 1) < 3e-3
+    assert abs(((zc ** 3).mean())) < 1e-2 and abs((zc ** 4).mean() - 3) < 2e-2
+    # slice invariance: any window is the same function of the global key
+    z2 = ops.philox_normals(1234567, 1001, 4099)
+    assert torch.equal(z[1001:1001 + 4099], z2)
+    z3 = ops.philox_normals(7654321, 0, 1 << 10)
+    assert not torch.equal(z[:1024], z3)
+    # KS statistic against N(0,1)
+    from scipy import stats
+    ks = stats.kstest(zc[:200000], "norm").statistic
+    assert ks < 5e-3
