@@ -22,6 +22,8 @@
 //                          the [M, V] logits never reach HBM
 #include <cuda.h>
 #include <cudaTypedefs.h>
+#include <stdlib.h>
+
 #include <mutex>
 #include <unordered_map>
 
@@ -475,6 +477,11 @@ int gemm_launch(const void* A, int64_t lda, const void* B, int64_t ldb, int64_t 
   int bn = 128;
   const int64_t tiles256 = ((M + kBM - 1) / kBM) * ((N + 255) / 256);
   if (epi == ZO_EPI_CE || tiles256 >= num_sms()) bn = 256;
+  static const int force_bn = [] {
+    const char* e = getenv("ZO_GEMM_BN");   // tuning override (128 | 256)
+    return e ? atoi(e) : 0;
+  }();
+  if (epi != ZO_EPI_CE && (force_bn == 128 || force_bn == 256)) bn = force_bn;
   CUtensorMap ma, mb;
   int rc = get_map(A, K, M, lda, kBK, kBM, &ma);
   if (rc) return rc;

@@ -357,3 +357,8 @@ class DeviceStore:
                 if e & 4:
                     raise DimensionError("token id out of embedding range")
                 raise NumericError("non-finite logits")
+
+
+def init_model(config: ModelConfig, init_seed: int, device=None, init: str = "host") -> DeviceStore:
+    """zosim.init_model (model.py:203-229) returning a GPU-resident store."""
+    return DeviceStore(config, init_seed=init_seed, device=device, init=init)

@@ -1,0 +1,410 @@
+"""Zeroth-order optimizer API on the GPU (mirror of src/zosim/zo.py).
+
+Same names, arguments and error behaviour as the reference:
+
+  ZoHyper, ZoStep, zo_grad                       zo.py:42-84
+  perturb_block / perturb_params                 zo.py:90-113
+  update_block / update_params                   zo.py:116-130
+  mezo_step  (Alg. 1, eager)                     zo.py:136-168
+  dual_forward (Alg. 2, one block)               zo.py:181-224
+  flush_pending_update, StreamingZo (lazy)       zo.py:227-293
+
+What differs is where the work happens: parameters are the fp32 master
+``store.theta`` on the GPU; a perturbation writes the bf16/fp32 shadows the
+forward kernels read (never the master, so restore is free and exact); the
+whole-model step is ONE fused perturb/update launch + two forwards + a device
+projected-gradient kernel, with the update of step j folded into the
+perturbation pass of step j+1 (StreamingZo) or applied eagerly (mezo_step).
+
+``mgr`` selects the direction source: RngStateManager("philox") (default,
+in-register counter-based z) or RngStateManager("oracle") (the reference's
+numpy PCG64 z injected; perturb/update arithmetic then matches the reference
+bit for bit).
+"""
+
+from __future__ import annotations
+
+import json
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib as L
+from .engine import MINUS, PLUS, DeviceStore
+from .errors import DimensionError, NumericError, ProtocolError
+from .model import EMBEDDING, HEAD, Batch
+from .rng import PhiloxKey, RngStateManager
+
+
+@dataclass(frozen=True)
+class ZoHyper:
+    epsilon: float
+    lr: float
+    steps: int = 1
+
+    def validate(self) -> "ZoHyper":
+        if not self.epsilon > 0:
+            raise NumericError(f"epsilon must be > 0, got {self.epsilon}")
+        if not self.lr > 0:
+            raise NumericError(f"lr must be > 0, got {self.lr}")
+        if self.steps < 1:
+            raise NumericError(f"steps must be >= 1, got {self.steps}")
+        return self
+
+
+@dataclass
+class ZoStep:
+    iteration: int
+    seed: int
+    loss_pos: float
+    loss_neg: float
+    g: float
+
+    def to_json(self) -> str:
+        return json.dumps({"iter": self.iteration, "seed": self.seed, "loss_pos": self.loss_pos,
+                           "loss_neg": self.loss_neg, "g": self.g})
+
+
+def zo_grad(loss_pos: float, loss_neg: float, epsilon: float) -> float:
+    if epsilon == 0:
+        raise NumericError("epsilon must be nonzero")
+    return (loss_pos - loss_neg) / (2.0 * epsilon)
+
+
+# ---------------------------------------------------------------------------
+# scalar staging helpers
+# ---------------------------------------------------------------------------
+
+def _u64_as_i64(x: int) -> int:
+    return int(np.uint64(int(x) & ((1 << 64) - 1)).view(np.int64))
+
+
+def _scal_tensor(device, seed_cur=0, seed_prev=0, lr_g=0.0, pending=0) -> torch.Tensor:
+    h = np.zeros(4, dtype=np.int64)
+    h[0], h[1] = _u64_as_i64(seed_cur), _u64_as_i64(seed_prev)
+    h[2] = np.float64(lr_g).view(np.int64)
+    h[3] = pending
+    return torch.from_numpy(h).to(device)
+
+
+def _write_scal(store: DeviceStore, seed_cur: int, pending: bool) -> None:
+    """Host writes the iteration seed; keeps seed_prev / lr_g_prev left by
+    the device gradient kernel and sets the pending flag explicitly
+    (zo.py:267-271: a flag, not g != 0)."""
+    store.scal[0:1].fill_(_u64_as_i64(seed_cur))
+    store.scal[3:4].fill_(1 if pending else 0)
+
+
+def _oracle_z(mgr: RngStateManager, seed: int, n: int, device) -> torch.Tensor:
+    mgr.reset(seed)
+    return torch.from_numpy(mgr.generator(seed).standard_normal(n)).to(device)
+
+
+def _stage_batch(store: DeviceStore, batch: Batch):
+    batch.validate(store.config)
+    B, T = batch.token_ids.shape
+    wsp, wsn = store.workspace(PLUS, B, T), store.workspace(MINUS, B, T)
+    store.load_batch(wsp, batch.token_ids, batch.targets)
+    store.load_batch(wsn, batch.token_ids, batch.targets)
+    return wsp, wsn
+
+
+def _finish(store: DeviceStore, wsp, wsn, iteration: int, seed: int) -> ZoStep:
+    rec = store.record.cpu().numpy()          # synchronises the stream
+    store.check_errors(wsp, wsn)
+    return ZoStep(iteration, seed, float(rec[0]), float(rec[1]), float(rec[2]))
+
+
+# ---------------------------------------------------------------------------
+# whole-model steps (the hot path)
+# ---------------------------------------------------------------------------
+
+def mezo_step(store: DeviceStore, batch: Batch, hyper: ZoHyper, seed: int, mgr: RngStateManager | None = None,
+              iteration: int = 1) -> ZoStep:
+    """Alg. 1 (zo.py:136-168): L+ at theta+eps z, L- at theta-eps z, g, then
+    theta -= (lr g) z before returning."""
+    hyper.validate()
+    mgr = mgr or RngStateManager()
+    eps = hyper.epsilon
+    wsp, wsn = _stage_batch(store, batch)
+    zc = _oracle_z(mgr, seed, store.total_params, store.device) if mgr.oracle else None
+    zmode = L.ZO_Z_ORACLE if mgr.oracle else L.ZO_Z_PHILOX
+    _write_scal(store, seed, pending=False)
+    t = store.model_table
+    calls = store.perturb_call(t, L.ZO_PU_SHADOW_A | L.ZO_PU_SHADOW_B, +eps, -eps, zmode=zmode, z_cur=zc)
+    calls += store.forward_calls(PLUS, wsp, +eps, zmode=zmode, z_cur=zc)
+    calls += store.forward_calls(MINUS, wsn, -eps, zmode=zmode, z_cur=zc)
+    calls += store.grad_call(wsp, wsn, eps, hyper.lr)
+    calls += store.perturb_call(t, L.ZO_PU_UPDATE, 0.0, 0.0, sa=None, sb=None, zmode=zmode, z_prev=zc)
+    store.run(calls)
+    store.scal[3:4].fill_(0)                  # the update has been applied
+    return _finish(store, wsp, wsn, iteration, seed)
+
+
+class StreamingZo:
+    """Lazy-update executor (zo.py:245-293): the update of iteration j is
+    folded into iteration j+1's perturbation pass; ``flush`` applies the last
+    one.  Numerically identical to repeated ``mezo_step`` after flush."""
+
+    def __init__(self, store: DeviceStore, hyper: ZoHyper, mgr: RngStateManager | None = None):
+        self.store = store
+        self.hyper = hyper.validate()
+        self.mgr = mgr or RngStateManager()
+        self.iteration = 0
+        self.g_prev = 0.0
+        self.last_seed = None
+        self._pending = False
+        self._z_prev = None
+
+    def step_calls(self, wsp, wsn, zc=None, zp=None, update=True):
+        """One lazy step: fused (update_{j-1} + perturb_j) pass, both
+        directional forwards, device projected gradient.  With update=True the
+        kernel applies the pending update iff the device flag says so, which is
+        what lets a captured graph replay steps unchanged."""
+        s, eps = self.store, self.hyper.epsilon
+        zmode = L.ZO_Z_ORACLE if self.mgr.oracle else L.ZO_Z_PHILOX
+        flags = (L.ZO_PU_UPDATE if update else 0) | L.ZO_PU_SHADOW_A | L.ZO_PU_SHADOW_B
+        calls = s.perturb_call(s.model_table, flags, +eps, -eps, zmode=zmode, z_cur=zc, z_prev=zp)
+        calls += s.forward_calls(PLUS, wsp, +eps, zmode=zmode, z_cur=zc)
+        calls += s.forward_calls(MINUS, wsn, -eps, zmode=zmode, z_cur=zc)
+        calls += s.grad_call(wsp, wsn, eps, self.hyper.lr)
+        return calls
+
+    def step(self, batch: Batch, seed: int) -> ZoStep:
+        self.iteration += 1
+        self.mgr.reset(seed)
+        self.mgr.push_state(self.mgr.capture(seed))
+        apply_pending = self.iteration > 1 and self._pending
+        if apply_pending:
+            self.mgr.pop_state()
+        wsp, wsn = _stage_batch(self.store, batch)
+        zc = _oracle_z(self.mgr, seed, self.store.total_params, self.store.device) if self.mgr.oracle else None
+        _write_scal(self.store, seed, pending=apply_pending)
+        self.store.run(self.step_calls(wsp, wsn, zc, self._z_prev if apply_pending else None,
+                                       update=apply_pending or not self.mgr.oracle))
+        st = _finish(self.store, wsp, wsn, self.iteration, seed)
+        self.g_prev, self.last_seed, self._pending, self._z_prev = st.g, seed, True, zc
+        return st
+
+    def flush(self) -> None:
+        if not self._pending:
+            raise ProtocolError("flush with no pending update (double flush?)")
+        self.mgr.pop_state()
+        s = self.store
+        zmode = L.ZO_Z_ORACLE if self.mgr.oracle else L.ZO_Z_PHILOX
+        s.scal[3:4].fill_(1)
+        s.run(s.perturb_call(s.model_table, L.ZO_PU_UPDATE, 0.0, 0.0, sa=None, sb=None, zmode=zmode,
+                             z_prev=self._z_prev))
+        s.scal[3:4].fill_(0)
+        torch.cuda.current_stream().synchronize()
+        self._pending = False
+
+
+def flush_pending_update(store: DeviceStore, g_last: float, seed: int, mgr: RngStateManager, lr: float) -> None:
+    """zo.py:227-242: apply the deferred update of the most recent iteration
+    to every block."""
+    try:
+        mgr.pop_state()
+    except ProtocolError as e:
+        raise ProtocolError("flush with no pending update (double flush?)") from e
+    update_params(store, g_last, lr, mgr.generator(seed) if not mgr.oracle else _restart(mgr, seed))
+
+
+def _restart(mgr, seed):
+    mgr.reset(seed)
+    return mgr.generator(seed)
+
+
+# ---------------------------------------------------------------------------
+# per-block API (API parity with the reference; the step above is the fast path)
+# ---------------------------------------------------------------------------
+
+class DeviceBlock:
+    """One block of a DeviceStore, shaped like zosim.ParamBlock
+    (model.py:104-157): ``buf`` is the fp32 master view on the GPU."""
+
+    def __init__(self, store: DeviceStore, block_id: int):
+        self.store, self.block_id = store, block_id
+        bl = store.layouts[block_id]
+        self.kind, self.names, self.offsets, self.elem_count = bl.kind, bl.names, bl.offsets, bl.elem_count
+        self.shapes = bl.shapes
+        self.key0 = bl.key0
+        self.n_heads = store.config.n_heads
+        self.pert_scale = 0.0
+        self._zsrc = (L.ZO_Z_PHILOX, None, 0)     # (mode, z tensor | seed, z_key0) of the open cycle
+
+    @property
+    def buf(self) -> torch.Tensor:
+        return self.store.block_buf(self.block_id)
+
+    def tensor(self, name: str) -> torch.Tensor:
+        o = self.offsets[name]
+        n = int(np.prod(self.shapes[name]))
+        return self.buf[o:o + n].view(self.shapes[name])
+
+    @property
+    def nbytes(self) -> int:
+        return self.elem_count * 4
+
+
+def store_blocks(store: DeviceStore):
+    if not hasattr(store, "_blocks"):
+        store._blocks = [DeviceBlock(store, i) for i in range(len(store.layouts))]
+    return store._blocks
+
+
+def _draw(block: DeviceBlock, gen):
+    """(zmode, z tensor, seed) for one block; a numpy Generator is advanced
+    by exactly elem_count draws, like zo.py:96/124."""
+    if isinstance(gen, PhiloxKey):
+        return L.ZO_Z_PHILOX, None, gen.seed
+    if isinstance(gen, np.random.Generator):
+        return L.ZO_Z_ORACLE, torch.from_numpy(gen.standard_normal(block.elem_count)).to(block.store.device), 0
+    raise DimensionError(f"unsupported direction source {type(gen).__name__}")
+
+
+def perturb_block(block: DeviceBlock, scale: float, gen) -> None:
+    """zo.py:90-107: the block's forward view becomes base + cumulative_scale * z
+    (computed from the untouched master, so closing the cycle is exact)."""
+    s = block.store
+    zmode, z, seed = _draw(block, gen)
+    new_scale = block.pert_scale + scale
+    scal = _scal_tensor(s.device, seed_cur=seed)
+    t = s.block_tables[block.block_id]
+    fn = L.lib().zo_perturb_update
+    rc = fn(s.theta.data_ptr(), 0, t.segs.data_ptr(), t.prefix.data_ptr(), t.n_segs, t.n_tiles,
+            s.wsh[PLUS].data_ptr(), s.vsh[PLUS].data_ptr(), 0, 0, float(new_scale), 0.0, L.ZO_PU_SHADOW_A,
+            scal.data_ptr(), zmode, 0 if z is None else z.data_ptr(), 0, block.key0, L.stream_ptr())
+    L.check(rc)
+    block.pert_scale = new_scale
+    block._zsrc = (zmode, z if z is not None else seed, block.key0)
+    block._keepalive = scal
+
+
+def _refresh_view(block: DeviceBlock) -> None:
+    s = block.store
+    scal = _scal_tensor(s.device)
+    t = s.block_tables[block.block_id]
+    L.check(L.lib().zo_perturb_update(s.theta.data_ptr(), 0, t.segs.data_ptr(), t.prefix.data_ptr(), t.n_segs,
+                                      t.n_tiles, s.wsh[PLUS].data_ptr(), s.vsh[PLUS].data_ptr(), 0, 0, 0.0, 0.0,
+                                      L.ZO_PU_SHADOW_A, scal.data_ptr(), L.ZO_Z_PHILOX, 0, 0, 0, L.stream_ptr()))
+    block._keepalive = scal
+
+
+def perturb_params(store: DeviceStore, scale: float, gen) -> None:
+    for b in store_blocks(store):
+        perturb_block(b, scale, gen)
+
+
+def update_block(block: DeviceBlock, g: float, lr: float, gen) -> None:
+    """zo.py:116-125: theta <- theta - (lr*g) z, refused mid-perturbation."""
+    if block.pert_scale != 0.0:
+        raise ProtocolError(f"block {block.block_id} updated while a perturbation cycle is open "
+                            f"(cumulative scale {block.pert_scale})")
+    s = block.store
+    zmode, z, seed = _draw(block, gen)
+    scal = _scal_tensor(s.device, seed_prev=seed, lr_g=lr * g, pending=1)
+    t = s.block_tables[block.block_id]
+    rc = L.lib().zo_perturb_update(s.theta.data_ptr(), 0, t.segs.data_ptr(), t.prefix.data_ptr(), t.n_segs,
+                                   t.n_tiles, 0, 0, 0, 0, 0.0, 0.0, L.ZO_PU_UPDATE, scal.data_ptr(), zmode, 0,
+                                   0 if z is None else z.data_ptr(), block.key0, L.stream_ptr())
+    L.check(rc)
+    torch.cuda.current_stream().synchronize()
+
+
+def update_params(store: DeviceStore, g: float, lr: float, gen) -> None:
+    for b in store_blocks(store):
+        update_block(b, g, lr, gen)
+
+
+def forward_block(block: DeviceBlock, x) -> torch.Tensor:
+    """model.py:298-346 on the block's current (possibly perturbed) view.
+    Embedding takes token ids [B, T]; others take fp32 activations [B, T, d]
+    on the device; the head returns fp32 logits [B, T, V]."""
+    s, cfg = block.store, block.store.config
+    if block.kind == EMBEDDING:
+        ids = np.asarray(x.cpu() if torch.is_tensor(x) else x)
+        if ids.ndim != 2 or not np.issubdtype(ids.dtype, np.integer):
+            raise DimensionError("embedding block expects integer token ids of shape (batch, seq)")
+        B, T = ids.shape
+        if T > cfg.seq_len:
+            raise DimensionError(f"sequence length {T} exceeds positions {cfg.seq_len}")
+        ws = s.workspace(PLUS, B, T)
+        s.load_batch(ws, ids, np.zeros_like(ids))
+    else:
+        if not torch.is_tensor(x) or x.dim() != 3 or x.shape[2] != cfg.d_model:
+            raise DimensionError(f"{block.kind} block expects activations of shape (batch, seq, {cfg.d_model})")
+        B, T = x.shape[0], x.shape[1]
+        ws = s.workspace(PLUS, B, T)
+        ws.x[:, :cfg.d_model].copy_(x.reshape(B * T, cfg.d_model))
+    if block.kind != EMBEDDING and block.pert_scale == 0.0:
+        _refresh_view(block)          # unperturbed view = bf16/fp32 copy of the master
+    zmode, zsrc, zkey0 = block._zsrc
+    logits = None
+    if block.kind == HEAD:
+        logits = torch.empty(B * T, cfg.vocab_size, dtype=torch.float32, device=s.device)
+    calls = s.forward_calls(PLUS, ws, 0.0, blocks=[block.block_id], head_mode="logits", logits=logits)
+    if block.kind == EMBEDDING and block.pert_scale != 0.0:
+        fn, args = calls[0]
+        args = list(args)
+        args[9] = float(block.pert_scale)
+        if zmode == L.ZO_Z_PHILOX:
+            scal = _scal_tensor(s.device, seed_cur=zsrc)
+            args[10], args[11] = scal.data_ptr(), L.ZO_Z_PHILOX
+            block._keepalive2 = scal
+        else:
+            args[11], args[12], args[13] = L.ZO_Z_ORACLE, zsrc.data_ptr(), zkey0
+        calls = [(fn, tuple(args))]
+    s.run(calls)
+    if block.kind == HEAD:
+        logits += s.vview(PLUS, block.block_id, "b_out")
+        return logits.view(B, T, cfg.vocab_size)
+    s.check_errors(ws)
+    return ws.x[:, :cfg.d_model].clone().view(B, T, cfg.d_model)
+
+
+def forward(store: DeviceStore, token_ids) -> torch.Tensor:
+    """Full-model logits at the current (unperturbed or perturbed) views."""
+    x = token_ids
+    for b in store_blocks(store):
+        x = forward_block(b, x)
+    return x
+
+
+def loss(logits: torch.Tensor, batch: Batch) -> float:
+    """Mean CE over all positions in f64 (model.py:357-372)."""
+    if logits.dim() != 3:
+        raise DimensionError(f"logits must be (batch, seq, vocab), got shape {tuple(logits.shape)}")
+    tg = torch.as_tensor(np.asarray(batch.targets), device=logits.device).long()
+    if tuple(logits.shape[:2]) != tuple(tg.shape):
+        raise DimensionError("logits shape does not match targets")
+    l64 = logits.double()
+    if not torch.isfinite(l64).all():
+        raise NumericError("non-finite logits")
+    lse = torch.logsumexp(l64, dim=-1)
+    picked = l64.gather(-1, tg[..., None])[..., 0]
+    return float((lse - picked).mean())
+
+
+def dual_forward(block: DeviceBlock, hyper: ZoHyper, seed: int, mgr: RngStateManager, rs, lrs, g_prev: float,
+                 input_pos, input_neg, apply_pending: bool):
+    """Alg. 2 for one block (zo.py:181-224): optional deferred update, then
+    the +eps and -eps forwards and the closing restore."""
+    eps = hyper.epsilon
+    if apply_pending:
+        if lrs is None:
+            raise ProtocolError(f"block {block.block_id}: pending update but no previous-iteration RNG state")
+        mgr.restore(seed, lrs)
+        update_block(block, g_prev, hyper.lr, mgr.generator(seed))
+        lrs = mgr.capture(seed)
+    mgr.restore(seed, rs)
+    perturb_block(block, +eps, mgr.generator(seed))
+    out_pos = forward_block(block, input_pos)
+    mgr.restore(seed, rs)
+    perturb_block(block, -2.0 * eps, mgr.generator(seed))
+    out_neg = forward_block(block, input_neg)
+    mgr.restore(seed, rs)
+    perturb_block(block, +eps, mgr.generator(seed))
+    rs = mgr.capture(seed)
+    return out_pos, out_neg, rs, lrs

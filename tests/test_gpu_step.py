@@ -1,0 +1,283 @@
+"""Step-level parity of the GPU ZO step against the CPU oracle (which is
+itself pinned bit-exact to the reference by tests/test_oracle_golden.py).
+
+Tolerances (stated in DESIGN.md, section "Parity"):
+  perturb / update arithmetic with injected reference z: bit-exact
+  losses (bf16 operands, fp32 accumulate) vs the f32 reference: |dL| <= 2e-3
+  projected gradient: |dg| <= 2e-3 / eps
+  weights after K steps: |dtheta| <= K * lr * max|dg| * max|z| (+1 ulp slack)
+  GPU forward vs a torch fp32 emulation of the same bf16 roundings: 1e-3
+"""
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+from oracle import zo_oracle as O  # noqa: E402
+from paper_2507_03211_b200 import _lib as L  # noqa: E402
+from paper_2507_03211_b200 import zo  # noqa: E402
+from paper_2507_03211_b200.engine import MINUS, PLUS, DeviceStore  # noqa: E402
+from paper_2507_03211_b200.errors import DimensionError, NumericError, ProtocolError  # noqa: E402
+from paper_2507_03211_b200.model import Batch, ModelConfig  # noqa: E402
+from paper_2507_03211_b200.rng import RngStateManager, iteration_seeds  # noqa: E402
+
+EPS, LR = 1e-3, 1e-2
+CASES = {  # name: (vocab, d, heads, n_blocks, seq, batch, steps)
+    "tiny32": (16, 16, 2, 2, 8, 4, 3),
+    "ragged32": (7, 6, 2, 1, 6, 2, 2),
+    "mid32": (64, 32, 4, 2, 16, 2, 3),
+    "wide32": (96, 64, 4, 1, 32, 2, 2),
+    "hd64": (128, 128, 2, 2, 64, 2, 2),
+}
+
+
+def _cfg(name):
+    v, d, h, n, t, b, k = CASES[name]
+    return ModelConfig(v, d, h, n, t, "f32"), b, k
+
+
+def _oracle_model(cfg):
+    return O.Model(cfg.vocab_size, cfg.d_model, cfg.n_heads, cfg.n_blocks, cfg.seq_len, init_seed=7)
+
+
+def _batch(cfg, bsz, seed):
+    ids, tg = O.synthetic_batch(cfg.vocab_size, cfg.seq_len, bsz, seed)
+    return Batch(ids, tg)
+
+
+def _theta_blocks(store):
+    th = store.theta.cpu().numpy()
+    return [th[bl.key0:bl.key0 + bl.elem_count] for bl in store.layouts]
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_init_matches_reference_layout(name):
+    cfg, _, _ = _cfg(name)
+    store = DeviceStore(cfg, init_seed=7)
+    om = _oracle_model(cfg)
+    assert store.total_params == sum(om.sizes) == cfg.param_count()
+    for a, b in zip(_theta_blocks(store), om.blocks):
+        assert np.array_equal(a, b)
+
+
+def _shadow_tensor(store, s, bid, name, cfg):
+    """The perturbed copy of one reference tensor, read back from the shadows."""
+    d = cfg.d_model
+    vw = store.plan.views[bid]
+    if name in ("wq", "wk", "wv"):
+        w, _, _ = store.wview(s, bid, "qkv")
+        j = "qkv".index(name[1])
+        return w[:, j * d:(j + 1) * d].float().cpu().numpy()
+    if name in ("bq", "bk", "bv"):
+        j = "qkv".index(name[1])
+        return store.vview(s, bid, "bqkv")[j * d:(j + 1) * d].cpu().numpy()
+    if name in ("wo", "w1", "w2", "w_out"):
+        w, r, c = store.wview(s, bid, name)
+        return w[:, :c].float().cpu().numpy()
+    assert vw[name][0] == "v"
+    return store.vview(s, bid, name).cpu().numpy()
+
+
+def _bf16(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(torch.bfloat16).float().numpy()
+
+
+@pytest.mark.parametrize("name", ["tiny32", "ragged32", "mid32", "wide32"])
+def test_perturb_and_update_bit_exact_with_reference_z(name):
+    cfg, _, _ = _cfg(name)
+    store = DeviceStore(cfg, init_seed=7)
+    om = _oracle_model(cfg)
+    seed = 1234567
+    zs = O.z_stream(seed, om.sizes)
+    zc = torch.from_numpy(np.concatenate(zs)).cuda()
+    store.set_pending(0.0, 0, False)
+    store.run(store.perturb_call(store.model_table, L.ZO_PU_SHADOW_A | L.ZO_PU_SHADOW_B, +EPS, -EPS,
+                                 zmode=L.ZO_Z_ORACLE, z_cur=zc))
+    torch.cuda.synchronize()
+    for bl, base, z in zip(store.layouts, om.blocks, zs):
+        if bl.kind == "embedding":
+            continue
+        for s, sc in ((PLUS, +EPS), (MINUS, -EPS)):
+            pert = O.views(O.perturbed(base, sc, z), O.tensor_spec(cfg.vocab_size, cfg.d_model, cfg.seq_len,
+                                                                   bl.kind))
+            for tname in bl.names:
+                got = _shadow_tensor(store, s, bl.block_id, tname, cfg).reshape(pert[tname].shape)
+                want = pert[tname]
+                if tname.startswith("w"):
+                    want = _bf16(want)          # GEMM operands are bf16(reference f32 value)
+                assert np.array_equal(got, want), (bl.block_id, tname, s)
+    # update: theta <- f32(theta - (lr g) z), bit-exact
+    g = 0.3712345
+    store.set_pending(LR * g, seed, True)
+    store.run(store.perturb_call(store.model_table, L.ZO_PU_UPDATE, 0.0, 0.0, sa=None, sb=None,
+                                 zmode=L.ZO_Z_ORACLE, z_prev=zc))
+    for a, b, z in zip(_theta_blocks(store), om.blocks, zs):
+        assert np.array_equal(a, O.updated(b, g, LR, z))
+
+
+def _emulated_loss(store, s, ws, cfg, scale, emb_z):
+    """torch fp32 forward over the SAME bf16 shadows, rounding activations to
+    bf16 where the kernels do (LN out, qkv, ctx, gelu out)."""
+    d, H, hd, V = cfg.d_model, cfg.n_heads, cfg.head_dim, cfg.vocab_size
+    B, T = ws.batch, ws.seq
+    ids = ws.ids.long()
+    emb = store.layouts[0]
+    th = store.theta
+    tok = th[emb.key("tok_emb"):emb.key("tok_emb") + V * d].view(V, d)
+    pos = th[emb.key("pos_emb"):emb.key("pos_emb") + cfg.seq_len * d].view(cfg.seq_len, d)
+    zt = emb_z[:V * d].view(V, d)
+    zp = emb_z[V * d:].view(cfg.seq_len, d)
+    x = (tok[ids] + scale * zt[ids]) + (pos + scale * zp)[torch.arange(T, device="cuda").repeat(B)]
+    bf = lambda t: t.to(torch.bfloat16).float()  # noqa: E731
+
+    def ln(x, bid, gname, bname):
+        return bf(torch.nn.functional.layer_norm(x, (d,), store.vview(s, bid, gname), store.vview(s, bid, bname),
+                                                 eps=1e-5))
+
+    for bl in store.layouts[1:-1]:
+        i = bl.block_id
+        wqkv = store.wview(s, i, "qkv")[0][:, :3 * d].float()
+        h = ln(x, i, "ln1_g", "ln1_b")
+        qkv = bf(h @ wqkv + store.vview(s, i, "bqkv"))
+        q, k, v = (qkv[:, j * d:(j + 1) * d].view(B, T, H, hd).transpose(1, 2) for j in range(3))
+        ctx = bf(torch.nn.functional.scaled_dot_product_attention(q, k, v, is_causal=True)
+                 .transpose(1, 2).reshape(B * T, d))
+        x = x + (ctx @ store.wview(s, i, "wo")[0][:, :d].float() + store.vview(s, i, "bo"))
+        h2 = ln(x, i, "ln2_g", "ln2_b")
+        f = bf(torch.nn.functional.gelu(h2 @ store.wview(s, i, "w1")[0][:, :4 * d].float() + store.vview(s, i, "b1"),
+                                        approximate="tanh"))
+        x = x + (f @ store.wview(s, i, "w2")[0][:, :d].float() + store.vview(s, i, "b2"))
+    hb = store.layouts[-1].block_id
+    h = ln(x, hb, "lnf_g", "lnf_b")
+    logits = h @ store.wview(s, hb, "w_out")[0][:, :V].float() + store.vview(s, hb, "b_out")
+    return torch.nn.functional.cross_entropy(logits.double(), ws.tgt.long()).item()
+
+
+@pytest.mark.parametrize("name", ["tiny32", "mid32", "wide32", "hd64"])
+def test_forward_matches_torch_emulation_of_same_roundings(name):
+    cfg, bsz, _ = _cfg(name)
+    store = DeviceStore(cfg, init_seed=7)
+    seed = 99
+    batch = _batch(cfg, bsz, 5)
+    sz = zo.StreamingZo(store, zo.ZoHyper(EPS, LR))
+    rec = sz.step(batch, seed)
+    emb = store.layouts[0]
+    emb_z = torch.empty(emb.elem_count, device="cuda")
+    L.call("zo_philox_normals", seed, emb.key0, emb.elem_count, emb_z.data_ptr(), L.stream_ptr())
+    wsp, wsn = store.workspace(PLUS, bsz, cfg.seq_len), store.workspace(MINUS, bsz, cfg.seq_len)
+    lp = _emulated_loss(store, PLUS, wsp, cfg, +EPS, emb_z)
+    ln = _emulated_loss(store, MINUS, wsn, cfg, -EPS, emb_z)
+    assert abs(rec.loss_pos - lp) < 1e-3 and abs(rec.loss_neg - ln) < 1e-3
+
+
+@pytest.mark.parametrize("name", ["tiny32", "ragged32", "mid32", "wide32"])
+def test_streaming_oracle_mode_matches_reference(name):
+    cfg, bsz, steps = _cfg(name)
+    store = DeviceStore(cfg, init_seed=7)
+    om = _oracle_model(cfg)
+    lz = O.LazyZo(om, EPS, LR)
+    sz = zo.StreamingZo(store, zo.ZoHyper(EPS, LR), mgr=RngStateManager("oracle"))
+    dg = []
+    for j, s in enumerate(iteration_seeds(17, steps), 1):
+        ids, tg = O.synthetic_batch(cfg.vocab_size, cfg.seq_len, bsz, 100 + j)
+        ref = lz.step(ids, tg, s)
+        got = sz.step(Batch(ids, tg), s)
+        assert abs(got.loss_pos - ref[0]) <= 2e-3 and abs(got.loss_neg - ref[1]) <= 2e-3
+        assert abs(got.g - ref[2]) <= 2e-3 / EPS
+        dg.append(abs(got.g - ref[2]))
+    lz.flush()
+    sz.flush()
+    zmax = max(float(np.abs(np.concatenate(O.z_stream(s, om.sizes))).max()) for s in iteration_seeds(17, steps))
+    bound = steps * LR * max(dg) * zmax + 1e-6
+    for a, b in zip(_theta_blocks(store), om.blocks):
+        assert float(np.abs(a.astype(np.float64) - b).max()) <= bound
+
+
+def test_teacher_forced_trajectory_is_bit_exact():
+    """Feed the reference's own g into the GPU update: every step's weights
+    then match the f32 reference bit for bit (the arithmetic is exact; only
+    the bf16 forward differs)."""
+    cfg, bsz, steps = _cfg("mid32")
+    store = DeviceStore(cfg, init_seed=7)
+    om = _oracle_model(cfg)
+    for j, s in enumerate(iteration_seeds(3, 4), 1):
+        ids, tg = O.synthetic_batch(cfg.vocab_size, cfg.seq_len, bsz, 100 + j)
+        _, _, g = O.mezo_step(om, ids, tg, EPS, LR, s)
+        zc = torch.from_numpy(np.concatenate(O.z_stream(s, om.sizes))).cuda()
+        store.set_pending(LR * g, s, True)
+        store.run(store.perturb_call(store.model_table, L.ZO_PU_UPDATE, 0.0, 0.0, sa=None, sb=None,
+                                     zmode=L.ZO_Z_ORACLE, z_prev=zc))
+        for a, b in zip(_theta_blocks(store), om.blocks):
+            assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("name", ["tiny32", "mid32"])
+def test_philox_lazy_equals_eager_bit_exact(name):
+    cfg, bsz, steps = _cfg(name)
+    a, b = DeviceStore(cfg, 7), DeviceStore(cfg, 7)
+    h = zo.ZoHyper(EPS, LR)
+    sz = zo.StreamingZo(b, h)
+    for j, s in enumerate(iteration_seeds(11, 5), 1):
+        batch = _batch(cfg, bsz, 100 + j)
+        ra = zo.mezo_step(a, batch, h, s, iteration=j)
+        rb = sz.step(batch, s)
+        assert (ra.loss_pos, ra.loss_neg, ra.g) == (rb.loss_pos, rb.loss_neg, rb.g)
+    assert not torch.equal(a.theta, b.theta)
+    sz.flush()
+    assert torch.equal(a.theta, b.theta)
+
+
+def test_runs_are_deterministic_and_replicas_identical():
+    cfg, bsz, _ = _cfg("mid32")
+    stores = [DeviceStore(cfg, 7) for _ in range(2)]
+    recs = []
+    for st in stores:
+        sz = zo.StreamingZo(st, zo.ZoHyper(EPS, LR))
+        recs.append([sz.step(_batch(cfg, bsz, 7 + j), s) for j, s in enumerate(iteration_seeds(2, 3))])
+        sz.flush()
+    assert [(r.loss_pos, r.loss_neg, r.g) for r in recs[0]] == [(r.loss_pos, r.loss_neg, r.g) for r in recs[1]]
+    from paper_2507_03211_b200 import ops
+    assert ops.hash_u64(stores[0].theta).item() == ops.hash_u64(stores[1].theta).item()
+
+
+def test_per_block_api_matches_fused_step():
+    """perturb_params / forward / loss (the reference's per-block API) give the
+    same losses as the fused whole-model step, and the cycle restores exactly."""
+    cfg, bsz, _ = _cfg("mid32")
+    store = DeviceStore(cfg, 7)
+    batch = _batch(cfg, bsz, 3)
+    seed = 4242
+    before = store.theta.clone()
+    mgr = RngStateManager()
+    mgr.reset(seed)
+    zo.perturb_params(store, +EPS, mgr.generator(seed))
+    lp = zo.loss(zo.forward(store, batch.token_ids), batch)
+    zo.perturb_params(store, -2 * EPS, mgr.generator(seed))
+    ln = zo.loss(zo.forward(store, batch.token_ids), batch)
+    zo.perturb_params(store, +EPS, mgr.generator(seed))
+    assert torch.equal(store.theta, before)
+    with pytest.raises(ProtocolError):
+        zo.perturb_params(store, +EPS, mgr.generator(seed))
+        zo.update_params(store, 1.0, LR, mgr.generator(seed))
+    zo.perturb_params(store, -EPS, mgr.generator(seed))
+    ref = zo.mezo_step(store, batch, zo.ZoHyper(EPS, LR), seed)
+    assert abs(ref.loss_pos - lp) < 1e-5 and abs(ref.loss_neg - ln) < 1e-5
+
+
+def test_error_behaviour_matches_reference():
+    cfg, bsz, _ = _cfg("tiny32")
+    store = DeviceStore(cfg, 7)
+    h = zo.ZoHyper(EPS, LR)
+    bad = Batch(np.full((bsz, cfg.seq_len), 99), np.zeros((bsz, cfg.seq_len), dtype=np.int64))
+    with pytest.raises(Exception) as ei:
+        zo.mezo_step(store, bad, h, 1)
+    assert isinstance(ei.value, (DimensionError,)) or type(ei.value).__name__ == "ConfigurationError"
+    with pytest.raises(NumericError):
+        zo.mezo_step(store, _batch(cfg, bsz, 1), zo.ZoHyper(0.0, LR), 1)
+    sz = zo.StreamingZo(store, h)
+    sz.step(_batch(cfg, bsz, 1), 3)
+    sz.flush()
+    with pytest.raises(ProtocolError):
+        sz.flush()
