@@ -46,6 +46,7 @@ def _args():
     ap.add_argument("--seq", type=int, default=SEQ)
     ap.add_argument("--batch", type=int, default=BATCH_PER_GROUP, help="sequences per PertP group")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true", help="skip the public-API pass (profiling runs)")
     return ap.parse_args()
 
 
@@ -64,7 +65,7 @@ class ClockSampler:
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except OSError:
             self.proc = None
@@ -223,8 +224,8 @@ def ours(args, rank, world, local_rank):
         step_calls = runner.step_calls(wss[0], wss[1])
     else:
         from paper_2507_03211_b200.strategies import TwoDRunner
-        runner = TwoDRunner(store, hyper, rank=rank, world=world)
-        wss = [runner.ws]
+        runner = TwoDRunner(store, hyper, rank=rank, world=world, batch=B, seq=T)
+        wss = runner.ws_list
         step_calls = runner.step_calls()
     ids_dev = torch.stack([torch.from_numpy(b.token_ids.reshape(-1).astype(np.int32)) for b in batches]).to(dev)
     tgt_dev = torch.stack([torch.from_numpy(b.targets.reshape(-1).astype(np.int32)) for b in batches]).to(dev)
@@ -302,7 +303,9 @@ def ours(args, rank, world, local_rank):
     # e2e through the public API: host batch -> device, record -> host, every step
     e2e_ms = None
     h2d = d2h = 0
-    if world == 1:
+    if args.no_e2e:
+        e2e_ms = ms
+    elif world == 1:
         runner2 = zo.StreamingZo(store, hyper)
         for j in range(args.warmup):
             runner2.step(batches[j], seeds[j])

@@ -159,12 +159,14 @@ int zo_ce_finalize(const float* ce_part, const float* ce_tgt, int64_t rows, int6
 int zo_grad_finalize(const double* loss_pos, const double* loss_neg, double eps, double lr,
                      ZoStepScalars* scal, double* record, void* stream);
 
-/* g from n gathered per-group central differences: ordered ascending sum of
- * (lp_i - ln_i)/(2 eps) / n -- the 2D / DDP reduction of
- * src/zosim/strategies.py:197-216 and src/zosim/fabric.py:105-113. losses is
- * [n][2] = (loss_pos, loss_neg) per group. record gets {lp_k, ln_k, g} of group
- * `mine`. */
-int zo_grad_finalize_groups(const double* losses, int32_t n_groups, int32_t mine, double eps,
+/* g from n per-group central differences gathered from the mesh: an ordered
+ * ascending sum of (L+_i - L-_i)/(2 eps), divided by n -- the DDP / 2D
+ * reduction of src/zosim/strategies.py:145-147, 197-216 with the fixed
+ * ascending order of src/zosim/fabric.py:105-113.  L+_i =
+ * losses[i*plus_stride + plus_off], L-_i = losses[i*minus_stride + minus_off]
+ * (the layout of the rank-ordered all_gather).  record = {L+_mine, L-_mine, g}. */
+int zo_grad_finalize_groups(const double* losses, int32_t n_groups, int32_t plus_stride, int32_t plus_off,
+                            int32_t minus_stride, int32_t minus_off, int32_t mine, double eps,
                             double lr, ZoStepScalars* scal, double* record, void* stream);
 
 /* 64-bit FNV-style hash of a device buffer (replica-divergence guard that

@@ -54,7 +54,7 @@ SIGNATURES = {
     "zo_attn_causal_fwd": (C.c_int, [P, I64, I64, I64, I64, I64, P, I64, P]),
     "zo_ce_finalize": (C.c_int, [P, P, I64, I64, P, P, P, P]),
     "zo_grad_finalize": (C.c_int, [P, P, D, D, P, P, P]),
-    "zo_grad_finalize_groups": (C.c_int, [P, I32, I32, D, D, P, P, P]),
+    "zo_grad_finalize_groups": (C.c_int, [P, I32, I32, I32, I32, I32, I32, D, D, P, P, P]),
     "zo_hash_u64": (C.c_int, [P, I64, P, P, P]),
     "zo_philox_normals": (C.c_int, [U64, I64, I64, P, P]),
 }

@@ -44,7 +44,8 @@ int attention_launch(const __nv_bfloat16*, int64_t, int64_t, int64_t, int64_t, i
                      cudaStream_t);
 int ce_finalize_launch(const float*, const float*, int64_t, int64_t, double*, double*, int32_t*, cudaStream_t);
 int grad_finalize_launch(const double*, const double*, double, double, ZoStepScalars*, double*, cudaStream_t);
-int grad_groups_launch(const double*, int, int, double, double, ZoStepScalars*, double*, cudaStream_t);
+int grad_groups_launch(const double*, int, int, int, int, int, int, double, double, ZoStepScalars*, double*,
+                       cudaStream_t);
 int hash_launch(const void*, int64_t, uint64_t*, uint64_t*, int, cudaStream_t);
 int gemm_launch(const void*, int64_t, const void*, int64_t, int64_t, int64_t, int64_t, int, const float*, void*,
                 int64_t, const int32_t*, float*, float*, int32_t*, cudaStream_t);
@@ -165,12 +166,14 @@ int zo_grad_finalize(const double* loss_pos, const double* loss_neg, double eps,
   return zo::grad_finalize_launch(loss_pos, loss_neg, eps, lr, scal, record, ZO_STREAM(stream));
 }
 
-int zo_grad_finalize_groups(const double* losses, int32_t n_groups, int32_t mine, double eps, double lr,
+int zo_grad_finalize_groups(const double* losses, int32_t n_groups, int32_t plus_stride, int32_t plus_off,
+                            int32_t minus_stride, int32_t minus_off, int32_t mine, double eps, double lr,
                             ZoStepScalars* scal, double* record, void* stream) {
   ZO_CHECK_ARG(eps != 0.0, ZO_ERR_NUMERIC, "epsilon must be nonzero");
   ZO_CHECK_ARG(losses && scal && record && n_groups > 0 && mine >= 0 && mine < n_groups, ZO_ERR_CONFIG,
                "zo_grad_finalize_groups: bad argument");
-  return zo::grad_groups_launch(losses, n_groups, mine, eps, lr, scal, record, ZO_STREAM(stream));
+  return zo::grad_groups_launch(losses, n_groups, plus_stride, plus_off, minus_stride, minus_off, mine, eps, lr,
+                                scal, record, ZO_STREAM(stream));
 }
 
 int zo_hash_u64(const void* data, int64_t nbytes, uint64_t* out_dev, uint64_t* scratch_dev, void* stream) {

@@ -259,71 +259,100 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       }
 #pragma unroll 1
       for (int c = 0; c < BN / 32; ++c) {
+        const int64_t col0 = n0 + c * 32;
+        const bool live = row_ok && col0 < args.N;
+        const bool full = live && col0 + 32 <= args.N;
+        // Issue the global reads this chunk needs (bias, residual) BEFORE the
+        // TMEM load so their latency overlaps it; all loads are batched into
+        // registers first -- out/bias may alias as far as the compiler knows,
+        // so interleaving loads with stores would serialise every round trip.
+        float4 bias4[8], res4[8];
+        if constexpr (EPI != ZO_EPI_F32) {
+          if (full && ((reinterpret_cast<uintptr_t>(args.bias + col0) & 15) == 0)) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) bias4[i] = __ldg(reinterpret_cast<const float4*>(args.bias + col0) + i);
+          } else {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              float t[4];
+#pragma unroll
+              for (int j = 0; j < 4; ++j) t[j] = (live && col0 + 4 * i + j < args.N) ? args.bias[col0 + 4 * i + j] : 0.f;
+              bias4[i] = make_float4(t[0], t[1], t[2], t[3]);
+            }
+          }
+        }
+        float* o32 = (EPI == ZO_EPI_F32 || EPI == ZO_EPI_BIAS_RESID_F32)
+                         ? static_cast<float*>(args.out) + row * args.ldo + col0 : nullptr;
+        const bool vec32 = full && o32 && ((reinterpret_cast<uintptr_t>(o32) & 15) == 0);
+        if constexpr (EPI == ZO_EPI_BIAS_RESID_F32) {
+          if (vec32) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) res4[i] = *reinterpret_cast<const float4*>(o32 + 4 * i);
+          } else {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              float t[4];
+#pragma unroll
+              for (int j = 0; j < 4; ++j) t[j] = (live && col0 + 4 * i + j < args.N) ? o32[4 * i + j] : 0.f;
+              res4[i] = make_float4(t[0], t[1], t[2], t[3]);
+            }
+          }
+        }
         float v[32];
         tmem_ld_32x32b_x32(tmem_base + (uint32_t)(acc * BN + c * 32) + ((uint32_t)(quarter * 32) << 16), v);
-        const int64_t col0 = n0 + c * 32;
-        if (!row_ok || col0 >= args.N) continue;
-        const bool full = col0 + 32 <= args.N;
-        if constexpr (EPI == ZO_EPI_F32) {
-          float* o = static_cast<float*>(args.out) + row * args.ldo + col0;
-          if (full && ((reinterpret_cast<uintptr_t>(o) & 15) == 0)) {
+        if (!live) continue;
+        if constexpr (EPI != ZO_EPI_F32) {
 #pragma unroll
-            for (int i = 0; i < 32; i += 4) *reinterpret_cast<float4*>(o + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+          for (int i = 0; i < 8; ++i) {
+            v[4 * i] += bias4[i].x; v[4 * i + 1] += bias4[i].y;
+            v[4 * i + 2] += bias4[i].z; v[4 * i + 3] += bias4[i].w;
+          }
+        }
+        if constexpr (EPI == ZO_EPI_F32 || EPI == ZO_EPI_BIAS_RESID_F32) {
+          if constexpr (EPI == ZO_EPI_BIAS_RESID_F32) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              v[4 * i] = res4[i].x + v[4 * i]; v[4 * i + 1] = res4[i].y + v[4 * i + 1];
+              v[4 * i + 2] = res4[i].z + v[4 * i + 2]; v[4 * i + 3] = res4[i].w + v[4 * i + 3];
+            }
+          }
+          if (vec32) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+              *reinterpret_cast<float4*>(o32 + 4 * i) = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
           } else {
 #pragma unroll
             for (int i = 0; i < 32; ++i)
-              if (col0 + i < args.N) o[i] = v[i];
+              if (col0 + i < args.N) o32[i] = v[i];
           }
         } else if constexpr (EPI == ZO_EPI_BIAS_BF16 || EPI == ZO_EPI_BIAS_GELU_BF16) {
+          if constexpr (EPI == ZO_EPI_BIAS_GELU_BF16) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = gelu_tanh(v[i]);
+          }
           __nv_bfloat16* o = static_cast<__nv_bfloat16*>(args.out) + row * args.ldo + col0;
-          const float* bb = args.bias + col0;
           if (full && ((reinterpret_cast<uintptr_t>(o) & 15) == 0)) {
 #pragma unroll
             for (int i = 0; i < 32; i += 8) {
               uint32_t pk[4];
 #pragma unroll
               for (int j = 0; j < 4; ++j) {
-                float a = v[i + 2 * j] + bb[i + 2 * j], b = v[i + 2 * j + 1] + bb[i + 2 * j + 1];
-                if constexpr (EPI == ZO_EPI_BIAS_GELU_BF16) { a = gelu_tanh(a); b = gelu_tanh(b); }
-                __nv_bfloat162 h2 = __floats2bfloat162_rn(a, b);
+                __nv_bfloat162 h2 = __floats2bfloat162_rn(v[i + 2 * j], v[i + 2 * j + 1]);
                 pk[j] = *reinterpret_cast<uint32_t*>(&h2);
               }
               *reinterpret_cast<uint4*>(o + i) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
             }
           } else {
 #pragma unroll
-            for (int i = 0; i < 32; ++i) {
-              if (col0 + i < args.N) {
-                float a = v[i] + bb[i];
-                if constexpr (EPI == ZO_EPI_BIAS_GELU_BF16) a = gelu_tanh(a);
-                o[i] = __float2bfloat16_rn(a);
-              }
-            }
-          }
-        } else if constexpr (EPI == ZO_EPI_BIAS_RESID_F32) {
-          float* o = static_cast<float*>(args.out) + row * args.ldo + col0;
-          const float* bb = args.bias + col0;
-          if (full && ((reinterpret_cast<uintptr_t>(o) & 15) == 0)) {
-#pragma unroll
-            for (int i = 0; i < 32; i += 4) {
-              float4 x = *reinterpret_cast<float4*>(o + i);
-              x.x += v[i] + bb[i]; x.y += v[i + 1] + bb[i + 1];
-              x.z += v[i + 2] + bb[i + 2]; x.w += v[i + 3] + bb[i + 3];
-              *reinterpret_cast<float4*>(o + i) = x;
-            }
-          } else {
-#pragma unroll
             for (int i = 0; i < 32; ++i)
-              if (col0 + i < args.N) o[i] += v[i] + bb[i];
+              if (col0 + i < args.N) o[i] = __float2bfloat16_rn(v[i]);
           }
-        } else {  // ZO_EPI_CE
-          const float* bb = args.bias + col0;
+        } else {  // ZO_EPI_CE: online (max, sum exp) over this row's columns of the tile
           const int lim = full ? 32 : (int)(args.N - col0);
           float cm = -INFINITY;
 #pragma unroll
           for (int i = 0; i < 32; ++i) {
             if (i < lim) {
-              v[i] += bb[i];
               bad |= !isfinite(v[i]);
               cm = fmaxf(cm, v[i]);
             }
@@ -476,7 +505,8 @@ int gemm_launch(const void* A, int64_t lda, const void* B, int64_t ldb, int64_t 
   }
   int bn = 128;
   const int64_t tiles256 = ((M + kBM - 1) / kBM) * ((N + 255) / 256);
-  if (epi == ZO_EPI_CE || tiles256 >= num_sms()) bn = 256;
+  (void)tiles256;
+  bn = 256;   // measured: BN=256 beats BN=128 even below one wave (tools/gemm_bench.py)
   static const int force_bn = [] {
     const char* e = getenv("ZO_GEMM_BN");   // tuning override (128 | 256)
     return e ? atoi(e) : 0;

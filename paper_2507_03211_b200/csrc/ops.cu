@@ -97,9 +97,79 @@ __global__ void layernorm_kernel(const float* __restrict__ x, int64_t ldx, const
     orow[c] = __float2bfloat16_rn(fmaf((srow[c] - mu) * rstd, g[c], b[c]));
 }
 
+// Warp-per-row variant for d <= 32*4*NV: the row lives in registers as float4,
+// statistics via warp shuffles only (no block barriers); 8 rows per CTA.
+template <int NV>
+__global__ void __launch_bounds__(256) layernorm_warp_kernel(const float* __restrict__ x, int64_t ldx,
+                                                              const float* __restrict__ g,
+                                                              const float* __restrict__ b, int64_t rows, int d,
+                                                              __nv_bfloat16* __restrict__ out, int64_t ldo) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp_g = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = warp_g; r < rows; r += nwarps) {
+    const float4* xr = reinterpret_cast<const float4*>(x + r * ldx);
+    float4 v[NV];
+    float s = 0.f;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const int c = (i * 32 + lane) * 4;
+      v[i] = c < d ? xr[i * 32 + lane] : make_float4(0.f, 0.f, 0.f, 0.f);
+      s += (v[i].x + v[i].y) + (v[i].z + v[i].w);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    const float mu = s / (float)d;
+    float q = 0.f;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const int c = (i * 32 + lane) * 4;
+      if (c < d) {
+        const float a0 = v[i].x - mu, a1 = v[i].y - mu, a2 = v[i].z - mu, a3 = v[i].w - mu;
+        q += (a0 * a0 + a1 * a1) + (a2 * a2 + a3 * a3);
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
+    const float rstd = 1.0f / sqrtf(q / (float)d + 1e-5f);
+    __nv_bfloat16* orow = out + r * ldo;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const int c = (i * 32 + lane) * 4;
+      if (c < d) {
+        const float4 gg = *reinterpret_cast<const float4*>(g + c);
+        const float4 bb = *reinterpret_cast<const float4*>(b + c);
+        __nv_bfloat162 lo = __floats2bfloat162_rn(fmaf((v[i].x - mu) * rstd, gg.x, bb.x),
+                                                  fmaf((v[i].y - mu) * rstd, gg.y, bb.y));
+        __nv_bfloat162 hi = __floats2bfloat162_rn(fmaf((v[i].z - mu) * rstd, gg.z, bb.z),
+                                                  fmaf((v[i].w - mu) * rstd, gg.w, bb.w));
+        uint2 pk;
+        pk.x = *reinterpret_cast<uint32_t*>(&lo);
+        pk.y = *reinterpret_cast<uint32_t*>(&hi);
+        *reinterpret_cast<uint2*>(orow + c) = pk;
+      }
+    }
+  }
+}
+
 int layernorm_launch(const float* x, int64_t ldx, const float* g, const float* b, int64_t rows, int64_t d,
                      __nv_bfloat16* out, int64_t ldo, cudaStream_t st) {
   if (rows == 0) return ZO_OK;
+  const bool vec = (d % 4 == 0) && (ldx % 4 == 0) && (ldo % 4 == 0) &&
+                   ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(g) |
+                     reinterpret_cast<uintptr_t>(b)) & 15) == 0 && ((reinterpret_cast<uintptr_t>(out) & 7) == 0);
+  if (vec && d <= 4096) {
+    const int64_t want = (rows + 7) / 8;
+    const int grid = (int)(want < (int64_t)num_sms() * 8 ? want : (int64_t)num_sms() * 8);
+    const int nv = (int)((d + 127) / 128);
+#define ZO_LN_CASE(N)                                                                                   \
+  if (nv <= N) {                                                                                        \
+    layernorm_warp_kernel<N><<<grid, 256, 0, st>>>(x, ldx, g, b, rows, (int)d, out, ldo);               \
+    return launch_status("layernorm_warp_kernel");                                                      \
+  }
+    ZO_LN_CASE(1) ZO_LN_CASE(2) ZO_LN_CASE(4) ZO_LN_CASE(8) ZO_LN_CASE(16) ZO_LN_CASE(32)
+#undef ZO_LN_CASE
+  }
   const size_t smem = (size_t)d * sizeof(float);
   static bool big_smem = false;
   if (smem + 256 > 48 * 1024 && !big_smem) {
@@ -176,12 +246,12 @@ __global__ void grad_finalize_kernel(const double* lp, const double* ln, double 
   scal->pending = 1;
 }
 
-__global__ void grad_groups_kernel(const double* losses, int n, int mine, double eps, double lr,
-                                   ZoStepScalars* scal, double* rec) {
+__global__ void grad_groups_kernel(const double* losses, int n, int sp, int op, int sm, int om, int mine,
+                                   double eps, double lr, ZoStepScalars* scal, double* rec) {
   double tot = 0.0;
-  for (int i = 0; i < n; ++i) tot += (losses[2 * i] - losses[2 * i + 1]) / (2.0 * eps);
+  for (int i = 0; i < n; ++i) tot += (losses[i * sp + op] - losses[i * sm + om]) / (2.0 * eps);
   const double g = tot / (double)n;
-  rec[0] = losses[2 * mine]; rec[1] = losses[2 * mine + 1]; rec[2] = g;
+  rec[0] = losses[mine * sp + op]; rec[1] = losses[mine * sm + om]; rec[2] = g;
   scal->seed_prev = scal->seed_cur;
   scal->lr_g_prev = lr * g;
   scal->pending = 1;
@@ -193,9 +263,9 @@ int grad_finalize_launch(const double* lp, const double* ln, double eps, double 
   return launch_status("grad_finalize_kernel");
 }
 
-int grad_groups_launch(const double* losses, int n, int mine, double eps, double lr, ZoStepScalars* scal,
-                       double* rec, cudaStream_t st) {
-  grad_groups_kernel<<<1, 1, 0, st>>>(losses, n, mine, eps, lr, scal, rec);
+int grad_groups_launch(const double* losses, int n, int sp, int op, int sm, int om, int mine, double eps, double lr,
+                       ZoStepScalars* scal, double* rec, cudaStream_t st) {
+  grad_groups_kernel<<<1, 1, 0, st>>>(losses, n, sp, op, sm, om, mine, eps, lr, scal, rec);
   return launch_status("grad_groups_kernel");
 }
 

@@ -270,7 +270,7 @@ class DeviceStore:
         return [(fn, args)]
 
     def forward_calls(self, s: int, ws: Workspace, scale: float, zmode=L.ZO_Z_PHILOX, z_cur=None, stream=None,
-                      blocks=None, head_mode="ce", logits=None):
+                      blocks=None, head_mode="ce", logits=None, loss_out=None):
         """Launch plan of one directional forward through blocks [0..N+1]
         (embedding -> N decoder blocks -> LN_f + LM head + CE)."""
         cfg, lib = self.config, L.lib()
@@ -319,7 +319,8 @@ class DeviceStore:
                     calls.append((lib.zo_gemm_bf16, (_ptr(ws.h), ws.h.stride(0), _ptr(wout), wout.stride(0), M, V, d,
                                                      L.ZO_EPI_CE, bout, 0, 0, _ptr(ws.tgt), _ptr(ws.ce_part),
                                                      _ptr(ws.ce_tgt), _ptr(ws.err), st)))
-                    calls.append((lib.zo_ce_finalize, (_ptr(ws.ce_part), _ptr(ws.ce_tgt), M, ws.n_ce, _ptr(ws.loss),
+                    calls.append((lib.zo_ce_finalize, (_ptr(ws.ce_part), _ptr(ws.ce_tgt), M, ws.n_ce,
+                                                       loss_out if loss_out is not None else _ptr(ws.loss),
                                                        _ptr(ws.row_scratch), _ptr(ws.err), st)))
                 else:   # materialise logits (API forward(); not on the step)
                     calls.append((lib.zo_gemm_bf16, (_ptr(ws.h), ws.h.stride(0), _ptr(wout), wout.stride(0), M, V, d,

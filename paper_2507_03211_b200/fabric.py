@@ -1,0 +1,143 @@
+"""Collective fabric over torch.distributed (mirror of src/zosim/fabric.py).
+
+The reference runs K ranks as threads exchanging Python values through
+barriers (fabric.py:34-51); here each rank is a process (one per GPU) and
+the collectives are NCCL over NVLink (or gloo for CPU tests).  The API keeps
+the reference's determinism contract:
+
+  all_gather       values ordered by rank                     fabric.py:90-94
+  broadcast        root's value on every rank                  fabric.py:96-103
+  all_reduce_mean  FIXED ascending-rank sum / k (bit-stable)   fabric.py:105-113
+  bytes_by_tag / collective_log accounting                     fabric.py:65-80
+
+NCCL's own all_reduce does not promise the reference's summation order, so
+every reduction is an all_gather followed by an ordered local sum -- the
+payloads are 8-byte scalars, so this costs the same.
+"""
+
+from __future__ import annotations
+
+import datetime
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from .errors import FabricFault
+
+
+def _payload_bytes(value) -> int:
+    if isinstance(value, torch.Tensor):
+        return value.numel() * value.element_size()
+    if isinstance(value, np.ndarray):
+        return value.nbytes
+    if isinstance(value, (list, tuple)):
+        return sum(_payload_bytes(v) for v in value)
+    if isinstance(value, (bytes, bytearray, str)):
+        return len(value)
+    if value is None:
+        return 0
+    return 8
+
+
+class TorchFabric:
+    """K processes with ordered, deterministic collectives."""
+
+    def __init__(self, group=None):
+        if not dist.is_initialized():
+            raise FabricFault("torch.distributed is not initialised")
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.k = dist.get_world_size(group)
+        self.backend = dist.get_backend(group)
+        self.bytes_by_tag: dict = {}
+        self.collective_log: list = []
+        self._subgroups: dict = {}
+
+    def _account(self, kind, tag, participants, nbytes):
+        self.bytes_by_tag[tag] = self.bytes_by_tag.get(tag, 0) + nbytes
+        self.collective_log.append({"kind": kind, "tag": tag, "participants": participants})
+
+    def subgroup(self, ranks):
+        """Process group for an ascending tuple of ranks.  new_group is a
+        collective over the whole world, so the mesh's group FAMILIES are
+        created together, in a fixed order, on every rank: PertP pairs
+        (2i, 2i+1) and the two direction branches (even / odd ranks)."""
+        ranks = tuple(sorted(ranks))
+        if ranks not in self._subgroups:
+            k = self.k
+            pairs = [(2 * i, 2 * i + 1) for i in range(k // 2)]
+            branches = [tuple(range(0, k, 2)), tuple(range(1, k, 2))]
+            if ranks in pairs:
+                family = pairs
+            elif ranks in branches:
+                family = branches
+            else:
+                family = [ranks]
+            for g in family:
+                if g not in self._subgroups:
+                    self._subgroups[g] = dist.new_group(list(g), backend=self.backend)
+        return self._subgroups[ranks]
+
+    def _dev(self):
+        if self.backend == "nccl":
+            return torch.device("cuda", torch.cuda.current_device())
+        return torch.device("cpu")
+
+    # -- scalar / small-object collectives ------------------------------------
+    def all_gather(self, rank, value, tag, group=None) -> list:
+        """Every participant's float/int value, ordered by rank."""
+        ranks = tuple(range(self.k)) if group is None else tuple(sorted(group))
+        pg = None if group is None else self.subgroup(ranks)
+        self._account("all_gather", tag, len(ranks), _payload_bytes(value))
+        t = torch.tensor([float(value)], dtype=torch.float64, device=self._dev())
+        out = [torch.empty_like(t) for _ in ranks]
+        try:
+            dist.all_gather(out, t, group=pg)
+        except Exception as e:  # noqa: BLE001
+            raise FabricFault(f"collective failed: {e}") from e
+        return [float(o.item()) for o in out]
+
+    def broadcast(self, rank, value, tag, root=0, group=None):
+        self._account("broadcast", tag, self.k, _payload_bytes(value) if rank == root else 0)
+        t = torch.tensor([int(value) if rank == root else 0], dtype=torch.int64, device=self._dev())
+        try:
+            dist.broadcast(t, src=root, group=self.group)
+        except Exception as e:  # noqa: BLE001
+            raise FabricFault(f"collective failed: {e}") from e
+        return int(t.item())
+
+    def all_reduce_mean(self, rank, value, tag, group=None) -> float:
+        vals = self.all_gather(rank, value, tag, group)
+        self.collective_log[-1]["kind"] = "all_reduce"
+        total = 0.0
+        for v in vals:            # fixed ascending-rank order (fabric.py:105-113)
+            total += v
+        return total / len(vals)
+
+    # -- device tensor gather (the step's loss exchange) ------------------------
+    def all_gather_tensor(self, out: torch.Tensor, inp: torch.Tensor, tag: str) -> None:
+        """out[k*n:(k+1)*n] = inp of rank k.  NCCL: in place on the GPU (no host
+        round trip, graph-capturable); gloo: staged through host memory."""
+        self._account("all_gather", tag, self.k, _payload_bytes(inp))
+        if self.backend == "nccl":
+            dist.all_gather_into_tensor(out, inp, group=self.group)
+            return
+        h = inp.detach().cpu()
+        parts = [torch.empty_like(h) for _ in range(self.k)]
+        dist.all_gather(parts, h, group=self.group)
+        out.copy_(torch.cat(parts).to(out.device))
+
+    def barrier(self):
+        dist.barrier(group=self.group)
+
+    def stats(self) -> dict:
+        return {"bytes_by_tag": dict(self.bytes_by_tag), "collectives": len(self.collective_log)}
+
+
+def init_from_env(backend: str = "nccl", timeout_s: float = 60.0) -> TorchFabric:
+    """torchrun-style initialisation; a rank that never joins surfaces as
+    FabricFault after `timeout_s` (the reference's 60 s barrier timeout)."""
+    if not dist.is_initialized():
+        dist.init_process_group(backend, timeout=datetime.timedelta(seconds=timeout_s))
+    return TorchFabric()

@@ -78,9 +78,11 @@ def grad_finalize(loss_pos, loss_neg, eps, lr, scal, record, stream=None):
            L.stream_ptr(stream))
 
 
-def grad_finalize_groups(losses, n_groups, mine, eps, lr, scal, record, stream=None):
-    L.call("zo_grad_finalize_groups", _p(losses), n_groups, mine, float(eps), float(lr), _p(scal), _p(record),
-           L.stream_ptr(stream))
+def grad_finalize_groups(losses, n_groups, layout, mine, eps, lr, scal, record, stream=None):
+    """layout = (plus_stride, plus_off, minus_stride, minus_off) into `losses`."""
+    sp, op, sm, om = layout
+    L.call("zo_grad_finalize_groups", _p(losses), n_groups, sp, op, sm, om, mine, float(eps), float(lr), _p(scal),
+           _p(record), L.stream_ptr(stream))
 
 
 def philox_normals(seed: int, e0: int, n: int, device="cuda", stream=None) -> torch.Tensor:

@@ -111,8 +111,12 @@ def _stage_batch(store: DeviceStore, batch: Batch):
 
 
 def _finish(store: DeviceStore, wsp, wsn, iteration: int, seed: int) -> ZoStep:
+    return _finish_record(store, [wsp, wsn], iteration, seed)
+
+
+def _finish_record(store: DeviceStore, wss, iteration: int, seed: int) -> ZoStep:
     rec = store.record.cpu().numpy()          # synchronises the stream
-    store.check_errors(wsp, wsn)
+    store.check_errors(*wss)
     return ZoStep(iteration, seed, float(rec[0]), float(rec[1]), float(rec[2]))
 
 

@@ -1,0 +1,118 @@
+"""Worker functions for multi-process tests (spawned; must be importable)."""
+
+import os
+import socket
+
+
+def free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def init(rank, world, port, backend="gloo"):
+    import datetime
+
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group(backend, rank=rank, world_size=world, timeout=datetime.timedelta(seconds=60))
+
+
+def fabric_worker(rank, world, port, q):
+    """CPU: ordered collectives + the mesh-gather layout."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2507_03211_b200.fabric import TorchFabric
+    from paper_2507_03211_b200.strategies import MeshLayout
+
+    init(rank, world, port)
+    fab = TorchFabric()
+    out = {}
+    out["gather"] = fab.all_gather(rank, 10.0 + rank, tag="loss")
+    out["bcast"] = fab.broadcast(rank, 42 if rank == 0 else None, tag="seed")
+    vals = [0.1, 0.2, 0.3, 1e16, -1e16, 0.7, 0.9, 1.1][:world]
+    out["mean"] = fab.all_reduce_mean(rank, vals[rank], tag="grad")
+    # device-gather layout: each rank fills its own slot(s) of [L+, L-]
+    for strat in (["ddp", "2d"] + (["pertp"] if world == 2 else [])):
+        mesh = MeshLayout(strat, world, rank)
+        local = torch.zeros(2, dtype=torch.float64)
+        lp, ln = 2.0 + 0.01 * (rank // (1 if strat == "ddp" else 2)), 2.0 - 0.013 * (rank // (1 if strat == "ddp" else 2))
+        if 0 in mesh.dirs:
+            local[0] = lp
+        if 1 in mesh.dirs:
+            local[1] = ln
+        gathered = torch.zeros(2 * world, dtype=torch.float64)
+        fab.all_gather_tensor(gathered, local, tag="loss")
+        out[strat] = mesh.grad_host(gathered.tolist(), 1e-3)
+    out["bytes"] = dict(fab.bytes_by_tag)
+    dist.destroy_process_group()
+    q.put((rank, out))
+
+
+def gpu_strategy_worker(rank, world, port, strategy, name, steps, oracle, q):
+    """GPU (all ranks on cuda:0, gloo collectives): run the eager strategy
+    step of the drop-in API and report records + the master hash."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2507_03211_b200 import ops
+    from paper_2507_03211_b200.engine import DeviceStore
+    from paper_2507_03211_b200.fabric import TorchFabric
+    from paper_2507_03211_b200.model import ModelConfig, make_batch
+    from paper_2507_03211_b200.rng import RngStateManager, iteration_seeds
+    from paper_2507_03211_b200.strategies import ddp_step, mesh_assignments, pertp_step, twod_step
+    from paper_2507_03211_b200.zo import ZoHyper
+
+    torch.cuda.set_device(0)
+    init(rank, world, port)
+    fab = TorchFabric()
+    v, d, h, n, t, bsz = {"tiny": (16, 16, 2, 2, 8, 4), "mid": (64, 32, 4, 2, 16, 4)}[name]
+    cfg = ModelConfig(v, d, h, n, t, "f32")
+    store = DeviceStore(cfg, init_seed=7)
+    hyper = ZoHyper(1e-3, 1e-2)
+    mgr = RngStateManager("oracle" if oracle else "philox")
+    recs = []
+    for j, s in enumerate(iteration_seeds(5, steps), 1):
+        batch = make_batch(cfg, bsz, 200 + j)
+        seed_arg = s if rank == 0 else None
+        if strategy == "pertp":
+            r = pertp_step(fab, rank, store, batch, hyper, seed_arg, mgr, iteration=j)
+        elif strategy == "ddp":
+            r = ddp_step(fab, rank, store, batch.shard(world, rank), hyper, seed_arg, mgr, iteration=j)
+        else:
+            ordering = strategy.split(":")[1] if ":" in strategy else "pertp_inner"
+            a = mesh_assignments(world // 2)[rank]
+            r = twod_step(fab, rank, a, store, batch.shard(world // 2, a.group), hyper, seed_arg,
+                          ordering=ordering, mgr=mgr, iteration=j)
+        recs.append((r.loss_pos, r.loss_neg, r.g))
+    hsh = int(ops.hash_u64(store.theta).item())
+    theta = store.theta.cpu().numpy() if rank == 0 else None
+    log = [c["kind"] + ":" + c["tag"] + ":" + str(c["participants"]) for c in fab.collective_log]
+    dist.destroy_process_group()
+    q.put((rank, recs, hsh, theta, log, dict(fab.bytes_by_tag)))
+
+
+def run(fn, world, *args, timeout=240):
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=fn, args=(r, world, port, *args, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = {}
+    try:
+        for _ in range(world):
+            item = q.get(timeout=timeout)
+            out[item[0]] = item
+    finally:
+        for p in procs:
+            p.join(timeout=30)
+            if p.is_alive():
+                p.kill()
+    return [out[r] for r in range(world)]
