@@ -75,7 +75,7 @@ int zo_device_check(int dev) {
   return ZO_OK;
 }
 
-int64_t zo_perturb_tile_elems(void) { return 4096; }
+int64_t zo_perturb_tile_elems(void) { return 512; }
 
 int zo_perturb_update(float* theta, int64_t theta_key0, const ZoSegment* segs, const int64_t* tile_prefix,
                       int32_t n_segs, int64_t n_tiles, void* wsh_a, float* vsh_a, void* wsh_b, float* vsh_b,

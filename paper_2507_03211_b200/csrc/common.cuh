@@ -64,10 +64,10 @@ __host__ __device__ __forceinline__ u32x4 philox4x32_10(uint64_t ctr, uint64_t s
   uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
 #pragma unroll
   for (int r = 0; r < 10; ++r) {
-    const uint32_t hi0 = mulhi32(0xD2511F53u, c0), lo0 = 0xD2511F53u * c0;
-    const uint32_t hi1 = mulhi32(0xCD9E8D57u, c2), lo1 = 0xCD9E8D57u * c2;
-    const uint32_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
-    c0 = n0; c1 = lo1; c2 = n2; c3 = lo0;
+    const uint64_t p0 = (uint64_t)0xD2511F53u * c0;   // one IMAD.WIDE.U32: hi and lo
+    const uint64_t p1 = (uint64_t)0xCD9E8D57u * c2;
+    const uint32_t n0 = (uint32_t)(p1 >> 32) ^ c1 ^ k0, n2 = (uint32_t)(p0 >> 32) ^ c3 ^ k1;
+    c0 = n0; c1 = (uint32_t)p1; c2 = n2; c3 = (uint32_t)p0;
     k0 += 0x9E3779B9u; k1 += 0xBB67AE85u;
   }
   return {c0, c1, c2, c3};
@@ -76,13 +76,45 @@ __host__ __device__ __forceinline__ u32x4 philox4x32_10(uint64_t ctr, uint64_t s
 // Box-Muller on 24-bit uniforms: u1 in (0,1) (never 0), angle in [-pi, pi).
 // Fast MUFU intrinsics; outputs are a deterministic function of the bits.
 __device__ __forceinline__ void box_muller(uint32_t a, uint32_t b, float& z0, float& z1) {
-  const float u1 = (float)(a >> 8) * 5.9604644775390625e-08f + 2.98023223876953125e-08f;
-  const float ang = (float)(b >> 8) * 3.7450702706353989e-07f - 3.14159265358979f;  // 2pi/2^24
-  const float r = sqrtf(-1.3862943611198906f * __log2f(u1));                      // -2 ln2 log2(u)
+  // uniforms from the mantissa bits (no int->float conversion):
+  //   u1 = 2 - [1,2)  in (0, 1];   ang = pi * [2,4) - 3 pi  in [-pi, pi)
+  const float u1 = 2.0f - __uint_as_float(0x3F800000u | (a >> 9));
+  const float ang = fmaf(__uint_as_float(0x40000000u | (b >> 9)), 3.14159265358979f, -9.42477796076938f);
+  const float t = -1.3862943611198906f * __log2f(u1);                             // -2 ln u > 0
+  const float r = t > 0.f ? t * rsqrtf(t) : 0.f;   // sqrt via MUFU.RSQ; u1 can round to 1.0 (t = 0)
   float s, c;
   __sincosf(ang, &s, &c);
   z0 = r * c;
   z1 = r * s;
+}
+
+
+// ---------------------------------------------------------------------------
+// Keyed Philox for the streaming kernels: the 10 round keys of a seed are
+// computed once per thread (PhiloxKeys) and each round is 2 IMAD.WIDE.U32 +
+// 2 LOP3.  Produces exactly the words of philox4x32_10 (same z everywhere).
+// ---------------------------------------------------------------------------
+struct PhiloxKeys { uint32_t k0[10], k1[10]; };
+
+__host__ __device__ __forceinline__ PhiloxKeys philox_keys(uint64_t seed) {
+  PhiloxKeys k;
+  uint32_t a = (uint32_t)seed, b = (uint32_t)(seed >> 32);
+#pragma unroll
+  for (int r = 0; r < 10; ++r) { k.k0[r] = a; k.k1[r] = b; a += 0x9E3779B9u; b += 0xBB67AE85u; }
+  return k;
+}
+
+__device__ __forceinline__ u32x4 philox4x32_10_k(uint64_t ctr, const PhiloxKeys& k) {
+  uint32_t c0 = (uint32_t)ctr, c1 = (uint32_t)(ctr >> 32), c2 = 0u, c3 = 0u;
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint64_t p0 = (uint64_t)0xD2511F53u * c0;
+    const uint64_t p1 = (uint64_t)0xCD9E8D57u * c2;
+    const uint32_t n0 = (uint32_t)(p1 >> 32) ^ c1 ^ k.k0[r];
+    const uint32_t n2 = (uint32_t)(p0 >> 32) ^ c3 ^ k.k1[r];
+    c1 = (uint32_t)p1; c3 = (uint32_t)p0; c0 = n0; c2 = n2;
+  }
+  return {c0, c1, c2, c3};
 }
 
 struct f32x4 { float x, y, z, w; };
@@ -98,6 +130,14 @@ __device__ __forceinline__ f32x4 philox_normal4(uint64_t seed, uint64_t q) {
 __device__ __forceinline__ float philox_normal1(uint64_t seed, uint64_t e) {
   const f32x4 v = philox_normal4(seed, e >> 2);
   switch (e & 3) { case 0: return v.x; case 1: return v.y; case 2: return v.z; default: return v.w; }
+}
+
+__device__ __forceinline__ f32x4 philox_normal4_k(const PhiloxKeys& k, uint64_t q) {
+  const u32x4 r = philox4x32_10_k(q, k);
+  f32x4 o;
+  box_muller(r.x, r.y, o.x, o.y);
+  box_muller(r.z, r.w, o.z, o.w);
+  return o;
 }
 
 __device__ __forceinline__ float f4get(const f32x4& v, int i) {

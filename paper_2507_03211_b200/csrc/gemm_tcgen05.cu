@@ -33,7 +33,8 @@ namespace zo {
 
 constexpr int kBM = 128;
 constexpr int kBK = 64;
-constexpr int kGemmThreads = 192;
+constexpr int kGemmThreads = 320;   // warp 0 TMA, warp 1 MMA/TMEM, warps 2..9 epilogue
+constexpr int kEpiWarps = 8;
 
 template <int BN>
 struct GemmCfg {
@@ -42,7 +43,7 @@ struct GemmCfg {
   static constexpr int kBBytes = kBK * BN * 2;    // 32 KB / 16 KB
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kTmemCols = 2 * BN;        // double-buffered accumulator
-  static constexpr int kSmem = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int kSmem = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/ + kEpiWarps * 32 * 33 * 4;
 };
 
 struct GemmArgs {
@@ -144,6 +145,146 @@ __device__ __forceinline__ float gelu_tanh(float x) {
   return 0.5f * x * (1.0f + tanhf(c * (x + 0.044715f * x * x * x)));
 }
 
+// One 128 x BN accumulator tile from TMEM -> fused epilogue -> global.
+// Thread (quarter, lane) owns output row m0 + 32*quarter + lane.
+// Epilogue warp e (0..7) owns TMEM lane quarter (warp % 4) and column half
+// e / 4, so two warps share each quarter and each thread stores half a row.
+template <int BN, int EPI>
+__device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t tmem_base, int acc, int quarter,
+                                              int half, int lane, int64_t m0, int64_t n0, int64_t tn,
+                                              float* __restrict__ stg) {
+  // stg: this warp's 32 x 33 fp32 staging tile (row-padded: conflict-free both ways)
+  const int64_t row_base = m0 + quarter * 32;
+  const int64_t row = row_base + lane;
+  const bool row_ok = row < args.M;
+  float ce_m = -INFINITY, ce_s = 0.f;
+  int32_t tgt = -1;
+  bool bad = false;
+  if constexpr (EPI == ZO_EPI_CE) {
+    if (row_ok) tgt = args.targets[row];
+  }
+  constexpr int CH = BN / 64;   // 32-column chunks per half
+#pragma unroll 1
+  for (int c = half * CH; c < (half + 1) * CH; ++c) {
+    const int64_t col0 = n0 + c * 32;
+    const uint32_t taddr = tmem_base + (uint32_t)(acc * BN + c * 32) + ((uint32_t)(quarter * 32) << 16);
+    if constexpr (EPI == ZO_EPI_CE) {
+      // thread-per-row: online (max, sum exp) over this row's columns, target logit
+      float v[32];
+      tmem_ld_32x32b_x32(taddr, v);
+      if (!row_ok || col0 >= args.N) continue;
+      const int lim = col0 + 32 <= args.N ? 32 : (int)(args.N - col0);
+      float cm = -INFINITY;
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        if (i < lim) {
+          v[i] += __ldg(args.bias + col0 + i);
+          bad |= !isfinite(v[i]);
+          cm = fmaxf(cm, v[i]);
+        }
+      }
+      const float nm = fmaxf(ce_m, cm);
+      float s = ce_s * __expf(ce_m - nm);
+      if (ce_m == -INFINITY) s = 0.f;
+#pragma unroll
+      for (int i = 0; i < 32; ++i)
+        if (i < lim) s += __expf(v[i] - nm);
+      ce_m = nm;
+      ce_s = s;
+      if (tgt >= col0 && tgt < col0 + lim) {
+        const int ti = (int)(tgt - col0);
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          if (i == ti) args.ce_tgt[row] = v[i];
+      }
+    } else if constexpr (EPI == ZO_EPI_BIAS_BF16 || EPI == ZO_EPI_BIAS_GELU_BF16) {
+      // bf16 out: each thread writes 64 contiguous bytes of its row (4 x 16 B)
+      float4 bias4[8];
+      const bool full = row_ok && col0 + 32 <= args.N;
+      if (full && ((reinterpret_cast<uintptr_t>(args.bias + col0) & 15) == 0)) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) bias4[i] = __ldg(reinterpret_cast<const float4*>(args.bias + col0) + i);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          float t[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) t[j] = (col0 + 4 * i + j < args.N) ? args.bias[col0 + 4 * i + j] : 0.f;
+          bias4[i] = make_float4(t[0], t[1], t[2], t[3]);
+        }
+      }
+      float v[32];
+      tmem_ld_32x32b_x32(taddr, v);
+      if (!row_ok || col0 >= args.N) continue;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        v[4 * i] += bias4[i].x; v[4 * i + 1] += bias4[i].y;
+        v[4 * i + 2] += bias4[i].z; v[4 * i + 3] += bias4[i].w;
+      }
+      if constexpr (EPI == ZO_EPI_BIAS_GELU_BF16) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = gelu_tanh(v[i]);
+      }
+      __nv_bfloat16* o = static_cast<__nv_bfloat16*>(args.out) + row * args.ldo + col0;
+      if (full && ((reinterpret_cast<uintptr_t>(o) & 15) == 0)) {
+#pragma unroll
+        for (int i = 0; i < 32; i += 8) {
+          uint32_t pk[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            __nv_bfloat162 h2 = __floats2bfloat162_rn(v[i + 2 * j], v[i + 2 * j + 1]);
+            pk[j] = *reinterpret_cast<uint32_t*>(&h2);
+          }
+          *reinterpret_cast<uint4*>(o + i) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          if (col0 + i < args.N) o[i] = __float2bfloat16_rn(v[i]);
+      }
+    } else {
+      // column-per-lane after an smem transpose: every global access is one
+      // contiguous 128 B (fp32) / 64 B (bf16) run per warp instruction
+      const int64_t col = col0 + lane;
+      const bool col_ok = col < args.N;
+      float bias_c = 0.f;
+      if constexpr (EPI != ZO_EPI_F32) bias_c = col_ok ? __ldg(args.bias + col) : 0.f;
+      float res[32];
+      if constexpr (EPI == ZO_EPI_BIAS_RESID_F32) {
+        // residual reads issued before the TMEM load so their latency overlaps it
+        const float* xr = static_cast<const float*>(args.out) + row_base * args.ldo + col;
+#pragma unroll
+        for (int r = 0; r < 32; ++r) res[r] = (col_ok && row_base + r < args.M) ? xr[(int64_t)r * args.ldo] : 0.f;
+      }
+      float v[32];
+      tmem_ld_32x32b_x32(taddr, v);
+#pragma unroll
+      for (int i = 0; i < 32; ++i) stg[lane * 33 + i] = v[i];
+      __syncwarp();
+      if constexpr (EPI == ZO_EPI_F32 || EPI == ZO_EPI_BIAS_RESID_F32) {
+        float* o = static_cast<float*>(args.out) + row_base * args.ldo + col;
+#pragma unroll
+        for (int r = 0; r < 32; ++r) {
+          if (col_ok && row_base + r < args.M) {
+            float val = stg[r * 33 + lane];
+            if constexpr (EPI == ZO_EPI_BIAS_RESID_F32) val = res[r] + (val + bias_c);
+            o[(int64_t)r * args.ldo] = val;
+          }
+        }
+      }
+      __syncwarp();
+    }
+  }
+  if constexpr (EPI == ZO_EPI_CE) {
+    if (row_ok) {
+      const int64_t slot = tn * 2 + half;
+      args.ce_part[(row * args.ce_tiles + slot) * 2] = ce_m;
+      args.ce_part[(row * args.ce_tiles + slot) * 2 + 1] = ce_s;
+      if (bad) atomicOr(args.err, 2);
+    }
+  }
+}
+
 template <int BN, int EPI>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -162,6 +303,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   auto tfull_bar = [&](int a) { return bars + 8u * (2 * C::kStages + a); };
   auto tempty_bar = [&](int a) { return bars + 8u * (2 * C::kStages + 2 + a); };
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + C::kStages * C::kStageBytes + 8 * (2 * C::kStages + 4));
+  float* stg_all = reinterpret_cast<float*>(gbase + C::kStages * C::kStageBytes + 256);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t num_m = (args.M + kBM - 1) / kBM;
@@ -173,7 +315,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     prefetch_tmap(&tmA);
     prefetch_tmap(&tmB);
     for (int s = 0; s < C::kStages; ++s) { mbar_init(full_bar(s), 1); mbar_init(empty_bar(s), 1); }
-    for (int a = 0; a < 2; ++a) { mbar_init(tfull_bar(a), 1); mbar_init(tempty_bar(a), 128); }
+    for (int a = 0; a < 2; ++a) { mbar_init(tfull_bar(a), 1); mbar_init(tempty_bar(a), kEpiWarps); }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   if (warp == 1) {
@@ -240,148 +382,20 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   } else {
     // ============================ epilogue ================================
     const int quarter = warp & 3;   // TMEM lanes 32*quarter .. +31
+    const int half = (warp - 2) >> 2;
     int64_t local = 0;
     for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++local) {
       const int acc = (int)(local & 1);
       const uint32_t acc_phase = (uint32_t)((local >> 1) & 1);
       const int64_t m0 = (tile % num_m) * kBM;
       const int64_t tn = tile / num_m;
-      const int64_t n0 = tn * BN;
       mbar_wait(tfull_bar(acc), acc_phase);
       tc_fence_after();
-      const int64_t row = m0 + quarter * 32 + lane;
-      const bool row_ok = row < args.M;
-      float ce_m = -INFINITY, ce_s = 0.f;
-      int32_t tgt = -1;
-      bool bad = false;
-      if constexpr (EPI == ZO_EPI_CE) {
-        if (row_ok) tgt = args.targets[row];
-      }
-#pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
-        const int64_t col0 = n0 + c * 32;
-        const bool live = row_ok && col0 < args.N;
-        const bool full = live && col0 + 32 <= args.N;
-        // Issue the global reads this chunk needs (bias, residual) BEFORE the
-        // TMEM load so their latency overlaps it; all loads are batched into
-        // registers first -- out/bias may alias as far as the compiler knows,
-        // so interleaving loads with stores would serialise every round trip.
-        float4 bias4[8], res4[8];
-        if constexpr (EPI != ZO_EPI_F32) {
-          if (full && ((reinterpret_cast<uintptr_t>(args.bias + col0) & 15) == 0)) {
-#pragma unroll
-            for (int i = 0; i < 8; ++i) bias4[i] = __ldg(reinterpret_cast<const float4*>(args.bias + col0) + i);
-          } else {
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              float t[4];
-#pragma unroll
-              for (int j = 0; j < 4; ++j) t[j] = (live && col0 + 4 * i + j < args.N) ? args.bias[col0 + 4 * i + j] : 0.f;
-              bias4[i] = make_float4(t[0], t[1], t[2], t[3]);
-            }
-          }
-        }
-        float* o32 = (EPI == ZO_EPI_F32 || EPI == ZO_EPI_BIAS_RESID_F32)
-                         ? static_cast<float*>(args.out) + row * args.ldo + col0 : nullptr;
-        const bool vec32 = full && o32 && ((reinterpret_cast<uintptr_t>(o32) & 15) == 0);
-        if constexpr (EPI == ZO_EPI_BIAS_RESID_F32) {
-          if (vec32) {
-#pragma unroll
-            for (int i = 0; i < 8; ++i) res4[i] = *reinterpret_cast<const float4*>(o32 + 4 * i);
-          } else {
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              float t[4];
-#pragma unroll
-              for (int j = 0; j < 4; ++j) t[j] = (live && col0 + 4 * i + j < args.N) ? o32[4 * i + j] : 0.f;
-              res4[i] = make_float4(t[0], t[1], t[2], t[3]);
-            }
-          }
-        }
-        float v[32];
-        tmem_ld_32x32b_x32(tmem_base + (uint32_t)(acc * BN + c * 32) + ((uint32_t)(quarter * 32) << 16), v);
-        if (!live) continue;
-        if constexpr (EPI != ZO_EPI_F32) {
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            v[4 * i] += bias4[i].x; v[4 * i + 1] += bias4[i].y;
-            v[4 * i + 2] += bias4[i].z; v[4 * i + 3] += bias4[i].w;
-          }
-        }
-        if constexpr (EPI == ZO_EPI_F32 || EPI == ZO_EPI_BIAS_RESID_F32) {
-          if constexpr (EPI == ZO_EPI_BIAS_RESID_F32) {
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              v[4 * i] = res4[i].x + v[4 * i]; v[4 * i + 1] = res4[i].y + v[4 * i + 1];
-              v[4 * i + 2] = res4[i].z + v[4 * i + 2]; v[4 * i + 3] = res4[i].w + v[4 * i + 3];
-            }
-          }
-          if (vec32) {
-#pragma unroll
-            for (int i = 0; i < 8; ++i)
-              *reinterpret_cast<float4*>(o32 + 4 * i) = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
-          } else {
-#pragma unroll
-            for (int i = 0; i < 32; ++i)
-              if (col0 + i < args.N) o32[i] = v[i];
-          }
-        } else if constexpr (EPI == ZO_EPI_BIAS_BF16 || EPI == ZO_EPI_BIAS_GELU_BF16) {
-          if constexpr (EPI == ZO_EPI_BIAS_GELU_BF16) {
-#pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] = gelu_tanh(v[i]);
-          }
-          __nv_bfloat16* o = static_cast<__nv_bfloat16*>(args.out) + row * args.ldo + col0;
-          if (full && ((reinterpret_cast<uintptr_t>(o) & 15) == 0)) {
-#pragma unroll
-            for (int i = 0; i < 32; i += 8) {
-              uint32_t pk[4];
-#pragma unroll
-              for (int j = 0; j < 4; ++j) {
-                __nv_bfloat162 h2 = __floats2bfloat162_rn(v[i + 2 * j], v[i + 2 * j + 1]);
-                pk[j] = *reinterpret_cast<uint32_t*>(&h2);
-              }
-              *reinterpret_cast<uint4*>(o + i) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-            }
-          } else {
-#pragma unroll
-            for (int i = 0; i < 32; ++i)
-              if (col0 + i < args.N) o[i] = __float2bfloat16_rn(v[i]);
-          }
-        } else {  // ZO_EPI_CE: online (max, sum exp) over this row's columns of the tile
-          const int lim = full ? 32 : (int)(args.N - col0);
-          float cm = -INFINITY;
-#pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            if (i < lim) {
-              bad |= !isfinite(v[i]);
-              cm = fmaxf(cm, v[i]);
-            }
-          }
-          const float nm = fmaxf(ce_m, cm);
-          float s = ce_s * __expf(ce_m - nm);
-          if (ce_m == -INFINITY) s = 0.f;
-#pragma unroll
-          for (int i = 0; i < 32; ++i)
-            if (i < lim) s += __expf(v[i] - nm);
-          ce_m = nm;
-          ce_s = s;
-          if (tgt >= col0 && tgt < col0 + lim) {
-            const int ti = (int)(tgt - col0);
-#pragma unroll
-            for (int i = 0; i < 32; ++i)
-              if (i == ti) args.ce_tgt[row] = v[i];
-          }
-        }
-      }
-      if constexpr (EPI == ZO_EPI_CE) {
-        if (row_ok) {
-          args.ce_part[(row * args.ce_tiles + tn) * 2] = ce_m;
-          args.ce_part[(row * args.ce_tiles + tn) * 2 + 1] = ce_s;
-          if (bad) atomicOr(args.err, 2);
-        }
-      }
+      epilogue_tile<BN, EPI>(args, tmem_base, acc, quarter, half, lane, m0, tn * BN, tn,
+                             stg_all + (warp - 2) * 32 * 33);
       tc_fence_before();
-      mbar_arrive(tempty_bar(acc));
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tempty_bar(acc));
     }
   }
   __syncthreads();
@@ -389,6 +403,193 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem_base),
                  "r"((uint32_t)C::kTmemCols));
+  }
+}
+
+
+// ----------------------------------------------------------------------------
+// CTA-pair variant (tcgen05 cta_group::2): a cluster of 2 CTAs on one TPC
+// computes a 256 x 256 tile with M=256 UMMAs issued by the leader CTA.  Each
+// CTA stages its own 128 A rows and HALF of the B tile (128 columns), so per
+// pair and K-block the pair moves 64 KB for 8.4 MFLOP (128 FLOP/B, 1.5x the
+// single-CTA tile) -- the L2->SMEM feed, not the tensor pipe, bounds the
+// single-CTA kernel at these shapes.  TMEM: each CTA holds its 128 rows x 256
+// fp32 columns, double buffered (512 columns).
+//   full[s]   leader only; expects both CTAs' bytes (cta_group::2 TMA signals it)
+//   empty[s]  both CTAs; leader's tcgen05.commit multicasts to the pair
+//   tfull[a]  both CTAs; multicast commit
+//   tempty[a] leader only; 16 arrivals = 8 epilogue warps x 2 CTAs (remote)
+// ----------------------------------------------------------------------------
+constexpr int k2Stages = 5;   // leaves room for a co-resident perturb CTA (side stream)
+constexpr int k2ABytes = kBM * kBK * 2;        // 16 KB: this CTA's 128 rows
+constexpr int k2BBytes = kBK * 128 * 2;        // 16 KB: this CTA's half of B
+constexpr int k2StageBytes = k2ABytes + k2BBytes;
+constexpr int k2Smem = k2Stages * k2StageBytes + 1024 + 256 + kEpiWarps * 32 * 33 * 4;
+static_assert(k2Smem <= 232448, "pair kernel smem");
+
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void tma_load_2d_cg2(uint32_t dst, const CUtensorMap* map, uint32_t bar_cluster, int c0,
+                                                int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%2, %3}], [%4];\n" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar_cluster)
+      : "memory");
+}
+__device__ __forceinline__ void tc_commit_pair(uint32_t bar) {
+  asm volatile(
+      "{\n.reg .b16 m;\nmov.b16 m, 3;\n"
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], m;\n}\n" ::"r"(
+          bar)
+      : "memory");
+}
+__device__ __forceinline__ void tc_mma_f16_pair(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                                uint32_t accumulate) {
+  asm volatile(
+      "{\n.reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+template <int EPI>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
+    gemm_tcgen05_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                             const GemmArgs args) {
+  constexpr int BN = 256;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  const uint32_t base = (raw + 1023u) & ~1023u;
+  uint8_t* gbase = smem_raw + (base - raw);
+  const uint32_t sA = base;
+  const uint32_t sB = base + k2Stages * k2ABytes;
+  const uint32_t bars = base + k2Stages * k2StageBytes;
+  auto full_bar = [&](int s) { return bars + 8u * s; };
+  auto empty_bar = [&](int s) { return bars + 8u * (k2Stages + s); };
+  auto tfull_bar = [&](int a) { return bars + 8u * (2 * k2Stages + a); };
+  auto tempty_bar = [&](int a) { return bars + 8u * (2 * k2Stages + 2 + a); };
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + k2Stages * k2StageBytes + 8 * (2 * k2Stages + 4));
+  float* stg_all = reinterpret_cast<float*>(gbase + k2Stages * k2StageBytes + 256);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  const int64_t cluster_id = blockIdx.x >> 1, n_clusters = gridDim.x >> 1;
+  const int64_t num_m = (args.M + 2 * kBM - 1) / (2 * kBM);
+  const int64_t num_n = (args.N + BN - 1) / BN;
+  const int64_t tiles = num_m * num_n;
+  const int nk = (int)((args.K + kBK - 1) / kBK);
+
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&tmA);
+    prefetch_tmap(&tmB);
+    for (int s = 0; s < k2Stages; ++s) { mbar_init(full_bar(s), 1); mbar_init(empty_bar(s), 1); }
+    for (int a = 0; a < 2; ++a) { mbar_init(tfull_bar(a), 1); mbar_init(tempty_bar(a), 2 * kEpiWarps); }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tmem_slot)),
+                 "r"(512u));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n");
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ====== TMA producer (both CTAs): own A rows + own half of B ======
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int64_t tile = cluster_id; tile < tiles; tile += n_clusters) {
+        const int m0 = (int)((tile % num_m) * (2 * kBM) + rank * kBM);
+        const int n0 = (int)((tile / num_m) * BN + rank * 128);
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_wait(empty_bar(stage), phase ^ 1u);
+          if (leader) mbar_expect_tx(full_bar(stage), (uint32_t)(2 * k2StageBytes));
+          const uint32_t fb = mapa_shared(full_bar(stage), 0);
+          tma_load_2d_cg2(sA + stage * k2ABytes, &tmA, fb, kb * kBK, m0);
+          tma_load_2d_cg2(sB + stage * k2BBytes, &tmB, fb, n0, kb * kBK);
+          tma_load_2d_cg2(sB + stage * k2BBytes + kBK * 128, &tmB, fb, n0 + 64, kb * kBK);
+          if (++stage == k2Stages) { stage = 0; phase ^= 1u; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ====== MMA issuer (leader CTA only): M=256 x N=256 per instruction ======
+    if (leader) {
+      const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) | ((uint32_t)(BN >> 3) << 17) |
+                             ((uint32_t)(256 >> 4) << 24);
+      int stage = 0;
+      uint32_t phase = 0;
+      int64_t local = 0;
+      for (int64_t tile = cluster_id; tile < tiles; tile += n_clusters, ++local) {
+        const int acc = (int)(local & 1);
+        const uint32_t acc_phase = (uint32_t)((local >> 1) & 1);
+        mbar_wait(tempty_bar(acc), acc_phase ^ 1u);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_wait(full_bar(stage), phase);
+          tc_fence_after();
+          if (lane == 0) {
+            const uint32_t a0 = sA + stage * k2ABytes;
+            const uint32_t b0 = sB + stage * k2BBytes;
+#pragma unroll
+            for (int kk = 0; kk < kBK / 16; ++kk) {
+              const uint64_t ad = desc_sw128(a0 + kk * 32, 16, 1024);
+              const uint64_t bd = desc_sw128(b0 + kk * 2048, kBK * 128, 1024);
+              tc_mma_f16_pair(d_tmem, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
+            }
+            tc_commit_pair(empty_bar(stage));
+          }
+          __syncwarp();
+          if (++stage == k2Stages) { stage = 0; phase ^= 1u; }
+        }
+        if (lane == 0) tc_commit_pair(tfull_bar(acc));
+        __syncwarp();
+      }
+    }
+  } else {
+    // ====== epilogue (both CTAs): this CTA's 128 rows x 256 columns ======
+    const int quarter = warp & 3;
+    const int half = (warp - 2) >> 2;
+    int64_t local = 0;
+    for (int64_t tile = cluster_id; tile < tiles; tile += n_clusters, ++local) {
+      const int acc = (int)(local & 1);
+      const uint32_t acc_phase = (uint32_t)((local >> 1) & 1);
+      const int64_t m0 = (tile % num_m) * (2 * kBM) + rank * kBM;
+      const int64_t tn = tile / num_m;
+      mbar_wait(tfull_bar(acc), acc_phase);
+      tc_fence_after();
+      epilogue_tile<BN, EPI>(args, tmem_base, acc, quarter, half, lane, m0, tn * BN, tn,
+                             stg_all + (warp - 2) * 32 * 33);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(mapa_shared(tempty_bar(acc), 0));
+    }
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;\n" ::"r"(tmem_base), "r"(512u));
   }
 }
 
@@ -485,9 +686,39 @@ int launch_bn(int epi, const CUtensorMap& ma, const CUtensorMap& mb, const GemmA
   return ZO_ERR_CONFIG;
 }
 
+
+template <int EPI>
+int launch_pair_t(const CUtensorMap& ma, const CUtensorMap& mb, const GemmArgs& a, cudaStream_t st) {
+  static bool attr_done = false;
+  if (!attr_done) {
+    cudaError_t e = cudaFuncSetAttribute(gemm_tcgen05_pair_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         k2Smem);
+    if (e != cudaSuccess) { set_error("gemm pair smem attribute: %s", cudaGetErrorString(e)); return ZO_ERR_CUDA; }
+    attr_done = true;
+  }
+  const int64_t tiles = ((a.M + 255) / 256) * ((a.N + 255) / 256);
+  const int64_t pairs = num_sms() / 2;
+  const int grid = 2 * (int)(tiles < pairs ? tiles : pairs);
+  gemm_tcgen05_pair_kernel<EPI><<<grid, kGemmThreads, k2Smem, st>>>(ma, mb, a);
+  return launch_status("gemm_tcgen05_pair_kernel");
+}
+
+int launch_pair(int epi, const CUtensorMap& ma, const CUtensorMap& mb, const GemmArgs& a, cudaStream_t st) {
+  switch (epi) {
+    case ZO_EPI_F32: return launch_pair_t<ZO_EPI_F32>(ma, mb, a, st);
+    case ZO_EPI_BIAS_BF16: return launch_pair_t<ZO_EPI_BIAS_BF16>(ma, mb, a, st);
+    case ZO_EPI_BIAS_GELU_BF16: return launch_pair_t<ZO_EPI_BIAS_GELU_BF16>(ma, mb, a, st);
+    case ZO_EPI_BIAS_RESID_F32: return launch_pair_t<ZO_EPI_BIAS_RESID_F32>(ma, mb, a, st);
+    case ZO_EPI_CE: return launch_pair_t<ZO_EPI_CE>(ma, mb, a, st);
+  }
+  set_error("zo_gemm_bf16: unknown epilogue %d", epi);
+  return ZO_ERR_CONFIG;
+}
+
 }  // namespace
 
-int64_t gemm_ce_tiles(int64_t N) { return (N + 255) / 256; }
+int64_t gemm_ce_tiles(int64_t N) { return 2 * ((N + 255) / 256); }   // one partial per 128-column half
+
 
 int gemm_launch(const void* A, int64_t lda, const void* B, int64_t ldb, int64_t M, int64_t N, int64_t K, int epi,
                 const float* bias, void* out, int64_t ldo, const int32_t* targets, float* ce_part, float* ce_tgt,
@@ -518,6 +749,11 @@ int gemm_launch(const void* A, int64_t lda, const void* B, int64_t ldb, int64_t 
   rc = get_map(B, N, K, ldb, 64, kBK, &mb);
   if (rc) return rc;
   GemmArgs a{M, N, K, bias, out, ldo, targets, ce_part, ce_tgt, err, gemm_ce_tiles(N)};
+  static const int pair_mode = [] {
+    const char* e = getenv("ZO_GEMM_PAIR");   // 0: single-CTA only, 1: CTA pairs when M > 128 (default)
+    return e ? atoi(e) : 1;
+  }();
+  if (pair_mode && M > kBM && bn == 256) return launch_pair(epi, ma, mb, a, st);
   return bn == 256 ? launch_bn<256>(epi, ma, mb, a, st) : launch_bn<128>(epi, ma, mb, a, st);
 }
 

@@ -194,12 +194,14 @@ __global__ void ce_rows_kernel(const float* __restrict__ part, const float* __re
   bool bad = false;
   for (int64_t i = 0; i < n_tiles; ++i) {
     const float v = p[2 * i];
+    if (v == -INFINITY && p[2 * i + 1] == 0.f) continue;   // empty (out-of-range) partial
     if (!isfinite(v)) bad = true;
     m = fmax(m, (double)v);
   }
   double s = 0.0;
   for (int64_t i = 0; i < n_tiles; ++i) {
     const float ps = p[2 * i + 1];
+    if (p[2 * i] == -INFINITY && ps == 0.f) continue;
     if (!isfinite(ps)) bad = true;
     s += (double)ps * exp((double)p[2 * i] - m);
   }

@@ -16,9 +16,10 @@
 
 namespace zo {
 
-constexpr int kPuThreads = 256;
+constexpr int kPuThreads = 128;   // small CTAs: one co-resides with a GEMM CTA per SM
 constexpr int kPuGroupsPerThread = 4;
-constexpr int64_t kPuTile = (int64_t)kPuThreads * kPuGroupsPerThread * 4;  // elements per tile
+constexpr int64_t kPuTile = 32 * kPuGroupsPerThread * 4;  // elements per warp tile (512)
+constexpr int kPuMaxSmemSegs = 4096;   // prefix entries staged in shared memory (32 KB)
 
 __device__ __forceinline__ void store_shadow(const ZoSegment& s, __nv_bfloat16* w, float* v,
                                              int64_t di, float val) {
@@ -27,8 +28,139 @@ __device__ __forceinline__ void store_shadow(const ZoSegment& s, __nv_bfloat16* 
 }
 
 template <int ZMODE>
-__global__ void __launch_bounds__(kPuThreads) perturb_update_kernel(const PuParams p) {
-  __shared__ int s_seg;
+__device__ __forceinline__ void pu_group(const PuParams& p, const ZoSegment& s, int64_t q, int64_t e0, int64_t e1,
+                                         int64_t drow, float (&th)[4], bool full, bool theta_vec, bool pending,
+                                         bool need_z, bool want_sh, const bool (&sh)[2], const float (&sc32)[2],
+                                         uint64_t seed_cur, uint64_t seed_prev, double lrg64, float lrg32) {
+  const int64_t eg = q << 2;
+  if (pending) {
+    if constexpr (ZMODE == ZO_Z_PHILOX) {
+      const f32x4 zp = philox_normal4(seed_prev, (uint64_t)q);
+      th[0] = fmaf(-lrg32, zp.x, th[0]); th[1] = fmaf(-lrg32, zp.y, th[1]);
+      th[2] = fmaf(-lrg32, zp.z, th[2]); th[3] = fmaf(-lrg32, zp.w, th[3]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int64_t e = eg + i;
+        if (e >= e0 && e < e1)
+          th[i] = __double2float_rn(__dsub_rn((double)th[i], __dmul_rn(lrg64, p.z_prev[e - p.z_key0])));
+      }
+    }
+    if (full && theta_vec) {
+      *reinterpret_cast<float4*>(p.theta + (eg - p.theta_key0)) = make_float4(th[0], th[1], th[2], th[3]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if (eg + i >= e0 && eg + i < e1) p.theta[eg + i - p.theta_key0] = th[i];
+    }
+  }
+  if (!want_sh) return;
+  float zc[4] = {0.f, 0.f, 0.f, 0.f};
+  double zc64[4] = {0.0, 0.0, 0.0, 0.0};
+  if (need_z) {
+    if constexpr (ZMODE == ZO_Z_PHILOX) {
+      const f32x4 z4 = philox_normal4(seed_cur, (uint64_t)q);
+      zc[0] = z4.x; zc[1] = z4.y; zc[2] = z4.z; zc[3] = z4.w;
+    } else {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int64_t e = eg + i;
+        if (e >= e0 && e < e1) zc64[i] = p.z_cur[e - p.z_key0];
+      }
+    }
+  }
+#pragma unroll
+  for (int d = 0; d < 2; ++d) {
+    if (!sh[d]) continue;
+    float v[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      if (p.scale[d] == 0.0) v[i] = th[i];
+      else if constexpr (ZMODE == ZO_Z_PHILOX) v[i] = fmaf(sc32[d], zc[i], th[i]);
+      else v[i] = __double2float_rn(__dadd_rn((double)th[i], __dmul_rn(p.scale[d], zc64[i])));
+    }
+    const int64_t di = eg + drow;
+    if (full && ((di & 3) == 0)) {
+      if (s.kind == ZO_SHADOW_BF16) {
+        __nv_bfloat162 lo2 = __floats2bfloat162_rn(v[0], v[1]);
+        __nv_bfloat162 hi2 = __floats2bfloat162_rn(v[2], v[3]);
+        uint2 packed;
+        packed.x = *reinterpret_cast<uint32_t*>(&lo2);
+        packed.y = *reinterpret_cast<uint32_t*>(&hi2);
+        *reinterpret_cast<uint2*>(p.wsh[d] + di) = packed;
+      } else {
+        *reinterpret_cast<float4*>(p.vsh[d] + di) = make_float4(v[0], v[1], v[2], v[3]);
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if (eg + i >= e0 && eg + i < e1) store_shadow(s, p.wsh[d], p.vsh[d], di + i, v[i]);
+    }
+  }
+}
+
+
+// Fast tile: Philox direction, every group full and 16-B aligned (all real
+// model tensors).  Straight-line code, 32-bit in-tile indexing, keyed Philox.
+__device__ __forceinline__ void pu_tile_fast(const PuParams& p, int64_t e0, int ngroups, int64_t dbase,
+                                             bool pending, bool want_sh, bool need_z, const bool (&sh)[2],
+                                             const float (&sc32)[2], const PhiloxKeys& kc, const PhiloxKeys& kp,
+                                             float lrg32, int kind, int lane) {
+  float4* tp = reinterpret_cast<float4*>(p.theta + (e0 - p.theta_key0));
+  const uint64_t qa = (uint64_t)(e0 >> 2);
+  const bool full = ngroups == 32 * kPuGroupsPerThread;
+  float4 th[kPuGroupsPerThread];
+#pragma unroll
+  for (int g = 0; g < kPuGroupsPerThread; ++g) {
+    const int idx = lane + 32 * g;
+    if (full || idx < ngroups) th[g] = tp[idx];
+  }
+#pragma unroll
+  for (int g = 0; g < kPuGroupsPerThread; ++g) {
+    const int idx = lane + 32 * g;
+    if (!full && idx >= ngroups) continue;
+    const uint64_t q = qa + (uint64_t)idx;
+    float4 t = th[g];
+    if (pending) {
+      const f32x4 zp = philox_normal4_k(kp, q);
+      t.x = fmaf(-lrg32, zp.x, t.x); t.y = fmaf(-lrg32, zp.y, t.y);
+      t.z = fmaf(-lrg32, zp.z, t.z); t.w = fmaf(-lrg32, zp.w, t.w);
+      tp[idx] = t;
+    }
+    if (!want_sh) continue;
+    f32x4 z = {0.f, 0.f, 0.f, 0.f};
+    if (need_z) z = philox_normal4_k(kc, q);
+#pragma unroll
+    for (int d = 0; d < 2; ++d) {
+      if (!sh[d]) continue;
+      const float a = fmaf(sc32[d], z.x, t.x), b = fmaf(sc32[d], z.y, t.y);
+      const float c = fmaf(sc32[d], z.z, t.z), e = fmaf(sc32[d], z.w, t.w);
+      if (kind == ZO_SHADOW_BF16) {
+        __nv_bfloat162 lo2 = __floats2bfloat162_rn(a, b), hi2 = __floats2bfloat162_rn(c, e);
+        uint2 pk;
+        pk.x = *reinterpret_cast<uint32_t*>(&lo2);
+        pk.y = *reinterpret_cast<uint32_t*>(&hi2);
+        reinterpret_cast<uint2*>(p.wsh[d] + dbase)[idx] = pk;
+      } else {
+        reinterpret_cast<float4*>(p.vsh[d] + dbase)[idx] = make_float4(a, b, c, e);
+      }
+    }
+  }
+}
+
+// Warp-independent streaming: each warp owns 512-element tiles (32 lanes x 4
+// groups of 4 elements, +1 group when a tile starts mid-group), looks up its
+// segment by binary search in the shared-memory prefix table and never
+// synchronises with other warps, so loads of one warp overlap the
+// Philox/Box-Muller math and stores of the others.  Each lane issues all of
+// its theta loads (float4, coalesced 512 B per warp per group) before any math.
+template <int ZMODE>
+__global__ void __launch_bounds__(kPuThreads, 6) perturb_update_kernel(const PuParams p) {
+  extern __shared__ int64_t s_prefix[];
+  const bool prefix_in_smem = p.n_segs + 1 <= kPuMaxSmemSegs;
+  if (prefix_in_smem)
+    for (int i = threadIdx.x; i <= p.n_segs; i += kPuThreads) s_prefix[i] = p.prefix[i];
+  __syncthreads();
   const bool pending = (p.flags & ZO_PU_UPDATE) && p.scal->pending != 0;
   const uint64_t seed_cur = p.scal->seed_cur;
   const uint64_t seed_prev = p.scal->seed_prev;
@@ -38,120 +170,81 @@ __global__ void __launch_bounds__(kPuThreads) perturb_update_kernel(const PuPara
   const float sc32[2] = {(float)p.scale[0], (float)p.scale[1]};
   const bool need_z = (sh[0] && p.scale[0] != 0.0) || (sh[1] && p.scale[1] != 0.0);
   const bool theta_vec = ((p.theta_key0 & 3) == 0) && ((reinterpret_cast<uintptr_t>(p.theta) & 15) == 0);
+  constexpr int G = kPuGroupsPerThread + 1;
+  const int lane = threadIdx.x & 31;
+  const PhiloxKeys kc = philox_keys(seed_cur), kp = philox_keys(seed_prev);
+  const int64_t warp0 = (blockIdx.x * (int64_t)kPuThreads + threadIdx.x) >> 5;
+  const int64_t n_warps = ((int64_t)gridDim.x * kPuThreads) >> 5;
 
-  for (int64_t t = blockIdx.x; t < p.n_tiles; t += gridDim.x) {
-    if (threadIdx.x == 0) {  // segment owning tile t: largest i with prefix[i] <= t
-      int lo = 0, hi = p.n_segs - 1;
+  for (int64_t t = warp0; t < p.n_tiles; t += n_warps) {
+    int lo = 0, hi = p.n_segs - 1;          // warp-uniform search (LDS broadcast reads)
+    if (prefix_in_smem) {
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (s_prefix[mid] <= t) lo = mid; else hi = mid - 1;
+      }
+    } else {
       while (lo < hi) {
         const int mid = (lo + hi + 1) >> 1;
         if (p.prefix[mid] <= t) lo = mid; else hi = mid - 1;
       }
-      s_seg = lo;
     }
-    __syncthreads();
-    const int si = s_seg;
-    __syncthreads();
-    const ZoSegment s = p.segs[si];
-    const int64_t tpr = (s.cols + kPuTile - 1) / kPuTile;
-    const int64_t local = t - p.prefix[si];
-    const int64_t row = local / tpr;
-    const int64_t c0 = (local % tpr) * kPuTile;
+    const ZoSegment s = p.segs[lo];
+    const uint32_t local = (uint32_t)(t - (prefix_in_smem ? s_prefix[lo] : p.prefix[lo]));
+    int64_t row, c0;
+    if (s.rows == 1) {                      // flat tensor: no division
+      row = 0;
+      c0 = (int64_t)local * kPuTile;
+    } else {
+      const uint32_t tpr = (uint32_t)((s.cols + kPuTile - 1) / kPuTile);
+      row = local / tpr;
+      c0 = (int64_t)(local - (uint32_t)row * tpr) * kPuTile;
+    }
     const int64_t c1 = min(c0 + kPuTile, s.cols);
-    const int64_t rk = s.src + row * s.cols;         // key of (row, col 0)
+    const int64_t rk = s.src + row * s.cols;
     const int64_t e0 = rk + c0, e1 = rk + c1;
-    const int64_t drow = s.dst + row * s.dst_ld - rk;  // shadow index = key + drow
+    const int64_t drow = s.dst + row * s.dst_ld - rk;
     const bool want_sh = s.kind != ZO_SHADOW_NONE;
+    const int64_t qa = e0 >> 2, qb = (e1 + 3) >> 2;
+    if (ZMODE == ZO_Z_PHILOX && theta_vec && ((e0 | e1 | (e0 + drow)) & 3) == 0) {
+      pu_tile_fast(p, e0, (int)((e1 - e0) >> 2), e0 + drow, pending, want_sh, need_z, sh, sc32, kc, kp, lrg32,
+                   s.kind, lane);
+      continue;
+    }
 
-    for (int64_t q = (e0 >> 2) + threadIdx.x; q < ((e1 + 3) >> 2); q += kPuThreads) {
+    float th[G][4];
+    bool fullg[G];
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const int64_t q = qa + lane + (int64_t)g * 32;
       const int64_t eg = q << 2;
-      float th[4];
-      const bool full = eg >= e0 && eg + 4 <= e1;
-      if (full && theta_vec) {
+      fullg[g] = q < qb && eg >= e0 && eg + 4 <= e1;
+      if (fullg[g] && theta_vec) {
         const float4 v4 = *reinterpret_cast<const float4*>(p.theta + (eg - p.theta_key0));
-        th[0] = v4.x; th[1] = v4.y; th[2] = v4.z; th[3] = v4.w;
+        th[g][0] = v4.x; th[g][1] = v4.y; th[g][2] = v4.z; th[g][3] = v4.w;
       } else {
 #pragma unroll
         for (int i = 0; i < 4; ++i)
-          th[i] = (eg + i >= e0 && eg + i < e1) ? p.theta[eg + i - p.theta_key0] : 0.f;
+          th[g][i] = (q < qb && eg + i >= e0 && eg + i < e1) ? p.theta[eg + i - p.theta_key0] : 0.f;
       }
-
-      if (pending) {
-        if constexpr (ZMODE == ZO_Z_PHILOX) {
-          const f32x4 zp = philox_normal4(seed_prev, (uint64_t)q);
+    }
 #pragma unroll
-          for (int i = 0; i < 4; ++i) th[i] = fmaf(-lrg32, f4get(zp, i), th[i]);
-        } else {
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const int64_t e = eg + i;
-            if (e >= e0 && e < e1) {
-              const double z = p.z_prev[e - p.z_key0];
-              th[i] = __double2float_rn(__dsub_rn((double)th[i], __dmul_rn(lrg64, z)));
-            }
-          }
-        }
-        if (full && theta_vec) {
-          *reinterpret_cast<float4*>(p.theta + (eg - p.theta_key0)) = make_float4(th[0], th[1], th[2], th[3]);
-        } else {
-#pragma unroll
-          for (int i = 0; i < 4; ++i)
-            if (eg + i >= e0 && eg + i < e1) p.theta[eg + i - p.theta_key0] = th[i];
-        }
-      }
-
-      if (!want_sh) continue;
-      float zc[4] = {0.f, 0.f, 0.f, 0.f};
-      double zc64[4] = {0.0, 0.0, 0.0, 0.0};
-      if (need_z) {
-        if constexpr (ZMODE == ZO_Z_PHILOX) {
-          const f32x4 z4 = philox_normal4(seed_cur, (uint64_t)q);
-          zc[0] = z4.x; zc[1] = z4.y; zc[2] = z4.z; zc[3] = z4.w;
-        } else {
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const int64_t e = eg + i;
-            if (e >= e0 && e < e1) zc64[i] = p.z_cur[e - p.z_key0];
-          }
-        }
-      }
-#pragma unroll
-      for (int d = 0; d < 2; ++d) {
-        if (!sh[d]) continue;
-        float v[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          if (p.scale[d] == 0.0) v[i] = th[i];
-          else if constexpr (ZMODE == ZO_Z_PHILOX) v[i] = fmaf(sc32[d], zc[i], th[i]);
-          else v[i] = __double2float_rn(__dadd_rn((double)th[i], __dmul_rn(p.scale[d], zc64[i])));
-        }
-        const int64_t di = eg + drow;
-        if (full && ((di & 3) == 0)) {
-          if (s.kind == ZO_SHADOW_BF16) {
-            __nv_bfloat162 lo2 = __floats2bfloat162_rn(v[0], v[1]);
-            __nv_bfloat162 hi2 = __floats2bfloat162_rn(v[2], v[3]);
-            uint2 packed;
-            packed.x = *reinterpret_cast<uint32_t*>(&lo2);
-            packed.y = *reinterpret_cast<uint32_t*>(&hi2);
-            *reinterpret_cast<uint2*>(p.wsh[d] + di) = packed;
-          } else {
-            *reinterpret_cast<float4*>(p.vsh[d] + di) = make_float4(v[0], v[1], v[2], v[3]);
-          }
-        } else {
-#pragma unroll
-          for (int i = 0; i < 4; ++i)
-            if (eg + i >= e0 && eg + i < e1) store_shadow(s, p.wsh[d], p.vsh[d], di + i, v[i]);
-        }
-      }
+    for (int g = 0; g < G; ++g) {
+      const int64_t q = qa + lane + (int64_t)g * 32;
+      if (q < qb)
+        pu_group<ZMODE>(p, s, q, e0, e1, drow, th[g], fullg[g], theta_vec, pending, need_z, want_sh, sh, sc32,
+                        seed_cur, seed_prev, lrg64, lrg32);
     }
   }
 }
 
 int perturb_update_launch(const PuParams& p, int zmode, cudaStream_t stream) {
   if (p.n_tiles <= 0) return ZO_OK;
-  const int64_t want = (int64_t)num_sms() * 8;   // 8 x 256 threads resident per SM
+  const int64_t want = (int64_t)num_sms() * 6;   // 6 x 128 threads per SM when the SM is free
   const int grid = (int)(p.n_tiles < want ? p.n_tiles : want);
-  if (zmode == ZO_Z_PHILOX) perturb_update_kernel<ZO_Z_PHILOX><<<grid, kPuThreads, 0, stream>>>(p);
-  else perturb_update_kernel<ZO_Z_ORACLE><<<grid, kPuThreads, 0, stream>>>(p);
+  const size_t smem = p.n_segs + 1 <= kPuMaxSmemSegs ? (size_t)(p.n_segs + 1) * sizeof(int64_t) : 0;
+  if (zmode == ZO_Z_PHILOX) perturb_update_kernel<ZO_Z_PHILOX><<<grid, kPuThreads, smem, stream>>>(p);
+  else perturb_update_kernel<ZO_Z_ORACLE><<<grid, kPuThreads, smem, stream>>>(p);
   return launch_status("perturb_update_kernel");
 }
 

@@ -151,10 +151,12 @@ class StreamingZo:
     folded into iteration j+1's perturbation pass; ``flush`` applies the last
     one.  Numerically identical to repeated ``mezo_step`` after flush."""
 
-    def __init__(self, store: DeviceStore, hyper: ZoHyper, mgr: RngStateManager | None = None):
+    def __init__(self, store: DeviceStore, hyper: ZoHyper, mgr: RngStateManager | None = None,
+                 overlap: bool = False):
         self.store = store
         self.hyper = hyper.validate()
         self.mgr = mgr or RngStateManager()
+        self.overlap = overlap and not self.mgr.oracle
         self.iteration = 0
         self.g_prev = 0.0
         self.last_seed = None
@@ -175,6 +177,33 @@ class StreamingZo:
         calls += s.grad_call(wsp, wsn, eps, self.hyper.lr)
         return calls
 
+    def overlapped_step_calls(self, wsp, wsn, side_stream=None):
+        """Same step, pipelined across two streams: the per-block fused
+        update+perturb passes (HBM-bound) run on a side stream one block ahead
+        of the +eps forward (tensor-core-bound) on the current stream, which
+        waits per block on an event.  The -eps forward follows on the main
+        stream.  Numerically identical to step_calls (same kernels, same
+        per-element arithmetic; only the launch granularity changes)."""
+        if self.mgr.oracle:
+            raise ProtocolError("the overlapped plan runs the Philox direction only")
+        s, eps = self.store, self.hyper.epsilon
+        main = torch.cuda.current_stream()
+        side = side_stream or _side_stream(s)
+        nb = len(s.layouts)
+        evs = _block_events(s, nb)
+        start = evs[-1]
+        flags = L.ZO_PU_UPDATE | L.ZO_PU_SHADOW_A | L.ZO_PU_SHADOW_B
+        calls = [(_record_and_wait, (start, main, side))]
+        for b in range(nb):
+            calls += s.perturb_call(s.block_tables[b], flags, +eps, -eps, stream=side)
+            calls.append((_record, (evs[b], side)))
+        for b in range(nb):
+            calls.append((_wait, (main, evs[b])))
+            calls += s.forward_calls(PLUS, wsp, +eps, blocks=[b])
+        calls += s.forward_calls(MINUS, wsn, -eps)
+        calls += s.grad_call(wsp, wsn, eps, self.hyper.lr)
+        return calls
+
     def step(self, batch: Batch, seed: int) -> ZoStep:
         self.iteration += 1
         self.mgr.reset(seed)
@@ -185,8 +214,11 @@ class StreamingZo:
         wsp, wsn = _stage_batch(self.store, batch)
         zc = _oracle_z(self.mgr, seed, self.store.total_params, self.store.device) if self.mgr.oracle else None
         _write_scal(self.store, seed, pending=apply_pending)
-        self.store.run(self.step_calls(wsp, wsn, zc, self._z_prev if apply_pending else None,
-                                       update=apply_pending or not self.mgr.oracle))
+        if self.overlap:
+            self.store.run(self.overlapped_step_calls(wsp, wsn))
+        else:
+            self.store.run(self.step_calls(wsp, wsn, zc, self._z_prev if apply_pending else None,
+                                           update=apply_pending or not self.mgr.oracle))
         st = _finish(self.store, wsp, wsn, self.iteration, seed)
         self.g_prev, self.last_seed, self._pending, self._z_prev = st.g, seed, True, zc
         return st
@@ -203,6 +235,34 @@ class StreamingZo:
         s.scal[3:4].fill_(0)
         torch.cuda.current_stream().synchronize()
         self._pending = False
+
+
+def _side_stream(store: DeviceStore):
+    if not hasattr(store, "_side"):
+        store._side = torch.cuda.Stream(device=store.device)
+    return store._side
+
+
+def _block_events(store: DeviceStore, n: int):
+    if getattr(store, "_evs", None) is None or len(store._evs) != n + 1:
+        store._evs = [torch.cuda.Event() for _ in range(n + 1)]
+    return store._evs
+
+
+def _record_and_wait(ev, main, side):
+    ev.record(main)
+    side.wait_event(ev)
+    return 0
+
+
+def _record(ev, stream):
+    ev.record(stream)
+    return 0
+
+
+def _wait(stream, ev):
+    stream.wait_event(ev)
+    return 0
 
 
 def flush_pending_update(store: DeviceStore, g_last: float, seed: int, mgr: RngStateManager, lr: float) -> None:

@@ -28,8 +28,8 @@ def test_library_loads_and_exports_every_symbol():
     for name in _declared():
         assert hasattr(dll, name), name
     assert dll.zo_version().decode().startswith("zo_b200")
-    assert dll.zo_perturb_tile_elems() == 4096
-    assert dll.zo_gemm_ce_tiles(50272) == 197
+    assert dll.zo_perturb_tile_elems() == 512
+    assert dll.zo_gemm_ce_tiles(50272) == 394
 
 
 def test_sass_is_sm100a_tcgen05():

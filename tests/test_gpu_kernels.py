@@ -122,3 +122,14 @@ def test_philox_distribution_and_slice_invariance():
     from scipy import stats
     ks = stats.kstest(zc[:200000], "norm").statistic
     assert ks < 5e-3
+
+
+def test_philox_normals_finite_over_a_large_window():
+    """u1 rounds to exactly 1.0 with probability 2^-24 per Box-Muller pair: a
+    2^27-element window contains several such events; all outputs must be
+    finite (a NaN here would poison theta through the folded update)."""
+    for seed in (1, 0x123456789ABCDEF):
+        z = ops.philox_normals(seed, 0, 1 << 27)
+        assert bool(torch.isfinite(z).all())
+        assert float(z.abs().max()) < 6.5
+        del z

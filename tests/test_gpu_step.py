@@ -281,3 +281,19 @@ def test_error_behaviour_matches_reference():
     sz.flush()
     with pytest.raises(ProtocolError):
         sz.flush()
+
+
+def test_overlapped_two_stream_step_is_bit_identical():
+    """Per-block perturb passes on a side stream overlapping the +eps forward
+    give exactly the serial plan's records and weights."""
+    cfg, bsz, _ = _cfg("mid32")
+    a, b = DeviceStore(cfg, 7), DeviceStore(cfg, 7)
+    h = zo.ZoHyper(EPS, LR)
+    sa, sb = zo.StreamingZo(a, h), zo.StreamingZo(b, h, overlap=True)
+    for j, s in enumerate(iteration_seeds(13, 4), 1):
+        batch = _batch(cfg, bsz, 300 + j)
+        ra, rb = sa.step(batch, s), sb.step(batch, s)
+        assert (ra.loss_pos, ra.loss_neg, ra.g) == (rb.loss_pos, rb.loss_neg, rb.g)
+    sa.flush()
+    sb.flush()
+    assert torch.equal(a.theta, b.theta)
