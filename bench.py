@@ -47,7 +47,8 @@ def _args():
     ap.add_argument("--batch", type=int, default=BATCH_PER_GROUP, help="sequences per PertP group")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true", help="skip the public-API pass (profiling runs)")
-    ap.add_argument("--serial", action="store_true", help="no perturb/forward stream overlap")
+    ap.add_argument("--overlap", action="store_true",
+                    help="per-block perturb passes on a side stream ahead of the +eps forward")
     return ap.parse_args()
 
 
@@ -220,9 +221,9 @@ def ours(args, rank, world, local_rank):
                for j in range(1, args.warmup + args.steps + 1)]
 
     if world == 1:
-        runner = zo.StreamingZo(store, hyper, overlap=not args.serial)
+        runner = zo.StreamingZo(store, hyper, overlap=args.overlap)
         wss = [store.workspace(PLUS, B, T), store.workspace(MINUS, B, T)]
-        step_calls = (runner.step_calls(wss[0], wss[1]) if args.serial
+        step_calls = (runner.step_calls(wss[0], wss[1]) if (not args.overlap)
                       else runner.overlapped_step_calls(wss[0], wss[1]))
     else:
         from paper_2507_03211_b200.strategies import TwoDRunner
@@ -299,9 +300,21 @@ def ours(args, rank, world, local_rank):
         t = torch.tensor([ms], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    # instrumented pass over the same steps: per-kernel CUDA-event durations
+    # instrumented pass over the same steps: per-kernel CUDA-event durations.
+    # Kernels of concurrent streams would overlap their event windows, so the
+    # instrumented replay runs the two directional forwards serialised.
+    if world == 1:
+        runner.dual_stream = False
+        step_calls[:] = (runner.step_calls(wss[0], wss[1]) if not args.overlap
+                         else runner.overlapped_step_calls(wss[0], wss[1]))
+        pert_set.clear()
+        pert_set.update(i for i, (fn, _) in enumerate(step_calls) if fn.__name__ == "zo_perturb_update")
+        gemm_set.clear()
+        gemm_set.update(i for i, (fn, _) in enumerate(step_calls) if fn.__name__ == "zo_gemm_bf16")
     for j in range(args.warmup, args.warmup + args.steps):
         one_step(j, instrument=True)
+    if world == 1:
+        runner.dual_stream = True
     torch.cuda.synchronize()
     per_step = {}
     for jj, a, b in pert_ev:
@@ -317,7 +330,7 @@ def ours(args, rank, world, local_rank):
     if args.no_e2e:
         e2e_ms = ms
     elif world == 1:
-        runner2 = zo.StreamingZo(store, hyper, overlap=not args.serial)
+        runner2 = zo.StreamingZo(store, hyper, overlap=args.overlap)
         for j in range(args.warmup):
             runner2.step(batches[j], seeds[j])
         torch.cuda.synchronize()
@@ -352,7 +365,7 @@ def ours(args, rank, world, local_rank):
                  "unit": "GB/s", "frac": pert_gbs / hbm, "traffic": None, "peak_kind": f"{peak_kind} HBM copy",
                  "share_of_step": pert_share,
                  "algorithmic": f"{bytes_per_param} B/param x {P} params per step "
-                                f"({'one launch per block on a side stream, overlapping the +eps forward' if world == 1 and not args.serial else 'one launch'})"}
+                                f"({'one launch per block on a side stream, overlapping the +eps forward' if world == 1 and args.overlap else 'one launch'})"}
     dominant = roof_gemm if gemm_share >= pert_share else roof_pert
     other = roof_pert if dominant is roof_gemm else roof_gemm
     line = {
@@ -386,12 +399,18 @@ def main():
     if args.impl == "reference":
         reference_arm(args, rank, world)
         return
+    if os.environ.get("ZO_BENCH_SHARE_GPU"):
+        local_rank = 0          # test mode: all ranks on one GPU (timings meaningless)
     if world > 1:
         import torch
         import torch.distributed as dist
 
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
+        backend = os.environ.get("ZO_DIST_BACKEND", "nccl")   # gloo only for single-GPU tests
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
+        else:
+            dist.init_process_group(backend)
     try:
         ours(args, rank, world, local_rank)
     finally:

@@ -132,6 +132,36 @@ __device__ __forceinline__ float philox_normal1(uint64_t seed, uint64_t e) {
   switch (e & 3) { case 0: return v.x; case 1: return v.y; case 2: return v.z; default: return v.w; }
 }
 
+// Four Philox4x32-10 streams in lockstep: each round key is formed once and
+// shared by the four counters (and the four dependency chains interleave).
+template <int N>
+__device__ __forceinline__ void philox4x32_10_xn(const uint64_t (&ctr)[N], uint64_t seed, u32x4 (&out)[N]) {
+  uint32_t c0[N], c1[N], c2[N], c3[N];
+#pragma unroll
+  for (int i = 0; i < N; ++i) { c0[i] = (uint32_t)ctr[i]; c1[i] = (uint32_t)(ctr[i] >> 32); c2[i] = 0u; c3[i] = 0u; }
+  uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      const uint64_t p0 = (uint64_t)0xD2511F53u * c0[i];
+      const uint64_t p1 = (uint64_t)0xCD9E8D57u * c2[i];
+      const uint32_t n0 = (uint32_t)(p1 >> 32) ^ c1[i] ^ k0, n2 = (uint32_t)(p0 >> 32) ^ c3[i] ^ k1;
+      c0[i] = n0; c1[i] = (uint32_t)p1; c2[i] = n2; c3[i] = (uint32_t)p0;
+    }
+    k0 += 0x9E3779B9u; k1 += 0xBB67AE85u;
+  }
+#pragma unroll
+  for (int i = 0; i < N; ++i) out[i] = {c0[i], c1[i], c2[i], c3[i]};
+}
+
+__device__ __forceinline__ f32x4 normals_from_bits(const u32x4& r) {
+  f32x4 o;
+  box_muller(r.x, r.y, o.x, o.y);
+  box_muller(r.z, r.w, o.z, o.w);
+  return o;
+}
+
 __device__ __forceinline__ f32x4 philox_normal4_k(const PhiloxKeys& k, uint64_t q) {
   const u32x4 r = philox4x32_10_k(q, k);
   f32x4 o;

@@ -140,9 +140,18 @@ __device__ __forceinline__ uint32_t make_idesc() {
          ((uint32_t)(kBM >> 4) << 24);
 }
 
+// tanh-GELU (model.py:286-289).  tanh via MUFU.TANH (rel. error ~2^-11), far
+// below the bf16 rounding of the output that follows.
+__device__ __forceinline__ float tanh_fast(float x) {
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 __device__ __forceinline__ float gelu_tanh(float x) {
   const float c = 0.7978845608028654f;  // sqrt(2/pi)
-  return 0.5f * x * (1.0f + tanhf(c * (x + 0.044715f * x * x * x)));
+  const float u = c * fmaf(0.044715f * x, x * x, x);
+  const float hx = 0.5f * x;
+  return fmaf(hx, tanh_fast(u), hx);
 }
 
 // One 128 x BN accumulator tile from TMEM -> fused epilogue -> global.

@@ -101,35 +101,46 @@ __device__ __forceinline__ void pu_group(const PuParams& p, const ZoSegment& s, 
 
 
 // Fast tile: Philox direction, every group full and 16-B aligned (all real
-// model tensors).  Straight-line code, 32-bit in-tile indexing, keyed Philox.
+// model tensors).  Straight-line code, 32-bit in-tile indexing; the lane's 4
+// groups run their Philox streams in lockstep (philox4x32_10_xn).
 __device__ __forceinline__ void pu_tile_fast(const PuParams& p, int64_t e0, int ngroups, int64_t dbase,
                                              bool pending, bool want_sh, bool need_z, const bool (&sh)[2],
-                                             const float (&sc32)[2], const PhiloxKeys& kc, const PhiloxKeys& kp,
+                                             const float (&sc32)[2], uint64_t seed_cur, uint64_t seed_prev,
                                              float lrg32, int kind, int lane) {
+  constexpr int G = kPuGroupsPerThread;
   float4* tp = reinterpret_cast<float4*>(p.theta + (e0 - p.theta_key0));
   const uint64_t qa = (uint64_t)(e0 >> 2);
-  const bool full = ngroups == 32 * kPuGroupsPerThread;
-  float4 th[kPuGroupsPerThread];
+  const bool full = ngroups == 32 * G;
+  float4 th[G];
+  uint64_t q[G];
 #pragma unroll
-  for (int g = 0; g < kPuGroupsPerThread; ++g) {
+  for (int g = 0; g < G; ++g) {
     const int idx = lane + 32 * g;
+    q[g] = qa + (uint64_t)idx;
     if (full || idx < ngroups) th[g] = tp[idx];
   }
+  if (pending) {
+    u32x4 r[G];
+    philox4x32_10_xn<G>(q, seed_prev, r);
 #pragma unroll
-  for (int g = 0; g < kPuGroupsPerThread; ++g) {
+    for (int g = 0; g < G; ++g) {
+      const int idx = lane + 32 * g;
+      const f32x4 zp = normals_from_bits(r[g]);
+      th[g].x = fmaf(-lrg32, zp.x, th[g].x); th[g].y = fmaf(-lrg32, zp.y, th[g].y);
+      th[g].z = fmaf(-lrg32, zp.z, th[g].z); th[g].w = fmaf(-lrg32, zp.w, th[g].w);
+      if (full || idx < ngroups) tp[idx] = th[g];
+    }
+  }
+  if (!want_sh) return;
+  u32x4 r[G];
+  if (need_z) philox4x32_10_xn<G>(q, seed_cur, r);
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
     const int idx = lane + 32 * g;
     if (!full && idx >= ngroups) continue;
-    const uint64_t q = qa + (uint64_t)idx;
-    float4 t = th[g];
-    if (pending) {
-      const f32x4 zp = philox_normal4_k(kp, q);
-      t.x = fmaf(-lrg32, zp.x, t.x); t.y = fmaf(-lrg32, zp.y, t.y);
-      t.z = fmaf(-lrg32, zp.z, t.z); t.w = fmaf(-lrg32, zp.w, t.w);
-      tp[idx] = t;
-    }
-    if (!want_sh) continue;
     f32x4 z = {0.f, 0.f, 0.f, 0.f};
-    if (need_z) z = philox_normal4_k(kc, q);
+    if (need_z) z = normals_from_bits(r[g]);
+    const float4 t = th[g];
 #pragma unroll
     for (int d = 0; d < 2; ++d) {
       if (!sh[d]) continue;
@@ -155,7 +166,7 @@ __device__ __forceinline__ void pu_tile_fast(const PuParams& p, int64_t e0, int 
 // Philox/Box-Muller math and stores of the others.  Each lane issues all of
 // its theta loads (float4, coalesced 512 B per warp per group) before any math.
 template <int ZMODE>
-__global__ void __launch_bounds__(kPuThreads, 6) perturb_update_kernel(const PuParams p) {
+__global__ void __launch_bounds__(kPuThreads, 4) perturb_update_kernel(const PuParams p) {
   extern __shared__ int64_t s_prefix[];
   const bool prefix_in_smem = p.n_segs + 1 <= kPuMaxSmemSegs;
   if (prefix_in_smem)
@@ -172,7 +183,6 @@ __global__ void __launch_bounds__(kPuThreads, 6) perturb_update_kernel(const PuP
   const bool theta_vec = ((p.theta_key0 & 3) == 0) && ((reinterpret_cast<uintptr_t>(p.theta) & 15) == 0);
   constexpr int G = kPuGroupsPerThread + 1;
   const int lane = threadIdx.x & 31;
-  const PhiloxKeys kc = philox_keys(seed_cur), kp = philox_keys(seed_prev);
   const int64_t warp0 = (blockIdx.x * (int64_t)kPuThreads + threadIdx.x) >> 5;
   const int64_t n_warps = ((int64_t)gridDim.x * kPuThreads) >> 5;
 
@@ -207,8 +217,8 @@ __global__ void __launch_bounds__(kPuThreads, 6) perturb_update_kernel(const PuP
     const bool want_sh = s.kind != ZO_SHADOW_NONE;
     const int64_t qa = e0 >> 2, qb = (e1 + 3) >> 2;
     if (ZMODE == ZO_Z_PHILOX && theta_vec && ((e0 | e1 | (e0 + drow)) & 3) == 0) {
-      pu_tile_fast(p, e0, (int)((e1 - e0) >> 2), e0 + drow, pending, want_sh, need_z, sh, sc32, kc, kp, lrg32,
-                   s.kind, lane);
+      pu_tile_fast(p, e0, (int)((e1 - e0) >> 2), e0 + drow, pending, want_sh, need_z, sh, sc32, seed_cur,
+                   seed_prev, lrg32, s.kind, lane);
       continue;
     }
 
@@ -240,7 +250,7 @@ __global__ void __launch_bounds__(kPuThreads, 6) perturb_update_kernel(const PuP
 
 int perturb_update_launch(const PuParams& p, int zmode, cudaStream_t stream) {
   if (p.n_tiles <= 0) return ZO_OK;
-  const int64_t want = (int64_t)num_sms() * 6;   // 6 x 128 threads per SM when the SM is free
+  const int64_t want = (int64_t)num_sms() * 8;   // 8 x 128 threads per SM
   const int grid = (int)(p.n_tiles < want ? p.n_tiles : want);
   const size_t smem = p.n_segs + 1 <= kPuMaxSmemSegs ? (size_t)(p.n_segs + 1) * sizeof(int64_t) : 0;
   if (zmode == ZO_Z_PHILOX) perturb_update_kernel<ZO_Z_PHILOX><<<grid, kPuThreads, smem, stream>>>(p);

@@ -114,6 +114,13 @@ class ShadowPlan:
         self.v_elems = self.v_elems + 4
 
 
+def block_extent(plan: ShadowPlan, bid: int):
+    """(w_lo, w_hi, v_lo, v_hi): the contiguous shadow ranges of one block."""
+    ws = [(o, o + r * ld) for (b, o, r, c, ld) in plan.views[bid].values() if b == "w"]
+    vs = [(o, o + c) for (b, o, r, c, ld) in plan.views[bid].values() if b == "v"]
+    return (min(a for a, _ in ws), max(b for _, b in ws), min(a for a, _ in vs), max(b for _, b in vs))
+
+
 class SegTable:
     """Device copy of a segment list + its tile prefix."""
 
@@ -225,6 +232,9 @@ class DeviceStore:
         bl = self.layouts[bid]
         return self.theta[bl.key0:bl.key0 + bl.elem_count]
 
+    def theta_ptr(self, key: int) -> int:
+        return _ptr(self.theta) + 4 * key
+
     def wview(self, s: int, bid: int, name: str):
         buf, off, rows, cols, ld = self.plan.views[bid][name]
         assert buf == "w"
@@ -270,29 +280,33 @@ class DeviceStore:
         return [(fn, args)]
 
     def forward_calls(self, s: int, ws: Workspace, scale: float, zmode=L.ZO_Z_PHILOX, z_cur=None, stream=None,
-                      blocks=None, head_mode="ce", logits=None, loss_out=None):
+                      blocks=None, head_mode="ce", logits=None, loss_out=None, slots=None, scal=None):
         """Launch plan of one directional forward through blocks [0..N+1]
-        (embedding -> N decoder blocks -> LN_f + LM head + CE)."""
+        (embedding -> N decoder blocks -> LN_f + LM head + CE).  ``slots``
+        maps block ids to objects with the same wview / vview / theta_ptr
+        interface when those blocks live outside this store (offload)."""
         cfg, lib = self.config, L.lib()
         d, H, hd, V = cfg.d_model, cfg.n_heads, cfg.head_dim, cfg.vocab_size
         M, B, T = ws.M, ws.batch, ws.seq
         st = L.stream_ptr(stream)
         calls = []
         blocks = range(len(self.layouts)) if blocks is None else blocks
+        scal_p = _ptr(scal) if scal is not None else _ptr(self.scal)
         for bid in blocks:
             bl = self.layouts[bid]
+            src = (slots or {}).get(bid, self)
             if bl.kind == EMBEDDING:
                 calls.append((lib.zo_embed_fwd, (
-                    _ptr(self.theta) + 4 * bl.key("tok_emb"), bl.key("tok_emb"),
-                    _ptr(self.theta) + 4 * bl.key("pos_emb"), bl.key("pos_emb"),
-                    _ptr(ws.ids), B, T, d, V, float(scale), _ptr(self.scal), zmode, _ptr(z_cur), 0,
+                    src.theta_ptr(bl.key("tok_emb")), bl.key("tok_emb"),
+                    src.theta_ptr(bl.key("pos_emb")), bl.key("pos_emb"),
+                    _ptr(ws.ids), B, T, d, V, float(scale), scal_p, zmode, _ptr(z_cur), 0,
                     _ptr(ws.x), ws.x.stride(0), _ptr(ws.err), st)))
             elif bl.kind == TRANSFORMER:
-                v = lambda n: _ptr(self.vview(s, bid, n))  # noqa: E731
-                wq, _, _ = self.wview(s, bid, "qkv")
-                wo, _, _ = self.wview(s, bid, "wo")
-                w1, _, _ = self.wview(s, bid, "w1")
-                w2, _, _ = self.wview(s, bid, "w2")
+                v = lambda n: _ptr(src.vview(s, bid, n))  # noqa: E731
+                wq, _, _ = src.wview(s, bid, "qkv")
+                wo, _, _ = src.wview(s, bid, "wo")
+                w1, _, _ = src.wview(s, bid, "w1")
+                w2, _, _ = src.wview(s, bid, "w2")
                 ldx, ldh = ws.x.stride(0), ws.h.stride(0)
                 calls += [
                     (lib.zo_layernorm_fwd, (_ptr(ws.x), ldx, v("ln1_g"), v("ln1_b"), M, d, _ptr(ws.h), ldh, st)),
@@ -310,11 +324,11 @@ class DeviceStore:
                                         L.ZO_EPI_BIAS_RESID_F32, v("b2"), _ptr(ws.x), ldx, 0, 0, 0, 0, st)),
                 ]
             else:
-                wout, _, _ = self.wview(s, bid, "w_out")
-                calls.append((lib.zo_layernorm_fwd, (_ptr(ws.x), ws.x.stride(0), _ptr(self.vview(s, bid, "lnf_g")),
-                                                     _ptr(self.vview(s, bid, "lnf_b")), M, d, _ptr(ws.h),
+                wout, _, _ = src.wview(s, bid, "w_out")
+                calls.append((lib.zo_layernorm_fwd, (_ptr(ws.x), ws.x.stride(0), _ptr(src.vview(s, bid, "lnf_g")),
+                                                     _ptr(src.vview(s, bid, "lnf_b")), M, d, _ptr(ws.h),
                                                      ws.h.stride(0), st)))
-                bout = _ptr(self.vview(s, bid, "b_out"))
+                bout = _ptr(src.vview(s, bid, "b_out"))
                 if head_mode == "ce":
                     calls.append((lib.zo_gemm_bf16, (_ptr(ws.h), ws.h.stride(0), _ptr(wout), wout.stride(0), M, V, d,
                                                      L.ZO_EPI_CE, bout, 0, 0, _ptr(ws.tgt), _ptr(ws.ce_part),

@@ -1,0 +1,544 @@
+"""Block-streaming ZO runtime with CPU parameter offload (mirror of
+src/zosim/scheduler.py:201-423, the ZO2 schedule of Alg. 3).
+
+The fp32 master lives in pinned host memory (HostStore).  The embedding and
+the LM head stay device-resident (scheduler.py:231-239); transformer blocks
+stream through ``n_slots`` device slots.  Three real CUDA streams replace the
+reference's simulated U / C / O queues (scheduler.py:131-198):
+
+  U(i)  upload stream    H2D copy of block i's fp32 master into a free slot
+                         (with N ranks: each rank copies its 1/N slice over its
+                         own PCIe link, then an all-gather over NVLink fills the
+                         rest -- comm.py:314-328)
+  C(i)  compute stream   fused update_{j-1} + perturb_j pass on the slot, then
+                         both directional forwards of block i
+  O(i)  offload stream   D2H of the updated master (with N ranks: own slice
+                         only -- comm.py:331-342)
+
+Event edges reproduce the reference's op graph (scheduler.py:285-322): C(i)
+waits U(i) and follows C(i-1) on its stream; O(i) waits C(i); U(i+n_slots)
+waits O(i) (slot reuse), so in steady state O(i-1) / C(i) / U(i+1) overlap.
+The update of iteration j is applied to each block on the device right before
+it is perturbed in iteration j+1 (the host master lags one update,
+test_offload.py:130-150); ``flush`` applies the last one.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import time
+
+import numpy as np
+import torch
+
+from . import _lib as L
+from .engine import MINUS, PLUS, SegTable, ShadowPlan, Workspace, block_extent
+from .errors import ConfigurationError, ConsistencyError, ProtocolError
+from .model import EMBEDDING, HEAD, TRANSFORMER, Batch, ModelConfig, init_block_host, model_layout
+from .rng import RngStateManager
+from .zo import ZoHyper, ZoStep, _u64_as_i64
+
+UPLOAD, COMPUTE, OFFLOAD = "upload", "compute", "offload"
+
+
+class HostStore:
+    """The model's fp32 master in pinned host memory, in key order
+    (the reference's ParamStore, model.py:160-200).
+
+    ``shared``: path of a shared-memory file (e.g. under /dev/shm) holding the
+    master, so the one-process-per-GPU ranks of a node all see ONE host master
+    -- each rank uploads / writes back only its own slices (comm.py:314-342).
+    The creator (``init`` != "attach") fills it; other ranks attach with
+    init="attach" after a barrier.  The mapping is page-locked with
+    cudaHostRegister so H2D/D2H run at full PCIe rate."""
+
+    def __init__(self, config: ModelConfig, init_seed: int = 7, init: str = "host", device=None,
+                 shared: str | None = None):
+        config.validate()
+        self.config, self.init_seed = config, init_seed
+        self.layouts = model_layout(config)
+        self.total_params = sum(b.elem_count for b in self.layouts)
+        self.shared = shared
+        if shared is None:
+            self.theta = torch.empty(self.total_params, dtype=torch.float32, pin_memory=True)
+        else:
+            import os
+
+            if init != "attach":
+                with open(shared, "wb") as f:
+                    f.truncate(self.total_params * 4)
+            self.theta = torch.from_file(shared, shared=True, size=self.total_params, dtype=torch.float32)
+            rc = torch.cuda.cudart().cudaHostRegister(self.theta.data_ptr(), self.total_params * 4, 0)
+            self._registered = int(rc) == 0
+            _ = os
+        if init == "attach":
+            return
+        if init == "host":
+            for bl in self.layouts:
+                self.block_buf(bl.block_id).copy_(torch.from_numpy(init_block_host(config, bl, init_seed)))
+        elif init == "philox":
+            from .engine import DeviceStore  # noqa: F401  (library / device checks)
+
+            dev = torch.device(device or f"cuda:{torch.cuda.current_device()}")
+            seed = (0x1A2B3C4D << 32) ^ int(init_seed)
+            chunk = 1 << 26
+            for bl in self.layouts:
+                for name in bl.names:
+                    k, n = bl.key(name), bl.size(name)
+                    dst = self.theta[k:k + n]
+                    if name.endswith("_g"):
+                        dst.fill_(1.0)
+                    elif name.startswith("b") or name.endswith("_b"):
+                        dst.zero_()
+                    else:
+                        for o in range(0, n, chunk):
+                            m = min(chunk, n - o)
+                            z = torch.empty(m, dtype=torch.float32, device=dev)
+                            L.call("zo_philox_normals", seed, k + o, m, z.data_ptr(), L.stream_ptr())
+                            dst[o:o + m].copy_(z.mul_(0.02).cpu())
+        elif init != "none":
+            raise ConfigurationError(f"unknown init {init!r}")
+
+    def block_buf(self, bid: int) -> torch.Tensor:
+        bl = self.layouts[bid]
+        return self.theta[bl.key0:bl.key0 + bl.elem_count]
+
+    def close(self):
+        if self.shared is not None and getattr(self, "_registered", False):
+            torch.cuda.cudart().cudaHostUnregister(self.theta.data_ptr())
+            self._registered = False
+
+    def checksum(self) -> str:
+        h = hashlib.sha256()
+        for bl in self.layouts:
+            h.update(self.block_buf(bl.block_id).numpy().tobytes())
+        return h.hexdigest()
+
+
+class BlockSlot:
+    """Device buffers for one block: fp32 master copy + per-direction shadows,
+    exposing the same wview / vview / theta_ptr interface as DeviceStore so
+    the forward launch plans can read a streamed block."""
+
+    def __init__(self, plan: ShadowPlan, layouts, template_bid: int, dirs, device, pad_to: int = 0,
+                 shadows: bool = True):
+        self.plan, self.layouts = plan, layouts
+        bl = layouts[template_bid]
+        n = max(bl.elem_count, pad_to)
+        self.theta = torch.zeros(n, dtype=torch.float32, device=device)
+        self.wsh, self.vsh = [None, None], [None, None]
+        if shadows and bl.kind != EMBEDDING:
+            wlo, whi, vlo, vhi = block_extent(plan, template_bid)
+            for s in dirs:
+                self.wsh[s] = torch.zeros(whi - wlo, dtype=torch.bfloat16, device=device)
+                self.vsh[s] = torch.zeros(vhi - vlo, dtype=torch.float32, device=device)
+        self.bid = template_bid
+
+    def bind(self, bid: int):
+        self.bid = bid
+        return self
+
+    @property
+    def key0(self) -> int:
+        return self.layouts[self.bid].key0
+
+    def theta_ptr(self, key: int) -> int:
+        return self.theta.data_ptr() + 4 * (key - self.key0)
+
+    def wview(self, s: int, bid: int, name: str):
+        b, off, rows, cols, ld = self.plan.views[bid][name]
+        wlo = block_extent(self.plan, bid)[0]
+        return self.wsh[s][off - wlo:off - wlo + rows * ld].view(rows, ld), rows, cols
+
+    def vview(self, s: int, bid: int, name: str) -> torch.Tensor:
+        b, off, rows, cols, ld = self.plan.views[bid][name]
+        vlo = block_extent(self.plan, bid)[2]
+        return self.vsh[s][off - vlo:off - vlo + cols]
+
+
+def rebased_table(plan: ShadowPlan, bid: int, device) -> SegTable:
+    """The block's perturb segments with shadow offsets relative to its slot."""
+    if plan.views[bid]:
+        wlo, _, vlo, _ = block_extent(plan, bid)
+    else:
+        wlo = vlo = 0
+    segs = []
+    for (src, rows, cols, dst, ld, kind) in plan.segments[bid]:
+        if kind == L.ZO_SHADOW_BF16:
+            dst -= wlo
+        elif kind == L.ZO_SHADOW_F32:
+            dst -= vlo
+        segs.append((src, rows, cols, dst, ld, kind))
+    return SegTable(segs, device)
+
+
+# -----------------------------------------------------------------------------
+# slicing (comm.py:106-119, 314-358)
+# -----------------------------------------------------------------------------
+
+class SliceLayout:
+    """Ceil-width slices, owner i = rank i, last one may be short
+    (comm.py:106-119)."""
+
+    def __init__(self, block_id: int, total: int, n: int):
+        if n < 1:
+            raise ConfigurationError(f"slice count must be >= 1, got {n}")
+        self.block_id, self.total, self.n = block_id, total, n
+        self.width = -(-total // n)
+        self.slices = []
+        off = 0
+        for owner in range(n):
+            length = max(min(self.width, total - off), 0)
+            self.slices.append((owner, off, length))
+            off += length
+
+    @classmethod
+    def build(cls, block_id: int, total: int, n: int) -> "SliceLayout":
+        return cls(block_id, total, n)
+
+
+def apply_thread_aligned_layout(store, n: int) -> dict:
+    """Fix per-block slice boundaries once (comm.py:345-358); changing n later
+    is a ProtocolError."""
+    plan = getattr(store, "slice_plan", None)
+    if plan is not None:
+        if plan["n"] != n:
+            raise ProtocolError(f"slice layout already fixed for n={plan['n']}; changing to n={n} requires "
+                                "re-initialization")
+        return plan
+    store.slice_plan = {"n": n, "layouts": {bl.block_id: SliceLayout(bl.block_id, bl.elem_count, n)
+                                            for bl in store.layouts}}
+    return store.slice_plan
+
+
+def sliced_upload(host_block: torch.Tensor, slot_theta: torch.Tensor, layout: SliceLayout, fabric, rank: int,
+                  stream=None):
+    """Phase 1: this rank's slice host -> device over its PCIe link; phase 2:
+    the peers' slices arrive by an all-gather of the slot (NVLink), never
+    from the host (comm.py:314-328).  slot_theta is padded to n * width."""
+    owner, off, ln = layout.slices[rank]
+    w = layout.width
+    with torch.cuda.stream(stream) if stream is not None else _null():
+        if ln:
+            slot_theta[rank * w:rank * w + ln].copy_(host_block[off:off + ln], non_blocking=True)
+        if layout.n > 1:
+            fabric.all_gather_tensor(slot_theta[:layout.n * w], slot_theta[rank * w:(rank + 1) * w], tag="param")
+
+
+def sliced_offload(slot_theta: torch.Tensor, host_block: torch.Tensor, layout: SliceLayout, rank: int,
+                   stream=None):
+    """Each rank writes back only its owned slice (comm.py:331-342)."""
+    owner, off, ln = layout.slices[rank]
+    with torch.cuda.stream(stream) if stream is not None else _null():
+        if ln:
+            host_block[off:off + ln].copy_(slot_theta[off:off + ln], non_blocking=True)
+
+
+class _null:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        return False
+
+
+def check_slices_identical(fabric, rank: int, slot_theta: torch.Tensor, n: int):
+    """Divergence guard before offload (comm.py:336-340)."""
+    from .ops import hash_u64
+
+    h = int(hash_u64(slot_theta[:n]).item()) & ((1 << 64) - 1)
+    got = list(zip(fabric.all_gather(rank, float(h & 0xFFFFFFFF), tag="checksum"),
+                   fabric.all_gather(rank, float(h >> 32), tag="checksum")))
+    if len(set(got)) != 1:
+        raise ConsistencyError("device replicas diverged; offload would reassemble a corrupt block")
+
+
+# -----------------------------------------------------------------------------
+# the runtime
+# -----------------------------------------------------------------------------
+
+class OffloadedZo:
+    """ZO2 streaming runtime over one GPU (or one rank of a sliced mesh).
+
+    ``mode``: "streams" (U/C/O overlapped on three CUDA streams) or "serial"
+    (everything on one stream; the equivalence oracle, scheduler.py:324-341).
+    With ``fabric`` (world N): sliced H2D + all-gather / own-slice D2H, and
+    the loss exchange of the strategy in ``strategy`` ("mezo" for both
+    directions per rank (ZO-DDP when N > 1), "2d" for one direction per rank).
+    """
+
+    def __init__(self, host: HostStore, hyper: ZoHyper, batch: int, device=None, n_slots: int = 3,
+                 mode: str = "streams", fabric=None, strategy: str = "mezo", trace: bool = False):
+        if mode not in ("streams", "serial"):
+            raise ProtocolError(f"unknown scheduler mode {mode!r}")
+        if n_slots < 2:
+            raise ConfigurationError("need at least 2 block slots")
+        self.host, self.hyper, self.mode, self.trace = host, hyper.validate(), mode, trace
+        cfg = self.config = host.config
+        self.device = torch.device(device or f"cuda:{torch.cuda.current_device()}")
+        L.lib()
+        self.layouts = host.layouts
+        self.plan = ShadowPlan(cfg, self.layouts)
+        self.fabric = fabric
+        self.world = fabric.k if fabric is not None else 1
+        self.rank = fabric.rank if fabric is not None else 0
+        from .strategies import MeshLayout
+        self.mesh = MeshLayout("ddp" if strategy == "mezo" else strategy, self.world, self.rank) \
+            if fabric is not None else None
+        self.dirs = self.mesh.dirs if self.mesh is not None else (PLUS, MINUS)
+        if fabric is not None:
+            apply_thread_aligned_layout(host, self.world)
+        emb, head = self.layouts[0].block_id, self.layouts[-1].block_id
+        self.wids = [bl.block_id for bl in self.layouts if bl.kind == TRANSFORMER]
+        pad = lambda bid: (-(-self.layouts[bid].elem_count // self.world)) * self.world  # noqa: E731
+        self.persistent = {emb: BlockSlot(self.plan, self.layouts, emb, self.dirs, self.device, pad(emb)),
+                           head: BlockSlot(self.plan, self.layouts, head, self.dirs, self.device, pad(head))}
+        tpl = self.wids[0] if self.wids else head
+        self.slots = [BlockSlot(self.plan, self.layouts, tpl, self.dirs, self.device, pad(tpl))
+                      for _ in range(n_slots)]
+        self.tables = {bl.block_id: rebased_table(self.plan, bl.block_id, self.device) for bl in self.layouts}
+        for bid, slot in self.persistent.items():      # embedding + head stay on the device
+            self._upload(bid, slot, None)
+        torch.cuda.synchronize()
+        self.scal = torch.zeros(4, dtype=torch.int64, device=self.device)
+        self.record = torch.zeros(3, dtype=torch.float64, device=self.device)
+        self.local = torch.zeros(2, dtype=torch.float64, device=self.device)
+        self.gathered = torch.zeros(2 * self.world, dtype=torch.float64, device=self.device)
+        self.ws = {s: Workspace(cfg, batch, cfg.seq_len, self.device) for s in self.dirs}
+        self.streams = {COMPUTE: torch.cuda.current_stream(self.device)}
+        if mode == "streams":
+            self.streams[UPLOAD] = torch.cuda.Stream(self.device)
+            self.streams[OFFLOAD] = torch.cuda.Stream(self.device)
+        else:
+            self.streams[UPLOAD] = self.streams[OFFLOAD] = self.streams[COMPUTE]
+        self.iteration, self.g_prev, self.last_seed, self._pending = 0, 0.0, None, False
+        self.timelines = []
+        self.uploaded_params = self.offloaded_params = 0
+
+    # -- byte movement --------------------------------------------------------------
+    def _upload(self, bid, slot, stream):
+        slot.bind(bid)
+        hb = self.host.block_buf(bid)
+        if self.fabric is None:
+            with torch.cuda.stream(stream) if stream is not None else _null():
+                slot.theta[:hb.numel()].copy_(hb, non_blocking=True)
+        else:
+            sliced_upload(hb, slot.theta, self.host.slice_plan["layouts"][bid], self.fabric, self.rank, stream)
+
+    def _offload(self, bid, slot, stream):
+        hb = self.host.block_buf(bid)
+        if self.fabric is None:
+            with torch.cuda.stream(stream):
+                hb.copy_(slot.theta[:hb.numel()], non_blocking=True)
+        else:
+            sliced_offload(slot.theta, hb, self.host.slice_plan["layouts"][bid], self.rank, stream)
+
+    # -- compute --------------------------------------------------------------------
+    def _perturb(self, bid, slot, flags, stream):
+        t, eps = self.tables[bid], self.hyper.epsilon
+        sa = PLUS if PLUS in self.dirs else None
+        sb = MINUS if MINUS in self.dirs else None
+        wa = slot.wsh[PLUS].data_ptr() if sa is not None and slot.wsh[PLUS] is not None else 0
+        va = slot.vsh[PLUS].data_ptr() if sa is not None and slot.vsh[PLUS] is not None else 0
+        wb = slot.wsh[MINUS].data_ptr() if sb is not None and slot.wsh[MINUS] is not None else 0
+        vb = slot.vsh[MINUS].data_ptr() if sb is not None and slot.vsh[MINUS] is not None else 0
+        L.check(L.lib().zo_perturb_update(slot.theta.data_ptr(), slot.key0, t.segs.data_ptr(), t.prefix.data_ptr(),
+                                          t.n_segs, t.n_tiles, wa, va, wb, vb, +eps, -eps, flags,
+                                          self.scal.data_ptr(), L.ZO_Z_PHILOX, 0, 0, 0, int(stream.cuda_stream)))
+
+    def _shadow_flags(self):
+        f = 0
+        if PLUS in self.dirs:
+            f |= L.ZO_PU_SHADOW_A
+        if MINUS in self.dirs:
+            f |= L.ZO_PU_SHADOW_B
+        return f
+
+    def _compute(self, bid, slot, stream):
+        """C(i): fused update+perturb of the block, then each direction's forward."""
+        self._perturb(bid, slot, L.ZO_PU_UPDATE | self._shadow_flags(), stream)
+        eps = self.hyper.epsilon
+        for s in self.dirs:
+            loss_out = self.local.data_ptr() + 8 * s
+            calls = _store_view(self).forward_calls(s, self.ws[s], +eps if s == PLUS else -eps,
+                                                    stream=stream, blocks=[bid], slots={bid: slot},
+                                                    scal=self.scal, loss_out=loss_out)
+            for fn, args in calls:
+                L.check(fn(*args))
+
+    def _finalize(self, stream):
+        eps, lr = self.hyper.epsilon, self.hyper.lr
+        st = int(stream.cuda_stream)
+        if self.fabric is None:
+            L.check(L.lib().zo_grad_finalize(self.local.data_ptr(), self.local.data_ptr() + 8, float(eps),
+                                             float(lr), self.scal.data_ptr(), self.record.data_ptr(), st))
+        else:
+            with torch.cuda.stream(stream):
+                self.fabric.all_gather_tensor(self.gathered, self.local, tag="loss")
+            sp, op, sm, om = self.mesh.layout
+            L.check(L.lib().zo_grad_finalize_groups(self.gathered.data_ptr(), self.mesh.n_groups, sp, op, sm, om,
+                                                    self.mesh.group, float(eps), float(lr), self.scal.data_ptr(),
+                                                    self.record.data_ptr(), st))
+
+    # -- one iteration (scheduler.py:243-283) -----------------------------------------
+    def step(self, batch: Batch, seed: int) -> ZoStep:
+        self.iteration += 1
+        batch.validate(self.config)
+        B, T = batch.token_ids.shape
+        for ws in self.ws.values():
+            if ws.batch != B or ws.seq != T:
+                raise ConfigurationError("batch shape differs from the runtime's workspace")
+            _load(ws, batch)
+        self.scal[0:1].fill_(_u64_as_i64(seed))
+        self.scal[3:4].fill_(1 if self._pending else 0)
+        cs, us, os_ = self.streams[COMPUTE], self.streams[UPLOAD], self.streams[OFFLOAD]
+        ev = {}
+        rec = []
+
+        def mark(kind, bid, stream):
+            e = torch.cuda.Event(enable_timing=self.trace)
+            e.record(stream)
+            ev[(kind, bid)] = e
+            return e
+
+        t0 = torch.cuda.Event(enable_timing=self.trace)
+        t0.record(cs)
+        start = mark("start", -1, cs)
+        us.wait_event(start)
+        os_.wait_event(start)
+        emb, head = self.layouts[0].block_id, self.layouts[-1].block_id
+        n = len(self.slots)
+        if self.wids:
+            s0 = self.slots[0]
+            e0 = torch.cuda.Event(enable_timing=self.trace)
+            e0.record(us)
+            self._upload(self.wids[0], s0, us)
+            mark(UPLOAD, self.wids[0], us)
+            rec.append((UPLOAD, self.wids[0], e0))
+        e_c = torch.cuda.Event(enable_timing=self.trace)
+        e_c.record(cs)
+        self._compute(emb, self.persistent[emb], cs)
+        mark(COMPUTE, emb, cs)
+        rec.append((COMPUTE, emb, e_c))
+        for idx, i in enumerate(self.wids):
+            slot = self.slots[idx % n]
+            if idx + 1 < len(self.wids):                       # U(i+1) into the next slot once it is free
+                nxt, nslot = self.wids[idx + 1], self.slots[(idx + 1) % n]
+                if idx + 1 - n >= 0:
+                    us.wait_event(ev[(OFFLOAD, self.wids[idx + 1 - n])])
+                eu = torch.cuda.Event(enable_timing=self.trace)
+                eu.record(us)
+                self._upload(nxt, nslot, us)
+                mark(UPLOAD, nxt, us)
+                rec.append((UPLOAD, nxt, eu))
+            cs.wait_event(ev[(UPLOAD, i)])                        # C(i) after U(i) (and C(i-1): same stream)
+            ec = torch.cuda.Event(enable_timing=self.trace)
+            ec.record(cs)
+            self._compute(i, slot, cs)
+            mark(COMPUTE, i, cs)
+            rec.append((COMPUTE, i, ec))
+            os_.wait_event(ev[(COMPUTE, i)])                       # O(i) after C(i)
+            eo = torch.cuda.Event(enable_timing=self.trace)
+            eo.record(os_)
+            self._offload(i, slot, os_)
+            mark(OFFLOAD, i, os_)
+            rec.append((OFFLOAD, i, eo))
+        eh = torch.cuda.Event(enable_timing=self.trace)
+        eh.record(cs)
+        self._compute(head, self.persistent[head], cs)
+        self._finalize(cs)
+        mark(COMPUTE, head, cs)
+        rec.append((COMPUTE, head, eh))
+        cs.wait_event(mark("tail", -1, os_))
+        r = self.record.cpu().numpy()
+        for ws in self.ws.values():
+            e = int(ws.err.item())
+            if e:
+                ws.err.zero_()
+                from .errors import DimensionError, NumericError
+                raise DimensionError("token id out of embedding range") if e & 4 else NumericError("non-finite logits")
+        if self.trace:
+            self.timelines.append([{"op": k, "block_id": b, "stream": k, "start": t0.elapsed_time(e),
+                                    "end": t0.elapsed_time(ev[(k, b)])} for k, b, e in rec])
+        self.uploaded_params += sum(self.layouts[i].elem_count for i in self.wids)
+        self.offloaded_params += sum(self.layouts[i].elem_count for i in self.wids)
+        st = ZoStep(self.iteration, seed, float(r[0]), float(r[1]), float(r[2]))
+        self.g_prev, self.last_seed, self._pending = st.g, seed, True
+        return st
+
+    # -- end of run (scheduler.py:393-415) ------------------------------------------------
+    def flush(self) -> None:
+        """Apply the last iteration's deferred update to every block and sync
+        the device-resident blocks back to the host."""
+        if not self._pending:
+            raise ProtocolError("flush with no pending update (double flush?)")
+        cs = self.streams[COMPUTE]
+        self.scal[3:4].fill_(1)
+        for i in self.wids:
+            slot = self.slots[0]
+            self._upload(i, slot, cs)
+            self._perturb(i, slot, L.ZO_PU_UPDATE, cs)
+            self._offload(i, slot, cs)
+            cs.synchronize()
+        for bid, slot in self.persistent.items():
+            self._perturb(bid, slot, L.ZO_PU_UPDATE, cs)
+        self.scal[3:4].fill_(0)
+        self.sync_host()
+        self._pending = False
+
+    def sync_host(self) -> None:
+        """Copy the persistent device blocks back to the host master."""
+        cs = self.streams[COMPUTE]
+        for bid, slot in self.persistent.items():
+            hb = self.host.block_buf(bid)
+            with torch.cuda.stream(cs):
+                hb.copy_(slot.theta[:hb.numel()], non_blocking=True)
+        cs.synchronize()
+
+    @property
+    def last_timeline(self):
+        return self.timelines[-1] if self.timelines else []
+
+    def makespan(self) -> float:
+        tl = self.last_timeline
+        return max(e["end"] for e in tl) if tl else float("nan")
+
+
+def _load(ws: Workspace, batch: Batch):
+    ids = np.asarray(batch.token_ids).reshape(-1).astype(np.int32)
+    tg = np.asarray(batch.targets).reshape(-1).astype(np.int32)
+    ws.ids.copy_(torch.from_numpy(ids))
+    ws.tgt.copy_(torch.from_numpy(tg))
+
+
+class _StoreView:
+    """Adapter giving OffloadedZo the DeviceStore.forward_calls builder
+    without allocating a resident master."""
+
+    def __init__(self, rt: OffloadedZo):
+        from .engine import DeviceStore
+
+        self.config, self.layouts, self.plan = rt.config, rt.layouts, rt.plan
+        self.scal = rt.scal
+        self._fc = DeviceStore.forward_calls.__get__(self)
+
+    def forward_calls(self, *a, **k):
+        return self._fc(*a, **k)
+
+
+def _store_view(rt: OffloadedZo) -> _StoreView:
+    if not hasattr(rt, "_sv"):
+        rt._sv = _StoreView(rt)
+    return rt._sv
+
+
+def activation_nbytes(config: ModelConfig, batch_size: int) -> int:
+    """Device bytes of one directional activation tensor (scheduler.py:435-438), fp32 residual."""
+    return batch_size * config.seq_len * config.d_model * 4
+
+
+def time_step(rt: OffloadedZo, batch: Batch, seed: int) -> float:
+    torch.cuda.synchronize()
+    t = time.perf_counter()
+    rt.step(batch, seed)
+    return time.perf_counter() - t

@@ -157,6 +157,7 @@ class StreamingZo:
         self.hyper = hyper.validate()
         self.mgr = mgr or RngStateManager()
         self.overlap = overlap and not self.mgr.oracle
+        self.dual_stream = True
         self.iteration = 0
         self.g_prev = 0.0
         self.last_seed = None
@@ -172,8 +173,18 @@ class StreamingZo:
         zmode = L.ZO_Z_ORACLE if self.mgr.oracle else L.ZO_Z_PHILOX
         flags = (L.ZO_PU_UPDATE if update else 0) | L.ZO_PU_SHADOW_A | L.ZO_PU_SHADOW_B
         calls = s.perturb_call(s.model_table, flags, +eps, -eps, zmode=zmode, z_cur=zc, z_prev=zp)
-        calls += s.forward_calls(PLUS, wsp, +eps, zmode=zmode, z_cur=zc)
-        calls += s.forward_calls(MINUS, wsn, -eps, zmode=zmode, z_cur=zc)
+        if self.dual_stream:
+            # the two directional forwards are independent: run -eps on a side
+            # stream so each fills the other's partial GEMM waves
+            main, side = torch.cuda.current_stream(), _side_stream(s)
+            ev = _block_events(s, len(s.layouts))
+            calls.append((_record_and_wait, (ev[0], main, side)))
+            calls += s.forward_calls(PLUS, wsp, +eps, zmode=zmode, z_cur=zc)
+            calls += s.forward_calls(MINUS, wsn, -eps, zmode=zmode, z_cur=zc, stream=side)
+            calls.append((_record_and_wait, (ev[1], side, main)))
+        else:
+            calls += s.forward_calls(PLUS, wsp, +eps, zmode=zmode, z_cur=zc)
+            calls += s.forward_calls(MINUS, wsn, -eps, zmode=zmode, z_cur=zc)
         calls += s.grad_call(wsp, wsn, eps, self.hyper.lr)
         return calls
 

@@ -116,3 +116,72 @@ def run(fn, world, *args, timeout=240):
             if p.is_alive():
                 p.kill()
     return [out[r] for r in range(world)]
+
+
+DEEP = (64, 32, 4, 5, 16)
+
+
+def sliced_offload_worker(rank, world, port, strategy, steps, q):
+    """OffloadedZo with sliced H2D + all-gather / own-slice D2H (gloo, one GPU)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2507_03211_b200.fabric import TorchFabric
+    from paper_2507_03211_b200.model import ModelConfig, make_batch
+    from paper_2507_03211_b200.rng import iteration_seeds
+    from paper_2507_03211_b200.scheduler import HostStore, OffloadedZo
+    from paper_2507_03211_b200.zo import ZoHyper
+
+    torch.cuda.set_device(0)
+    init(rank, world, port)
+    fab = TorchFabric()
+    cfg = ModelConfig(*DEEP, "f32")
+    path = f"/dev/shm/zo_b200_test_{port}"
+    if rank == 0:
+        host = HostStore(cfg, 7, shared=path)
+    fab.barrier()
+    if rank != 0:
+        host = HostStore(cfg, 7, init="attach", shared=path)
+    rt = OffloadedZo(host, ZoHyper(1e-3, 1e-2), batch=4 // world, fabric=fab, strategy=strategy)
+    recs = []
+    for j, s in enumerate(iteration_seeds(9, steps), 1):
+        r = rt.step(make_batch(cfg, 4, 40 + j).shard(world, rank), s)
+        recs.append((r.loss_pos, r.loss_neg, r.g))
+    rt.flush()
+    torch.cuda.synchronize()
+    fab.barrier()                     # every rank has written its slices back
+    theta = host.theta.numpy().copy()
+    host.close()
+    fab.barrier()
+    if rank == 0:
+        os.unlink(path)
+    dist.destroy_process_group()
+    q.put((rank, recs, theta))
+
+
+def gpu_strategy_worker_theta(rank, world, port, strategy, steps, q):
+    """Resident eager strategy step on the DEEP config (reference for the
+    sliced offload test)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2507_03211_b200.engine import DeviceStore
+    from paper_2507_03211_b200.fabric import TorchFabric
+    from paper_2507_03211_b200.model import ModelConfig, make_batch
+    from paper_2507_03211_b200.rng import iteration_seeds
+    from paper_2507_03211_b200.strategies import ddp_step
+    from paper_2507_03211_b200.zo import ZoHyper
+
+    torch.cuda.set_device(0)
+    init(rank, world, port)
+    fab = TorchFabric()
+    cfg = ModelConfig(*DEEP, "f32")
+    store = DeviceStore(cfg, 7)
+    recs = []
+    for j, s in enumerate(iteration_seeds(9, steps), 1):
+        r = ddp_step(fab, rank, store, make_batch(cfg, 4, 40 + j).shard(world, rank), ZoHyper(1e-3, 1e-2),
+                     s if rank == 0 else None, iteration=j)
+        recs.append((r.loss_pos, r.loss_neg, r.g))
+    theta = store.theta.cpu().numpy()
+    dist.destroy_process_group()
+    q.put((rank, recs, theta))

@@ -1,0 +1,32 @@
+"""CPU checks of the offload host logic: slice layouts vs the reference
+fixtures (comm.py:106-119) and the fixed-at-init layout protocol."""
+
+import pytest
+
+from paper_2507_03211_b200.errors import ConfigurationError, ProtocolError
+from paper_2507_03211_b200.scheduler import SliceLayout, apply_thread_aligned_layout
+
+
+def test_slice_layouts_match_reference(golden):
+    for total, n, owner, off, ln in golden["comm/layouts"]:
+        lay = SliceLayout.build(0, int(total), int(n))
+        assert lay.slices[int(owner)] == (owner, off, ln)
+        assert sum(s[2] for s in lay.slices) == total
+
+
+def test_slice_layout_rejects_zero():
+    with pytest.raises(ConfigurationError):
+        SliceLayout.build(0, 10, 0)
+
+
+def test_layout_fixed_at_init():
+    class S:
+        from paper_2507_03211_b200.model import ModelConfig, model_layout
+        layouts = model_layout(ModelConfig(16, 16, 2, 2, 8, "f32"))
+
+    s = S()
+    p = apply_thread_aligned_layout(s, 4)
+    assert apply_thread_aligned_layout(s, 4) is p
+    assert p["layouts"][1].width == -(-s.layouts[1].elem_count // 4)
+    with pytest.raises(ProtocolError):
+        apply_thread_aligned_layout(s, 2)
