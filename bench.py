@@ -339,8 +339,8 @@ def ours(args, rank, world, local_rank):
             runner2.step(batches[j], seeds[j])
         torch.cuda.synchronize()
         e2e_ms = (time.perf_counter() - t0) * 1e3 / args.steps
-        h2d = 2 * 2 * M * 4          # ids + targets (int32) into both directional workspaces
-        d2h = 3 * 8 + 2 * 4          # ZoStep record (f64 x3) + error flags
+        h2d = 2 * M * 4              # ids + targets (int32), shared by both directional workspaces
+        d2h = 3 * 8 + 2 * 4          # ZoStep record (f64 x3) + 2 error flags (int32)
     else:
         e2e_ms, h2d, d2h = runner.e2e(batches, seeds, args.warmup, args.steps)
 

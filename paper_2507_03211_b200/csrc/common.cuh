@@ -80,10 +80,14 @@ __device__ __forceinline__ void box_muller(uint32_t a, uint32_t b, float& z0, fl
   //   u1 = 2 - [1,2)  in (0, 1];   ang = pi * [2,4) - 3 pi  in [-pi, pi)
   const float u1 = 2.0f - __uint_as_float(0x3F800000u | (a >> 9));
   const float ang = fmaf(__uint_as_float(0x40000000u | (b >> 9)), 3.14159265358979f, -9.42477796076938f);
-  const float t = -1.3862943611198906f * __log2f(u1);                             // -2 ln u > 0
-  const float r = t > 0.f ? t * rsqrtf(t) : 0.f;   // sqrt via MUFU.RSQ; u1 can round to 1.0 (t = 0)
-  float s, c;
-  __sincosf(ang, &s, &c);
+  // single MUFU ops, flush-to-zero (u1 >= 2^-23 and |ang| <= pi: no denormals)
+  float lg, rs, s, c;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(lg) : "f"(u1));
+  const float t = -1.3862943611198906f * lg;                                      // -2 ln u >= 0
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(rs) : "f"(t));
+  const float r = t > 0.f ? t * rs : 0.f;          // u1 == 1 gives t = 0 (rsqrt = inf)
+  asm("sin.approx.ftz.f32 %0, %1;" : "=f"(s) : "f"(ang));
+  asm("cos.approx.ftz.f32 %0, %1;" : "=f"(c) : "f"(ang));
   z0 = r * c;
   z1 = r * s;
 }

@@ -100,62 +100,75 @@ __device__ __forceinline__ void pu_group(const PuParams& p, const ZoSegment& s, 
 }
 
 
-// Fast tile: Philox direction, every group full and 16-B aligned (all real
-// model tensors).  Straight-line code, 32-bit in-tile indexing; the lane's 4
-// groups run their Philox streams in lockstep (philox4x32_10_xn).
-__device__ __forceinline__ void pu_tile_fast(const PuParams& p, int64_t e0, int ngroups, int64_t dbase,
-                                             bool pending, bool want_sh, bool need_z, const bool (&sh)[2],
-                                             const float (&sc32)[2], uint64_t seed_cur, uint64_t seed_prev,
-                                             float lrg32, int kind, int lane) {
+// Fast tile: Philox direction, every group 16-B aligned (all real model
+// tensors).  Specialised at compile time on (pending update, shadows, bf16) so
+// the hot loop has no runtime-flag branches; 32-bit lane offsets from per-tile
+// base pointers; the lane's groups run their Philox streams in lockstep.
+template <bool PEND, bool BF16>
+__device__ __forceinline__ void pu_tile_fast_t(const PuParams& p, int64_t e0, int ngroups, int64_t dbase,
+                                               bool SA, bool SB, float sa, float sb, uint64_t seed_cur,
+                                               uint64_t seed_prev, float lrg32, int lane) {
   constexpr int G = kPuGroupsPerThread;
-  float4* tp = reinterpret_cast<float4*>(p.theta + (e0 - p.theta_key0));
-  const uint64_t qa = (uint64_t)(e0 >> 2);
+  float4* tp = reinterpret_cast<float4*>(p.theta + (e0 - p.theta_key0)) + lane;
+  const uint64_t qa = (uint64_t)(e0 >> 2) + (uint64_t)lane;
   const bool full = ngroups == 32 * G;
   float4 th[G];
   uint64_t q[G];
 #pragma unroll
   for (int g = 0; g < G; ++g) {
-    const int idx = lane + 32 * g;
-    q[g] = qa + (uint64_t)idx;
-    if (full || idx < ngroups) th[g] = tp[idx];
+    q[g] = qa + (uint64_t)(32 * g);
+    if (full || lane + 32 * g < ngroups) th[g] = tp[32 * g];
   }
-  if (pending) {
+  if constexpr (PEND) {
     u32x4 r[G];
     philox4x32_10_xn<G>(q, seed_prev, r);
 #pragma unroll
     for (int g = 0; g < G; ++g) {
-      const int idx = lane + 32 * g;
       const f32x4 zp = normals_from_bits(r[g]);
       th[g].x = fmaf(-lrg32, zp.x, th[g].x); th[g].y = fmaf(-lrg32, zp.y, th[g].y);
       th[g].z = fmaf(-lrg32, zp.z, th[g].z); th[g].w = fmaf(-lrg32, zp.w, th[g].w);
-      if (full || idx < ngroups) tp[idx] = th[g];
+      if (full || lane + 32 * g < ngroups) tp[32 * g] = th[g];
     }
   }
-  if (!want_sh) return;
-  u32x4 r[G];
-  if (need_z) philox4x32_10_xn<G>(q, seed_cur, r);
+  if (SA || SB) {
+    u32x4 r[G];
+    philox4x32_10_xn<G>(q, seed_cur, r);
 #pragma unroll
-  for (int g = 0; g < G; ++g) {
-    const int idx = lane + 32 * g;
-    if (!full && idx >= ngroups) continue;
-    f32x4 z = {0.f, 0.f, 0.f, 0.f};
-    if (need_z) z = normals_from_bits(r[g]);
-    const float4 t = th[g];
+    for (int g = 0; g < G; ++g) {
+      if (!full && lane + 32 * g >= ngroups) continue;
+      const f32x4 z = normals_from_bits(r[g]);
+      const float4 t = th[g];
 #pragma unroll
-    for (int d = 0; d < 2; ++d) {
-      if (!sh[d]) continue;
-      const float a = fmaf(sc32[d], z.x, t.x), b = fmaf(sc32[d], z.y, t.y);
-      const float c = fmaf(sc32[d], z.z, t.z), e = fmaf(sc32[d], z.w, t.w);
-      if (kind == ZO_SHADOW_BF16) {
-        __nv_bfloat162 lo2 = __floats2bfloat162_rn(a, b), hi2 = __floats2bfloat162_rn(c, e);
-        uint2 pk;
-        pk.x = *reinterpret_cast<uint32_t*>(&lo2);
-        pk.y = *reinterpret_cast<uint32_t*>(&hi2);
-        reinterpret_cast<uint2*>(p.wsh[d] + dbase)[idx] = pk;
-      } else {
-        reinterpret_cast<float4*>(p.vsh[d] + dbase)[idx] = make_float4(a, b, c, e);
+      for (int d = 0; d < 2; ++d) {
+        if ((d == 0 && !SA) || (d == 1 && !SB)) continue;   // warp-uniform
+        const float sc = d == 0 ? sa : sb;
+        const float a = fmaf(sc, z.x, t.x), b = fmaf(sc, z.y, t.y);
+        const float c = fmaf(sc, z.z, t.z), e = fmaf(sc, z.w, t.w);
+        if constexpr (BF16) {
+          __nv_bfloat162 lo2 = __floats2bfloat162_rn(a, b), hi2 = __floats2bfloat162_rn(c, e);
+          uint2 pk;
+          pk.x = *reinterpret_cast<uint32_t*>(&lo2);
+          pk.y = *reinterpret_cast<uint32_t*>(&hi2);
+          (reinterpret_cast<uint2*>(p.wsh[d] + dbase) + lane)[32 * g] = pk;
+        } else {
+          (reinterpret_cast<float4*>(p.vsh[d] + dbase) + lane)[32 * g] = make_float4(a, b, c, e);
+        }
       }
     }
+  }
+}
+
+__device__ __forceinline__ void pu_tile_fast(const PuParams& p, int64_t e0, int ngroups, int64_t dbase,
+                                             bool pending, bool want_sh, const bool (&sh)[2],
+                                             const float (&sc32)[2], uint64_t seed_cur, uint64_t seed_prev,
+                                             float lrg32, int kind, int lane) {
+  const bool sa = want_sh && sh[0], sb = want_sh && sh[1];
+  if (kind == ZO_SHADOW_BF16) {
+    if (pending) pu_tile_fast_t<true, true>(p, e0, ngroups, dbase, sa, sb, sc32[0], sc32[1], seed_cur, seed_prev, lrg32, lane);
+    else pu_tile_fast_t<false, true>(p, e0, ngroups, dbase, sa, sb, sc32[0], sc32[1], seed_cur, seed_prev, lrg32, lane);
+  } else {
+    if (pending) pu_tile_fast_t<true, false>(p, e0, ngroups, dbase, sa, sb, sc32[0], sc32[1], seed_cur, seed_prev, lrg32, lane);
+    else pu_tile_fast_t<false, false>(p, e0, ngroups, dbase, sa, sb, sc32[0], sc32[1], seed_cur, seed_prev, lrg32, lane);
   }
 }
 
@@ -216,9 +229,10 @@ __global__ void __launch_bounds__(kPuThreads, 4) perturb_update_kernel(const PuP
     const int64_t drow = s.dst + row * s.dst_ld - rk;
     const bool want_sh = s.kind != ZO_SHADOW_NONE;
     const int64_t qa = e0 >> 2, qb = (e1 + 3) >> 2;
-    if (ZMODE == ZO_Z_PHILOX && theta_vec && ((e0 | e1 | (e0 + drow)) & 3) == 0) {
-      pu_tile_fast(p, e0, (int)((e1 - e0) >> 2), e0 + drow, pending, want_sh, need_z, sh, sc32, seed_cur,
-                   seed_prev, lrg32, s.kind, lane);
+    const bool any_sh = want_sh && (sh[0] || sh[1]);
+    if (ZMODE == ZO_Z_PHILOX && theta_vec && ((e0 | e1 | (e0 + drow)) & 3) == 0 && (need_z || !any_sh)) {
+      pu_tile_fast(p, e0, (int)((e1 - e0) >> 2), e0 + drow, pending, want_sh, sh, sc32, seed_cur, seed_prev,
+                   lrg32, s.kind, lane);
       continue;
     }
 

@@ -246,9 +246,15 @@ class DeviceStore:
         return self.vsh[s][off:off + cols]
 
     def workspace(self, s: int, batch: int, seq: int) -> Workspace:
+        """Per-direction activations; both directions of a batch shape share
+        the device token-id / target buffers (one H2D per step, not two)."""
         key = (s, batch, seq)
         if key not in self._ws:
-            self._ws[key] = Workspace(self.config, batch, seq, self.device)
+            ws = Workspace(self.config, batch, seq, self.device)
+            other = self._ws.get((1 - s, batch, seq))
+            if other is not None:
+                ws.ids, ws.tgt = other.ids, other.tgt
+            self._ws[key] = ws
         return self._ws[key]
 
     # -- scalar state ----------------------------------------------------------
@@ -361,17 +367,43 @@ class DeviceStore:
             raise DimensionError(f"batch shape {ids.shape} does not match workspace ({ws.batch}, {ws.seq})")
         if ids.size and (ids.min() < 0 or ids.max() >= self.config.vocab_size):
             raise DimensionError("token id out of embedding range")
-        ws.ids.copy_(torch.from_numpy(ids.reshape(-1).astype(np.int32)), non_blocking=False)
-        ws.tgt.copy_(torch.from_numpy(tg.reshape(-1).astype(np.int32)), non_blocking=False)
+        M = ids.size
+        stage = getattr(self, "_stage", None)
+        if stage is None or stage.shape[1] < M:
+            stage = self._stage = torch.empty(2, max(M, 1), dtype=torch.int32, pin_memory=True)
+        st = stage.numpy()
+        st[0, :M] = ids.reshape(-1)
+        st[1, :M] = tg.reshape(-1)
+        torch.cuda.current_stream().synchronize() if getattr(self, "_stage_busy", False) else None
+        ws.ids.copy_(stage[0, :M], non_blocking=True)       # pinned -> device, async
+        ws.tgt.copy_(stage[1, :M], non_blocking=True)
+        self._stage_busy = True
 
-    def check_errors(self, *wss):
-        for ws in wss:
-            e = int(ws.err.item())
+    def check_errors(self, *wss, flags=None):
+        errs = flags if flags is not None else [int(ws.err.item()) for ws in wss]
+        for ws, e in zip(wss, errs):
             if e:
                 ws.err.zero_()
                 if e & 4:
                     raise DimensionError("token id out of embedding range")
                 raise NumericError("non-finite logits")
+
+    def read_step(self, wss):
+        """One D2H for the step record and the error flags (pinned, then a
+        single stream sync)."""
+        out = getattr(self, "_readback", None)
+        if out is None:
+            out = self._readback = torch.empty(3, dtype=torch.float64, pin_memory=True)
+            self._errback = torch.empty(4, dtype=torch.int32, pin_memory=True)
+        out.copy_(self.record, non_blocking=True)
+        for i, ws in enumerate(wss[:4]):
+            self._errback[i:i + 1].copy_(ws.err, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        self._stage_busy = False
+        errs = [int(v) for v in self._errback.numpy()[:len(wss[:4])]]
+        self.check_errors(*wss[:4], flags=errs)
+        h = out.numpy()
+        return float(h[0]), float(h[1]), float(h[2])
 
 
 def init_model(config: ModelConfig, init_seed: int, device=None, init: str = "host") -> DeviceStore:

@@ -105,8 +105,7 @@ def _stage_batch(store: DeviceStore, batch: Batch):
     batch.validate(store.config)
     B, T = batch.token_ids.shape
     wsp, wsn = store.workspace(PLUS, B, T), store.workspace(MINUS, B, T)
-    store.load_batch(wsp, batch.token_ids, batch.targets)
-    store.load_batch(wsn, batch.token_ids, batch.targets)
+    store.load_batch(wsp, batch.token_ids, batch.targets)     # ids/targets are shared by both
     return wsp, wsn
 
 
@@ -115,9 +114,8 @@ def _finish(store: DeviceStore, wsp, wsn, iteration: int, seed: int) -> ZoStep:
 
 
 def _finish_record(store: DeviceStore, wss, iteration: int, seed: int) -> ZoStep:
-    rec = store.record.cpu().numpy()          # synchronises the stream
-    store.check_errors(*wss)
-    return ZoStep(iteration, seed, float(rec[0]), float(rec[1]), float(rec[2]))
+    lp, ln, g = store.read_step(list(wss))     # one D2H + one sync
+    return ZoStep(iteration, seed, lp, ln, g)
 
 
 # ---------------------------------------------------------------------------
