@@ -3,6 +3,7 @@
 // the ZO_ERR_* codes; kernels live in perturb.cu / ops.cu / attention.cu /
 // gemm_tcgen05.cu.
 #include <stdarg.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <mutex>
@@ -18,6 +19,14 @@ void set_error(const char* fmt, ...) {
   va_start(ap, fmt);
   vsnprintf(g_err, sizeof(g_err), fmt, ap);
   va_end(ap);
+}
+
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("ZO_PDL");   // 1 enables programmatic dependent launch (measured: no gain yet)
+    return e && e[0] == '1';
+  }();
+  return on;
 }
 
 int num_sms() {

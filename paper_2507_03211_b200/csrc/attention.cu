@@ -19,6 +19,8 @@ namespace zo {
 __global__ void attn_simt_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ldq, int seq, int heads,
                                  int hd, __nv_bfloat16* __restrict__ ctx, int64_t ldc, float scale) {
   extern __shared__ float sbuf[];  // per warp: seq scores
+  pdl_trigger();
+  pdl_wait();
   const int warps = blockDim.x >> 5, w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t qidx = (int64_t)blockIdx.x * warps + w;   // over B*H*T
   const int64_t total = (int64_t)gridDim.y * heads * seq;  // gridDim.y = batch
@@ -102,6 +104,8 @@ __global__ void __launch_bounds__(128) flash_attn_kernel(const __nv_bfloat16* __
                                                          int64_t ldc, float scale_log2) {
   constexpr int BQ = 64, BK = 64, CH = HD / 8;
   extern __shared__ __align__(128) uint8_t smem[];
+  pdl_trigger();
+  pdl_wait();
   uint8_t* sQ = smem;
   uint8_t* sK = smem + BQ * HD * 2;            // 2 stages
   uint8_t* sV = sK + 2 * BK * HD * 2;          // 2 stages
@@ -258,6 +262,8 @@ __global__ void __launch_bounds__(256) flash_attn_q128_kernel(const __nv_bfloat1
                                                               int64_t ldc, float scale_log2) {
   constexpr int BQ = 128, BK = 64, CH = HD / 8;
   extern __shared__ __align__(128) uint8_t smem[];
+  pdl_trigger();
+  pdl_wait();
   uint8_t* sQ = smem;                              // [128][HD]
   uint8_t* sK = smem + BQ * HD * 2;                // 2 stages of [64][HD]
   uint8_t* sV = sK + 2 * BK * HD * 2;              // 2 stages
@@ -410,12 +416,20 @@ __global__ void __launch_bounds__(256) flash_attn_q128_kernel(const __nv_bfloat1
   }
 }
 
+int attention_tc_launch(const __nv_bfloat16* qkv, int64_t ldq, int64_t batch, int64_t seq, int64_t heads,
+                        __nv_bfloat16* ctx, int64_t ldc, cudaStream_t st);
+
 int attention_launch(const __nv_bfloat16* qkv, int64_t ldq, int64_t batch, int64_t seq, int64_t heads,
                      int64_t hd, __nv_bfloat16* ctx, int64_t ldc, cudaStream_t st) {
   if (batch * seq == 0) return ZO_OK;
   const float scale = 1.0f / sqrtf((float)hd);
   const bool aligned = (ldq % 8 == 0) && (ldc % 8 == 0) &&
                        ((reinterpret_cast<uintptr_t>(qkv) & 15) == 0) && ((reinterpret_cast<uintptr_t>(ctx) & 3) == 0);
+  static const int use_tc = [] {
+    const char* e = getenv("ZO_ATTN_TC");   // 0: the mma.sync kernels (A/B testing)
+    return e ? atoi(e) : 1;
+  }();
+  if (hd == 64 && aligned && use_tc) return attention_tc_launch(qkv, ldq, batch, seq, heads, ctx, ldc, st);
   static const int variant = [] {
     const char* e = getenv("ZO_ATTN_Q64");   // 1: the 64-query kernel (A/B testing)
     return e ? atoi(e) : 0;
@@ -425,7 +439,7 @@ int attention_launch(const __nv_bfloat16* qkv, int64_t ldq, int64_t batch, int64
     const float sl2 = scale * 1.4426950408889634f;
     if (hd == 64) {
       const int smem = (128 + 4 * 64) * 64 * 2;     // 48 KB
-      flash_attn_q128_kernel<64><<<grid, 256, smem, st>>>(qkv, ldq, (int)seq, (int)heads, ctx, ldc, sl2);
+      launch_k(flash_attn_q128_kernel<64>, grid, dim3(256), smem, st, qkv, ldq, (int)seq, (int)heads, ctx, ldc, sl2);
     } else {
       const int smem = (128 + 4 * 64) * 128 * 2;    // 96 KB
       static bool attr = false;
@@ -433,7 +447,7 @@ int attention_launch(const __nv_bfloat16* qkv, int64_t ldq, int64_t batch, int64
         cudaFuncSetAttribute(flash_attn_q128_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         attr = true;
       }
-      flash_attn_q128_kernel<128><<<grid, 256, smem, st>>>(qkv, ldq, (int)seq, (int)heads, ctx, ldc, sl2);
+      launch_k(flash_attn_q128_kernel<128>, grid, dim3(256), smem, st, qkv, ldq, (int)seq, (int)heads, ctx, ldc, sl2);
     }
     return launch_status("flash_attn_q128_kernel");
   }
@@ -442,11 +456,11 @@ int attention_launch(const __nv_bfloat16* qkv, int64_t ldq, int64_t batch, int64
     const float sl2 = scale * 1.4426950408889634f;
     if (hd == 64) {
       const int smem = 64 * 64 * 2 * 5;
-      flash_attn_kernel<64><<<grid, 128, smem, st>>>(qkv, ldq, (int)seq, (int)heads, ctx, ldc, sl2);
+      launch_k(flash_attn_kernel<64>, grid, dim3(128), smem, st, qkv, ldq, (int)seq, (int)heads, ctx, ldc, sl2);
     } else {
       const int smem = 64 * 128 * 2 * 5;
       cudaFuncSetAttribute(flash_attn_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-      flash_attn_kernel<128><<<grid, 128, smem, st>>>(qkv, ldq, (int)seq, (int)heads, ctx, ldc, sl2);
+      launch_k(flash_attn_kernel<128>, grid, dim3(128), smem, st, qkv, ldq, (int)seq, (int)heads, ctx, ldc, sl2);
     }
     return launch_status("flash_attn_kernel");
   }
@@ -455,7 +469,8 @@ int attention_launch(const __nv_bfloat16* qkv, int64_t ldq, int64_t batch, int64
   const size_t smem = (size_t)warps * seq * sizeof(float);
   if (smem > 48 * 1024) cudaFuncSetAttribute(attn_simt_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const dim3 grid((unsigned)((heads * seq + warps - 1) / warps), (unsigned)batch);
-  attn_simt_kernel<<<grid, warps * 32, smem, st>>>(qkv, ldq, (int)seq, (int)heads, (int)hd, ctx, ldc, scale);
+  launch_k(attn_simt_kernel, grid, dim3(warps * 32), smem, st, qkv, ldq, (int)seq, (int)heads, (int)hd, ctx, ldc,
+           scale);
   return launch_status("attn_simt_kernel");
 }
 

@@ -1,0 +1,321 @@
+// Causal attention on the 5th-generation tensor cores (src/zosim/model.py:
+// 325-332), head_dim 64.  One CTA per SM, persistent over (query tile of 128,
+// head, batch) work items, heaviest (latest) query tiles first.
+//
+//   warp 0      TMA producer: Q tile (once per item), K/V blocks of 128 keys
+//               (2-stage ring) from the fused QKV activation
+//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer:
+//                 S_j  = Q K_j^T      M=128 N=128 K=64   -> TMEM S[j%2]
+//                 PV_j = P_j V_j      M=128 N=64  K=128  -> TMEM PV[j%2]
+//               S_{j+1} is issued before PV_j so the tensor core computes the
+//               next scores while the softmax warps work on the current ones
+//   warps 2..5  softmax, one thread per query row: S from TMEM, causal mask,
+//               online max / sum (fp32, exp2), P = bf16(exp2(s - m)) written
+//               straight into shared memory in the UMMA K-major SW128 layout,
+//               O = O * alpha + PV_j kept in registers, final O / l to global.
+// TMEM: S0 [0,128) S1 [128,256) PV0 [256,320) PV1 [320,384) of 512 columns.
+#include <stdlib.h>
+
+#include "common.cuh"
+#include "tc_ptx.cuh"
+
+namespace zo {
+
+int tma_map_bf16(const void* ptr, int64_t inner, int64_t outer, int64_t ld, int box_in, int box_out,
+                 CUtensorMap* out);
+
+namespace {
+
+constexpr int kAttnThreads = 192;
+constexpr int kTileBytes = 128 * 64 * 2;     // 16 KB: 128 rows x 64 bf16 (Q, K, V tiles)
+constexpr int kPBytes = 128 * 128 * 2;       // 32 KB: P tile, two 64-key K-chunks
+// smem: Q | K[2] | V[2] | P[2] | barriers
+constexpr int kOffQ = 0;
+constexpr int kOffK = kOffQ + kTileBytes;
+constexpr int kOffV = kOffK + 2 * kTileBytes;
+constexpr int kOffP = kOffV + 2 * kTileBytes;
+constexpr int kOffBar = kOffP + 2 * kPBytes;
+constexpr int kAttnSmem = kOffBar + 256 + 1024;
+
+struct AttnArgs {
+  int batch, seq, heads, ldc;
+  int64_t d;            // heads * 64
+  int n_qt;             // query tiles per sequence
+  int items;
+  float sl2;            // log2(e) / sqrt(hd)
+  __nv_bfloat16* ctx;
+};
+
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+}
+
+__global__ void __launch_bounds__(kAttnThreads, 1)
+    attn_tc_kernel(const __grid_constant__ CUtensorMap tm, const AttnArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  const uint32_t base = (raw + 1023u) & ~1023u;
+  uint8_t* gbase = smem_raw + (base - raw);
+  const uint32_t sQ = base + kOffQ, sK = base + kOffK, sV = base + kOffV, sP = base + kOffP;
+  const uint32_t bars = base + kOffBar;
+  // barriers: 0 q_full, 1 q_empty, 2-3 kv_full, 4-5 kv_empty, 6-7 s_full, 8-9 s_empty,
+  //           10-11 p_full, 12-13 p_empty, 14-15 pv_full, 16-17 pv_empty
+  auto bar = [&](int i) { return bars + 8u * i; };
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + kOffBar + 8 * 18);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&tm);
+    mbar_init(bar(0), 1); mbar_init(bar(1), 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(bar(2 + i), 1); mbar_init(bar(4 + i), 1);
+      mbar_init(bar(6 + i), 1); mbar_init(bar(8 + i), 4);
+      mbar_init(bar(10 + i), 4); mbar_init(bar(12 + i), 1);
+      mbar_init(bar(14 + i), 1); mbar_init(bar(16 + i), 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tmem_slot)),
+                 "r"(512u));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  pdl_trigger();
+  pdl_wait();
+
+  const int n_bh = a.batch * a.heads;
+  auto item_coords = [&](int it, int& qt, int& h, int& b) {
+    qt = a.n_qt - 1 - it / n_bh;           // heavy (late) query tiles first
+    const int bh = it % n_bh;
+    h = bh % a.heads;
+    b = bh / a.heads;
+  };
+  auto n_blocks = [&](int qt) {
+    const int by_causal = qt + 1;
+    const int by_len = (a.seq + 127) / 128;
+    return by_causal < by_len ? by_causal : by_len;
+  };
+
+  if (warp == 0) {
+    // ================= TMA producer =================
+    if (lane == 0) {
+      uint32_t kvc = 0, it_local = 0;
+      for (int it = blockIdx.x; it < a.items; it += gridDim.x, ++it_local) {
+        int qt, h, b;
+        item_coords(it, qt, h, b);
+        const int row0 = b * a.seq;
+        mbar_wait(bar(1), (it_local & 1u) ^ 1u);
+        mbar_expect_tx(bar(0), kTileBytes);
+        tma_load_2d(sQ, &tm, bar(0), h * 64, row0 + qt * 128);
+        const int nkb = n_blocks(qt);
+        for (int j = 0; j < nkb; ++j, ++kvc) {
+          const uint32_t st = kvc & 1u, ph = (kvc >> 1) & 1u;
+          mbar_wait(bar(4 + st), ph ^ 1u);
+          mbar_expect_tx(bar(2 + st), 2 * kTileBytes);
+          tma_load_2d(sK + st * kTileBytes, &tm, bar(2 + st), (int)(a.d + h * 64), row0 + j * 128);
+          tma_load_2d(sV + st * kTileBytes, &tm, bar(2 + st), (int)(2 * a.d + h * 64), row0 + j * 128);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ================= MMA issuer =================
+    // S: A = Q (K-major), B = K (K-major), M=N=128.  PV: A = P (K-major),
+    // B = V (MN-major: hd contiguous), M=128, N=64.
+    const uint32_t idesc_s = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(128 >> 3) << 17) |
+                             ((uint32_t)(128 >> 4) << 24);
+    const uint32_t idesc_pv = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) | ((uint32_t)(64 >> 3) << 17) |
+                              ((uint32_t)(128 >> 4) << 24);
+    uint32_t kvc = 0, sc = 0, it_local = 0;
+    auto issue_pv = [&](uint32_t c, uint32_t kv) {
+      const uint32_t pb = c & 1u, ph = (c >> 1) & 1u, st = kv & 1u;
+      mbar_wait(bar(10 + pb), ph);               // P_c written
+      mbar_wait(bar(16 + pb), ph ^ 1u);          // PV buffer drained by the softmax warps
+      tc_fence_after();
+      if (lane == 0) {
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {         // 128 keys = 8 x K16
+          const uint64_t ad = desc_sw128(sP + pb * kPBytes + (kk >> 2) * kTileBytes + (kk & 3) * 32, 16, 1024);
+          const uint64_t bd = desc_sw128(sV + st * kTileBytes + kk * 2048, 8192, 1024);
+          tc_mma_f16(tmem + 256 + pb * 64, ad, bd, idesc_pv, kk != 0 ? 1u : 0u);
+        }
+        tc_commit(bar(14 + pb));                  // PV ready
+        tc_commit(bar(4 + st));                   // K/V stage free
+        tc_commit(bar(12 + pb));                  // P buffer free
+      }
+      __syncwarp();
+    };
+    for (int it = blockIdx.x; it < a.items; it += gridDim.x, ++it_local) {
+      int qt, h, b;
+      item_coords(it, qt, h, b);
+      const int nkb = n_blocks(qt);
+      mbar_wait(bar(0), it_local & 1u);
+      for (int j = 0; j < nkb; ++j) {
+        const uint32_t c = sc + j, kv = kvc + j;
+        const uint32_t sb = c & 1u, ph = (c >> 1) & 1u;
+        mbar_wait(bar(2 + (kv & 1u)), (kv >> 1) & 1u);   // K_j, V_j landed
+        mbar_wait(bar(8 + sb), ph ^ 1u);                 // S buffer free
+        tc_fence_after();
+        if (lane == 0) {
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) {
+            const uint64_t ad = desc_sw128(sQ + kk * 32, 16, 1024);
+            const uint64_t bd = desc_sw128(sK + (kv & 1u) * kTileBytes + kk * 32, 16, 1024);
+            tc_mma_f16(tmem + sb * 128, ad, bd, idesc_s, kk != 0 ? 1u : 0u);
+          }
+          tc_commit(bar(6 + sb));                 // S ready
+          if (j == nkb - 1) tc_commit(bar(1));    // Q no longer needed
+        }
+        __syncwarp();
+        if (j >= 1) issue_pv(c - 1, kv - 1);
+      }
+      issue_pv(sc + nkb - 1, kvc + nkb - 1);
+      sc += nkb;
+      kvc += nkb;
+    }
+  } else {
+    // ================= softmax / output =================
+    const int quarter = warp & 3;
+    const int r = quarter * 32 + lane;           // row of the 128-query tile
+    const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+    uint32_t sc = 0;
+    for (int it = blockIdx.x; it < a.items; it += gridDim.x) {
+      int qt, h, b;
+      item_coords(it, qt, h, b);
+      const int nkb = n_blocks(qt);
+      const int qi = qt * 128 + r;
+      float m = -INFINITY, l = 0.f;
+      float o[64];
+#pragma unroll
+      for (int i = 0; i < 64; ++i) o[i] = 0.f;
+      for (int j = 0; j < nkb; ++j) {
+        const uint32_t c = sc + j, sb = c & 1u, ph = (c >> 1) & 1u;
+        const bool need_mask = (j * 128 + 127 > qt * 128) || ((j + 1) * 128 > a.seq);
+        mbar_wait(bar(6 + sb), ph);
+        tc_fence_after();
+        // pass 1: row max of the valid scores
+        float mx = -INFINITY;
+#pragma unroll 1
+        for (int ch = 0; ch < 4; ++ch) {
+          float v[32];
+          tmem_ld_32x32b_x32(tmem + sb * 128 + ch * 32 + lane_off, v);
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const int ki = j * 128 + ch * 32 + i;
+            const bool ok = !need_mask || (ki <= qi && ki < a.seq);
+            mx = fmaxf(mx, ok ? v[i] : -INFINITY);
+          }
+        }
+        const float m_new = fmaxf(m, mx);
+        const float mb = m_new == -INFINITY ? 0.f : m_new * a.sl2;
+        const float alpha = m == -INFINITY ? 0.f : exp2f(fmaf(m, a.sl2, -mb));
+        // P buffer free (the PV MMA two blocks ago has read it)
+        mbar_wait(bar(12 + sb), ph ^ 1u);
+        // pass 2: P = exp2(s*sl2 - m*sl2) -> bf16 -> smem (K-major SW128)
+        float sum = 0.f;
+        const uint32_t prow = sP + sb * kPBytes;
+#pragma unroll 1
+        for (int ch = 0; ch < 4; ++ch) {
+          float v[32];
+          tmem_ld_32x32b_x32(tmem + sb * 128 + ch * 32 + lane_off, v);
+          uint32_t pk[16];
+#pragma unroll
+          for (int i = 0; i < 32; i += 2) {
+            const int ki = j * 128 + ch * 32 + i;
+            const bool ok0 = !need_mask || (ki <= qi && ki < a.seq);
+            const bool ok1 = !need_mask || (ki + 1 <= qi && ki + 1 < a.seq);
+            const float p0 = ok0 ? exp2f(fmaf(v[i], a.sl2, -mb)) : 0.f;
+            const float p1 = ok1 ? exp2f(fmaf(v[i + 1], a.sl2, -mb)) : 0.f;
+            sum += p0 + p1;
+            __nv_bfloat162 h2 = __floats2bfloat162_rn(p0, p1);
+            pk[i >> 1] = *reinterpret_cast<uint32_t*>(&h2);
+          }
+          // keys [ch*32, ch*32+32) = 4 16-byte chunks of the row; K-chunk = ch / 2
+          const uint32_t region = prow + (ch >> 1) * kTileBytes + r * 128;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int chunk = (ch & 1) * 4 + q;
+            const uint32_t addr = region + ((chunk ^ (r & 7)) << 4);
+            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};\n" ::"r"(addr), "r"(pk[4 * q]),
+                         "r"(pk[4 * q + 1]), "r"(pk[4 * q + 2]), "r"(pk[4 * q + 3])
+                         : "memory");
+          }
+        }
+        tc_fence_before();
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) { mbar_arrive(bar(8 + sb)); mbar_arrive(bar(10 + sb)); }   // S read, P written
+        l = fmaf(l, alpha, sum);
+        m = m_new;
+        // O = O * alpha + P_j V_j
+        mbar_wait(bar(14 + sb), ph);
+        tc_fence_after();
+#pragma unroll
+        for (int half = 0; half < 2; ++half) {
+          float v[32];
+          tmem_ld_32x32b_x32(tmem + 256 + sb * 64 + half * 32 + lane_off, v);
+#pragma unroll
+          for (int i = 0; i < 32; ++i) o[half * 32 + i] = fmaf(o[half * 32 + i], alpha, v[i]);
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(bar(16 + sb));
+      }
+      sc += nkb;
+      if (qi < a.seq) {
+        const float inv = l > 0.f ? 1.f / l : 0.f;
+        __nv_bfloat16* out = a.ctx + ((int64_t)b * a.seq + qi) * a.ldc + (int64_t)h * 64;
+#pragma unroll
+        for (int i = 0; i < 64; i += 8) {
+          uint32_t pk[4];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            __nv_bfloat162 h2 = __floats2bfloat162_rn(o[i + 2 * k] * inv, o[i + 2 * k + 1] * inv);
+            pk[k] = *reinterpret_cast<uint32_t*>(&h2);
+          }
+          *reinterpret_cast<uint4*>(out + i) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+        }
+      }
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(512u));
+  }
+}
+
+}  // namespace
+
+// head_dim 64, qkv / ctx leading dims multiples of 8, 16-byte aligned.
+int attention_tc_launch(const __nv_bfloat16* qkv, int64_t ldq, int64_t batch, int64_t seq, int64_t heads,
+                        __nv_bfloat16* ctx, int64_t ldc, cudaStream_t st) {
+  CUtensorMap tm;
+  const int64_t rows = batch * seq;
+  int rc = tma_map_bf16(qkv, 3 * heads * 64, rows, ldq, 64, 128, &tm);
+  if (rc) return rc;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kAttnSmem);
+    if (e != cudaSuccess) { set_error("attn_tc smem attribute: %s", cudaGetErrorString(e)); return ZO_ERR_CUDA; }
+    attr = true;
+  }
+  AttnArgs a;
+  a.batch = (int)batch;
+  a.seq = (int)seq;
+  a.heads = (int)heads;
+  a.ldc = (int)ldc;
+  a.d = heads * 64;
+  a.n_qt = (int)((seq + 127) / 128);
+  a.items = a.n_qt * (int)(batch * heads);
+  a.sl2 = 1.4426950408889634f / 8.0f;   // log2(e) / sqrt(64)
+  a.ctx = ctx;
+  const int grid = a.items < num_sms() ? a.items : num_sms();
+  launch_k(attn_tc_kernel, dim3(grid), dim3(kAttnThreads), kAttnSmem, st, tm, a);
+  return launch_status("attn_tc_kernel");
+}
+
+}  // namespace zo

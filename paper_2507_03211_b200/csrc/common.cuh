@@ -6,6 +6,8 @@
 #include <stdint.h>
 #include <stdio.h>
 
+#include <utility>
+
 #include "../../include/zo_b200.h"
 
 namespace zo {
@@ -205,6 +207,34 @@ struct PuParams {
   const double* z_prev;
   int64_t z_key0;
 };
+
+// ---------------------------------------------------------------------------
+// Programmatic dependent launch: every kernel lets its stream successor start
+// launching immediately (the successor's CTAs still only run where resources
+// free up), and waits for its predecessor's memory to be visible before
+// reading any input.  Both are no-ops for kernels launched without PDL.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+bool pdl_enabled();
+
+// cudaLaunchKernelEx with programmatic stream serialisation (PDL)
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                            Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 // ---------------------------------------------------------------------------
 // small PTX wrappers (mbarrier / TMA / tcgen05) for the GEMM

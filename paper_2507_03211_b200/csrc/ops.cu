@@ -16,6 +16,8 @@ __global__ void embed_kernel(const float* __restrict__ tok, int64_t tok_key0,
                              const int32_t* __restrict__ ids, int64_t seq, int64_t d, int64_t vocab,
                              double scale, const ZoStepScalars* scal, const double* z, int64_t z_key0,
                              float* __restrict__ x, int64_t ldx, int32_t* err) {
+  pdl_trigger();
+  pdl_wait();
   const int64_t m = blockIdx.x;
   const int64_t t = m % seq;
   int64_t id = ids[m];
@@ -49,11 +51,11 @@ int embed_launch(const float* tok, int64_t tok_key0, const float* pos, int64_t p
   if (rows == 0) return ZO_OK;
   const int threads = d >= 256 ? 256 : (int)((d + 31) / 32 * 32);
   if (zmode == ZO_Z_PHILOX)
-    embed_kernel<ZO_Z_PHILOX><<<(unsigned)rows, threads, 0, st>>>(tok, tok_key0, pos, pos_key0, ids, seq, d, vocab,
-                                                                  scale, scal, z, z_key0, x, ldx, err);
+    launch_k(embed_kernel<ZO_Z_PHILOX>, dim3((unsigned)rows), dim3(threads), 0, st, tok, tok_key0, pos, pos_key0, ids,
+             seq, d, vocab, scale, scal, z, z_key0, x, ldx, err);
   else
-    embed_kernel<ZO_Z_ORACLE><<<(unsigned)rows, threads, 0, st>>>(tok, tok_key0, pos, pos_key0, ids, seq, d, vocab,
-                                                                  scale, scal, z, z_key0, x, ldx, err);
+    launch_k(embed_kernel<ZO_Z_ORACLE>, dim3((unsigned)rows), dim3(threads), 0, st, tok, tok_key0, pos, pos_key0, ids,
+             seq, d, vocab, scale, scal, z, z_key0, x, ldx, err);
   return launch_status("embed_kernel");
 }
 
@@ -77,6 +79,8 @@ __global__ void layernorm_kernel(const float* __restrict__ x, int64_t ldx, const
                                  int64_t ldo) {
   extern __shared__ float srow[];
   __shared__ float red[32];
+  pdl_trigger();
+  pdl_wait();
   const float* xr = x + blockIdx.x * ldx;
   float s = 0.f;
   for (int64_t c = threadIdx.x; c < d; c += blockDim.x) {
@@ -104,6 +108,8 @@ __global__ void __launch_bounds__(256) layernorm_warp_kernel(const float* __rest
                                                               const float* __restrict__ g,
                                                               const float* __restrict__ b, int64_t rows, int d,
                                                               __nv_bfloat16* __restrict__ out, int64_t ldo) {
+  pdl_trigger();
+  pdl_wait();
   const int lane = threadIdx.x & 31;
   const int64_t warp_g = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -164,7 +170,7 @@ int layernorm_launch(const float* x, int64_t ldx, const float* g, const float* b
     const int nv = (int)((d + 127) / 128);
 #define ZO_LN_CASE(N)                                                                                   \
   if (nv <= N) {                                                                                        \
-    layernorm_warp_kernel<N><<<grid, 256, 0, st>>>(x, ldx, g, b, rows, (int)d, out, ldo);               \
+    launch_k(layernorm_warp_kernel<N>, dim3(grid), dim3(256), 0, st, x, ldx, g, b, rows, (int)d, out, ldo);    \
     return launch_status("layernorm_warp_kernel");                                                      \
   }
     ZO_LN_CASE(1) ZO_LN_CASE(2) ZO_LN_CASE(4) ZO_LN_CASE(8) ZO_LN_CASE(16) ZO_LN_CASE(32)
@@ -177,7 +183,7 @@ int layernorm_launch(const float* x, int64_t ldx, const float* g, const float* b
     big_smem = true;
   }
   const int threads = d >= 1024 ? 512 : (d >= 256 ? 256 : 64);
-  layernorm_kernel<<<(unsigned)rows, threads, smem, st>>>(x, ldx, g, b, d, out, ldo);
+  launch_k(layernorm_kernel, dim3((unsigned)rows), dim3(threads), smem, st, x, ldx, g, b, d, out, ldo);
   return launch_status("layernorm_kernel");
 }
 
@@ -187,6 +193,8 @@ int layernorm_launch(const float* x, int64_t ldx, const float* g, const float* b
 // ---------------------------------------------------------------------------
 __global__ void ce_rows_kernel(const float* __restrict__ part, const float* __restrict__ tgt, int64_t rows,
                                int64_t n_tiles, double* __restrict__ row_loss, int32_t* err) {
+  pdl_trigger();
+  pdl_wait();
   const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (r >= rows) return;
   const float* p = part + r * n_tiles * 2;
@@ -213,6 +221,8 @@ __global__ void ce_rows_kernel(const float* __restrict__ part, const float* __re
 
 __global__ void mean_f64_kernel(const double* __restrict__ v, int64_t n, double* out) {
   __shared__ double red[1024];
+  pdl_trigger();
+  pdl_wait();
   double s = 0.0;
   // contiguous chunk per thread, then a fixed-shape tree: deterministic
   const int64_t per = (n + blockDim.x - 1) / blockDim.x;
@@ -230,8 +240,9 @@ __global__ void mean_f64_kernel(const double* __restrict__ v, int64_t n, double*
 int ce_finalize_launch(const float* part, const float* tgt, int64_t rows, int64_t n_tiles, double* loss,
                        double* row_scratch, int32_t* err, cudaStream_t st) {
   if (rows == 0) return ZO_OK;
-  ce_rows_kernel<<<(unsigned)((rows + 127) / 128), 128, 0, st>>>(part, tgt, rows, n_tiles, row_scratch, err);
-  mean_f64_kernel<<<1, 1024, 0, st>>>(row_scratch, rows, loss);
+  launch_k(ce_rows_kernel, dim3((unsigned)((rows + 127) / 128)), dim3(128), 0, st, part, tgt, rows, n_tiles,
+           row_scratch, err);
+  launch_k(mean_f64_kernel, dim3(1), dim3(1024), 0, st, (const double*)row_scratch, rows, loss);
   return launch_status("ce_finalize");
 }
 
@@ -240,6 +251,7 @@ int ce_finalize_launch(const float* part, const float* tgt, int64_t rows, int64_
 // ---------------------------------------------------------------------------
 __global__ void grad_finalize_kernel(const double* lp, const double* ln, double eps, double lr,
                                      ZoStepScalars* scal, double* rec) {
+  pdl_wait();
   const double a = *lp, b = *ln;
   const double g = (a - b) / (2.0 * eps);
   rec[0] = a; rec[1] = b; rec[2] = g;
@@ -250,6 +262,7 @@ __global__ void grad_finalize_kernel(const double* lp, const double* ln, double 
 
 __global__ void grad_groups_kernel(const double* losses, int n, int sp, int op, int sm, int om, int mine,
                                    double eps, double lr, ZoStepScalars* scal, double* rec) {
+  pdl_wait();
   double tot = 0.0;
   for (int i = 0; i < n; ++i) tot += (losses[i * sp + op] - losses[i * sm + om]) / (2.0 * eps);
   const double g = tot / (double)n;
@@ -261,13 +274,13 @@ __global__ void grad_groups_kernel(const double* losses, int n, int sp, int op, 
 
 int grad_finalize_launch(const double* lp, const double* ln, double eps, double lr, ZoStepScalars* scal,
                          double* rec, cudaStream_t st) {
-  grad_finalize_kernel<<<1, 1, 0, st>>>(lp, ln, eps, lr, scal, rec);
+  launch_k(grad_finalize_kernel, dim3(1), dim3(1), 0, st, lp, ln, eps, lr, scal, rec);
   return launch_status("grad_finalize_kernel");
 }
 
 int grad_groups_launch(const double* losses, int n, int sp, int op, int sm, int om, int mine, double eps, double lr,
                        ZoStepScalars* scal, double* rec, cudaStream_t st) {
-  grad_groups_kernel<<<1, 1, 0, st>>>(losses, n, sp, op, sm, om, mine, eps, lr, scal, rec);
+  launch_k(grad_groups_kernel, dim3(1), dim3(1), 0, st, losses, n, sp, op, sm, om, mine, eps, lr, scal, rec);
   return launch_status("grad_groups_kernel");
 }
 

@@ -181,6 +181,8 @@ __device__ __forceinline__ void pu_tile_fast(const PuParams& p, int64_t e0, int 
 template <int ZMODE>
 __global__ void __launch_bounds__(kPuThreads, 4) perturb_update_kernel(const PuParams p) {
   extern __shared__ int64_t s_prefix[];
+  pdl_trigger();
+  pdl_wait();
   const bool prefix_in_smem = p.n_segs + 1 <= kPuMaxSmemSegs;
   if (prefix_in_smem)
     for (int i = threadIdx.x; i <= p.n_segs; i += kPuThreads) s_prefix[i] = p.prefix[i];
@@ -267,8 +269,8 @@ int perturb_update_launch(const PuParams& p, int zmode, cudaStream_t stream) {
   const int64_t want = (int64_t)num_sms() * 8;   // 8 x 128 threads per SM
   const int grid = (int)(p.n_tiles < want ? p.n_tiles : want);
   const size_t smem = p.n_segs + 1 <= kPuMaxSmemSegs ? (size_t)(p.n_segs + 1) * sizeof(int64_t) : 0;
-  if (zmode == ZO_Z_PHILOX) perturb_update_kernel<ZO_Z_PHILOX><<<grid, kPuThreads, smem, stream>>>(p);
-  else perturb_update_kernel<ZO_Z_ORACLE><<<grid, kPuThreads, smem, stream>>>(p);
+  if (zmode == ZO_Z_PHILOX) launch_k(perturb_update_kernel<ZO_Z_PHILOX>, dim3(grid), dim3(kPuThreads), smem, stream, p);
+  else launch_k(perturb_update_kernel<ZO_Z_ORACLE>, dim3(grid), dim3(kPuThreads), smem, stream, p);
   return launch_status("perturb_update_kernel");
 }
 

@@ -227,6 +227,35 @@ class DeviceStore:
                         L.call("zo_philox_normals", seed, k + o, m, z.data_ptr(), L.stream_ptr())
                         dst[o:o + m].copy_(z.mul_(0.02))
 
+    # -- ParamStore-compatible helpers (model.py:169-200) ----------------------
+    @property
+    def blocks(self):
+        from .zo import store_blocks
+
+        return store_blocks(self)
+
+    @property
+    def n_blocks(self) -> int:
+        return len(self.layouts)
+
+    @property
+    def total_bytes(self) -> int:
+        return self.total_params * 4
+
+    def checksum(self) -> str:
+        """SHA-256 over the fp32 block buffers in order -- equal to the
+        reference's ParamStore.checksum when the values are bit-identical."""
+        import hashlib
+
+        h = hashlib.sha256()
+        th = self.theta.cpu().numpy()
+        for bl in self.layouts:
+            h.update(th[bl.key0:bl.key0 + bl.elem_count].tobytes())
+        return h.hexdigest()
+
+    def equal(self, other) -> bool:
+        return bool(torch.equal(self.theta, other.theta))
+
     # -- views -----------------------------------------------------------------
     def block_buf(self, bid: int) -> torch.Tensor:
         bl = self.layouts[bid]

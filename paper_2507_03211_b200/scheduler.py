@@ -197,6 +197,14 @@ class SliceLayout:
         return cls(block_id, total, n)
 
 
+def sliced_upload_time(total: int, n: int, host_bw: float, peer_bw: float) -> float:
+    """The reference's analytic redistribution cost (comm.py:250-256), the
+    model the measured per-block upload is compared against:
+    T_comm = ceil(M/n)/BW_host + (M - ceil(M/n))/BW_peer."""
+    width = -(-total // n)
+    return width / host_bw + (total - width) / peer_bw
+
+
 def apply_thread_aligned_layout(store, n: int) -> dict:
     """Fix per-block slice boundaries once (comm.py:345-358); changing n later
     is a ProtocolError."""
