@@ -46,6 +46,12 @@ struct AttnArgs {
   __nv_bfloat16* ctx;
 };
 
+__device__ __forceinline__ float ex2_approx(float x) {   // MUFU.EX2; ex2(-inf) = 0
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
 }
@@ -196,44 +202,48 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         const bool need_mask = (j * 128 + 127 > qt * 128) || ((j + 1) * 128 > a.seq);
         mbar_wait(bar(6 + sb), ph);
         tc_fence_after();
-        // pass 1: row max of the valid scores
-        float mx = -INFINITY;
-#pragma unroll 1
-        for (int ch = 0; ch < 4; ++ch) {
-          float v[32];
-          tmem_ld_32x32b_x32(tmem + sb * 128 + ch * 32 + lane_off, v);
+        // all 128 scores of this row in registers: 4 TMEM loads in flight, one wait
+        uint32_t sv[4][32];
 #pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            const int ki = j * 128 + ch * 32 + i;
-            const bool ok = !need_mask || (ki <= qi && ki < a.seq);
-            mx = fmaxf(mx, ok ? v[i] : -INFINITY);
-          }
+        for (int ch = 0; ch < 4; ++ch) tmem_ld_32x32b_x32_nw(tmem + sb * 128 + ch * 32 + lane_off, sv[ch]);
+        tmem_wait_ld();
+        float mx0 = -INFINITY, mx1 = -INFINITY;
+        if (need_mask) {
+#pragma unroll
+          for (int ch = 0; ch < 4; ++ch)
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              const int ki = j * 128 + ch * 32 + i;
+              if (!(ki <= qi && ki < a.seq)) sv[ch][i] = __float_as_uint(-INFINITY);
+            }
         }
-        const float m_new = fmaxf(m, mx);
+#pragma unroll
+        for (int ch = 0; ch < 4; ++ch)
+#pragma unroll
+          for (int i = 0; i < 32; i += 2) {
+            mx0 = fmaxf(mx0, __uint_as_float(sv[ch][i]));
+            mx1 = fmaxf(mx1, __uint_as_float(sv[ch][i + 1]));
+          }
+        const float m_new = fmaxf(m, fmaxf(mx0, mx1));
         const float mb = m_new == -INFINITY ? 0.f : m_new * a.sl2;
-        const float alpha = m == -INFINITY ? 0.f : exp2f(fmaf(m, a.sl2, -mb));
+        const float alpha = m == -INFINITY ? 0.f : ex2_approx(fmaf(m, a.sl2, -mb));
         // P buffer free (the PV MMA two blocks ago has read it)
         mbar_wait(bar(12 + sb), ph ^ 1u);
-        // pass 2: P = exp2(s*sl2 - m*sl2) -> bf16 -> smem (K-major SW128)
-        float sum = 0.f;
+        // P = exp2(s*sl2 - m*sl2) -> bf16 -> smem (K-major SW128)
+        float sum0 = 0.f, sum1 = 0.f;
         const uint32_t prow = sP + sb * kPBytes;
-#pragma unroll 1
+#pragma unroll
         for (int ch = 0; ch < 4; ++ch) {
-          float v[32];
-          tmem_ld_32x32b_x32(tmem + sb * 128 + ch * 32 + lane_off, v);
           uint32_t pk[16];
 #pragma unroll
           for (int i = 0; i < 32; i += 2) {
-            const int ki = j * 128 + ch * 32 + i;
-            const bool ok0 = !need_mask || (ki <= qi && ki < a.seq);
-            const bool ok1 = !need_mask || (ki + 1 <= qi && ki + 1 < a.seq);
-            const float p0 = ok0 ? exp2f(fmaf(v[i], a.sl2, -mb)) : 0.f;
-            const float p1 = ok1 ? exp2f(fmaf(v[i + 1], a.sl2, -mb)) : 0.f;
-            sum += p0 + p1;
+            const float p0 = ex2_approx(fmaf(__uint_as_float(sv[ch][i]), a.sl2, -mb));
+            const float p1 = ex2_approx(fmaf(__uint_as_float(sv[ch][i + 1]), a.sl2, -mb));
+            sum0 += p0;
+            sum1 += p1;
             __nv_bfloat162 h2 = __floats2bfloat162_rn(p0, p1);
             pk[i >> 1] = *reinterpret_cast<uint32_t*>(&h2);
           }
-          // keys [ch*32, ch*32+32) = 4 16-byte chunks of the row; K-chunk = ch / 2
           const uint32_t region = prow + (ch >> 1) * kTileBytes + r * 128;
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
@@ -244,6 +254,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
                          : "memory");
           }
         }
+        const float sum = sum0 + sum1;
         tc_fence_before();
         fence_proxy_async_smem();
         __syncwarp();
@@ -253,12 +264,16 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         // O = O * alpha + P_j V_j
         mbar_wait(bar(14 + sb), ph);
         tc_fence_after();
+        {
+          uint32_t pv[2][32];
+          tmem_ld_32x32b_x32_nw(tmem + 256 + sb * 64 + lane_off, pv[0]);
+          tmem_ld_32x32b_x32_nw(tmem + 256 + sb * 64 + 32 + lane_off, pv[1]);
+          tmem_wait_ld();
 #pragma unroll
-        for (int half = 0; half < 2; ++half) {
-          float v[32];
-          tmem_ld_32x32b_x32(tmem + 256 + sb * 64 + half * 32 + lane_off, v);
-#pragma unroll
-          for (int i = 0; i < 32; ++i) o[half * 32 + i] = fmaf(o[half * 32 + i], alpha, v[i]);
+          for (int i = 0; i < 32; ++i) {
+            o[i] = fmaf(o[i], alpha, __uint_as_float(pv[0][i]));
+            o[32 + i] = fmaf(o[32 + i], alpha, __uint_as_float(pv[1][i]));
+          }
         }
         tc_fence_before();
         __syncwarp();
