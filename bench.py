@@ -47,9 +47,23 @@ def _args():
     ap.add_argument("--batch", type=int, default=BATCH_PER_GROUP, help="sequences per PertP group")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true", help="skip the public-API pass (profiling runs)")
-    ap.add_argument("--overlap", action="store_true",
-                    help="per-block perturb passes on a side stream ahead of the +eps forward")
+    ap.add_argument("--overlap", default="none", choices=["none", "blocks", "background"],
+                    help="blocks: per-block perturb passes on a side stream ahead of the +eps forward; "
+                         "background: one co-resident perturb pass gated per block by device counters")
     return ap.parse_args()
+
+
+def _plan(args):
+    return {"none": False, "blocks": "blocks", "background": "background"}[args.overlap]
+
+
+def _plan_text(args, world):
+    if world > 1 or args.overlap == "none":
+        return "one launch; timed alone in a serialised replay"
+    if args.overlap == "blocks":
+        return "timed run: one launch per block on a side stream ahead of the +eps forward; timed alone in a serialised replay"
+    return ("timed run: block 0 full-width, the rest as one co-resident background launch gating each block's "
+            "forward by a device counter; timed alone in a serialised replay")
 
 
 # ----------------------------------------------------------------------------
@@ -221,10 +235,10 @@ def ours(args, rank, world, local_rank):
                for j in range(1, args.warmup + args.steps + 1)]
 
     if world == 1:
-        runner = zo.StreamingZo(store, hyper, overlap=args.overlap)
+        runner = zo.StreamingZo(store, hyper, overlap=_plan(args))
         wss = [store.workspace(PLUS, B, T), store.workspace(MINUS, B, T)]
-        step_calls = (runner.step_calls(wss[0], wss[1]) if (not args.overlap)
-                      else runner.overlapped_step_calls(wss[0], wss[1]))
+        step_calls = {"none": runner.step_calls, "blocks": runner.overlapped_step_calls,
+                      "background": runner.background_step_calls}[args.overlap](wss[0], wss[1])
     else:
         from paper_2507_03211_b200.strategies import TwoDRunner
         runner = TwoDRunner(store, hyper, rank=rank, world=world, batch=B, seq=T)
@@ -305,8 +319,7 @@ def ours(args, rank, world, local_rank):
     # instrumented replay runs the two directional forwards serialised.
     if world == 1:
         runner.dual_stream = False
-        step_calls[:] = (runner.step_calls(wss[0], wss[1]) if not args.overlap
-                         else runner.overlapped_step_calls(wss[0], wss[1]))
+        step_calls[:] = runner.step_calls(wss[0], wss[1])
         pert_set.clear()
         pert_set.update(i for i, (fn, _) in enumerate(step_calls) if fn.__name__ == "zo_perturb_update")
         gemm_set.clear()
@@ -330,7 +343,7 @@ def ours(args, rank, world, local_rank):
     if args.no_e2e:
         e2e_ms = ms
     elif world == 1:
-        runner2 = zo.StreamingZo(store, hyper, overlap=args.overlap)
+        runner2 = zo.StreamingZo(store, hyper, overlap=_plan(args))
         for j in range(args.warmup):
             runner2.step(batches[j], seeds[j])
         torch.cuda.synchronize()
@@ -365,7 +378,7 @@ def ours(args, rank, world, local_rank):
                  "unit": "GB/s", "frac": pert_gbs / hbm, "traffic": None, "peak_kind": f"{peak_kind} HBM copy",
                  "share_of_step": pert_share,
                  "algorithmic": f"{bytes_per_param} B/param x {P} params per step "
-                                f"({'one launch per block on a side stream, overlapping the +eps forward' if world == 1 and args.overlap else 'one launch'})"}
+                                f"({_plan_text(args, world)})"}
     dominant = roof_gemm if gemm_share >= pert_share else roof_pert
     other = roof_pert if dominant is roof_gemm else roof_gemm
     line = {

@@ -67,7 +67,7 @@ typedef struct ZoSegment {
   int64_t dst;    /* element offset of the tensor inside its shadow buffer    */
   int64_t dst_ld; /* shadow row stride in elements (>= cols)                  */
   int32_t kind;   /* ZO_SHADOW_*                                              */
-  int32_t reserved;
+  int32_t reserved; /* block index (completion counters of zo_perturb_update_bg) */
 } ZoSegment;
 
 /* Per-iteration scalars, device-resident so a captured CUDA graph can replay
@@ -104,6 +104,19 @@ int zo_perturb_update(float* theta, int64_t theta_key0, const ZoSegment* segs,
                       const ZoStepScalars* scal, int32_t zmode,
                       const double* z_cur, const double* z_prev, int64_t z_key0,
                       void* stream);
+/* Same pass as a "background" kernel: one 4-warp CTA per SM sized to run
+ * beside the forward's GEMM / attention CTAs, Philox direction only.  After
+ * each tile it adds 1 to block_done[segment.reserved] (gpu-scope release), so
+ * a forward stream can start block b as soon as its tiles are done
+ * (zo_wait_counter) while the pass continues on later blocks. */
+int zo_perturb_update_bg(float* theta, int64_t theta_key0, const ZoSegment* segs,
+                         const int64_t* tile_prefix, int32_t n_segs, int64_t n_tiles,
+                         void* wsh_a, float* vsh_a, void* wsh_b, float* vsh_b,
+                         double scale_a, double scale_b, uint32_t flags,
+                         const ZoStepScalars* scal, int32_t* block_done, void* stream);
+/* Enqueue a one-thread kernel that returns once *counter >= target. */
+int zo_wait_counter(const int32_t* counter, int32_t target, void* stream);
+
 /* Tile granularity (elements) the host must use to build tile_prefix. */
 int64_t zo_perturb_tile_elems(void);
 

@@ -42,7 +42,8 @@ int num_sms() {
   return cached[dev];
 }
 
-int perturb_update_launch(const PuParams& p, int zmode, cudaStream_t stream);
+int perturb_update_launch(const PuParams& p, int zmode, cudaStream_t stream, bool background);
+int wait_counter_launch(const int32_t* counter, int32_t target, cudaStream_t stream);
 int philox_normals_launch(uint64_t seed, int64_t e0, int64_t n, float* out, cudaStream_t stream);
 int embed_launch(const float*, int64_t, const float*, int64_t, const int32_t*, int64_t, int64_t, int64_t, int64_t,
                  double, const ZoStepScalars*, int32_t, const double*, int64_t, float*, int64_t, int32_t*,
@@ -116,7 +117,40 @@ int zo_perturb_update(float* theta, int64_t theta_key0, const ZoSegment* segs, c
   p.z_cur = z_cur;
   p.z_prev = z_prev;
   p.z_key0 = z_key0;
-  return zo::perturb_update_launch(p, zmode, ZO_STREAM(stream));
+  p.block_done = nullptr;
+  return zo::perturb_update_launch(p, zmode, ZO_STREAM(stream), false);
+}
+
+int zo_perturb_update_bg(float* theta, int64_t theta_key0, const ZoSegment* segs, const int64_t* tile_prefix,
+                         int32_t n_segs, int64_t n_tiles, void* wsh_a, float* vsh_a, void* wsh_b, float* vsh_b,
+                         double scale_a, double scale_b, uint32_t flags, const ZoStepScalars* scal,
+                         int32_t* block_done, void* stream) {
+  ZO_CHECK_ARG(theta && segs && tile_prefix && scal && block_done, ZO_ERR_CONFIG, "zo_perturb_update_bg: null argument");
+  zo::PuParams p;
+  p.theta = theta;
+  p.theta_key0 = theta_key0;
+  p.segs = segs;
+  p.prefix = tile_prefix;
+  p.n_segs = n_segs;
+  p.n_tiles = n_tiles;
+  p.wsh[0] = static_cast<__nv_bfloat16*>(wsh_a);
+  p.wsh[1] = static_cast<__nv_bfloat16*>(wsh_b);
+  p.vsh[0] = vsh_a;
+  p.vsh[1] = vsh_b;
+  p.scale[0] = scale_a;
+  p.scale[1] = scale_b;
+  p.flags = flags;
+  p.scal = scal;
+  p.z_cur = nullptr;
+  p.z_prev = nullptr;
+  p.z_key0 = 0;
+  p.block_done = block_done;
+  return zo::perturb_update_launch(p, ZO_Z_PHILOX, ZO_STREAM(stream), true);
+}
+
+int zo_wait_counter(const int32_t* counter, int32_t target, void* stream) {
+  ZO_CHECK_ARG(counter, ZO_ERR_CONFIG, "zo_wait_counter: null counter");
+  return zo::wait_counter_launch(counter, target, ZO_STREAM(stream));
 }
 
 int zo_embed_fwd(const float* tok, int64_t tok_key0, const float* pos, int64_t pos_key0, const int32_t* ids,

@@ -9,7 +9,8 @@
 //                 PV_j = P_j V_j      M=128 N=64  K=128  -> TMEM PV[j%2]
 //               S_{j+1} is issued before PV_j so the tensor core computes the
 //               next scores while the softmax warps work on the current ones
-//   warps 2..5  softmax, one thread per query row: S from TMEM, causal mask,
+//   warps 2..9  softmax, two warps per query row group (each owns 64 of the 128
+//               key columns and 32 output columns): S from TMEM, causal mask,
 //               online max / sum (fp32, exp2), P = bf16(exp2(s - m)) written
 //               straight into shared memory in the UMMA K-major SW128 layout,
 //               O = O * alpha + PV_j kept in registers, final O / l to global.
@@ -26,16 +27,17 @@ int tma_map_bf16(const void* ptr, int64_t inner, int64_t outer, int64_t ld, int 
 
 namespace {
 
-constexpr int kAttnThreads = 192;
+constexpr int kAttnThreads = 320;   // producer, MMA, 8 softmax warps (2 per TMEM lane quarter)
 constexpr int kTileBytes = 128 * 64 * 2;     // 16 KB: 128 rows x 64 bf16 (Q, K, V tiles)
 constexpr int kPBytes = 128 * 128 * 2;       // 32 KB: P tile, two 64-key K-chunks
-// smem: Q | K[2] | V[2] | P[2] | barriers
+// smem: Q[2] | K[2] | V[2] | P[2] | barriers
 constexpr int kOffQ = 0;
-constexpr int kOffK = kOffQ + kTileBytes;
+constexpr int kOffK = kOffQ + 2 * kTileBytes;
 constexpr int kOffV = kOffK + 2 * kTileBytes;
 constexpr int kOffP = kOffV + 2 * kTileBytes;
 constexpr int kOffBar = kOffP + 2 * kPBytes;
-constexpr int kAttnSmem = kOffBar + 256 + 1024;
+constexpr int kOffRed = kOffBar + 256;                 // row-max / row-sum exchange [2][128] fp32
+constexpr int kAttnSmem = kOffRed + 2 * 128 * 4 + 1024;
 
 struct AttnArgs {
   int batch, seq, heads, ldc;
@@ -64,20 +66,22 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   uint8_t* gbase = smem_raw + (base - raw);
   const uint32_t sQ = base + kOffQ, sK = base + kOffK, sV = base + kOffV, sP = base + kOffP;
   const uint32_t bars = base + kOffBar;
-  // barriers: 0 q_full, 1 q_empty, 2-3 kv_full, 4-5 kv_empty, 6-7 s_full, 8-9 s_empty,
-  //           10-11 p_full, 12-13 p_empty, 14-15 pv_full, 16-17 pv_empty
+  // barriers: 0 q_full0, 1 q_empty0, 2-3 kv_full, 4-5 kv_empty, 6-7 s_full, 8-9 s_empty,
+  //           10-11 p_full, 12-13 p_empty, 14-15 pv_full, 16-17 pv_empty, 18 q_full1, 19 q_empty1
   auto bar = [&](int i) { return bars + 8u * i; };
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + kOffBar + 8 * 18);
+  auto qfull = [&](uint32_t qb) { return bar(qb ? 18 : 0); };
+  auto qempty = [&](uint32_t qb) { return bar(qb ? 19 : 1); };
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + kOffBar + 8 * 20);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tm);
-    mbar_init(bar(0), 1); mbar_init(bar(1), 1);
+    mbar_init(bar(0), 1); mbar_init(bar(1), 1); mbar_init(bar(18), 1); mbar_init(bar(19), 1);
     for (int i = 0; i < 2; ++i) {
       mbar_init(bar(2 + i), 1); mbar_init(bar(4 + i), 1);
-      mbar_init(bar(6 + i), 1); mbar_init(bar(8 + i), 4);
-      mbar_init(bar(10 + i), 4); mbar_init(bar(12 + i), 1);
-      mbar_init(bar(14 + i), 1); mbar_init(bar(16 + i), 4);
+      mbar_init(bar(6 + i), 1); mbar_init(bar(8 + i), 8);
+      mbar_init(bar(10 + i), 8); mbar_init(bar(12 + i), 1);
+      mbar_init(bar(14 + i), 1); mbar_init(bar(16 + i), 8);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
@@ -114,9 +118,10 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         int qt, h, b;
         item_coords(it, qt, h, b);
         const int row0 = b * a.seq;
-        mbar_wait(bar(1), (it_local & 1u) ^ 1u);
-        mbar_expect_tx(bar(0), kTileBytes);
-        tma_load_2d(sQ, &tm, bar(0), h * 64, row0 + qt * 128);
+        const uint32_t qb = it_local & 1u, qph = (it_local >> 1) & 1u;
+        mbar_wait(qempty(qb), qph ^ 1u);
+        mbar_expect_tx(qfull(qb), kTileBytes);
+        tma_load_2d(sQ + qb * kTileBytes, &tm, qfull(qb), h * 64, row0 + qt * 128);
         const int nkb = n_blocks(qt);
         for (int j = 0; j < nkb; ++j, ++kvc) {
           const uint32_t st = kvc & 1u, ph = (kvc >> 1) & 1u;
@@ -158,7 +163,8 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       int qt, h, b;
       item_coords(it, qt, h, b);
       const int nkb = n_blocks(qt);
-      mbar_wait(bar(0), it_local & 1u);
+      const uint32_t qb = it_local & 1u;
+      mbar_wait(qfull(qb), (it_local >> 1) & 1u);
       for (int j = 0; j < nkb; ++j) {
         const uint32_t c = sc + j, kv = kvc + j;
         const uint32_t sb = c & 1u, ph = (c >> 1) & 1u;
@@ -168,12 +174,12 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         if (lane == 0) {
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk) {
-            const uint64_t ad = desc_sw128(sQ + kk * 32, 16, 1024);
+            const uint64_t ad = desc_sw128(sQ + qb * kTileBytes + kk * 32, 16, 1024);
             const uint64_t bd = desc_sw128(sK + (kv & 1u) * kTileBytes + kk * 32, 16, 1024);
             tc_mma_f16(tmem + sb * 128, ad, bd, idesc_s, kk != 0 ? 1u : 0u);
           }
           tc_commit(bar(6 + sb));                 // S ready
-          if (j == nkb - 1) tc_commit(bar(1));    // Q no longer needed
+          if (j == nkb - 1) tc_commit(qempty(qb));  // Q buffer no longer needed
         }
         __syncwarp();
         if (j >= 1) issue_pv(c - 1, kv - 1);
@@ -184,56 +190,75 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     }
   } else {
     // ================= softmax / output =================
-    const int quarter = warp & 3;
-    const int r = quarter * 32 + lane;           // row of the 128-query tile
+    // warp pair (quarter q, half h): rows 32q..32q+31, key columns [64h, 64h+64)
+    // of S, output columns [32h, 32h+32).  Only the row max is exchanged.
+    const int quarter = warp & 3, half = (warp - 2) >> 2;
+    const int r = quarter * 32 + lane;
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+    float* red = reinterpret_cast<float*>(gbase + kOffRed);   // [2][128]
+    auto pair_sync = [&]() { asm volatile("bar.sync %0, 64;\n" ::"r"(1 + quarter) : "memory"); };
     uint32_t sc = 0;
     for (int it = blockIdx.x; it < a.items; it += gridDim.x) {
       int qt, h, b;
       item_coords(it, qt, h, b);
       const int nkb = n_blocks(qt);
       const int qi = qt * 128 + r;
-      float m = -INFINITY, l = 0.f;
-      float o[64];
+      float m = -INFINITY, l = 0.f, alpha_prev = 0.f;
+      float o[32];
 #pragma unroll
-      for (int i = 0; i < 64; ++i) o[i] = 0.f;
+      for (int i = 0; i < 32; ++i) o[i] = 0.f;
+      // O <- O * alpha_c + PV_c  (alpha_c rescales O to block c's running max)
+      auto accumulate_pv = [&](uint32_t cc, float al) {
+        const uint32_t pb = cc & 1u, pph = (cc >> 1) & 1u;
+        mbar_wait(bar(14 + pb), pph);
+        tc_fence_after();
+        uint32_t pv[32];
+        tmem_ld_32x32b_x32_nw(tmem + 256 + pb * 64 + half * 32 + lane_off, pv);
+        tmem_wait_ld();
+#pragma unroll
+        for (int i = 0; i < 32; ++i) o[i] = fmaf(o[i], al, __uint_as_float(pv[i]));
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(bar(16 + pb));
+      };
       for (int j = 0; j < nkb; ++j) {
         const uint32_t c = sc + j, sb = c & 1u, ph = (c >> 1) & 1u;
         const bool need_mask = (j * 128 + 127 > qt * 128) || ((j + 1) * 128 > a.seq);
         mbar_wait(bar(6 + sb), ph);
         tc_fence_after();
-        // all 128 scores of this row in registers: 4 TMEM loads in flight, one wait
-        uint32_t sv[4][32];
-#pragma unroll
-        for (int ch = 0; ch < 4; ++ch) tmem_ld_32x32b_x32_nw(tmem + sb * 128 + ch * 32 + lane_off, sv[ch]);
+        uint32_t sv[2][32];
+        tmem_ld_32x32b_x32_nw(tmem + sb * 128 + half * 64 + lane_off, sv[0]);
+        tmem_ld_32x32b_x32_nw(tmem + sb * 128 + half * 64 + 32 + lane_off, sv[1]);
         tmem_wait_ld();
-        float mx0 = -INFINITY, mx1 = -INFINITY;
         if (need_mask) {
 #pragma unroll
-          for (int ch = 0; ch < 4; ++ch)
+          for (int ch = 0; ch < 2; ++ch)
 #pragma unroll
             for (int i = 0; i < 32; ++i) {
-              const int ki = j * 128 + ch * 32 + i;
+              const int ki = j * 128 + half * 64 + ch * 32 + i;
               if (!(ki <= qi && ki < a.seq)) sv[ch][i] = __float_as_uint(-INFINITY);
             }
         }
+        float mx0 = -INFINITY, mx1 = -INFINITY;
 #pragma unroll
-        for (int ch = 0; ch < 4; ++ch)
+        for (int ch = 0; ch < 2; ++ch)
 #pragma unroll
           for (int i = 0; i < 32; i += 2) {
             mx0 = fmaxf(mx0, __uint_as_float(sv[ch][i]));
             mx1 = fmaxf(mx1, __uint_as_float(sv[ch][i + 1]));
           }
-        const float m_new = fmaxf(m, fmaxf(mx0, mx1));
+        red[half * 128 + r] = fmaxf(mx0, mx1);
+        pair_sync();
+        const float mx = fmaxf(red[r], red[128 + r]);
+        pair_sync();                              // both read before the next block overwrites
+        const float m_new = fmaxf(m, mx);
         const float mb = m_new == -INFINITY ? 0.f : m_new * a.sl2;
         const float alpha = m == -INFINITY ? 0.f : ex2_approx(fmaf(m, a.sl2, -mb));
-        // P buffer free (the PV MMA two blocks ago has read it)
-        mbar_wait(bar(12 + sb), ph ^ 1u);
-        // P = exp2(s*sl2 - m*sl2) -> bf16 -> smem (K-major SW128)
+        mbar_wait(bar(12 + sb), ph ^ 1u);         // P buffer free
         float sum0 = 0.f, sum1 = 0.f;
-        const uint32_t prow = sP + sb * kPBytes;
+        const uint32_t region = sP + sb * kPBytes + half * kTileBytes + r * 128;   // this half's K-chunk
 #pragma unroll
-        for (int ch = 0; ch < 4; ++ch) {
+        for (int ch = 0; ch < 2; ++ch) {
           uint32_t pk[16];
 #pragma unroll
           for (int i = 0; i < 32; i += 2) {
@@ -244,47 +269,36 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
             __nv_bfloat162 h2 = __floats2bfloat162_rn(p0, p1);
             pk[i >> 1] = *reinterpret_cast<uint32_t*>(&h2);
           }
-          const uint32_t region = prow + (ch >> 1) * kTileBytes + r * 128;
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
-            const int chunk = (ch & 1) * 4 + q;
+            const int chunk = ch * 4 + q;
             const uint32_t addr = region + ((chunk ^ (r & 7)) << 4);
             asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};\n" ::"r"(addr), "r"(pk[4 * q]),
                          "r"(pk[4 * q + 1]), "r"(pk[4 * q + 2]), "r"(pk[4 * q + 3])
                          : "memory");
           }
         }
-        const float sum = sum0 + sum1;
         tc_fence_before();
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) { mbar_arrive(bar(8 + sb)); mbar_arrive(bar(10 + sb)); }   // S read, P written
-        l = fmaf(l, alpha, sum);
+        l = fmaf(l, alpha, sum0 + sum1);          // this half's running sum
         m = m_new;
-        // O = O * alpha + P_j V_j
-        mbar_wait(bar(14 + sb), ph);
-        tc_fence_after();
-        {
-          uint32_t pv[2][32];
-          tmem_ld_32x32b_x32_nw(tmem + 256 + sb * 64 + lane_off, pv[0]);
-          tmem_ld_32x32b_x32_nw(tmem + 256 + sb * 64 + 32 + lane_off, pv[1]);
-          tmem_wait_ld();
-#pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            o[i] = fmaf(o[i], alpha, __uint_as_float(pv[0][i]));
-            o[32 + i] = fmaf(o[32 + i], alpha, __uint_as_float(pv[1][i]));
-          }
-        }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(bar(16 + sb));
+        // deferred: fold PV of the PREVIOUS block (ready while we computed this one)
+        if (j > 0) accumulate_pv(c - 1, alpha_prev);
+        alpha_prev = alpha;
       }
+      accumulate_pv(sc + nkb - 1, alpha_prev);
       sc += nkb;
+      red[half * 128 + r] = l;
+      pair_sync();
+      const float lt = red[r] + red[128 + r];
+      pair_sync();
       if (qi < a.seq) {
-        const float inv = l > 0.f ? 1.f / l : 0.f;
-        __nv_bfloat16* out = a.ctx + ((int64_t)b * a.seq + qi) * a.ldc + (int64_t)h * 64;
+        const float inv = lt > 0.f ? 1.f / lt : 0.f;
+        __nv_bfloat16* out = a.ctx + ((int64_t)b * a.seq + qi) * a.ldc + (int64_t)h * 64 + half * 32;
 #pragma unroll
-        for (int i = 0; i < 64; i += 8) {
+        for (int i = 0; i < 32; i += 8) {
           uint32_t pk[4];
 #pragma unroll
           for (int k = 0; k < 4; ++k) {

@@ -83,11 +83,10 @@ __device__ __forceinline__ void box_muller(uint32_t a, uint32_t b, float& z0, fl
   const float u1 = 2.0f - __uint_as_float(0x3F800000u | (a >> 9));
   const float ang = fmaf(__uint_as_float(0x40000000u | (b >> 9)), 3.14159265358979f, -9.42477796076938f);
   // single MUFU ops, flush-to-zero (u1 >= 2^-23 and |ang| <= pi: no denormals)
-  float lg, rs, s, c;
+  float lg, r, s, c;
   asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(lg) : "f"(u1));
   const float t = -1.3862943611198906f * lg;                                      // -2 ln u >= 0
-  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(rs) : "f"(t));
-  const float r = t > 0.f ? t * rs : 0.f;          // u1 == 1 gives t = 0 (rsqrt = inf)
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(t));                          // one MUFU, sqrt(0) = 0
   asm("sin.approx.ftz.f32 %0, %1;" : "=f"(s) : "f"(ang));
   asm("cos.approx.ftz.f32 %0, %1;" : "=f"(c) : "f"(ang));
   z0 = r * c;
@@ -206,6 +205,7 @@ struct PuParams {
   const double* z_cur;
   const double* z_prev;
   int64_t z_key0;
+  int32_t* block_done;   // optional: per-block tile-completion counters (segment.reserved = block)
 };
 
 // ---------------------------------------------------------------------------

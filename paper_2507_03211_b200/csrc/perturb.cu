@@ -101,24 +101,29 @@ __device__ __forceinline__ void pu_group(const PuParams& p, const ZoSegment& s, 
 
 
 // Fast tile: Philox direction, every group 16-B aligned (all real model
-// tensors).  Specialised at compile time on (pending update, shadows, bf16) so
-// the hot loop has no runtime-flag branches; 32-bit lane offsets from per-tile
-// base pointers; the lane's groups run their Philox streams in lockstep.
-template <bool PEND, bool BF16>
-__device__ __forceinline__ void pu_tile_fast_t(const PuParams& p, int64_t e0, int ngroups, int64_t dbase,
-                                               bool SA, bool SB, float sa, float sb, uint64_t seed_cur,
-                                               uint64_t seed_prev, float lrg32, int lane) {
-  constexpr int G = kPuGroupsPerThread;
+// tensors).  Specialised at compile time on (pending update, bf16) so the hot
+// loop has no runtime-flag branches; 32-bit lane offsets from per-tile base
+// pointers; the lane's groups run their Philox streams in lockstep.  The
+// caller loads theta (one tile ahead).
+template <int G>
+__device__ __forceinline__ void pu_load_fast(const PuParams& p, int64_t e0, int ngroups, int lane, float4 (&th)[G]) {
+  const float4* tp = reinterpret_cast<const float4*>(p.theta + (e0 - p.theta_key0)) + lane;
+  const bool full = ngroups >= 32 * G;
+#pragma unroll
+  for (int g = 0; g < G; ++g)
+    if (full || lane + 32 * g < ngroups) th[g] = tp[32 * g];
+}
+
+template <bool PEND, bool BF16, int G>
+__device__ __forceinline__ void pu_compute_fast(const PuParams& p, int64_t e0, int ngroups, int64_t dbase,
+                                                bool SA, bool SB, float sa, float sb, uint64_t seed_cur,
+                                                uint64_t seed_prev, float lrg32, int lane, float4 (&th)[G]) {
   float4* tp = reinterpret_cast<float4*>(p.theta + (e0 - p.theta_key0)) + lane;
   const uint64_t qa = (uint64_t)(e0 >> 2) + (uint64_t)lane;
-  const bool full = ngroups == 32 * G;
-  float4 th[G];
+  const bool full = ngroups >= 32 * G;
   uint64_t q[G];
 #pragma unroll
-  for (int g = 0; g < G; ++g) {
-    q[g] = qa + (uint64_t)(32 * g);
-    if (full || lane + 32 * g < ngroups) th[g] = tp[32 * g];
-  }
+  for (int g = 0; g < G; ++g) q[g] = qa + (uint64_t)(32 * g);
   if constexpr (PEND) {
     u32x4 r[G];
     philox4x32_10_xn<G>(q, seed_prev, r);
@@ -158,28 +163,170 @@ __device__ __forceinline__ void pu_tile_fast_t(const PuParams& p, int64_t e0, in
   }
 }
 
-__device__ __forceinline__ void pu_tile_fast(const PuParams& p, int64_t e0, int ngroups, int64_t dbase,
-                                             bool pending, bool want_sh, const bool (&sh)[2],
-                                             const float (&sc32)[2], uint64_t seed_cur, uint64_t seed_prev,
-                                             float lrg32, int kind, int lane) {
-  const bool sa = want_sh && sh[0], sb = want_sh && sh[1];
-  if (kind == ZO_SHADOW_BF16) {
-    if (pending) pu_tile_fast_t<true, true>(p, e0, ngroups, dbase, sa, sb, sc32[0], sc32[1], seed_cur, seed_prev, lrg32, lane);
-    else pu_tile_fast_t<false, true>(p, e0, ngroups, dbase, sa, sb, sc32[0], sc32[1], seed_cur, seed_prev, lrg32, lane);
-  } else {
-    if (pending) pu_tile_fast_t<true, false>(p, e0, ngroups, dbase, sa, sb, sc32[0], sc32[1], seed_cur, seed_prev, lrg32, lane);
-    else pu_tile_fast_t<false, false>(p, e0, ngroups, dbase, sa, sb, sc32[0], sc32[1], seed_cur, seed_prev, lrg32, lane);
+// Background tile body: all four theta groups are loaded up front (the
+// memory parallelism a 4-warp CTA needs), then one Philox chain at a time
+// (registers stay under the 80 that let the CTA sit beside a GEMM CTA).
+template <bool PEND, bool BF16>
+__device__ __forceinline__ void pu_tile_bg_t(const PuParams& p, int64_t e0, int ngroups, int64_t dbase,
+                                             bool SA, bool SB, float sa, float sb, uint64_t seed_cur,
+                                             uint64_t seed_prev, float lrg32, int lane) {
+  constexpr int G = kPuGroupsPerThread;
+  float4* tp = reinterpret_cast<float4*>(p.theta + (e0 - p.theta_key0)) + lane;
+  const uint64_t qa = (uint64_t)(e0 >> 2) + (uint64_t)lane;
+  const bool full = ngroups == 32 * G;
+  float4 th[G];
+#pragma unroll
+  for (int g = 0; g < G; ++g)
+    if (full || lane + 32 * g < ngroups) th[g] = tp[32 * g];
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    if (!full && lane + 32 * g >= ngroups) break;
+    const uint64_t q = qa + (uint64_t)(32 * g);
+    float4 t = th[g];
+    if constexpr (PEND) {
+      const f32x4 zp = philox_normal4(seed_prev, q);
+      t.x = fmaf(-lrg32, zp.x, t.x); t.y = fmaf(-lrg32, zp.y, t.y);
+      t.z = fmaf(-lrg32, zp.z, t.z); t.w = fmaf(-lrg32, zp.w, t.w);
+      tp[32 * g] = t;
+    }
+    if (SA || SB) {
+      const f32x4 z = philox_normal4(seed_cur, q);
+#pragma unroll
+      for (int d = 0; d < 2; ++d) {
+        if ((d == 0 && !SA) || (d == 1 && !SB)) continue;
+        const float sc = d == 0 ? sa : sb;
+        const float a = fmaf(sc, z.x, t.x), b = fmaf(sc, z.y, t.y);
+        const float c = fmaf(sc, z.z, t.z), e = fmaf(sc, z.w, t.w);
+        if constexpr (BF16) {
+          __nv_bfloat162 lo2 = __floats2bfloat162_rn(a, b), hi2 = __floats2bfloat162_rn(c, e);
+          uint2 pk;
+          pk.x = *reinterpret_cast<uint32_t*>(&lo2);
+          pk.y = *reinterpret_cast<uint32_t*>(&hi2);
+          (reinterpret_cast<uint2*>(p.wsh[d] + dbase) + lane)[32 * g] = pk;
+        } else {
+          (reinterpret_cast<float4*>(p.vsh[d] + dbase) + lane)[32 * g] = make_float4(a, b, c, e);
+        }
+      }
+    }
   }
 }
 
-// Warp-independent streaming: each warp owns 512-element tiles (32 lanes x 4
-// groups of 4 elements, +1 group when a tile starts mid-group), looks up its
-// segment by binary search in the shared-memory prefix table and never
-// synchronises with other warps, so loads of one warp overlap the
-// Philox/Box-Muller math and stores of the others.  Each lane issues all of
-// its theta loads (float4, coalesced 512 B per warp per group) before any math.
+__device__ __forceinline__ void pu_tile_fast(const PuParams& p, int64_t e0, int ngroups, int64_t dbase,
+                                             bool pending, bool want_sh, const bool (&sh)[2],
+                                             const float (&sc32)[2], uint64_t seed_cur, uint64_t seed_prev,
+                                             float lrg32, int kind, int lane, float4 (&th)[kPuGroupsPerThread]) {
+  constexpr int G = kPuGroupsPerThread;
+  const bool sa = want_sh && sh[0], sb = want_sh && sh[1];
+  if (kind == ZO_SHADOW_BF16) {
+    if (pending) pu_compute_fast<true, true, G>(p, e0, ngroups, dbase, sa, sb, sc32[0], sc32[1], seed_cur, seed_prev, lrg32, lane, th);
+    else pu_compute_fast<false, true, G>(p, e0, ngroups, dbase, sa, sb, sc32[0], sc32[1], seed_cur, seed_prev, lrg32, lane, th);
+  } else {
+    if (pending) pu_compute_fast<true, false, G>(p, e0, ngroups, dbase, sa, sb, sc32[0], sc32[1], seed_cur, seed_prev, lrg32, lane, th);
+    else pu_compute_fast<false, false, G>(p, e0, ngroups, dbase, sa, sb, sc32[0], sc32[1], seed_cur, seed_prev, lrg32, lane, th);
+  }
+}
+
+__device__ __forceinline__ void pu_tile_bg(const PuParams& p, int64_t e0, int ngroups, int64_t dbase,
+                                           bool pending, bool want_sh, const bool (&sh)[2],
+                                           const float (&sc32)[2], uint64_t seed_cur, uint64_t seed_prev,
+                                           float lrg32, int kind, int lane) {
+  const bool sa = want_sh && sh[0], sb = want_sh && sh[1];
+  if (kind == ZO_SHADOW_BF16) {
+    if (pending) pu_tile_bg_t<true, true>(p, e0, ngroups, dbase, sa, sb, sc32[0], sc32[1], seed_cur, seed_prev, lrg32, lane);
+    else pu_tile_bg_t<false, true>(p, e0, ngroups, dbase, sa, sb, sc32[0], sc32[1], seed_cur, seed_prev, lrg32, lane);
+  } else {
+    if (pending) pu_tile_bg_t<true, false>(p, e0, ngroups, dbase, sa, sb, sc32[0], sc32[1], seed_cur, seed_prev, lrg32, lane);
+    else pu_tile_bg_t<false, false>(p, e0, ngroups, dbase, sa, sb, sc32[0], sc32[1], seed_cur, seed_prev, lrg32, lane);
+  }
+}
+
+// publish one finished tile of a block: every lane fences its own stores at
+// gpu scope, then one lane bumps the block counter
+__device__ __forceinline__ void tile_done(const PuParams& p, int32_t block) {
+  __threadfence();
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) atomicAdd(p.block_done + block, 1);
+}
+
+// Generic tile (unaligned groups, oracle z, shadow-less segments): one group
+// per lane at a time, element-guarded; rare, so kept register-light.
 template <int ZMODE>
-__global__ void __launch_bounds__(kPuThreads, 4) perturb_update_kernel(const PuParams p) {
+__device__ __noinline__ void pu_tile_generic(const PuParams& p, const ZoSegment& s, int64_t e0, int64_t e1,
+                                             int64_t drow, bool theta_vec, bool pending, bool need_z,
+                                             const bool (&sh)[2], const float (&sc32)[2], uint64_t seed_cur,
+                                             uint64_t seed_prev, double lrg64, float lrg32, int lane) {
+  const bool want_sh = s.kind != ZO_SHADOW_NONE;
+  const int64_t qa = e0 >> 2, qb = (e1 + 3) >> 2;
+  for (int64_t q = qa + lane; q < qb; q += 32) {
+    const int64_t eg = q << 2;
+    const bool full = eg >= e0 && eg + 4 <= e1;
+    float th[4];
+    if (full && theta_vec) {
+      const float4 v4 = *reinterpret_cast<const float4*>(p.theta + (eg - p.theta_key0));
+      th[0] = v4.x; th[1] = v4.y; th[2] = v4.z; th[3] = v4.w;
+    } else {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) th[i] = (eg + i >= e0 && eg + i < e1) ? p.theta[eg + i - p.theta_key0] : 0.f;
+    }
+    pu_group<ZMODE>(p, s, q, e0, e1, drow, th, full, theta_vec, pending, need_z, want_sh, sh, sc32, seed_cur,
+                    seed_prev, lrg64, lrg32);
+  }
+}
+
+// Walks the tiles of a contiguous chunk in order: one prefix search per
+// chunk, then row / column-tile counters advance without division.
+struct PuCursor {
+  int si;
+  int64_t t, seg_end;          // current tile, first tile of the next segment
+  ZoSegment s;
+  uint32_t tpr, row, ct;       // tiles per row, row, column tile
+
+  __device__ __forceinline__ void load_seg(const PuParams& p, const int64_t* pref, int64_t local) {
+    s = p.segs[si];
+    seg_end = pref[si + 1];
+    tpr = (uint32_t)((s.cols + kPuTile - 1) / kPuTile);
+    if (s.rows == 1) { row = 0; ct = (uint32_t)local; }
+    else { row = (uint32_t)local / tpr; ct = (uint32_t)local - row * tpr; }
+  }
+  __device__ __forceinline__ void seek(const PuParams& p, const int64_t* pref, int64_t t0) {
+    int lo = 0, hi = p.n_segs - 1;     // last segment with pref[lo] <= t0 (skips empty segments)
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (pref[mid] <= t0) lo = mid; else hi = mid - 1;
+    }
+    si = lo;
+    t = t0;
+    load_seg(p, pref, t0 - pref[lo]);
+  }
+  __device__ __forceinline__ void next(const PuParams& p, const int64_t* pref) {
+    ++t;
+    if (t >= seg_end) {
+      do { ++si; } while (pref[si + 1] <= t);
+      load_seg(p, pref, 0);
+    } else if (++ct == tpr && s.rows > 1) {
+      ct = 0;
+      ++row;
+    }
+  }
+  // tile extent in theta keys and the destination offset (dst - src) of its row
+  __device__ __forceinline__ void geo(int64_t& e0, int64_t& e1, int64_t& drow) const {
+    const int64_t c0 = (int64_t)ct * kPuTile;
+    const int64_t c1 = min(c0 + kPuTile, s.cols);
+    const int64_t rk = s.src + (int64_t)row * s.cols;
+    e0 = rk + c0;
+    e1 = rk + c1;
+    drow = s.dst + (int64_t)row * s.dst_ld - rk;
+  }
+};
+
+// Warp-independent streaming over chunks of kPuChunk consecutive tiles (512
+// elements each = 32 lanes x 4 groups of 4).  Warps never synchronise with
+// each other; within a chunk the next fast tile's theta is loaded before the
+// current tile's Philox/Box-Muller math, so the loads overlap the compute.
+constexpr int kPuChunk = 8;
+
+template <int ZMODE, bool BG>
+__device__ __forceinline__ void perturb_update_body(const PuParams& p) {
   extern __shared__ int64_t s_prefix[];
   pdl_trigger();
   pdl_wait();
@@ -187,6 +334,7 @@ __global__ void __launch_bounds__(kPuThreads, 4) perturb_update_kernel(const PuP
   if (prefix_in_smem)
     for (int i = threadIdx.x; i <= p.n_segs; i += kPuThreads) s_prefix[i] = p.prefix[i];
   __syncthreads();
+  const int64_t* pref = prefix_in_smem ? s_prefix : p.prefix;
   const bool pending = (p.flags & ZO_PU_UPDATE) && p.scal->pending != 0;
   const uint64_t seed_cur = p.scal->seed_cur;
   const uint64_t seed_prev = p.scal->seed_prev;
@@ -196,82 +344,100 @@ __global__ void __launch_bounds__(kPuThreads, 4) perturb_update_kernel(const PuP
   const float sc32[2] = {(float)p.scale[0], (float)p.scale[1]};
   const bool need_z = (sh[0] && p.scale[0] != 0.0) || (sh[1] && p.scale[1] != 0.0);
   const bool theta_vec = ((p.theta_key0 & 3) == 0) && ((reinterpret_cast<uintptr_t>(p.theta) & 15) == 0);
-  constexpr int G = kPuGroupsPerThread + 1;
+  const bool fast_ok = ZMODE == ZO_Z_PHILOX && theta_vec;
   const int lane = threadIdx.x & 31;
   const int64_t warp0 = (blockIdx.x * (int64_t)kPuThreads + threadIdx.x) >> 5;
   const int64_t n_warps = ((int64_t)gridDim.x * kPuThreads) >> 5;
+  const int64_t n_chunks = (p.n_tiles + kPuChunk - 1) / kPuChunk;
 
-  for (int64_t t = warp0; t < p.n_tiles; t += n_warps) {
-    int lo = 0, hi = p.n_segs - 1;          // warp-uniform search (LDS broadcast reads)
-    if (prefix_in_smem) {
-      while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (s_prefix[mid] <= t) lo = mid; else hi = mid - 1;
-      }
-    } else {
-      while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (p.prefix[mid] <= t) lo = mid; else hi = mid - 1;
-      }
-    }
-    const ZoSegment s = p.segs[lo];
-    const uint32_t local = (uint32_t)(t - (prefix_in_smem ? s_prefix[lo] : p.prefix[lo]));
-    int64_t row, c0;
-    if (s.rows == 1) {                      // flat tensor: no division
-      row = 0;
-      c0 = (int64_t)local * kPuTile;
-    } else {
-      const uint32_t tpr = (uint32_t)((s.cols + kPuTile - 1) / kPuTile);
-      row = local / tpr;
-      c0 = (int64_t)(local - (uint32_t)row * tpr) * kPuTile;
-    }
-    const int64_t c1 = min(c0 + kPuTile, s.cols);
-    const int64_t rk = s.src + row * s.cols;
-    const int64_t e0 = rk + c0, e1 = rk + c1;
-    const int64_t drow = s.dst + row * s.dst_ld - rk;
-    const bool want_sh = s.kind != ZO_SHADOW_NONE;
-    const int64_t qa = e0 >> 2, qb = (e1 + 3) >> 2;
-    const bool any_sh = want_sh && (sh[0] || sh[1]);
-    if (ZMODE == ZO_Z_PHILOX && theta_vec && ((e0 | e1 | (e0 + drow)) & 3) == 0 && (need_z || !any_sh)) {
-      pu_tile_fast(p, e0, (int)((e1 - e0) >> 2), e0 + drow, pending, want_sh, sh, sc32, seed_cur, seed_prev,
-                   lrg32, s.kind, lane);
-      continue;
-    }
-
-    float th[G][4];
-    bool fullg[G];
+  for (int64_t c = warp0; c < n_chunks; c += n_warps) {
+    const int64_t t_end = min((c + 1) * kPuChunk, p.n_tiles);
+    PuCursor cur;
+    cur.seek(p, pref, c * kPuChunk);
+    int64_t e0, e1, drow;
+    cur.geo(e0, e1, drow);
+    auto is_fast = [&](const ZoSegment& s, int64_t a0, int64_t a1, int64_t dr) {
+      const bool any_sh = s.kind != ZO_SHADOW_NONE && (sh[0] || sh[1]);
+      return fast_ok && ((a0 | a1 | (a0 + dr)) & 3) == 0 && (need_z || !any_sh);
+    };
+    bool fast = is_fast(cur.s, e0, e1, drow);
+    float4 th[kPuGroupsPerThread];
+    if (!BG && fast) pu_load_fast<kPuGroupsPerThread>(p, e0, (int)((e1 - e0) >> 2), lane, th);
+    while (true) {
+      const ZoSegment s = cur.s;
+      const int64_t ce0 = e0, ce1 = e1, cdrow = drow;
+      const bool cfast = fast;
+      float4 thc[kPuGroupsPerThread];
 #pragma unroll
-    for (int g = 0; g < G; ++g) {
-      const int64_t q = qa + lane + (int64_t)g * 32;
-      const int64_t eg = q << 2;
-      fullg[g] = q < qb && eg >= e0 && eg + 4 <= e1;
-      if (fullg[g] && theta_vec) {
-        const float4 v4 = *reinterpret_cast<const float4*>(p.theta + (eg - p.theta_key0));
-        th[g][0] = v4.x; th[g][1] = v4.y; th[g][2] = v4.z; th[g][3] = v4.w;
+      for (int g = 0; g < kPuGroupsPerThread; ++g) thc[g] = th[g];
+      const bool more = cur.t + 1 < t_end;
+      if (more) {                                   // prefetch the next tile's theta
+        cur.next(p, pref);
+        cur.geo(e0, e1, drow);
+        fast = is_fast(cur.s, e0, e1, drow);
+        if (!BG && fast) pu_load_fast<kPuGroupsPerThread>(p, e0, (int)((e1 - e0) >> 2), lane, th);
+      }
+      if (cfast) {
+        if constexpr (BG)
+          pu_tile_bg(p, ce0, (int)((ce1 - ce0) >> 2), ce0 + cdrow, pending, s.kind != ZO_SHADOW_NONE, sh, sc32,
+                     seed_cur, seed_prev, lrg32, s.kind, lane);
+        else
+          pu_tile_fast(p, ce0, (int)((ce1 - ce0) >> 2), ce0 + cdrow, pending, s.kind != ZO_SHADOW_NONE, sh, sc32,
+                       seed_cur, seed_prev, lrg32, s.kind, lane, thc);
       } else {
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-          th[g][i] = (q < qb && eg + i >= e0 && eg + i < e1) ? p.theta[eg + i - p.theta_key0] : 0.f;
+        pu_tile_generic<ZMODE>(p, s, ce0, ce1, cdrow, theta_vec, pending, need_z, sh, sc32, seed_cur, seed_prev,
+                               lrg64, lrg32, lane);
       }
-    }
-#pragma unroll
-    for (int g = 0; g < G; ++g) {
-      const int64_t q = qa + lane + (int64_t)g * 32;
-      if (q < qb)
-        pu_group<ZMODE>(p, s, q, e0, e1, drow, th[g], fullg[g], theta_vec, pending, need_z, want_sh, sh, sc32,
-                        seed_cur, seed_prev, lrg64, lrg32);
+      if (p.block_done) tile_done(p, s.reserved);
+      if (!more) break;
     }
   }
 }
 
-int perturb_update_launch(const PuParams& p, int zmode, cudaStream_t stream) {
+template <int ZMODE>
+__global__ void __launch_bounds__(kPuThreads, 4) perturb_update_kernel(const PuParams p) {
+  perturb_update_body<ZMODE, false>(p);
+}
+
+// 88 registers x 4 warps fit in what a 168-register 10-warp GEMM CTA leaves
+template <int ZMODE>
+__global__ void __maxnreg__(88) perturb_update_bg_kernel(const PuParams p) {
+  perturb_update_body<ZMODE, true>(p);
+}
+
+int perturb_update_launch(const PuParams& p, int zmode, cudaStream_t stream, bool background) {
   if (p.n_tiles <= 0) return ZO_OK;
-  const int64_t want = (int64_t)num_sms() * 8;   // 8 x 128 threads per SM
+  const int64_t want = (int64_t)num_sms() * (background ? 1 : 8);
   const int grid = (int)(p.n_tiles < want ? p.n_tiles : want);
   const size_t smem = p.n_segs + 1 <= kPuMaxSmemSegs ? (size_t)(p.n_segs + 1) * sizeof(int64_t) : 0;
-  if (zmode == ZO_Z_PHILOX) launch_k(perturb_update_kernel<ZO_Z_PHILOX>, dim3(grid), dim3(kPuThreads), smem, stream, p);
-  else launch_k(perturb_update_kernel<ZO_Z_ORACLE>, dim3(grid), dim3(kPuThreads), smem, stream, p);
+  if (background) {
+    if (zmode == ZO_Z_PHILOX)
+      launch_k(perturb_update_bg_kernel<ZO_Z_PHILOX>, dim3(grid), dim3(kPuThreads), smem, stream, p);
+    else
+      launch_k(perturb_update_bg_kernel<ZO_Z_ORACLE>, dim3(grid), dim3(kPuThreads), smem, stream, p);
+  } else {
+    if (zmode == ZO_Z_PHILOX)
+      launch_k(perturb_update_kernel<ZO_Z_PHILOX>, dim3(grid), dim3(kPuThreads), smem, stream, p);
+    else
+      launch_k(perturb_update_kernel<ZO_Z_ORACLE>, dim3(grid), dim3(kPuThreads), smem, stream, p);
+  }
   return launch_status("perturb_update_kernel");
+}
+
+// spin until *counter >= target (one thread); gates a forward stream on the
+// background perturb pass having finished a block
+__global__ void wait_counter_kernel(const int32_t* counter, int32_t target) {
+  int32_t v;
+  while (true) {
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(counter) : "memory");
+    if (v >= target) break;
+    __nanosleep(256);
+  }
+}
+
+int wait_counter_launch(const int32_t* counter, int32_t target, cudaStream_t stream) {
+  wait_counter_kernel<<<1, 1, 0, stream>>>(counter, target);
+  return launch_status("wait_counter_kernel");
 }
 
 // ---------------------------------------------------------------------------

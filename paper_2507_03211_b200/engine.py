@@ -124,13 +124,17 @@ def block_extent(plan: ShadowPlan, bid: int):
 class SegTable:
     """Device copy of a segment list + its tile prefix."""
 
-    def __init__(self, segs, device):
+    def __init__(self, segs, device, block_ids=None):
         tile = int(L.lib().zo_perturb_tile_elems())
         arr = (L.ZoSegment * max(1, len(segs)))()
         prefix = np.zeros(len(segs) + 1, dtype=np.int64)
-        for i, (src, rows, cols, dst, ld, kind) in enumerate(segs):
-            arr[i] = L.ZoSegment(src, rows, cols, dst, ld, kind, 0)
-            prefix[i + 1] = prefix[i] + rows * ((cols + tile - 1) // tile)
+        block_ids = block_ids or [0] * len(segs)
+        self.block_tiles = {}     # block id -> tiles (the completion target of zo_perturb_update_bg)
+        for i, ((src, rows, cols, dst, ld, kind), bid) in enumerate(zip(segs, block_ids)):
+            arr[i] = L.ZoSegment(src, rows, cols, dst, ld, kind, bid)
+            n = rows * ((cols + tile - 1) // tile)
+            prefix[i + 1] = prefix[i] + n
+            self.block_tiles[bid] = self.block_tiles.get(bid, 0) + n
         raw = np.frombuffer(bytes(arr), dtype=np.uint8).copy()
         self.segs = torch.from_numpy(raw).to(device)
         self.prefix = torch.from_numpy(prefix).to(device)
@@ -198,9 +202,10 @@ class DeviceStore:
         for s in self.directions:
             self.wsh[s] = torch.zeros(self.plan.w_elems, dtype=torch.bfloat16, device=self.device)
             self.vsh[s] = torch.zeros(self.plan.v_elems, dtype=torch.float32, device=self.device)
-        self.block_tables = {bid: SegTable(segs, self.device) for bid, segs in self.plan.segments.items()}
-        self.model_table = SegTable([s for bid in sorted(self.plan.segments) for s in self.plan.segments[bid]],
-                                    self.device)
+        self.block_tables = {bid: SegTable(segs, self.device, [bid] * len(segs))
+                             for bid, segs in self.plan.segments.items()}
+        self.model_table = self.range_table(0, len(self.layouts))
+        self.block_done = torch.zeros(len(self.layouts), dtype=torch.int32, device=self.device)
         self.scal = torch.zeros(4, dtype=torch.int64, device=self.device)   # ZoStepScalars
         self.record = torch.zeros(3, dtype=torch.float64, device=self.device)
         self._ws = {}
@@ -303,7 +308,27 @@ class DeviceStore:
         return {"seed_cur": int(h[0]), "seed_prev": int(h[1]), "lr_g_prev": float(h[2:3].view(np.float64)[0]),
                 "pending": int(h[3])}
 
+    def range_table(self, lo: int, hi: int) -> SegTable:
+        """Segment table of blocks [lo, hi) in block order, segments tagged
+        with their block id."""
+        bids = [b for b in sorted(self.plan.segments) if lo <= b < hi]
+        return SegTable([x for b in bids for x in self.plan.segments[b]], self.device,
+                        [b for b in bids for _ in self.plan.segments[b]])
+
     # -- launch plans ----------------------------------------------------------
+    def perturb_bg_call(self, table: SegTable, flags: int, scale_a: float, scale_b: float, stream=None):
+        """Background pass (Philox only): one CTA per SM beside the forward,
+        bumping ``block_done[b]`` per finished tile of block b."""
+        fn = L.lib().zo_perturb_update_bg
+        args = (_ptr(self.theta), 0, _ptr(table.segs), _ptr(table.prefix), table.n_segs, table.n_tiles,
+                _ptr(self.wsh[PLUS]), _ptr(self.vsh[PLUS]), _ptr(self.wsh[MINUS]), _ptr(self.vsh[MINUS]),
+                float(scale_a), float(scale_b), flags, _ptr(self.scal), _ptr(self.block_done),
+                L.stream_ptr(stream))
+        return [(fn, args)]
+
+    def wait_block_call(self, bid: int, target: int, stream=None):
+        return [(L.lib().zo_wait_counter, (_ptr(self.block_done) + 4 * bid, int(target), L.stream_ptr(stream)))]
+
     def perturb_call(self, table: SegTable, flags: int, scale_a: float, scale_b: float, sa=PLUS, sb=MINUS,
                      zmode=L.ZO_Z_PHILOX, z_cur=None, z_prev=None, stream=None):
         fn = L.lib().zo_perturb_update

@@ -150,11 +150,15 @@ class StreamingZo:
     one.  Numerically identical to repeated ``mezo_step`` after flush."""
 
     def __init__(self, store: DeviceStore, hyper: ZoHyper, mgr: RngStateManager | None = None,
-                 overlap: bool = False):
+                 overlap: bool | str = False):
         self.store = store
         self.hyper = hyper.validate()
         self.mgr = mgr or RngStateManager()
-        self.overlap = overlap and not self.mgr.oracle
+        # False: one fused pass, then the forwards; "blocks" (or True): per-block
+        # passes on a side stream gated by events; "background": one co-resident
+        # pass gated per block by device counters
+        plan = {False: None, True: "blocks", "blocks": "blocks", "background": "background"}[overlap]
+        self.overlap = plan if not self.mgr.oracle else None
         self.dual_stream = True
         self.iteration = 0
         self.g_prev = 0.0
@@ -213,6 +217,41 @@ class StreamingZo:
         calls += s.grad_call(wsp, wsn, eps, self.hyper.lr)
         return calls
 
+    def background_step_calls(self, wsp, wsn):
+        """Same step with the fused update+perturb pass as a co-resident
+        background kernel: block 0 (the embedding, needed first) runs as a
+        full-width pass, the rest as zo_perturb_update_bg on a third stream,
+        and both directional forwards wait per block on its completion
+        counter (zo_wait_counter) instead of on the whole pass.  Same kernels'
+        per-element arithmetic as step_calls, so results are identical."""
+        if self.mgr.oracle:
+            raise ProtocolError("the background plan runs the Philox direction only")
+        s, eps = self.store, self.hyper.epsilon
+        nb = len(s.layouts)
+        main, side, pstream = torch.cuda.current_stream(), _side_stream(s), _perturb_stream(s)
+        if not hasattr(s, "_bg_events"):
+            s._bg_events = [torch.cuda.Event() for _ in range(4)]
+        ev = s._bg_events
+        if not hasattr(s, "_bg_tables"):
+            s._bg_tables = (s.range_table(0, 1), s.range_table(1, nb))
+        head, rest = s._bg_tables
+        flags = L.ZO_PU_UPDATE | L.ZO_PU_SHADOW_A | L.ZO_PU_SHADOW_B
+        calls = [(_record_and_wait, (ev[0], main, pstream)),
+                 (_zero_on, (s.block_done, pstream))]
+        calls += s.perturb_call(head, flags, +eps, -eps, stream=pstream)
+        calls.append((_record, (ev[1], pstream)))            # block 0 done, counters reset
+        calls += s.perturb_bg_call(rest, flags, +eps, -eps, stream=pstream)
+        calls.append((_record, (ev[2], pstream)))
+        calls += [(_wait, (main, ev[1])), (_wait, (side, ev[1]))]
+        for b in range(nb):
+            for sgn, ws, st in ((PLUS, wsp, None), (MINUS, wsn, side)):
+                if b > 0:
+                    calls += s.wait_block_call(b, rest.block_tiles[b], stream=st)
+                calls += s.forward_calls(sgn, ws, eps if sgn == PLUS else -eps, blocks=[b], stream=st)
+        calls += [(_record_and_wait, (ev[3], side, main)), (_wait, (main, ev[2]))]
+        calls += s.grad_call(wsp, wsn, eps, self.hyper.lr)
+        return calls
+
     def step(self, batch: Batch, seed: int) -> ZoStep:
         self.iteration += 1
         self.mgr.reset(seed)
@@ -223,8 +262,10 @@ class StreamingZo:
         wsp, wsn = _stage_batch(self.store, batch)
         zc = _oracle_z(self.mgr, seed, self.store.total_params, self.store.device) if self.mgr.oracle else None
         _write_scal(self.store, seed, pending=apply_pending)
-        if self.overlap:
+        if self.overlap == "blocks":
             self.store.run(self.overlapped_step_calls(wsp, wsn))
+        elif self.overlap == "background":
+            self.store.run(self.background_step_calls(wsp, wsn))
         else:
             self.store.run(self.step_calls(wsp, wsn, zc, self._z_prev if apply_pending else None,
                                            update=apply_pending or not self.mgr.oracle))
@@ -250,6 +291,18 @@ def _side_stream(store: DeviceStore):
     if not hasattr(store, "_side"):
         store._side = torch.cuda.Stream(device=store.device)
     return store._side
+
+
+def _perturb_stream(store: DeviceStore):
+    if not hasattr(store, "_pstream"):
+        store._pstream = torch.cuda.Stream(device=store.device)
+    return store._pstream
+
+
+def _zero_on(t: torch.Tensor, stream):
+    with torch.cuda.stream(stream):
+        t.zero_()
+    return 0
 
 
 def _block_events(store: DeviceStore, n: int):

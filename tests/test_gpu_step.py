@@ -20,7 +20,7 @@ from paper_2507_03211_b200 import _lib as L  # noqa: E402
 from paper_2507_03211_b200 import zo  # noqa: E402
 from paper_2507_03211_b200.engine import MINUS, PLUS, DeviceStore  # noqa: E402
 from paper_2507_03211_b200.errors import DimensionError, NumericError, ProtocolError  # noqa: E402
-from paper_2507_03211_b200.model import Batch, ModelConfig  # noqa: E402
+from paper_2507_03211_b200.model import Batch, ModelConfig, make_batch  # noqa: E402
 from paper_2507_03211_b200.rng import RngStateManager, iteration_seeds  # noqa: E402
 
 EPS, LR = 1e-3, 1e-2
@@ -283,17 +283,40 @@ def test_error_behaviour_matches_reference():
         sz.flush()
 
 
-def test_overlapped_two_stream_step_is_bit_identical():
+@pytest.mark.parametrize("plan", ["blocks", "background"])
+def test_overlapped_step_is_bit_identical(plan):
     """Per-block perturb passes on a side stream overlapping the +eps forward
-    give exactly the serial plan's records and weights."""
+    ("blocks"), or one co-resident pass gating each block's forwards through
+    device counters ("background"), give exactly the serial plan's records
+    and weights."""
     cfg, bsz, _ = _cfg("mid32")
     a, b = DeviceStore(cfg, 7), DeviceStore(cfg, 7)
     h = zo.ZoHyper(EPS, LR)
-    sa, sb = zo.StreamingZo(a, h), zo.StreamingZo(b, h, overlap=True)
+    sa, sb = zo.StreamingZo(a, h), zo.StreamingZo(b, h, overlap=plan)
     for j, s in enumerate(iteration_seeds(13, 4), 1):
         batch = _batch(cfg, bsz, 300 + j)
         ra, rb = sa.step(batch, s), sb.step(batch, s)
         assert (ra.loss_pos, ra.loss_neg, ra.g) == (rb.loss_pos, rb.loss_neg, rb.g)
+    sa.flush()
+    sb.flush()
+    assert torch.equal(a.theta, b.theta)
+
+
+def test_background_plan_at_width_matches_serial():
+    """The background plan on a wider model (many tiles per block, unaligned
+    vocab rows through the generic path) equals the serial plan; the block
+    counters end at each block's tile count."""
+    cfg = ModelConfig(1000, 256, 4, 3, 64, "f32")
+    a, b = DeviceStore(cfg, 7), DeviceStore(cfg, 7)
+    h = zo.ZoHyper(EPS, LR)
+    sa, sb = zo.StreamingZo(a, h), zo.StreamingZo(b, h, overlap="background")
+    for j, s in enumerate(iteration_seeds(21, 3), 1):
+        batch = make_batch(cfg, 2, 500 + j)
+        ra, rb = sa.step(batch, s), sb.step(batch, s)
+        assert (ra.loss_pos, ra.loss_neg, ra.g) == (rb.loss_pos, rb.loss_neg, rb.g)
+    done = b.block_done.cpu().tolist()
+    rest = b._bg_tables[1]
+    assert done[1:] == [rest.block_tiles[i] for i in range(1, len(b.layouts))]
     sa.flush()
     sb.flush()
     assert torch.equal(a.theta, b.theta)

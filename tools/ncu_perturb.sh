@@ -1,4 +1,7 @@
 #!/bin/bash
+# full ncu capture of the fused update+perturb pass (first timed launch of tools/perturb_bench.py)
 export PYTHONPATH=$PWD
-timeout 600 ncu --set full --import-source on --clock-control none -k regex:perturb_update -s 2 -c 1 \
-  -o gpurun_out/prof_perturb2 python tools/perturb_bench.py > gpurun_out/ncu_p2.log 2>&1
+mkdir -p gpurun_out
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:perturb_update_kernel -s 2 -c 1 \
+  -o gpurun_out/prof_perturb3 python tools/perturb_bench.py > gpurun_out/ncu_p3.log 2>&1
+tail -3 gpurun_out/ncu_p3.log
