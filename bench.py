@@ -47,6 +47,7 @@ def _args():
     ap.add_argument("--batch", type=int, default=BATCH_PER_GROUP, help="sequences per PertP group")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true", help="skip the public-API pass (profiling runs)")
+    ap.add_argument("--no-graph", action="store_true", help="launch the step eagerly instead of replaying a CUDA graph")
     ap.add_argument("--overlap", default="none", choices=["none", "blocks", "background"],
                     help="blocks: per-block perturb passes on a side stream ahead of the +eps forward; "
                          "background: one co-resident perturb pass gated per block by device counters")
@@ -267,6 +268,9 @@ def ours(args, rank, world, local_rank):
             ws.tgt.copy_(tgt_dev[j])
         store.scal[0:1].fill_(zo._u64_as_i64(seeds[j]))
         store.scal[3:4].fill_(1 if j > 0 else 0)
+        if world == 1 and not instrument and not args.no_graph and j > 0:
+            runner._replay(wss[0], wss[1])         # the captured step (same launches)
+            return
         for i, (fn, a) in enumerate(step_calls):
             timed = instrument and (i in pert_set or i in gemm_set)
             if timed:
@@ -343,7 +347,7 @@ def ours(args, rank, world, local_rank):
     if args.no_e2e:
         e2e_ms = ms
     elif world == 1:
-        runner2 = zo.StreamingZo(store, hyper, overlap=_plan(args))
+        runner2 = zo.StreamingZo(store, hyper, overlap=_plan(args), graph=not args.no_graph)
         for j in range(args.warmup):
             runner2.step(batches[j], seeds[j])
         torch.cuda.synchronize()
@@ -388,7 +392,9 @@ def ours(args, rank, world, local_rank):
         "data": "synthetic tokens, random-init (Philox) weights",
         "config": {"workload": f"{args.model} ZO-SGD step (zosim arch), seq {T}, batch {B} per PertP group",
                    "global_batch": B * n_groups, "seq_len": T, "parallelism": strategy, "eps": EPS, "lr": LR,
-                   "params": P, "l2": "inputs > L2 (fp32 master 4 B/param + bf16 shadows stream every step)"},
+                   "params": P, "l2": "inputs > L2 (fp32 master 4 B/param + bf16 shadows stream every step)",
+                   "perturb_plan": args.overlap,
+                   "launch": "eager" if (args.no_graph or world > 1) else "CUDA graph replay per step"},
         "roofline": dominant, "roofline_other": other,
         "perturb_kernel_gbs": pert_gbs,
         "clocks": clk.summary(),

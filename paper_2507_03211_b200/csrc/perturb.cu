@@ -114,13 +114,16 @@ __device__ __forceinline__ void pu_load_fast(const PuParams& p, int64_t e0, int 
     if (full || lane + 32 * g < ngroups) th[g] = tp[32 * g];
 }
 
-template <bool PEND, bool BF16, int G>
+// FULL: a whole 512-element tile with both shadows written (the common case,
+// no per-group guards or per-direction branches)
+template <bool PEND, bool BF16, int G, bool FULL = false>
 __device__ __forceinline__ void pu_compute_fast(const PuParams& p, int64_t e0, int ngroups, int64_t dbase,
                                                 bool SA, bool SB, float sa, float sb, uint64_t seed_cur,
                                                 uint64_t seed_prev, float lrg32, int lane, float4 (&th)[G]) {
+  if constexpr (FULL) { SA = true; SB = true; }
   float4* tp = reinterpret_cast<float4*>(p.theta + (e0 - p.theta_key0)) + lane;
   const uint64_t qa = (uint64_t)(e0 >> 2) + (uint64_t)lane;
-  const bool full = ngroups >= 32 * G;
+  const bool full = FULL || ngroups >= 32 * G;
   uint64_t q[G];
 #pragma unroll
   for (int g = 0; g < G; ++g) q[g] = qa + (uint64_t)(32 * g);
@@ -217,7 +220,15 @@ __device__ __forceinline__ void pu_tile_fast(const PuParams& p, int64_t e0, int 
                                              float lrg32, int kind, int lane, float4 (&th)[kPuGroupsPerThread]) {
   constexpr int G = kPuGroupsPerThread;
   const bool sa = want_sh && sh[0], sb = want_sh && sh[1];
-  if (kind == ZO_SHADOW_BF16) {
+  if (sa && sb && ngroups == 32 * G) {
+    if (kind == ZO_SHADOW_BF16) {
+      if (pending) pu_compute_fast<true, true, G, true>(p, e0, ngroups, dbase, sa, sb, sc32[0], sc32[1], seed_cur, seed_prev, lrg32, lane, th);
+      else pu_compute_fast<false, true, G, true>(p, e0, ngroups, dbase, sa, sb, sc32[0], sc32[1], seed_cur, seed_prev, lrg32, lane, th);
+    } else {
+      if (pending) pu_compute_fast<true, false, G, true>(p, e0, ngroups, dbase, sa, sb, sc32[0], sc32[1], seed_cur, seed_prev, lrg32, lane, th);
+      else pu_compute_fast<false, false, G, true>(p, e0, ngroups, dbase, sa, sb, sc32[0], sc32[1], seed_cur, seed_prev, lrg32, lane, th);
+    }
+  } else if (kind == ZO_SHADOW_BF16) {
     if (pending) pu_compute_fast<true, true, G>(p, e0, ngroups, dbase, sa, sb, sc32[0], sc32[1], seed_cur, seed_prev, lrg32, lane, th);
     else pu_compute_fast<false, true, G>(p, e0, ngroups, dbase, sa, sb, sc32[0], sc32[1], seed_cur, seed_prev, lrg32, lane, th);
   } else {
@@ -251,7 +262,7 @@ __device__ __forceinline__ void tile_done(const PuParams& p, int32_t block) {
 // Generic tile (unaligned groups, oracle z, shadow-less segments): one group
 // per lane at a time, element-guarded; rare, so kept register-light.
 template <int ZMODE>
-__device__ __noinline__ void pu_tile_generic(const PuParams& p, const ZoSegment& s, int64_t e0, int64_t e1,
+__device__ __forceinline__ void pu_tile_generic(const PuParams& p, const ZoSegment& s, int64_t e0, int64_t e1,
                                              int64_t drow, bool theta_vec, bool pending, bool need_z,
                                              const bool (&sh)[2], const float (&sc32)[2], uint64_t seed_cur,
                                              uint64_t seed_prev, double lrg64, float lrg32, int lane) {
@@ -394,8 +405,8 @@ __device__ __forceinline__ void perturb_update_body(const PuParams& p) {
   }
 }
 
-template <int ZMODE>
-__global__ void __launch_bounds__(kPuThreads, 4) perturb_update_kernel(const PuParams p) {
+template <int ZMODE, int MINB = 4>
+__global__ void __launch_bounds__(kPuThreads, MINB) perturb_update_kernel(const PuParams p) {
   perturb_update_body<ZMODE, false>(p);
 }
 
@@ -407,7 +418,10 @@ __global__ void __maxnreg__(88) perturb_update_bg_kernel(const PuParams p) {
 
 int perturb_update_launch(const PuParams& p, int zmode, cudaStream_t stream, bool background) {
   if (p.n_tiles <= 0) return ZO_OK;
-  const int64_t want = (int64_t)num_sms() * (background ? 1 : 8);
+  static const int occ = [] { const char* e = getenv("ZO_PU_OCC"); return e ? atoi(e) : 4; }();
+  static const int waves = [] { const char* e = getenv("ZO_PU_WAVES"); return e ? atoi(e) : 2; }();
+  // two resident waves of chunks: late-starting CTAs even out the tail
+  const int64_t want = (int64_t)num_sms() * (background ? 1 : occ * waves);
   const int grid = (int)(p.n_tiles < want ? p.n_tiles : want);
   const size_t smem = p.n_segs + 1 <= kPuMaxSmemSegs ? (size_t)(p.n_segs + 1) * sizeof(int64_t) : 0;
   if (background) {
@@ -416,7 +430,11 @@ int perturb_update_launch(const PuParams& p, int zmode, cudaStream_t stream, boo
     else
       launch_k(perturb_update_bg_kernel<ZO_Z_ORACLE>, dim3(grid), dim3(kPuThreads), smem, stream, p);
   } else {
-    if (zmode == ZO_Z_PHILOX)
+    if (zmode == ZO_Z_PHILOX && occ == 5)
+      launch_k(perturb_update_kernel<ZO_Z_PHILOX, 5>, dim3(grid), dim3(kPuThreads), smem, stream, p);
+    else if (zmode == ZO_Z_PHILOX && occ == 6)
+      launch_k(perturb_update_kernel<ZO_Z_PHILOX, 6>, dim3(grid), dim3(kPuThreads), smem, stream, p);
+    else if (zmode == ZO_Z_PHILOX)
       launch_k(perturb_update_kernel<ZO_Z_PHILOX>, dim3(grid), dim3(kPuThreads), smem, stream, p);
     else
       launch_k(perturb_update_kernel<ZO_Z_ORACLE>, dim3(grid), dim3(kPuThreads), smem, stream, p);

@@ -150,7 +150,7 @@ class StreamingZo:
     one.  Numerically identical to repeated ``mezo_step`` after flush."""
 
     def __init__(self, store: DeviceStore, hyper: ZoHyper, mgr: RngStateManager | None = None,
-                 overlap: bool | str = False):
+                 overlap: bool | str = False, graph: bool = True):
         self.store = store
         self.hyper = hyper.validate()
         self.mgr = mgr or RngStateManager()
@@ -160,6 +160,10 @@ class StreamingZo:
         plan = {False: None, True: "blocks", "blocks": "blocks", "background": "background"}[overlap]
         self.overlap = plan if not self.mgr.oracle else None
         self.dual_stream = True
+        # Philox steps replay one captured CUDA graph per batch shape (the
+        # step's scalars are device-resident, so the launches never change)
+        self.graph = graph and not self.mgr.oracle
+        self._graphs = {}
         self.iteration = 0
         self.g_prev = 0.0
         self.last_seed = None
@@ -252,6 +256,27 @@ class StreamingZo:
         calls += s.grad_call(wsp, wsn, eps, self.hyper.lr)
         return calls
 
+    def _plan(self, wsp, wsn, zc=None, zp=None, update=True):
+        if self.overlap == "blocks":
+            return self.overlapped_step_calls(wsp, wsn)
+        if self.overlap == "background":
+            return self.background_step_calls(wsp, wsn)
+        return self.step_calls(wsp, wsn, zc, zp, update=update)
+
+    def _replay(self, wsp, wsn):
+        """Capture the step's launches once per (batch shape, plan) -- the
+        first step ran eagerly, so one-time kernel attributes and TMA
+        descriptors already exist -- then replay the graph on the current
+        stream, after this step's batch upload and seed write."""
+        key = (wsp.batch, wsp.seq, self.overlap, self.dual_stream)
+        g = self._graphs.get(key)
+        if g is None:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, capture_error_mode="thread_local"):
+                self.store.run(self._plan(wsp, wsn))      # stream handles bound inside the capture
+            self._graphs[key] = g
+        g.replay()
+
     def step(self, batch: Batch, seed: int) -> ZoStep:
         self.iteration += 1
         self.mgr.reset(seed)
@@ -262,13 +287,11 @@ class StreamingZo:
         wsp, wsn = _stage_batch(self.store, batch)
         zc = _oracle_z(self.mgr, seed, self.store.total_params, self.store.device) if self.mgr.oracle else None
         _write_scal(self.store, seed, pending=apply_pending)
-        if self.overlap == "blocks":
-            self.store.run(self.overlapped_step_calls(wsp, wsn))
-        elif self.overlap == "background":
-            self.store.run(self.background_step_calls(wsp, wsn))
+        if self.graph and self.iteration > 1:
+            self._replay(wsp, wsn)
         else:
-            self.store.run(self.step_calls(wsp, wsn, zc, self._z_prev if apply_pending else None,
-                                           update=apply_pending or not self.mgr.oracle))
+            self.store.run(self._plan(wsp, wsn, zc, self._z_prev if apply_pending else None,
+                                      update=apply_pending or not self.mgr.oracle))
         st = _finish(self.store, wsp, wsn, self.iteration, seed)
         self.g_prev, self.last_seed, self._pending, self._z_prev = st.g, seed, True, zc
         return st

@@ -320,3 +320,23 @@ def test_background_plan_at_width_matches_serial():
     sa.flush()
     sb.flush()
     assert torch.equal(a.theta, b.theta)
+
+
+@pytest.mark.parametrize("plan", [False, "background"])
+def test_graph_replay_equals_eager(plan):
+    """Philox steps replayed from a captured CUDA graph give exactly the eager
+    launches' records and weights (seeds / pending flag / g live on the
+    device, so one graph serves every step)."""
+    cfg, bsz, _ = _cfg("mid32")
+    a, b = DeviceStore(cfg, 7), DeviceStore(cfg, 7)
+    h = zo.ZoHyper(EPS, LR)
+    sa = zo.StreamingZo(a, h, overlap=plan, graph=False)
+    sb = zo.StreamingZo(b, h, overlap=plan, graph=True)
+    for j, s in enumerate(iteration_seeds(17, 5), 1):
+        batch = _batch(cfg, bsz, 700 + j)
+        ra, rb = sa.step(batch, s), sb.step(batch, s)
+        assert (ra.loss_pos, ra.loss_neg, ra.g) == (rb.loss_pos, rb.loss_neg, rb.g)
+    assert len(sb._graphs) == 1
+    sa.flush()
+    sb.flush()
+    assert torch.equal(a.theta, b.theta)
