@@ -44,7 +44,7 @@ struct GemmCfg {
   static constexpr int kBBytes = kBK * BN * 2;    // 32 KB / 16 KB
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kTmemCols = 2 * BN;        // double-buffered accumulator
-  static constexpr int kSmem = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/ + kEpiWarps * 32 * 33 * 4;
+  static constexpr int kSmem = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
 };
 
 struct GemmArgs {
@@ -85,11 +85,21 @@ __device__ __forceinline__ float gelu_tanh(float x) {
 // Thread (quarter, lane) owns output row m0 + 32*quarter + lane.
 // Epilogue warp e (0..7) owns TMEM lane quarter (warp % 4) and column half
 // e / 4, so two warps share each quarter and each thread stores half a row.
+__device__ __forceinline__ void ld_v8_na(const float* p, float* v) {
+  asm volatile("ld.global.L1::no_allocate.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7])
+               : "l"(p));
+}
+__device__ __forceinline__ void st_v8(float* p, const float* v) {
+  asm volatile("st.global.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "f"(v[0]), "f"(v[1]), "f"(v[2]),
+               "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7])
+               : "memory");
+}
+
 template <int BN, int EPI>
 __device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t tmem_base, int acc, int quarter,
                                               int half, int lane, int64_t m0, int64_t n0, int64_t tn,
-                                              float* __restrict__ stg) {
-  // stg: this warp's 32 x 33 fp32 staging tile (row-padded: conflict-free both ways)
+                                              float* __restrict__ /*unused*/) {
   const int64_t row_base = m0 + quarter * 32;
   const int64_t row = row_base + lane;
   const bool row_ok = row < args.M;
@@ -179,36 +189,52 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t tme
           if (col0 + i < args.N) o[i] = __float2bfloat16_rn(v[i]);
       }
     } else {
-      // column-per-lane after an smem transpose: every global access is one
-      // contiguous 128 B (fp32) / 64 B (bf16) run per warp instruction
-      const int64_t col = col0 + lane;
-      const bool col_ok = col < args.N;
-      float bias_c = 0.f;
-      if constexpr (EPI != ZO_EPI_F32) bias_c = col_ok ? __ldg(args.bias + col) : 0.f;
+      // fp32 out (+ residual): row-per-thread like the bf16 path, 32 B
+      // (full-sector) accesses, no shared-memory staging -- the tensor core's
+      // operand reads already keep the SM's shared-memory pipe ~93% busy
+      float* o = static_cast<float*>(args.out) + row * args.ldo + col0;
+      const bool full = row_ok && col0 + 32 <= args.N;
+      const bool vec = full && ((reinterpret_cast<uintptr_t>(o) & 31) == 0) &&
+                       (EPI == ZO_EPI_F32 || (reinterpret_cast<uintptr_t>(args.bias + col0) & 15) == 0);
       float res[32];
       if constexpr (EPI == ZO_EPI_BIAS_RESID_F32) {
-        // residual reads issued before the TMEM load so their latency overlaps it
-        const float* xr = static_cast<const float*>(args.out) + row_base * args.ldo + col;
+        // residual (the previous contents of out) read before the TMEM load so
+        // the latency overlaps it
+        if (vec) {
 #pragma unroll
-        for (int r = 0; r < 32; ++r) res[r] = (col_ok && row_base + r < args.M) ? xr[(int64_t)r * args.ldo] : 0.f;
+          for (int i = 0; i < 4; ++i) ld_v8_na(o + 8 * i, res + 8 * i);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) res[i] = (row_ok && col0 + i < args.N) ? o[i] : 0.f;
+        }
       }
       float v[32];
       tmem_ld_32x32b_x32(taddr, v);
+      if (!row_ok || col0 >= args.N) continue;
+      if constexpr (EPI == ZO_EPI_BIAS_RESID_F32) {
+        if (vec) {
 #pragma unroll
-      for (int i = 0; i < 32; ++i) stg[lane * 33 + i] = v[i];
-      __syncwarp();
-      if constexpr (EPI == ZO_EPI_F32 || EPI == ZO_EPI_BIAS_RESID_F32) {
-        float* o = static_cast<float*>(args.out) + row_base * args.ldo + col;
-#pragma unroll
-        for (int r = 0; r < 32; ++r) {
-          if (col_ok && row_base + r < args.M) {
-            float val = stg[r * 33 + lane];
-            if constexpr (EPI == ZO_EPI_BIAS_RESID_F32) val = res[r] + (val + bias_c);
-            o[(int64_t)r * args.ldo] = val;
+          for (int i = 0; i < 8; ++i) {
+            const float4 b4 = __ldg(reinterpret_cast<const float4*>(args.bias + col0) + i);
+            v[4 * i] = res[4 * i] + (v[4 * i] + b4.x);
+            v[4 * i + 1] = res[4 * i + 1] + (v[4 * i + 1] + b4.y);
+            v[4 * i + 2] = res[4 * i + 2] + (v[4 * i + 2] + b4.z);
+            v[4 * i + 3] = res[4 * i + 3] + (v[4 * i + 3] + b4.w);
           }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            if (col0 + i < args.N) v[i] = res[i] + (v[i] + args.bias[col0 + i]);
         }
       }
-      __syncwarp();
+      if (vec) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) st_v8(o + 8 * i, v + 8 * i);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          if (col0 + i < args.N) o[i] = v[i];
+      }
     }
   }
   if constexpr (EPI == ZO_EPI_CE) {
@@ -358,11 +384,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 //   tfull[a]  both CTAs; multicast commit
 //   tempty[a] leader only; 16 arrivals = 8 epilogue warps x 2 CTAs (remote)
 // ----------------------------------------------------------------------------
-constexpr int k2Stages = 5;   // leaves room for a co-resident perturb CTA (side stream)
+#ifndef ZO_K2_STAGES
+#define ZO_K2_STAGES 6
+#endif
+constexpr int k2Stages = ZO_K2_STAGES;   // 6 x 32 KB operand stages (no epilogue staging buffer)
 constexpr int k2ABytes = kBM * kBK * 2;        // 16 KB: this CTA's 128 rows
 constexpr int k2BBytes = kBK * 128 * 2;        // 16 KB: this CTA's half of B
 constexpr int k2StageBytes = k2ABytes + k2BBytes;
-constexpr int k2Smem = k2Stages * k2StageBytes + 1024 + 256 + kEpiWarps * 32 * 33 * 4;
+constexpr int k2Smem = k2Stages * k2StageBytes + 1024 + 256;
 static_assert(k2Smem <= 232448, "pair kernel smem");
 
 __device__ __forceinline__ uint32_t cluster_ctarank() {
