@@ -249,11 +249,11 @@ def ours(args, rank, world, local_rank):
     tgt_dev = torch.stack([torch.from_numpy(b.targets.reshape(-1).astype(np.int32)) for b in batches]).to(dev)
 
     pert_set = {i for i, (fn, _) in enumerate(step_calls) if fn.__name__ == "zo_perturb_update"}
-    gemm_idx = [i for i, (fn, _) in enumerate(step_calls) if fn.__name__ == "zo_gemm_bf16"]
+    gemm_idx = [i for i, (fn, _) in enumerate(step_calls) if fn.__name__.startswith("zo_gemm_bf16")]
     streams = {int(torch.cuda.current_stream().cuda_stream): torch.cuda.current_stream()}
     if hasattr(store, "_side"):
         streams[int(store._side.cuda_stream)] = store._side
-    n_launch = sum(2 if fn.__name__ == "zo_ce_finalize" else 1 for fn, _ in step_calls)
+    n_launch = sum(2 if fn.__name__ == "zo_ce_finalize" else 1 for fn, _ in step_calls if fn.__name__.startswith("zo_"))
     if world > 1:
         n_launch += 0   # collectives are NCCL kernels, not ours
 
@@ -327,7 +327,7 @@ def ours(args, rank, world, local_rank):
         pert_set.clear()
         pert_set.update(i for i, (fn, _) in enumerate(step_calls) if fn.__name__ == "zo_perturb_update")
         gemm_set.clear()
-        gemm_set.update(i for i, (fn, _) in enumerate(step_calls) if fn.__name__ == "zo_gemm_bf16")
+        gemm_set.update(i for i, (fn, _) in enumerate(step_calls) if fn.__name__.startswith("zo_gemm_bf16"))
     for j in range(args.warmup, args.warmup + args.steps):
         one_step(j, instrument=True)
     if world == 1:

@@ -152,6 +152,19 @@ int zo_gemm_bf16(const void* A, int64_t lda, const void* B, int64_t ldb,
                  const int32_t* targets, float* ce_part, float* ce_tgt,
                  int32_t* err_flag, void* stream);
 /* number of N tiles the ZO_EPI_CE epilogue writes per row for a given N */
+/* Same GEMM with a caller-owned workspace (zero-initialised once, reusable
+ * by later calls on the same stream; not shared by concurrent calls): the
+ * CTA-pair kernel then splits its last waves along K ("stream-K") so every
+ * SM stays busy, with a fixed, deterministic reduction order.  A null or
+ * too-small workspace gives the plain data-parallel schedule. */
+int zo_gemm_bf16_ws(const void* A, int64_t lda, const void* B, int64_t ldb,
+                    int64_t M, int64_t N, int64_t K, int32_t epilogue,
+                    const float* bias, void* out, int64_t ldo,
+                    const int32_t* targets, float* ce_part, float* ce_tgt,
+                    int32_t* err_flag, void* workspace, int64_t workspace_bytes,
+                    void* stream);
+/* Workspace bytes zo_gemm_bf16_ws needs for an M x N x K problem (0: none). */
+int64_t zo_gemm_workspace_bytes(int64_t M, int64_t N, int64_t K);
 int64_t zo_gemm_ce_tiles(int64_t N);
 
 /* Causal exact-softmax attention (src/zosim/model.py:325-332): qkv rows are

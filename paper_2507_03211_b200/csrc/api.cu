@@ -58,7 +58,8 @@ int grad_groups_launch(const double*, int, int, int, int, int, int, double, doub
                        cudaStream_t);
 int hash_launch(const void*, int64_t, uint64_t*, uint64_t*, int, cudaStream_t);
 int gemm_launch(const void*, int64_t, const void*, int64_t, int64_t, int64_t, int64_t, int, const float*, void*,
-                int64_t, const int32_t*, float*, float*, int32_t*, cudaStream_t);
+                int64_t, const int32_t*, float*, float*, int32_t*, void*, int64_t, cudaStream_t);
+int64_t gemm_workspace_bytes(int64_t M, int64_t N, int64_t K);
 int64_t gemm_ce_tiles(int64_t N);
 
 }  // namespace zo
@@ -181,8 +182,23 @@ int zo_gemm_bf16(const void* A, int64_t lda, const void* B, int64_t ldb, int64_t
                ZO_ERR_CONFIG, "zo_gemm_bf16: missing epilogue buffers");
   ZO_CHECK_ARG(epilogue == ZO_EPI_F32 || epilogue == ZO_EPI_CE || bias, ZO_ERR_CONFIG, "zo_gemm_bf16: bias required");
   return zo::gemm_launch(A, lda, B, ldb, M, N, K, epilogue, bias, out, ldo, targets, ce_part, ce_tgt, err_flag,
-                         ZO_STREAM(stream));
+                         nullptr, 0, ZO_STREAM(stream));
 }
+
+int zo_gemm_bf16_ws(const void* A, int64_t lda, const void* B, int64_t ldb, int64_t M, int64_t N, int64_t K,
+                    int32_t epilogue, const float* bias, void* out, int64_t ldo, const int32_t* targets,
+                    float* ce_part, float* ce_tgt, int32_t* err_flag, void* workspace, int64_t workspace_bytes,
+                    void* stream) {
+  ZO_CHECK_ARG(A && B, ZO_ERR_CONFIG, "zo_gemm_bf16_ws: null operand");
+  ZO_CHECK_ARG(epilogue == ZO_EPI_CE ? (targets && ce_part && ce_tgt && bias && err_flag) : (out != nullptr),
+               ZO_ERR_CONFIG, "zo_gemm_bf16_ws: missing epilogue buffers");
+  ZO_CHECK_ARG(epilogue == ZO_EPI_F32 || epilogue == ZO_EPI_CE || bias, ZO_ERR_CONFIG,
+               "zo_gemm_bf16_ws: bias required");
+  return zo::gemm_launch(A, lda, B, ldb, M, N, K, epilogue, bias, out, ldo, targets, ce_part, ce_tgt, err_flag,
+                         workspace, workspace_bytes, ZO_STREAM(stream));
+}
+
+int64_t zo_gemm_workspace_bytes(int64_t M, int64_t N, int64_t K) { return zo::gemm_workspace_bytes(M, N, K); }
 
 int64_t zo_gemm_ce_tiles(int64_t N) { return zo::gemm_ce_tiles(N); }
 

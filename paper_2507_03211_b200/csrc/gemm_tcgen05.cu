@@ -57,7 +57,60 @@ struct GemmArgs {
   float* ce_tgt;
   int32_t* err;
   int64_t ce_tiles;
+  // stream-K tail (pair kernel): tiles [0, dp_tiles) data-parallel, the rest
+  // split into sk_units k-blocks spread evenly over the pairs (0 = off)
+  int64_t dp_tiles;
+  int64_t sk_units;
+  int32_t sk_pieces;    // max pieces per split tile
+  int32_t* sk_flags;    // [slot][16 epilogue warps], self-clearing
+  float* sk_part;       // [slot][16][32 rows x 128 cols] fp32 partial accumulators
 };
+
+constexpr int kSkWarpFloats = 32 * 128;   // one epilogue warp's share of a pair tile
+
+// One work item of a pair: a whole tile, or a k-range piece of a split tile.
+//   kind 0: whole tile; 1: partial (stored to `slot`, not finished here);
+//   kind 2: finisher (adds partials slot .. slot+npart-1 in k order, then the epilogue)
+struct SkItem {
+  int64_t tile, slot;
+  int kb0, kb1, kind, npart;
+};
+
+// Item i of pair c out of W.  Data-parallel tiles come first; the pair's
+// stream-K range is walked in DESCENDING tile order, so a pair's only
+// partial piece is its first item and a finisher (always a later item of
+// another pair) only ever waits on pieces that other pairs produce first.
+__device__ __forceinline__ bool sk_item(const GemmArgs& a, int64_t c, int64_t W, int nk, int64_t i, SkItem& it) {
+  const int64_t ndp = c < a.dp_tiles ? (a.dp_tiles - c + W - 1) / W : 0;
+  if (i < ndp) {
+    it.tile = c + i * W; it.kb0 = 0; it.kb1 = nk; it.kind = 0; it.slot = 0; it.npart = 0;
+    return true;
+  }
+  const int64_t U = a.sk_units;
+  if (U == 0) return false;
+  const int64_t u0 = c * U / W, u1 = (c + 1) * U / W;
+  if (u0 >= u1) return false;
+  const int64_t t = (u1 - 1) / nk - (i - ndp);
+  if (t < u0 / nk) return false;
+  const int64_t tb = t * nk;
+  it.tile = a.dp_tiles + t;
+  it.kb0 = (int)((u0 > tb ? u0 : tb) - tb);
+  it.kb1 = (int)((u1 < tb + nk ? u1 : tb + nk) - tb);
+  const int64_t first = ((tb + 1) * W - 1) / U;     // pair owning the tile's first k-block
+  const int64_t p1 = a.sk_pieces - 1;
+  it.slot = t * p1;
+  it.npart = 0;
+  if (it.kb1 < nk) { it.kind = 1; it.slot += c - first; }
+  else if (it.kb0 == 0) { it.kind = 0; }
+  else { it.kind = 2; it.npart = (int)(c - first); }
+  return true;
+}
+
+__device__ __forceinline__ int ld_acquire_s32(const int32_t* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 
 template <int BN>
 __device__ __forceinline__ uint32_t make_idesc() {
@@ -96,10 +149,54 @@ __device__ __forceinline__ void st_v8(float* p, const float* v) {
                : "memory");
 }
 
+// stream-K partial piece: this warp's 32 rows x 128 columns of the fp32
+// accumulator to the workspace (1 KB contiguous per warp store), then publish
+__device__ __forceinline__ void store_partial(uint32_t tmem_base, int acc, int quarter, int half, int lane,
+                                              float* dst, int32_t* flag) {
+#pragma unroll 1
+  for (int cc = 0; cc < 4; ++cc) {
+    const int c = half * 4 + cc;
+    const uint32_t taddr = tmem_base + (uint32_t)(acc * 256 + c * 32) + ((uint32_t)(quarter * 32) << 16);
+    float v[32];
+    tmem_ld_32x32b_x32(taddr, v);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) st_v8(dst + ((cc * 4 + j) * 32 + lane) * 8, v + 8 * j);
+  }
+  __threadfence();
+  __syncwarp();
+  if (lane == 0) asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(flag), "r"(1) : "memory");
+}
+
 template <int BN, int EPI>
 __device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t tmem_base, int acc, int quarter,
                                               int half, int lane, int64_t m0, int64_t n0, int64_t tn,
-                                              float* __restrict__ /*unused*/) {
+                                              const float* __restrict__ part = nullptr, int npart = 0,
+                                              int32_t* part_flags = nullptr) {
+  // stream-K finisher: wait for the earlier pieces of this warp's sub-tile
+  if (npart > 0) {
+    for (int p = 0; p < npart; ++p) {
+      const int32_t* f = part_flags + (int64_t)p * 16;
+      int64_t spins = 0;
+      while (ld_acquire_s32(f) == 0) {
+        __nanosleep(64);
+        if (++spins > (1ll << 26)) __trap();      // a lost producer would hang the GPU
+      }
+    }
+  }
+  // adds the partials of chunk c (this warp's half: local chunk cc) in k order
+  auto add_parts = [&](int c, float (&v)[32]) {
+    const int cc = c - half * (BN / 64);
+    for (int p = 0; p < npart; ++p) {
+      const float* src = part + (int64_t)p * 16 * kSkWarpFloats;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        float pv[8];
+        ld_v8_na(src + ((cc * 4 + j) * 32 + lane) * 8, pv);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) v[8 * j + e] += pv[e];
+      }
+    }
+  };
   const int64_t row_base = m0 + quarter * 32;
   const int64_t row = row_base + lane;
   const bool row_ok = row < args.M;
@@ -118,6 +215,7 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t tme
       // thread-per-row: online (max, sum exp) over this row's columns, target logit
       float v[32];
       tmem_ld_32x32b_x32(taddr, v);
+      if (npart > 0) add_parts(c, v);
       if (!row_ok || col0 >= args.N) continue;
       const int lim = col0 + 32 <= args.N ? 32 : (int)(args.N - col0);
       float cm = -INFINITY;
@@ -161,6 +259,7 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t tme
       }
       float v[32];
       tmem_ld_32x32b_x32(taddr, v);
+      if (npart > 0) add_parts(c, v);
       if (!row_ok || col0 >= args.N) continue;
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
@@ -210,6 +309,7 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t tme
       }
       float v[32];
       tmem_ld_32x32b_x32(taddr, v);
+      if (npart > 0) add_parts(c, v);
       if (!row_ok || col0 >= args.N) continue;
       if constexpr (EPI == ZO_EPI_BIAS_RESID_F32) {
         if (vec) {
@@ -236,6 +336,11 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t tme
           if (col0 + i < args.N) o[i] = v[i];
       }
     }
+  }
+  if (npart > 0) {            // self-clearing: the next launch finds 0
+    __syncwarp();
+    if (lane == 0)
+      for (int p = 0; p < npart; ++p) part_flags[(int64_t)p * 16] = 0;
   }
   if constexpr (EPI == ZO_EPI_CE) {
     if (row_ok) {
@@ -265,7 +370,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   auto tfull_bar = [&](int a) { return bars + 8u * (2 * C::kStages + a); };
   auto tempty_bar = [&](int a) { return bars + 8u * (2 * C::kStages + 2 + a); };
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + C::kStages * C::kStageBytes + 8 * (2 * C::kStages + 4));
-  float* stg_all = reinterpret_cast<float*>(gbase + C::kStages * C::kStageBytes + 256);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t num_m = (args.M + kBM - 1) / kBM;
@@ -355,8 +459,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const int64_t tn = tile / num_m;
       mbar_wait(tfull_bar(acc), acc_phase);
       tc_fence_after();
-      epilogue_tile<BN, EPI>(args, tmem_base, acc, quarter, half, lane, m0, tn * BN, tn,
-                             stg_all + (warp - 2) * 32 * 33);
+      epilogue_tile<BN, EPI>(args, tmem_base, acc, quarter, half, lane, m0, tn * BN, tn);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(tempty_bar(acc));
@@ -451,7 +554,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
   auto tfull_bar = [&](int a) { return bars + 8u * (2 * k2Stages + a); };
   auto tempty_bar = [&](int a) { return bars + 8u * (2 * k2Stages + 2 + a); };
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + k2Stages * k2StageBytes + 8 * (2 * k2Stages + 4));
-  float* stg_all = reinterpret_cast<float*>(gbase + k2Stages * k2StageBytes + 256);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_ctarank();
@@ -459,7 +561,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
   const int64_t cluster_id = blockIdx.x >> 1, n_clusters = gridDim.x >> 1;
   const int64_t num_m = (args.M + 2 * kBM - 1) / (2 * kBM);
   const int64_t num_n = (args.N + BN - 1) / BN;
-  const int64_t tiles = num_m * num_n;
   const int nk = (int)((args.K + kBK - 1) / kBK);
 
   if (warp == 0 && lane == 0) {
@@ -486,10 +587,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int64_t tile = cluster_id; tile < tiles; tile += n_clusters) {
+      SkItem it;
+      for (int64_t i = 0; sk_item(args, cluster_id, n_clusters, nk, i, it); ++i) {
+        const int64_t tile = it.tile;
         const int m0 = (int)((tile % num_m) * (2 * kBM) + rank * kBM);
         const int n0 = (int)((tile / num_m) * BN + rank * 128);
-        for (int kb = 0; kb < nk; ++kb) {
+        for (int kb = it.kb0; kb < it.kb1; ++kb) {
           mbar_wait(empty_bar(stage), phase ^ 1u);
           if (leader) mbar_expect_tx(full_bar(stage), (uint32_t)(2 * k2StageBytes));
           const uint32_t fb = mapa_shared(full_bar(stage), 0);
@@ -507,14 +610,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
                              ((uint32_t)(256 >> 4) << 24);
       int stage = 0;
       uint32_t phase = 0;
-      int64_t local = 0;
-      for (int64_t tile = cluster_id; tile < tiles; tile += n_clusters, ++local) {
+      SkItem it;
+      for (int64_t local = 0; sk_item(args, cluster_id, n_clusters, nk, local, it); ++local) {
         const int acc = (int)(local & 1);
         const uint32_t acc_phase = (uint32_t)((local >> 1) & 1);
         mbar_wait(tempty_bar(acc), acc_phase ^ 1u);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
-        for (int kb = 0; kb < nk; ++kb) {
+        for (int kb = it.kb0; kb < it.kb1; ++kb) {
           mbar_wait(full_bar(stage), phase);
           tc_fence_after();
           if (lane == 0) {
@@ -524,7 +627,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
             for (int kk = 0; kk < kBK / 16; ++kk) {
               const uint64_t ad = desc_sw128(a0 + kk * 32, 16, 1024);
               const uint64_t bd = desc_sw128(b0 + kk * 2048, kBK * 128, 1024);
-              tc_mma_f16_pair(d_tmem, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
+              tc_mma_f16_pair(d_tmem, ad, bd, idesc, (kb != it.kb0 || kk != 0) ? 1u : 0u);
             }
             tc_commit_pair(empty_bar(stage));
           }
@@ -539,16 +642,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     // ====== epilogue (both CTAs): this CTA's 128 rows x 256 columns ======
     const int quarter = warp & 3;
     const int half = (warp - 2) >> 2;
-    int64_t local = 0;
-    for (int64_t tile = cluster_id; tile < tiles; tile += n_clusters, ++local) {
+    const int64_t wslot = (int64_t)rank * kEpiWarps + (warp - 2);   // this warp's share of a pair tile
+    SkItem it;
+    for (int64_t local = 0; sk_item(args, cluster_id, n_clusters, nk, local, it); ++local) {
+      const int64_t tile = it.tile;
       const int acc = (int)(local & 1);
       const uint32_t acc_phase = (uint32_t)((local >> 1) & 1);
       const int64_t m0 = (tile % num_m) * (2 * kBM) + rank * kBM;
       const int64_t tn = tile / num_m;
       mbar_wait(tfull_bar(acc), acc_phase);
       tc_fence_after();
-      epilogue_tile<BN, EPI>(args, tmem_base, acc, quarter, half, lane, m0, tn * BN, tn,
-                             stg_all + (warp - 2) * 32 * 33);
+      if (it.kind == 1) {
+        store_partial(tmem_base, acc, quarter, half, lane, args.sk_part + (it.slot * 16 + wslot) * kSkWarpFloats,
+                      args.sk_flags + it.slot * 16 + wslot);
+      } else {
+        epilogue_tile<BN, EPI>(args, tmem_base, acc, quarter, half, lane, m0, tn * BN, tn,
+                               args.sk_part + (it.slot * 16 + wslot) * kSkWarpFloats, it.npart,
+                               args.sk_flags + it.slot * 16 + wslot);
+      }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(mapa_shared(tempty_bar(acc), 0));
@@ -667,7 +778,7 @@ int launch_pair_t(const CUtensorMap& ma, const CUtensorMap& mb, const GemmArgs& 
   }
   const int64_t tiles = ((a.M + 255) / 256) * ((a.N + 255) / 256);
   const int64_t pairs = num_sms() / 2;
-  const int grid = 2 * (int)(tiles < pairs ? tiles : pairs);
+  const int grid = 2 * (int)(a.sk_units ? pairs : (tiles < pairs ? tiles : pairs));
   launch_k(gemm_tcgen05_pair_kernel<EPI>, dim3(grid), dim3(kGemmThreads), k2Smem, st, ma, mb, a);
   return launch_status("gemm_tcgen05_pair_kernel");
 }
@@ -694,10 +805,42 @@ int tma_map_bf16(const void* ptr, int64_t inner, int64_t outer, int64_t ld, int 
 
 int64_t gemm_ce_tiles(int64_t N) { return 2 * ((N + 255) / 256); }   // one partial per 128-column half
 
+// Stream-K tail of the pair kernel.  With W pairs and T tiles, the last full
+// wave plus the partial one ((T mod W) + W tiles, or all T when T < W) are cut
+// into k-blocks spread evenly over all W pairs, so no pair idles in the last
+// wave.  Returns the workspace bytes it needs (0: not worthwhile).
+struct SkPlan {
+  int64_t dp_tiles, units, slots, bytes, flag_bytes;
+  int pieces;
+};
+
+SkPlan sk_plan(int64_t M, int64_t N, int64_t K) {
+  SkPlan pl{0, 0, 0, 0, 0, 1};
+  const int64_t W = num_sms() / 2;
+  const int64_t tiles = ((M + 255) / 256) * ((N + 255) / 256);
+  const int64_t nk = (K + kBK - 1) / kBK;
+  pl.dp_tiles = tiles;
+  if (M <= kBM || tiles % W == 0 || tiles * nk < 8 * W) return pl;
+  const int64_t full = tiles / W;
+  const int64_t dp = full >= 1 ? (full - 1) * W : 0;
+  const int64_t units = (tiles - dp) * nk;
+  const int64_t lmin = units / W;
+  if (lmin < 4) return pl;                     // pieces too small to pay for the fixup
+  pl.pieces = (int)((nk + lmin - 1) / lmin + 1);
+  pl.dp_tiles = dp;
+  pl.units = units;
+  pl.slots = (tiles - dp) * (pl.pieces - 1);
+  pl.flag_bytes = (pl.slots * 16 * 4 + 4095) / 4096 * 4096;
+  pl.bytes = pl.flag_bytes + pl.slots * 16 * (int64_t)kSkWarpFloats * 4;
+  return pl;
+}
+
+int64_t gemm_workspace_bytes(int64_t M, int64_t N, int64_t K) { return sk_plan(M, N, K).bytes; }
+
 
 int gemm_launch(const void* A, int64_t lda, const void* B, int64_t ldb, int64_t M, int64_t N, int64_t K, int epi,
                 const float* bias, void* out, int64_t ldo, const int32_t* targets, float* ce_part, float* ce_tgt,
-                int32_t* err, cudaStream_t st) {
+                int32_t* err, void* ws, int64_t ws_bytes, cudaStream_t st) {
   if (M == 0 || N == 0) return ZO_OK;
   if (K <= 0) { set_error("zo_gemm_bf16: K must be positive"); return ZO_ERR_CONFIG; }
   if (lda % 8 || ldb % 8 || lda < K || ldb < N) {
@@ -723,7 +866,18 @@ int gemm_launch(const void* A, int64_t lda, const void* B, int64_t ldb, int64_t 
   if (rc) return rc;
   rc = get_map(B, N, K, ldb, 64, kBK, &mb);
   if (rc) return rc;
-  GemmArgs a{M, N, K, bias, out, ldo, targets, ce_part, ce_tgt, err, gemm_ce_tiles(N)};
+  GemmArgs a{M, N, K, bias, out, ldo, targets, ce_part, ce_tgt, err, gemm_ce_tiles(N), 0, 0, 1, nullptr, nullptr};
+  a.dp_tiles = ((M + 255) / 256) * ((N + 255) / 256);
+  if (ws && (reinterpret_cast<uintptr_t>(ws) & 255) == 0) {
+    const SkPlan pl = sk_plan(M, N, K);
+    if (pl.units && pl.bytes <= ws_bytes) {
+      a.dp_tiles = pl.dp_tiles;
+      a.sk_units = pl.units;
+      a.sk_pieces = pl.pieces;
+      a.sk_flags = static_cast<int32_t*>(ws);
+      a.sk_part = reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + pl.flag_bytes);
+    }
+  }
   static const int pair_mode = [] {
     const char* e = getenv("ZO_GEMM_PAIR");   // 0: single-CTA only, 1: CTA pairs when M > 128 (default)
     return e ? atoi(e) : 1;

@@ -23,6 +23,8 @@ from __future__ import annotations
 
 import ctypes as C
 
+import os
+
 import numpy as np
 import torch
 
@@ -164,6 +166,23 @@ class Workspace:
         self.ids = torch.zeros(M, dtype=torch.int32, device=device)
         self.tgt = torch.zeros(M, dtype=torch.int32, device=device)
         self.err = torch.zeros(1, dtype=torch.int32, device=device)
+        # optional stream-K workspace of this direction's GEMMs (zeroed once;
+        # the kernels leave their flags cleared), sized for the largest one.
+        # Off by default: at these shapes the finisher's partial reduction,
+        # always a pair's last item, costs more than the partial wave it fills
+        # (tools/gemm_bench.py).
+        self.gemm_ws = None
+        if os.environ.get("ZO_GEMM_SK", "0") == "1":
+            lib = L.lib()
+            need = max(int(lib.zo_gemm_workspace_bytes(M, n, k))
+                       for n, k in ((3 * d, d), (d, d), (4 * d, d), (d, 4 * d), (v, d)))
+            self.gemm_ws = torch.zeros(max(need, 256), dtype=torch.uint8, device=device)
+
+    def gemm(self, lib, *args):
+        """(fn, args) of one GEMM launch; args are zo_gemm_bf16's, stream last."""
+        if self.gemm_ws is None:
+            return (lib.zo_gemm_bf16, args)
+        return (lib.zo_gemm_bf16_ws, (*args[:-1], self.gemm_ws.data_ptr(), self.gemm_ws.numel(), args[-1]))
 
 
 def _ptr(t):
@@ -370,17 +389,17 @@ class DeviceStore:
                 ldx, ldh = ws.x.stride(0), ws.h.stride(0)
                 calls += [
                     (lib.zo_layernorm_fwd, (_ptr(ws.x), ldx, v("ln1_g"), v("ln1_b"), M, d, _ptr(ws.h), ldh, st)),
-                    (lib.zo_gemm_bf16, (_ptr(ws.h), ldh, _ptr(wq), wq.stride(0), M, 3 * d, d, L.ZO_EPI_BIAS_BF16,
+                    ws.gemm(lib, *(_ptr(ws.h), ldh, _ptr(wq), wq.stride(0), M, 3 * d, d, L.ZO_EPI_BIAS_BF16,
                                         v("bqkv"), _ptr(ws.qkv), ws.qkv.stride(0), 0, 0, 0, 0, st)),
                     (lib.zo_attn_causal_fwd, (_ptr(ws.qkv), ws.qkv.stride(0), B, T, H, hd, _ptr(ws.ctx),
                                               ws.ctx.stride(0), st)),
-                    (lib.zo_gemm_bf16, (_ptr(ws.ctx), ws.ctx.stride(0), _ptr(wo), wo.stride(0), M, d, d,
+                    ws.gemm(lib, *(_ptr(ws.ctx), ws.ctx.stride(0), _ptr(wo), wo.stride(0), M, d, d,
                                         L.ZO_EPI_BIAS_RESID_F32, v("bo"), _ptr(ws.x), ldx, 0, 0, 0, 0, st)),
                     (lib.zo_layernorm_fwd, (_ptr(ws.x), ldx, v("ln2_g"), v("ln2_b"), M, d, _ptr(ws.h), ldh, st)),
-                    (lib.zo_gemm_bf16, (_ptr(ws.h), ldh, _ptr(w1), w1.stride(0), M, 4 * d, d,
+                    ws.gemm(lib, *(_ptr(ws.h), ldh, _ptr(w1), w1.stride(0), M, 4 * d, d,
                                         L.ZO_EPI_BIAS_GELU_BF16, v("b1"), _ptr(ws.ff), ws.ff.stride(0), 0, 0, 0, 0,
                                         st)),
-                    (lib.zo_gemm_bf16, (_ptr(ws.ff), ws.ff.stride(0), _ptr(w2), w2.stride(0), M, d, 4 * d,
+                    ws.gemm(lib, *(_ptr(ws.ff), ws.ff.stride(0), _ptr(w2), w2.stride(0), M, d, 4 * d,
                                         L.ZO_EPI_BIAS_RESID_F32, v("b2"), _ptr(ws.x), ldx, 0, 0, 0, 0, st)),
                 ]
             else:
@@ -390,14 +409,14 @@ class DeviceStore:
                                                      ws.h.stride(0), st)))
                 bout = _ptr(src.vview(s, bid, "b_out"))
                 if head_mode == "ce":
-                    calls.append((lib.zo_gemm_bf16, (_ptr(ws.h), ws.h.stride(0), _ptr(wout), wout.stride(0), M, V, d,
+                    calls.append(ws.gemm(lib, *(_ptr(ws.h), ws.h.stride(0), _ptr(wout), wout.stride(0), M, V, d,
                                                      L.ZO_EPI_CE, bout, 0, 0, _ptr(ws.tgt), _ptr(ws.ce_part),
                                                      _ptr(ws.ce_tgt), _ptr(ws.err), st)))
                     calls.append((lib.zo_ce_finalize, (_ptr(ws.ce_part), _ptr(ws.ce_tgt), M, ws.n_ce,
                                                        loss_out if loss_out is not None else _ptr(ws.loss),
                                                        _ptr(ws.row_scratch), _ptr(ws.err), st)))
                 else:   # materialise logits (API forward(); not on the step)
-                    calls.append((lib.zo_gemm_bf16, (_ptr(ws.h), ws.h.stride(0), _ptr(wout), wout.stride(0), M, V, d,
+                    calls.append(ws.gemm(lib, *(_ptr(ws.h), ws.h.stride(0), _ptr(wout), wout.stride(0), M, V, d,
                                                      L.ZO_EPI_F32, 0, _ptr(logits), logits.stride(0), 0, 0, 0, 0,
                                                      st)))
         return calls

@@ -77,6 +77,49 @@ def test_gemm_ce_epilogue_and_finalize(M, V, K):
     torch.testing.assert_close(tl.double(), logits.gather(1, tg.long()[:, None])[:, 0], rtol=1e-4, atol=1e-3)
 
 
+# shapes whose last wave is split along K (stream-K tail): 64 / 192 / 1576
+# tiles of 256 x 256 over the pairs, and a K=8192 case with 3 pieces per tile
+SK_SHAPES = [(2048, 2048, 2048), (2048, 6144, 2048), (2048, 2048, 8192), (1024, 4000, 1000), (512, 50272, 256)]
+
+
+@pytest.mark.parametrize("M,N,K", SK_SHAPES)
+def test_gemm_stream_k_epilogues(M, N, K):
+    """The stream-K schedule (workspace given) matches fp32 torch for every
+    epilogue, is bit-reproducible run to run, and leaves its flags cleared."""
+    ws = ops.gemm_workspace(M, N, K)
+    assert ws.numel() > 256                      # the schedule is active at these shapes
+    a, b = _rand(M, K, seed=21, scale=0.5), _rand(K, N, seed=22, scale=0.05)
+    bias = _rand(N, dtype=torch.float32, seed=23)
+    ref = a.float() @ b.float()
+    tol = dict(rtol=2e-3, atol=2e-3 * math.sqrt(K / 64))
+    out = torch.full((M, N), float("nan"), device=DEV)
+    ops.gemm(a, b, L.ZO_EPI_F32, out=out, workspace=ws)
+    torch.testing.assert_close(out, ref, **tol)
+    out2 = torch.full((M, N), float("nan"), device=DEV)
+    ops.gemm(a, b, L.ZO_EPI_F32, out=out2, workspace=ws)
+    assert torch.equal(out, out2)                # fixed reduction order
+    x = _rand(M, N, dtype=torch.float32, seed=24)
+    xr = x + (ref + bias)
+    ops.gemm(a, b, L.ZO_EPI_BIAS_RESID_F32, out=x, bias=bias, workspace=ws)
+    torch.testing.assert_close(x, xr, **tol)
+    o16 = torch.empty(M, N, device=DEV, dtype=torch.bfloat16)
+    ops.gemm(a, b, L.ZO_EPI_BIAS_GELU_BF16, out=o16, bias=bias, workspace=ws)
+    torch.testing.assert_close(o16.float(), torch.nn.functional.gelu(ref + bias, approximate="tanh"),
+                               rtol=1e-2, atol=1e-2)
+    tg = torch.randint(0, N, (M,), generator=torch.Generator().manual_seed(4)).to(DEV, torch.int32)
+    nt = ops.ce_tiles(N)
+    part, tl = torch.empty(M, nt, 2, device=DEV), torch.empty(M, device=DEV)
+    err = torch.zeros(1, dtype=torch.int32, device=DEV)
+    ops.gemm(a, b, L.ZO_EPI_CE, bias=bias, targets=tg, ce_part=part, ce_tgt=tl, err=err, workspace=ws)
+    loss, scratch = torch.empty(1, dtype=torch.float64, device=DEV), torch.empty(M, dtype=torch.float64, device=DEV)
+    ops.ce_finalize(part, tl, M, nt, loss, scratch, err)
+    cref = torch.nn.functional.cross_entropy((ref + bias).double(), tg.long())
+    assert err.item() == 0 and abs(loss.item() - cref.item()) < 1e-3
+    torch.cuda.synchronize()
+    nflag = int(ws[:4096].numel())
+    assert int(ws[:nflag].view(torch.int32).abs().sum().item()) == 0    # flags self-cleared
+
+
 @pytest.mark.parametrize("rows,d", [(64, 768), (513, 2048), (7, 6), (3, 12288)])
 def test_layernorm(rows, d):
     x = _rand(rows, d, dtype=torch.float32, seed=13) * 3 + 1
