@@ -114,6 +114,17 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(rows)}
 
 
+def _traffic():
+    """DRAM bytes per launch (perturb) / per step (all GEMM launches) from the
+    committed ncu capture of this bench (profiles/ncu_traffic.json, written by
+    tools/traffic_from_ncu.py from a `--metrics dram__bytes_*` launch list)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            return json.load(f)
+    except (OSError, ValueError):
+        return {}
+
+
 def _peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -307,8 +318,13 @@ def ours(args, rank, world, local_rank):
         if world > 1:
             dist.barrier()
         st.record()
+        nvtx = bool(os.environ.get("ZO_NVTX"))      # ncu --nvtx-include zo_step/ selects the timed steps
         for j in range(args.warmup, args.warmup + args.steps):
+            if nvtx:
+                torch.cuda.nvtx.range_push("zo_step")
             one_step(j)
+            if nvtx:
+                torch.cuda.nvtx.range_pop()
         en.record()
         torch.cuda.synchronize()
         if world > 1:
@@ -364,6 +380,7 @@ def ours(args, rank, world, local_rank):
     if rank != 0:
         return
     hbm, tf_sus, tf_burst, peak_kind = _peaks()
+    traffic = _traffic() if (args.model, T, B) == (MODEL, SEQ, BATCH_PER_GROUP) else {}
     P = store.total_params
     bytes_per_param = 12 if world == 1 else 10
     pert_avg = statistics.mean(p_ms)
@@ -376,10 +393,14 @@ def ours(args, rank, world, local_rank):
     pert_share = pert_avg / step_ms_per_rank
     roof_gemm = {"bound": "tensor", "kernel": "gemm_tcgen05_kernel (all QKV/O/FFN/LM-head launches)",
                  "achieved": gemm_tfs, "peak": tf_sus, "unit": "TFLOP/s", "frac": gemm_tfs / tf_sus,
-                 "traffic": None, "peak_kind": f"{peak_kind} sustained bf16", "share_of_step": gemm_share,
+                 "traffic": traffic.get("gemm_bytes_per_step") if world == 1 else None,
+                 "traffic_unit": "DRAM bytes per step, all GEMM launches (ncu)",
+                 "peak_kind": f"{peak_kind} sustained bf16", "share_of_step": gemm_share,
                  "algorithmic": "2*M*N*K per launch, M=B*T"}
     roof_pert = {"bound": "hbm", "kernel": "perturb_update_kernel", "achieved": pert_gbs, "peak": hbm,
-                 "unit": "GB/s", "frac": pert_gbs / hbm, "traffic": None, "peak_kind": f"{peak_kind} HBM copy",
+                 "unit": "GB/s", "frac": pert_gbs / hbm,
+                 "traffic": traffic.get("perturb_bytes_per_launch") if world == 1 else None,
+                 "traffic_algorithmic": P * bytes_per_param, "peak_kind": f"{peak_kind} HBM copy",
                  "share_of_step": pert_share,
                  "algorithmic": f"{bytes_per_param} B/param x {P} params per step "
                                 f"({_plan_text(args, world)})"}

@@ -191,32 +191,43 @@ int layernorm_launch(const float* x, int64_t ldx, const float* g, const float* b
 // cross-entropy finalize: per row combine the N-tile partials (fixed order),
 // then a single-CTA fixed-order f64 mean -- bit-stable run to run.
 // ---------------------------------------------------------------------------
+// One warp per row: lanes stride the row's (max, sum-exp) tile partials
+// (coalesced 8-B pairs), then fixed-shape xor-shuffle trees combine them,
+// so the result is deterministic run to run.
 __global__ void ce_rows_kernel(const float* __restrict__ part, const float* __restrict__ tgt, int64_t rows,
                                int64_t n_tiles, double* __restrict__ row_loss, int32_t* err) {
   pdl_trigger();
   pdl_wait();
-  const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const int64_t r = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
   if (r >= rows) return;
-  const float* p = part + r * n_tiles * 2;
+  const float2* p = reinterpret_cast<const float2*>(part + r * n_tiles * 2);
   double m = -INFINITY;
   bool bad = false;
-  for (int64_t i = 0; i < n_tiles; ++i) {
-    const float v = p[2 * i];
-    if (v == -INFINITY && p[2 * i + 1] == 0.f) continue;   // empty (out-of-range) partial
-    if (!isfinite(v)) bad = true;
-    m = fmax(m, (double)v);
+  for (int64_t i = lane; i < n_tiles; i += 32) {
+    const float2 v = p[i];
+    if (v.x == -INFINITY && v.y == 0.f) continue;   // empty (out-of-range) partial
+    if (!isfinite(v.x)) bad = true;
+    m = fmax(m, (double)v.x);
   }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
   double s = 0.0;
-  for (int64_t i = 0; i < n_tiles; ++i) {
-    const float ps = p[2 * i + 1];
-    if (p[2 * i] == -INFINITY && ps == 0.f) continue;
-    if (!isfinite(ps)) bad = true;
-    s += (double)ps * exp((double)p[2 * i] - m);
+  for (int64_t i = lane; i < n_tiles; i += 32) {
+    const float2 v = p[i];
+    if (v.x == -INFINITY && v.y == 0.f) continue;
+    if (!isfinite(v.y)) bad = true;
+    s += (double)v.y * exp((double)v.x - m);
   }
-  const float tl = tgt[r];
-  if (!isfinite(tl)) bad = true;
-  if (bad) atomicOr(err, 2);
-  row_loss[r] = m + log(s) - (double)tl;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  bad = __any_sync(0xffffffffu, bad);
+  if (lane == 0) {
+    const float tl = tgt[r];
+    if (!isfinite(tl)) bad = true;
+    if (bad) atomicOr(err, 2);
+    row_loss[r] = m + log(s) - (double)tl;
+  }
 }
 
 __global__ void mean_f64_kernel(const double* __restrict__ v, int64_t n, double* out) {
@@ -240,7 +251,7 @@ __global__ void mean_f64_kernel(const double* __restrict__ v, int64_t n, double*
 int ce_finalize_launch(const float* part, const float* tgt, int64_t rows, int64_t n_tiles, double* loss,
                        double* row_scratch, int32_t* err, cudaStream_t st) {
   if (rows == 0) return ZO_OK;
-  launch_k(ce_rows_kernel, dim3((unsigned)((rows + 127) / 128)), dim3(128), 0, st, part, tgt, rows, n_tiles,
+  launch_k(ce_rows_kernel, dim3((unsigned)((rows + 7) / 8)), dim3(256), 0, st, part, tgt, rows, n_tiles,
            row_scratch, err);
   launch_k(mean_f64_kernel, dim3(1), dim3(1024), 0, st, (const double*)row_scratch, rows, loss);
   return launch_status("ce_finalize");

@@ -472,6 +472,7 @@ class OffloadedZo:
         self.offloaded_params += sum(self.layouts[i].elem_count for i in self.wids)
         st = ZoStep(self.iteration, seed, float(r[0]), float(r[1]), float(r[2]))
         self.g_prev, self.last_seed, self._pending = st.g, seed, True
+        self.host.unflushed = True
         return st
 
     # -- end of run (scheduler.py:393-415) ------------------------------------------------
@@ -493,6 +494,7 @@ class OffloadedZo:
         self.scal[3:4].fill_(0)
         self.sync_host()
         self._pending = False
+        self.host.unflushed = False
 
     def sync_host(self) -> None:
         """Copy the persistent device blocks back to the host master."""

@@ -152,6 +152,7 @@ class MeshZo:
         s.run(self.step_calls())
         st = _finish_record(s, list(self.ws.values()), self.iteration, seed)
         self._pending, self.g_prev, self.last_seed = True, st.g, seed
+        s.unflushed = True
         return st
 
     def flush(self) -> None:
@@ -163,6 +164,7 @@ class MeshZo:
         s.scal[3:4].fill_(0)
         torch.cuda.current_stream().synchronize()
         self._pending = False
+        s.unflushed = False
 
 
 def _gather(fabric, gathered, local):

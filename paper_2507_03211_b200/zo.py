@@ -294,6 +294,7 @@ class StreamingZo:
                                       update=apply_pending or not self.mgr.oracle))
         st = _finish(self.store, wsp, wsn, self.iteration, seed)
         self.g_prev, self.last_seed, self._pending, self._z_prev = st.g, seed, True, zc
+        self.store.unflushed = True
         return st
 
     def flush(self) -> None:
@@ -308,6 +309,7 @@ class StreamingZo:
         s.scal[3:4].fill_(0)
         torch.cuda.current_stream().synchronize()
         self._pending = False
+        self.store.unflushed = False
 
 
 def _side_stream(store: DeviceStore):

@@ -79,6 +79,13 @@ def main():
         for b in store.blocks:
             out[f"{name}/final/{b.block_id}"] = b.buf.copy()
         out[f"{name}/final_sha"] = np.array(store.checksum())
+        # ZOPK checkpoint bytes of the trained store (model.py:381-401)
+        import tempfile
+        from zosim import save_checkpoint
+        with tempfile.TemporaryDirectory() as td:
+            p = os.path.join(td, "ck.zopk")
+            save_checkpoint(store, p)
+            out[f"{name}/ckpt"] = np.frombuffer(open(p, "rb").read(), dtype=np.uint8).copy()
 
         # lazy streaming and the offload scheduler (must match eager)
         lazy = init_model(cfg, 7)
