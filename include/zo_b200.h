@@ -58,6 +58,11 @@ extern "C" {
 #define ZO_EPI_BIAS_GELU_BF16 2 /* out bf16 = gelu_tanh(acc + bias) (FFN up)      */
 #define ZO_EPI_BIAS_RESID_F32 3 /* out f32 += (acc + bias)        (O-proj, FFN down) */
 #define ZO_EPI_CE 4           /* LM head: per-row partial max/sum-exp + target logit */
+#define ZO_EPI_BIAS_RELU_BF16 5 /* out bf16 = relu(acc + bias)    (real-OPT FFN up) */
+/* OR-ed into `epilogue`: B is given transposed, [N, K] row-major (K
+ * contiguous, ldb >= K) -- e.g. a tied LM head reading the [V, d] token
+ * embedding.  Supported with ZO_EPI_F32 and ZO_EPI_CE. */
+#define ZO_GEMM_B_KMAJOR 0x100
 
 /* One tensor of a parameter block, as the perturb/update kernel sees it. */
 typedef struct ZoSegment {

@@ -21,6 +21,8 @@ ZO_Z_PHILOX, ZO_Z_ORACLE = 0, 1
 ZO_SHADOW_BF16, ZO_SHADOW_F32, ZO_SHADOW_NONE = 0, 1, 2
 ZO_PU_UPDATE, ZO_PU_SHADOW_A, ZO_PU_SHADOW_B = 1, 2, 4
 ZO_EPI_F32, ZO_EPI_BIAS_BF16, ZO_EPI_BIAS_GELU_BF16, ZO_EPI_BIAS_RESID_F32, ZO_EPI_CE = 0, 1, 2, 3, 4
+ZO_EPI_BIAS_RELU_BF16 = 5
+ZO_GEMM_B_KMAJOR = 0x100
 
 
 class ZoSegment(C.Structure):

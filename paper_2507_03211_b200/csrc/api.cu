@@ -178,9 +178,10 @@ int zo_gemm_bf16(const void* A, int64_t lda, const void* B, int64_t ldb, int64_t
                  int32_t epilogue, const float* bias, void* out, int64_t ldo, const int32_t* targets, float* ce_part,
                  float* ce_tgt, int32_t* err_flag, void* stream) {
   ZO_CHECK_ARG(A && B, ZO_ERR_CONFIG, "zo_gemm_bf16: null operand");
-  ZO_CHECK_ARG(epilogue == ZO_EPI_CE ? (targets && ce_part && ce_tgt && bias && err_flag) : (out != nullptr),
+  const int32_t epi = epilogue & ~ZO_GEMM_B_KMAJOR;
+  ZO_CHECK_ARG(epi == ZO_EPI_CE ? (targets && ce_part && ce_tgt && err_flag) : (out != nullptr),
                ZO_ERR_CONFIG, "zo_gemm_bf16: missing epilogue buffers");
-  ZO_CHECK_ARG(epilogue == ZO_EPI_F32 || epilogue == ZO_EPI_CE || bias, ZO_ERR_CONFIG, "zo_gemm_bf16: bias required");
+  ZO_CHECK_ARG(epi == ZO_EPI_F32 || epi == ZO_EPI_CE || bias, ZO_ERR_CONFIG, "zo_gemm_bf16: bias required");
   return zo::gemm_launch(A, lda, B, ldb, M, N, K, epilogue, bias, out, ldo, targets, ce_part, ce_tgt, err_flag,
                          nullptr, 0, ZO_STREAM(stream));
 }
@@ -190,9 +191,10 @@ int zo_gemm_bf16_ws(const void* A, int64_t lda, const void* B, int64_t ldb, int6
                     float* ce_part, float* ce_tgt, int32_t* err_flag, void* workspace, int64_t workspace_bytes,
                     void* stream) {
   ZO_CHECK_ARG(A && B, ZO_ERR_CONFIG, "zo_gemm_bf16_ws: null operand");
-  ZO_CHECK_ARG(epilogue == ZO_EPI_CE ? (targets && ce_part && ce_tgt && bias && err_flag) : (out != nullptr),
+  const int32_t epi = epilogue & ~ZO_GEMM_B_KMAJOR;
+  ZO_CHECK_ARG(epi == ZO_EPI_CE ? (targets && ce_part && ce_tgt && err_flag) : (out != nullptr),
                ZO_ERR_CONFIG, "zo_gemm_bf16_ws: missing epilogue buffers");
-  ZO_CHECK_ARG(epilogue == ZO_EPI_F32 || epilogue == ZO_EPI_CE || bias, ZO_ERR_CONFIG,
+  ZO_CHECK_ARG(epi == ZO_EPI_F32 || epi == ZO_EPI_CE || bias, ZO_ERR_CONFIG,
                "zo_gemm_bf16_ws: bias required");
   return zo::gemm_launch(A, lda, B, ldb, M, N, K, epilogue, bias, out, ldo, targets, ce_part, ce_tgt, err_flag,
                          workspace, workspace_bytes, ZO_STREAM(stream));

@@ -5,6 +5,8 @@
 //   A: activations, row-major, K contiguous          -> UMMA K-major operand
 //   B: weights in the reference's (d_in, d_out) layout, N contiguous
 //      (src/zosim/model.py:325 `h @ W`)                 -> UMMA MN-major operand
+//      or, with ZO_GEMM_B_KMAJOR, B^T stored [N, K] row-major (K contiguous:
+//      a tied LM head reading the [V, d] token embedding) -> UMMA K-major
 //
 // Persistent, warp-specialised CTA (192 threads, 1 CTA per SM):
 //   warp 0      TMA producer (one lane): A 128x64 box + B 64x64 boxes per stage
@@ -17,6 +19,7 @@
 // Epilogues (the ops that follow each GEMM in model.py:325-344):
 //   ZO_EPI_BIAS_BF16       qkv  = h @ Wqkv + b                 (bf16 out)
 //   ZO_EPI_BIAS_GELU_BF16  f    = gelu_tanh(h2 @ W1 + b1)      (bf16 out)
+//   ZO_EPI_BIAS_RELU_BF16  f    = relu(h2 @ W1 + b1)           (bf16 out, real OPT)
 //   ZO_EPI_BIAS_RESID_F32  x   += ctx @ Wo + bo / f @ W2 + b2  (fp32 residual)
 //   ZO_EPI_CE              per-row (max, sum exp) of logits + target logit;
 //                          the [M, V] logits never reach HBM
@@ -112,11 +115,11 @@ __device__ __forceinline__ int ld_acquire_s32(const int32_t* p) {
   return v;
 }
 
-template <int BN>
+template <int BN, bool BKM = false>
 __device__ __forceinline__ uint32_t make_idesc() {
   // c_format F32 [4,6)=1, a_format BF16 [7,10)=1, b_format BF16 [10,13)=1,
-  // a_major K (bit 15 = 0), b_major MN (bit 16 = 1), N>>3 at [17,23), M>>4 at [24,29)
-  return (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) | ((uint32_t)(BN >> 3) << 17) |
+  // a_major K (bit 15 = 0), b_major MN (bit 16 = 1) or K (0), N>>3 at [17,23), M>>4 at [24,29)
+  return (1u << 4) | (1u << 7) | (1u << 10) | (BKM ? 0u : (1u << 16)) | ((uint32_t)(BN >> 3) << 17) |
          ((uint32_t)(kBM >> 4) << 24);
 }
 
@@ -219,10 +222,11 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t tme
       if (!row_ok || col0 >= args.N) continue;
       const int lim = col0 + 32 <= args.N ? 32 : (int)(args.N - col0);
       float cm = -INFINITY;
+      const bool has_bias = args.bias != nullptr;   // a tied head has no bias (real OPT)
 #pragma unroll
       for (int i = 0; i < 32; ++i) {
         if (i < lim) {
-          v[i] += __ldg(args.bias + col0 + i);
+          if (has_bias) v[i] += __ldg(args.bias + col0 + i);
           bad |= !isfinite(v[i]);
           cm = fmaxf(cm, v[i]);
         }
@@ -241,7 +245,7 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t tme
         for (int i = 0; i < 32; ++i)
           if (i == ti) args.ce_tgt[row] = v[i];
       }
-    } else if constexpr (EPI == ZO_EPI_BIAS_BF16 || EPI == ZO_EPI_BIAS_GELU_BF16) {
+    } else if constexpr (EPI == ZO_EPI_BIAS_BF16 || EPI == ZO_EPI_BIAS_GELU_BF16 || EPI == ZO_EPI_BIAS_RELU_BF16) {
       // bf16 out: each thread writes 64 contiguous bytes of its row (4 x 16 B)
       float4 bias4[8];
       const bool full = row_ok && col0 + 32 <= args.N;
@@ -269,6 +273,10 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t tme
       if constexpr (EPI == ZO_EPI_BIAS_GELU_BF16) {
 #pragma unroll
         for (int i = 0; i < 32; ++i) v[i] = gelu_tanh(v[i]);
+      }
+      if constexpr (EPI == ZO_EPI_BIAS_RELU_BF16) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i], 0.f);
       }
       __nv_bfloat16* o = static_cast<__nv_bfloat16*>(args.out) + row * args.ldo + col0;
       if (full && ((reinterpret_cast<uintptr_t>(o) & 15) == 0)) {
@@ -352,7 +360,7 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t tme
   }
 }
 
-template <int BN, int EPI>
+template <int BN, int EPI, bool BKM>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                         const GemmArgs args) {
@@ -408,16 +416,20 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           mbar_wait(empty_bar(stage), phase ^ 1u);
           mbar_expect_tx(full_bar(stage), (uint32_t)C::kStageBytes);
           tma_load_2d(sA + stage * C::kABytes, &tmA, full_bar(stage), kb * kBK, m0);
+          if constexpr (BKM) {
+            tma_load_2d(sB + stage * C::kBBytes, &tmB, full_bar(stage), kb * kBK, n0);   // BN rows x 64 k
+          } else {
 #pragma unroll
-          for (int j = 0; j < BN / 64; ++j)
-            tma_load_2d(sB + stage * C::kBBytes + j * (kBK * 128), &tmB, full_bar(stage), n0 + 64 * j, kb * kBK);
+            for (int j = 0; j < BN / 64; ++j)
+              tma_load_2d(sB + stage * C::kBBytes + j * (kBK * 128), &tmB, full_bar(stage), n0 + 64 * j, kb * kBK);
+          }
           if (++stage == C::kStages) { stage = 0; phase ^= 1u; }
         }
       }
     }
   } else if (warp == 1) {
     // ============================ MMA issuer ==============================
-    const uint32_t idesc = make_idesc<BN>();
+    const uint32_t idesc = make_idesc<BN, BKM>();
     int stage = 0;
     uint32_t phase = 0;
     int64_t local = 0;
@@ -436,7 +448,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 #pragma unroll
           for (int kk = 0; kk < kBK / 16; ++kk) {
             const uint64_t ad = desc_sw128(a0 + kk * 32, 16, 1024);
-            const uint64_t bd = desc_sw128(b0 + kk * 2048, kBK * 128, 1024);
+            const uint64_t bd = BKM ? desc_sw128(b0 + kk * 32, 16, 1024) : desc_sw128(b0 + kk * 2048, kBK * 128, 1024);
             tc_mma_f16(d_tmem, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
           }
           tc_commit(empty_bar(stage));   // frees the smem slot once these MMAs retire
@@ -537,7 +549,7 @@ __device__ __forceinline__ void tc_mma_f16_pair(uint32_t d_tmem, uint64_t adesc,
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
 
-template <int EPI>
+template <int EPI, bool BKM>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     gemm_tcgen05_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                              const GemmArgs args) {
@@ -597,8 +609,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
           if (leader) mbar_expect_tx(full_bar(stage), (uint32_t)(2 * k2StageBytes));
           const uint32_t fb = mapa_shared(full_bar(stage), 0);
           tma_load_2d_cg2(sA + stage * k2ABytes, &tmA, fb, kb * kBK, m0);
-          tma_load_2d_cg2(sB + stage * k2BBytes, &tmB, fb, n0, kb * kBK);
-          tma_load_2d_cg2(sB + stage * k2BBytes + kBK * 128, &tmB, fb, n0 + 64, kb * kBK);
+          if constexpr (BKM) {
+            tma_load_2d_cg2(sB + stage * k2BBytes, &tmB, fb, kb * kBK, n0);    // 128 rows x 64 k
+          } else {
+            tma_load_2d_cg2(sB + stage * k2BBytes, &tmB, fb, n0, kb * kBK);
+            tma_load_2d_cg2(sB + stage * k2BBytes + kBK * 128, &tmB, fb, n0 + 64, kb * kBK);
+          }
           if (++stage == k2Stages) { stage = 0; phase ^= 1u; }
         }
       }
@@ -606,8 +622,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
   } else if (warp == 1) {
     // ====== MMA issuer (leader CTA only): M=256 x N=256 per instruction ======
     if (leader) {
-      const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) | ((uint32_t)(BN >> 3) << 17) |
-                             ((uint32_t)(256 >> 4) << 24);
+      const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (BKM ? 0u : (1u << 16)) |
+                             ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
       int stage = 0;
       uint32_t phase = 0;
       SkItem it;
@@ -626,7 +642,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
 #pragma unroll
             for (int kk = 0; kk < kBK / 16; ++kk) {
               const uint64_t ad = desc_sw128(a0 + kk * 32, 16, 1024);
-              const uint64_t bd = desc_sw128(b0 + kk * 2048, kBK * 128, 1024);
+              const uint64_t bd =
+                  BKM ? desc_sw128(b0 + kk * 32, 16, 1024) : desc_sw128(b0 + kk * 2048, kBK * 128, 1024);
               tc_mma_f16_pair(d_tmem, ad, bd, idesc, (kb != it.kb0 || kk != 0) ? 1u : 0u);
             }
             tc_commit_pair(empty_bar(stage));
@@ -737,28 +754,37 @@ int get_map(const void* ptr, int64_t inner, int64_t outer, int64_t ld, int box_i
   return ZO_OK;
 }
 
-template <int BN, int EPI>
+template <int BN, int EPI, bool BKM = false>
 int launch_t(const CUtensorMap& ma, const CUtensorMap& mb, const GemmArgs& a, cudaStream_t st) {
   using C = GemmCfg<BN>;
   static bool attr_done = false;   // per-instantiation (benign race: idempotent)
   if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_tcgen05_kernel<BN, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(gemm_tcgen05_kernel<BN, EPI, BKM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          C::kSmem);
     if (e != cudaSuccess) { set_error("gemm smem attribute: %s", cudaGetErrorString(e)); return ZO_ERR_CUDA; }
     attr_done = true;
   }
   const int64_t tiles = ((a.M + kBM - 1) / kBM) * ((a.N + BN - 1) / BN);
   const int grid = (int)(tiles < num_sms() ? tiles : num_sms());
-  launch_k(gemm_tcgen05_kernel<BN, EPI>, dim3(grid), dim3(kGemmThreads), C::kSmem, st, ma, mb, a);
+  launch_k(gemm_tcgen05_kernel<BN, EPI, BKM>, dim3(grid), dim3(kGemmThreads), C::kSmem, st, ma, mb, a);
   return launch_status("gemm_tcgen05_kernel");
 }
 
 template <int BN>
-int launch_bn(int epi, const CUtensorMap& ma, const CUtensorMap& mb, const GemmArgs& a, cudaStream_t st) {
+int launch_bn(int epi, bool bkm, const CUtensorMap& ma, const CUtensorMap& mb, const GemmArgs& a, cudaStream_t st) {
+  if (bkm) {
+    switch (epi) {
+      case ZO_EPI_F32: return launch_t<BN, ZO_EPI_F32, true>(ma, mb, a, st);
+      case ZO_EPI_CE: return launch_t<BN, ZO_EPI_CE, true>(ma, mb, a, st);
+    }
+    set_error("zo_gemm_bf16: ZO_GEMM_B_KMAJOR supports the F32 and CE epilogues only (got %d)", epi);
+    return ZO_ERR_CONFIG;
+  }
   switch (epi) {
     case ZO_EPI_F32: return launch_t<BN, ZO_EPI_F32>(ma, mb, a, st);
     case ZO_EPI_BIAS_BF16: return launch_t<BN, ZO_EPI_BIAS_BF16>(ma, mb, a, st);
     case ZO_EPI_BIAS_GELU_BF16: return launch_t<BN, ZO_EPI_BIAS_GELU_BF16>(ma, mb, a, st);
+    case ZO_EPI_BIAS_RELU_BF16: return launch_t<BN, ZO_EPI_BIAS_RELU_BF16>(ma, mb, a, st);
     case ZO_EPI_BIAS_RESID_F32: return launch_t<BN, ZO_EPI_BIAS_RESID_F32>(ma, mb, a, st);
     case ZO_EPI_CE: return launch_t<BN, ZO_EPI_CE>(ma, mb, a, st);
   }
@@ -767,11 +793,11 @@ int launch_bn(int epi, const CUtensorMap& ma, const CUtensorMap& mb, const GemmA
 }
 
 
-template <int EPI>
+template <int EPI, bool BKM = false>
 int launch_pair_t(const CUtensorMap& ma, const CUtensorMap& mb, const GemmArgs& a, cudaStream_t st) {
   static bool attr_done = false;
   if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_tcgen05_pair_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(gemm_tcgen05_pair_kernel<EPI, BKM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          k2Smem);
     if (e != cudaSuccess) { set_error("gemm pair smem attribute: %s", cudaGetErrorString(e)); return ZO_ERR_CUDA; }
     attr_done = true;
@@ -779,15 +805,25 @@ int launch_pair_t(const CUtensorMap& ma, const CUtensorMap& mb, const GemmArgs& 
   const int64_t tiles = ((a.M + 255) / 256) * ((a.N + 255) / 256);
   const int64_t pairs = num_sms() / 2;
   const int grid = 2 * (int)(a.sk_units ? pairs : (tiles < pairs ? tiles : pairs));
-  launch_k(gemm_tcgen05_pair_kernel<EPI>, dim3(grid), dim3(kGemmThreads), k2Smem, st, ma, mb, a);
+  launch_k(gemm_tcgen05_pair_kernel<EPI, BKM>, dim3(grid), dim3(kGemmThreads), k2Smem, st, ma, mb, a);
   return launch_status("gemm_tcgen05_pair_kernel");
 }
 
-int launch_pair(int epi, const CUtensorMap& ma, const CUtensorMap& mb, const GemmArgs& a, cudaStream_t st) {
+int launch_pair(int epi, bool bkm, const CUtensorMap& ma, const CUtensorMap& mb, const GemmArgs& a,
+                cudaStream_t st) {
+  if (bkm) {
+    switch (epi) {
+      case ZO_EPI_F32: return launch_pair_t<ZO_EPI_F32, true>(ma, mb, a, st);
+      case ZO_EPI_CE: return launch_pair_t<ZO_EPI_CE, true>(ma, mb, a, st);
+    }
+    set_error("zo_gemm_bf16: ZO_GEMM_B_KMAJOR supports the F32 and CE epilogues only (got %d)", epi);
+    return ZO_ERR_CONFIG;
+  }
   switch (epi) {
     case ZO_EPI_F32: return launch_pair_t<ZO_EPI_F32>(ma, mb, a, st);
     case ZO_EPI_BIAS_BF16: return launch_pair_t<ZO_EPI_BIAS_BF16>(ma, mb, a, st);
     case ZO_EPI_BIAS_GELU_BF16: return launch_pair_t<ZO_EPI_BIAS_GELU_BF16>(ma, mb, a, st);
+    case ZO_EPI_BIAS_RELU_BF16: return launch_pair_t<ZO_EPI_BIAS_RELU_BF16>(ma, mb, a, st);
     case ZO_EPI_BIAS_RESID_F32: return launch_pair_t<ZO_EPI_BIAS_RESID_F32>(ma, mb, a, st);
     case ZO_EPI_CE: return launch_pair_t<ZO_EPI_CE>(ma, mb, a, st);
   }
@@ -841,10 +877,13 @@ int64_t gemm_workspace_bytes(int64_t M, int64_t N, int64_t K) { return sk_plan(M
 int gemm_launch(const void* A, int64_t lda, const void* B, int64_t ldb, int64_t M, int64_t N, int64_t K, int epi,
                 const float* bias, void* out, int64_t ldo, const int32_t* targets, float* ce_part, float* ce_tgt,
                 int32_t* err, void* ws, int64_t ws_bytes, cudaStream_t st) {
+  const bool bkm = (epi & ZO_GEMM_B_KMAJOR) != 0;
+  epi &= ~ZO_GEMM_B_KMAJOR;
   if (M == 0 || N == 0) return ZO_OK;
   if (K <= 0) { set_error("zo_gemm_bf16: K must be positive"); return ZO_ERR_CONFIG; }
-  if (lda % 8 || ldb % 8 || lda < K || ldb < N) {
-    set_error("zo_gemm_bf16: lda/ldb must be multiples of 8 and >= K/N (lda=%lld ldb=%lld)", (long long)lda,
+  if (lda % 8 || ldb % 8 || lda < K || ldb < (bkm ? K : N)) {
+    set_error("zo_gemm_bf16: lda/ldb must be multiples of 8 and >= K / (N, or K with B_KMAJOR) (lda=%lld ldb=%lld)",
+              (long long)lda,
               (long long)ldb);
     return ZO_ERR_CONFIG;
   }
@@ -864,7 +903,13 @@ int gemm_launch(const void* A, int64_t lda, const void* B, int64_t ldb, int64_t 
   CUtensorMap ma, mb;
   int rc = get_map(A, K, M, lda, kBK, kBM, &ma);
   if (rc) return rc;
-  rc = get_map(B, N, K, ldb, 64, kBK, &mb);
+  static const int pair_mode = [] {
+    const char* e = getenv("ZO_GEMM_PAIR");   // 0: single-CTA only, 1: CTA pairs when M > 128 (default)
+    return e ? atoi(e) : 1;
+  }();
+  const bool pair = pair_mode && M > kBM && bn == 256;
+  // B tile: MN-major 64-column boxes, or K-major (rows = N) boxes of 128 (pair half) / BN rows
+  rc = bkm ? get_map(B, K, N, ldb, kBK, pair ? 128 : bn, &mb) : get_map(B, N, K, ldb, 64, kBK, &mb);
   if (rc) return rc;
   GemmArgs a{M, N, K, bias, out, ldo, targets, ce_part, ce_tgt, err, gemm_ce_tiles(N), 0, 0, 1, nullptr, nullptr};
   a.dp_tiles = ((M + 255) / 256) * ((N + 255) / 256);
@@ -878,12 +923,8 @@ int gemm_launch(const void* A, int64_t lda, const void* B, int64_t ldb, int64_t 
       a.sk_part = reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + pl.flag_bytes);
     }
   }
-  static const int pair_mode = [] {
-    const char* e = getenv("ZO_GEMM_PAIR");   // 0: single-CTA only, 1: CTA pairs when M > 128 (default)
-    return e ? atoi(e) : 1;
-  }();
-  if (pair_mode && M > kBM && bn == 256) return launch_pair(epi, ma, mb, a, st);
-  return bn == 256 ? launch_bn<256>(epi, ma, mb, a, st) : launch_bn<128>(epi, ma, mb, a, st);
+  if (pair) return launch_pair(epi, bkm, ma, mb, a, st);
+  return bn == 256 ? launch_bn<256>(epi, bkm, ma, mb, a, st) : launch_bn<128>(epi, bkm, ma, mb, a, st);
 }
 
 }  // namespace zo

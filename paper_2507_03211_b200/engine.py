@@ -66,11 +66,21 @@ class ShadowPlan:
             self.v_elems = off + n
             return off
 
+        tied = config.arch == "opt"     # real OPT: the LM head reads the token embedding
         for bl in layouts:
             vw, segs = {}, []
             if bl.kind == EMBEDDING:
+                if tied:
+                    # bf16 shadow of tok_emb [V, d] = the head's K-major B operand;
+                    # the gather still perturbs the fp32 rows it reads
+                    o, ld = walloc(v, d)
+                    vw["tok_emb"] = ("w", o, v, d, ld)
                 for name in bl.names:
-                    segs.append((bl.key(name), 1, bl.size(name), 0, bl.size(name), L.ZO_SHADOW_NONE))
+                    if tied and name == "tok_emb":
+                        segs.append((bl.key(name), v, d, o, ld, L.ZO_SHADOW_BF16) if ld != d else
+                                    (bl.key(name), 1, v * d, o, v * d, L.ZO_SHADOW_BF16))
+                    else:
+                        segs.append((bl.key(name), 1, bl.size(name), 0, bl.size(name), L.ZO_SHADOW_NONE))
             elif bl.kind == TRANSFORMER:
                 qo, qld = walloc(d, 3 * d)
                 vw["qkv"] = ("w", qo, d, 3 * d, qld)
@@ -96,6 +106,10 @@ class ShadowPlan:
                             segs.append((k, r, c, o, ld, L.ZO_SHADOW_BF16))
                     else:
                         segs.append((k, 1, n, vw[name][1], n, L.ZO_SHADOW_F32))
+            elif tied:  # real-OPT head: final LayerNorm only
+                for name in bl.names:
+                    vw[name] = ("v", valloc(d), 1, d, d)
+                    segs.append((bl.key(name), 1, d, vw[name][1], d, L.ZO_SHADOW_F32))
             else:  # head
                 wo_, wld = walloc(d, v)
                 vw["w_out"] = ("w", wo_, d, v, wld)
@@ -118,8 +132,8 @@ class ShadowPlan:
 
 def block_extent(plan: ShadowPlan, bid: int):
     """(w_lo, w_hi, v_lo, v_hi): the contiguous shadow ranges of one block."""
-    ws = [(o, o + r * ld) for (b, o, r, c, ld) in plan.views[bid].values() if b == "w"]
-    vs = [(o, o + c) for (b, o, r, c, ld) in plan.views[bid].values() if b == "v"]
+    ws = [(o, o + r * ld) for (b, o, r, c, ld) in plan.views[bid].values() if b == "w"] or [(0, 0)]
+    vs = [(o, o + c) for (b, o, r, c, ld) in plan.views[bid].values() if b == "v"] or [(0, 0)]
     return (min(a for a, _ in ws), max(b for _, b in ws), min(a for a, _ in vs), max(b for _, b in vs))
 
 
@@ -366,6 +380,9 @@ class DeviceStore:
         interface when those blocks live outside this store (offload)."""
         cfg, lib = self.config, L.lib()
         d, H, hd, V = cfg.d_model, cfg.n_heads, cfg.head_dim, cfg.vocab_size
+        opt = cfg.arch == "opt"
+        pos_off = 2 * d if opt else 0                      # OPT position t reads row t + 2
+        ffn_epi = L.ZO_EPI_BIAS_RELU_BF16 if opt else L.ZO_EPI_BIAS_GELU_BF16
         M, B, T = ws.M, ws.batch, ws.seq
         st = L.stream_ptr(stream)
         calls = []
@@ -377,7 +394,7 @@ class DeviceStore:
             if bl.kind == EMBEDDING:
                 calls.append((lib.zo_embed_fwd, (
                     src.theta_ptr(bl.key("tok_emb")), bl.key("tok_emb"),
-                    src.theta_ptr(bl.key("pos_emb")), bl.key("pos_emb"),
+                    src.theta_ptr(bl.key("pos_emb") + pos_off), bl.key("pos_emb") + pos_off,
                     _ptr(ws.ids), B, T, d, V, float(scale), scal_p, zmode, _ptr(z_cur), 0,
                     _ptr(ws.x), ws.x.stride(0), _ptr(ws.err), st)))
             elif bl.kind == TRANSFORMER:
@@ -397,28 +414,32 @@ class DeviceStore:
                                         L.ZO_EPI_BIAS_RESID_F32, v("bo"), _ptr(ws.x), ldx, 0, 0, 0, 0, st)),
                     (lib.zo_layernorm_fwd, (_ptr(ws.x), ldx, v("ln2_g"), v("ln2_b"), M, d, _ptr(ws.h), ldh, st)),
                     ws.gemm(lib, *(_ptr(ws.h), ldh, _ptr(w1), w1.stride(0), M, 4 * d, d,
-                                        L.ZO_EPI_BIAS_GELU_BF16, v("b1"), _ptr(ws.ff), ws.ff.stride(0), 0, 0, 0, 0,
-                                        st)),
+                                        ffn_epi, v("b1"), _ptr(ws.ff), ws.ff.stride(0), 0, 0, 0, 0, st)),
                     ws.gemm(lib, *(_ptr(ws.ff), ws.ff.stride(0), _ptr(w2), w2.stride(0), M, d, 4 * d,
                                         L.ZO_EPI_BIAS_RESID_F32, v("b2"), _ptr(ws.x), ldx, 0, 0, 0, 0, st)),
                 ]
             else:
-                wout, _, _ = src.wview(s, bid, "w_out")
+                if opt:     # tied head: B = the token embedding's bf16 shadow [V, d], K-major, no bias
+                    emb = (slots or {}).get(0, self)
+                    wout, _, _ = emb.wview(s, 0, "tok_emb")
+                    bout, bflag = 0, L.ZO_GEMM_B_KMAJOR
+                else:
+                    wout, _, _ = src.wview(s, bid, "w_out")
+                    bout, bflag = _ptr(src.vview(s, bid, "b_out")), 0
                 calls.append((lib.zo_layernorm_fwd, (_ptr(ws.x), ws.x.stride(0), _ptr(src.vview(s, bid, "lnf_g")),
                                                      _ptr(src.vview(s, bid, "lnf_b")), M, d, _ptr(ws.h),
                                                      ws.h.stride(0), st)))
-                bout = _ptr(src.vview(s, bid, "b_out"))
                 if head_mode == "ce":
                     calls.append(ws.gemm(lib, *(_ptr(ws.h), ws.h.stride(0), _ptr(wout), wout.stride(0), M, V, d,
-                                                     L.ZO_EPI_CE, bout, 0, 0, _ptr(ws.tgt), _ptr(ws.ce_part),
+                                                     L.ZO_EPI_CE | bflag, bout, 0, 0, _ptr(ws.tgt), _ptr(ws.ce_part),
                                                      _ptr(ws.ce_tgt), _ptr(ws.err), st)))
                     calls.append((lib.zo_ce_finalize, (_ptr(ws.ce_part), _ptr(ws.ce_tgt), M, ws.n_ce,
                                                        loss_out if loss_out is not None else _ptr(ws.loss),
                                                        _ptr(ws.row_scratch), _ptr(ws.err), st)))
                 else:   # materialise logits (API forward(); not on the step)
                     calls.append(ws.gemm(lib, *(_ptr(ws.h), ws.h.stride(0), _ptr(wout), wout.stride(0), M, V, d,
-                                                     L.ZO_EPI_F32, 0, _ptr(logits), logits.stride(0), 0, 0, 0, 0,
-                                                     st)))
+                                                     L.ZO_EPI_F32 | bflag, 0, _ptr(logits), logits.stride(0), 0, 0,
+                                                     0, 0, st)))
         return calls
 
     def grad_call(self, ws_pos: Workspace, ws_neg: Workspace, eps: float, lr: float, stream=None):

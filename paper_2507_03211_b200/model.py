@@ -54,12 +54,16 @@ class ModelConfig:
         d, v, s = self.d_model, self.vocab_size, self.seq_len
         return (v * d + s * d) + self.n_blocks * (12 * d * d + 13 * d) + (2 * d + d * v + v)
 
+    arch = "zosim"
+
     def to_dict(self) -> dict:
         return asdict(self)
 
     @classmethod
     def from_dict(cls, d: dict) -> "ModelConfig":
         try:
+            if d.get("arch") == "opt":
+                return OPTConfig(**d).validate()
             return cls(**d).validate()
         except TypeError as e:
             raise ConfigurationError(f"bad model config: {e}") from e
@@ -68,6 +72,55 @@ class ModelConfig:
     def from_json(cls, path) -> "ModelConfig":
         with open(path) as f:
             return cls.from_dict(json.load(f))
+
+
+@dataclass(frozen=True)
+class OPTConfig(ModelConfig):
+    """Real OPT (HF ``OPTForCausalLM`` with do_layer_norm_before=True, i.e.
+    every size except 350m).  Differences from
+    the zosim architecture (model.py:81-101, 286-289, 339-344):
+      * ReLU FFN instead of tanh-GELU;
+      * learned positions with ``max_positions + 2`` rows, position t reads
+        row t + 2 (OPTLearnedPositionalEmbedding's offset);
+      * the LM head is tied to the token embedding and has no bias, so the
+        head block holds only the final LayerNorm.
+    Linear weights are kept in the (d_in, d_out) layout of the zosim blocks;
+    the HF loader (opt.py) transposes nn.Linear's (out, in)."""
+
+    max_positions: int = 2048
+    arch: str = "opt"
+
+    def validate(self) -> "OPTConfig":
+        super().validate()
+        if self.arch != "opt":
+            raise ConfigurationError(f"OPTConfig.arch must be 'opt', got {self.arch!r}")
+        if not isinstance(self.max_positions, int) or self.seq_len > self.max_positions:
+            raise ConfigurationError(f"seq_len={self.seq_len} exceeds max_positions={self.max_positions}")
+        return self
+
+    def param_count(self) -> int:
+        d, v = self.d_model, self.vocab_size
+        return (v * d + (self.max_positions + 2) * d) + self.n_blocks * (12 * d * d + 13 * d) + 2 * d
+
+
+# Real OPT family (facebook/opt-*; 350m is post-LN with a projected
+# embedding and is not covered)
+REAL_OPT_SHAPES = {
+    "opt-125m": dict(d_model=768, n_heads=12, n_blocks=12),
+    "opt-1.3b": dict(d_model=2048, n_heads=32, n_blocks=24),
+    "opt-2.7b": dict(d_model=2560, n_heads=32, n_blocks=32),
+    "opt-6.7b": dict(d_model=4096, n_heads=32, n_blocks=32),
+    "opt-13b": dict(d_model=5120, n_heads=40, n_blocks=40),
+    "opt-30b": dict(d_model=7168, n_heads=56, n_blocks=48),
+    "opt-66b": dict(d_model=9216, n_heads=72, n_blocks=64),
+    "opt-175b": dict(d_model=12288, n_heads=96, n_blocks=96),
+}
+
+
+def real_opt_config(name: str, seq_len: int, dtype: str = "f32", vocab_size: int = 50272,
+                    max_positions: int = 2048) -> OPTConfig:
+    return OPTConfig(vocab_size=vocab_size, seq_len=seq_len, dtype=dtype, max_positions=max_positions,
+                     **REAL_OPT_SHAPES[name]).validate()
 
 
 # OPT-family shapes on the zosim architecture (SURVEY.md section 8 shape sheet)
@@ -85,15 +138,20 @@ def opt_config(name: str, seq_len: int, dtype: str = "f32") -> ModelConfig:
 
 
 def block_tensor_spec(config: ModelConfig, kind: str):
-    """Ordered (name, shape) list of one block (model.py:81-101)."""
+    """Ordered (name, shape) list of one block (model.py:81-101); for
+    OPTConfig the real-OPT variant (positions table with the offset rows,
+    head = final LayerNorm only)."""
     d, v, s = config.d_model, config.vocab_size, config.seq_len
+    opt = config.arch == "opt"
     if kind == EMBEDDING:
-        return [("tok_emb", (v, d)), ("pos_emb", (s, d))]
+        return [("tok_emb", (v, d)), ("pos_emb", ((config.max_positions + 2) if opt else s, d))]
     if kind == TRANSFORMER:
         return [("ln1_g", (d,)), ("ln1_b", (d,)), ("wq", (d, d)), ("bq", (d,)), ("wk", (d, d)), ("bk", (d,)),
                 ("wv", (d, d)), ("bv", (d,)), ("wo", (d, d)), ("bo", (d,)), ("ln2_g", (d,)), ("ln2_b", (d,)),
                 ("w1", (d, 4 * d)), ("b1", (4 * d,)), ("w2", (4 * d, d)), ("b2", (d,))]
     if kind == HEAD:
+        if opt:
+            return [("lnf_g", (d,)), ("lnf_b", (d,))]
         return [("lnf_g", (d,)), ("lnf_b", (d,)), ("w_out", (d, v)), ("b_out", (v,))]
     raise ConfigurationError(f"unknown block kind {kind!r}")
 

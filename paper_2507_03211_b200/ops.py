@@ -24,14 +24,16 @@ def _ld(t):
 def gemm(a: torch.Tensor, b: torch.Tensor, epilogue: int, out=None, bias=None, m=None, n=None, k=None,
          targets=None, ce_part=None, ce_tgt=None, err=None, stream=None, workspace=None):
     """out (+)= epilogue(a[M,K] @ b[K,N]) on tcgen05.  a, b bf16 2-D with unit
-    inner stride; bias fp32 [N].  ``workspace`` (uint8, zero-initialised,
+    inner stride (b as [N, K] when ``epilogue`` carries ZO_GEMM_B_KMAJOR);
+    bias fp32 [N].  ``workspace`` (uint8, zero-initialised,
     gemm_workspace_bytes(M, N, K) long) enables the stream-K tail."""
     if a.dtype != torch.bfloat16 or b.dtype != torch.bfloat16:
         raise DimensionError("gemm operands must be bf16")
     M = m if m is not None else a.shape[0]
     K = k if k is not None else a.shape[1]
-    N = n if n is not None else b.shape[1]
-    if b.shape[0] < K or a.stride(-1) != 1 or b.stride(-1) != 1:
+    bkm = bool(epilogue & L.ZO_GEMM_B_KMAJOR)       # b given as [N, K] (K contiguous)
+    N = n if n is not None else b.shape[0 if bkm else 1]
+    if b.shape[1 if bkm else 0] < K or a.stride(-1) != 1 or b.stride(-1) != 1:
         raise DimensionError("gemm: operand shapes/strides do not match")
     ldo = 0 if out is None else _ld(out)
     if workspace is not None:

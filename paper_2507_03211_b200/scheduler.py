@@ -127,7 +127,7 @@ class BlockSlot:
         n = max(bl.elem_count, pad_to)
         self.theta = torch.zeros(n, dtype=torch.float32, device=device)
         self.wsh, self.vsh = [None, None], [None, None]
-        if shadows and bl.kind != EMBEDDING:
+        if shadows and plan.views[template_bid]:     # (a real-OPT embedding has the tied head's shadow)
             wlo, whi, vlo, vhi = block_extent(plan, template_bid)
             for s in dirs:
                 self.wsh[s] = torch.zeros(whi - wlo, dtype=torch.bfloat16, device=device)
@@ -368,8 +368,10 @@ class OffloadedZo:
         eps = self.hyper.epsilon
         for s in self.dirs:
             loss_out = self.local.data_ptr() + 8 * s
+            slots = dict(self.persistent)       # the tied OPT head reads the embedding slot
+            slots[bid] = slot
             calls = _store_view(self).forward_calls(s, self.ws[s], +eps if s == PLUS else -eps,
-                                                    stream=stream, blocks=[bid], slots={bid: slot},
+                                                    stream=stream, blocks=[bid], slots=slots,
                                                     scal=self.scal, loss_out=loss_out)
             for fn, args in calls:
                 L.check(fn(*args))

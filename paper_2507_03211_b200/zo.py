@@ -491,6 +491,10 @@ def forward_block(block: DeviceBlock, x) -> torch.Tensor:
         ws.x[:, :cfg.d_model].copy_(x.reshape(B * T, cfg.d_model))
     if block.kind != EMBEDDING and block.pert_scale == 0.0:
         _refresh_view(block)          # unperturbed view = bf16/fp32 copy of the master
+    if block.kind == HEAD and cfg.arch == "opt":
+        emb = store_blocks(s)[0]      # tied head: reads the embedding block's current view
+        if emb.pert_scale == 0.0:
+            _refresh_view(emb)
     zmode, zsrc, zkey0 = block._zsrc
     logits = None
     if block.kind == HEAD:
@@ -509,7 +513,8 @@ def forward_block(block: DeviceBlock, x) -> torch.Tensor:
         calls = [(fn, tuple(args))]
     s.run(calls)
     if block.kind == HEAD:
-        logits += s.vview(PLUS, block.block_id, "b_out")
+        if cfg.arch != "opt":
+            logits += s.vview(PLUS, block.block_id, "b_out")
         return logits.view(B, T, cfg.vocab_size)
     s.check_errors(ws)
     return ws.x[:, :cfg.d_model].clone().view(B, T, cfg.d_model)

@@ -77,6 +77,46 @@ def test_gemm_ce_epilogue_and_finalize(M, V, K):
     torch.testing.assert_close(tl.double(), logits.gather(1, tg.long()[:, None])[:, 0], rtol=1e-4, atol=1e-3)
 
 
+@pytest.mark.parametrize("M,N,K", [(256, 768, 256), (200, 304, 136), (2048, 8192, 2048), (64, 512, 128)])
+def test_gemm_relu_epilogue(M, N, K):
+    """real-OPT FFN up-projection: relu(h @ W1 + b1) -> bf16."""
+    a, b = _rand(M, K, seed=31, scale=0.5), _rand(K, N, seed=32, scale=0.1)
+    bias = _rand(N, dtype=torch.float32, seed=33)
+    out = torch.empty(M, N, device=DEV, dtype=torch.bfloat16)
+    ops.gemm(a, b, L.ZO_EPI_BIAS_RELU_BF16, out=out, bias=bias)
+    ref = torch.relu(a.float() @ b.float() + bias)
+    torch.testing.assert_close(out.float(), ref, rtol=1e-2, atol=1e-2)
+
+
+@pytest.mark.parametrize("M,N,K", [(128, 256, 64), (64, 96, 32), (256, 512, 512), (200, 304, 136),
+                                   (1000, 1000, 1000), (2048, 4096, 2048)])
+def test_gemm_b_kmajor_f32(M, N, K):
+    """B given transposed ([N, K], K contiguous): single-CTA and CTA-pair
+    kernels with the K-major UMMA B descriptor."""
+    a, bt = _rand(M, K, seed=34), _rand(N, K, seed=35)
+    out = torch.full((M, N), float("nan"), device=DEV)
+    ops.gemm(a, bt, L.ZO_EPI_F32 | L.ZO_GEMM_B_KMAJOR, out=out)
+    torch.cuda.synchronize()
+    torch.testing.assert_close(out, a.float() @ bt.float().t(), rtol=2e-3, atol=2e-3 * math.sqrt(K / 64))
+
+
+@pytest.mark.parametrize("M,V,K", [(64, 50272, 768), (512, 1000, 64), (32, 16, 16)])
+def test_gemm_tied_head_ce(M, V, K):
+    """Tied LM head: logits = h @ E^T with E the [V, d] embedding (K-major B)
+    and no bias, through the CE epilogue (real OPT)."""
+    a, emb = _rand(M, K, seed=36, scale=0.5), _rand(V, K, seed=37, scale=0.1)
+    tg = torch.randint(0, V, (M,), generator=torch.Generator().manual_seed(5)).to(DEV, torch.int32)
+    nt = ops.ce_tiles(V)
+    part, tl = torch.empty(M, nt, 2, device=DEV), torch.empty(M, device=DEV)
+    err = torch.zeros(1, dtype=torch.int32, device=DEV)
+    ops.gemm(a, emb, L.ZO_EPI_CE | L.ZO_GEMM_B_KMAJOR, targets=tg, ce_part=part, ce_tgt=tl, err=err)
+    loss, scratch = torch.empty(1, dtype=torch.float64, device=DEV), torch.empty(M, dtype=torch.float64, device=DEV)
+    ops.ce_finalize(part, tl, M, nt, loss, scratch, err)
+    logits = (a.float() @ emb.float().t()).double()
+    assert err.item() == 0
+    assert abs(loss.item() - torch.nn.functional.cross_entropy(logits, tg.long()).item()) < 1e-4
+
+
 # shapes whose last wave is split along K (stream-K tail): 64 / 192 / 1576
 # tiles of 256 x 256 over the pairs, and a K=8192 case with 3 pieces per tile
 SK_SHAPES = [(2048, 2048, 2048), (2048, 6144, 2048), (2048, 2048, 8192), (1024, 4000, 1000), (512, 50272, 256)]
