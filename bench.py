@@ -43,6 +43,9 @@ def _args():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--model", default=MODEL)
+    ap.add_argument("--arch", default="zosim", choices=["zosim", "opt"],
+                    help="zosim: the reference's architecture at OPT dims (the headline); opt: real OPT "
+                         "(ReLU, tied head, position offset) -- a comparison row")
     ap.add_argument("--seq", type=int, default=SEQ)
     ap.add_argument("--batch", type=int, default=BATCH_PER_GROUP, help="sequences per PertP group")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -52,6 +55,12 @@ def _args():
                     help="blocks: per-block perturb passes on a side stream ahead of the +eps forward; "
                          "background: one co-resident perturb pass gated per block by device counters")
     return ap.parse_args()
+
+
+def _config(args):
+    from paper_2507_03211_b200.model import opt_config, real_opt_config
+
+    return real_opt_config(args.model, args.seq) if args.arch == "opt" else opt_config(args.model, args.seq)
 
 
 def _plan(args):
@@ -192,7 +201,7 @@ def reference_arm(args, rank, world):
 
     if rank != 0:
         return
-    cfg = opt_config(args.model, args.seq)
+    cfg = _config(args)
     n_groups = max(1, args.gpus // 2)
     batch = args.batch * n_groups
     for _ in range(args.warmup):
@@ -228,7 +237,7 @@ def ours(args, rank, world, local_rank):
 
     torch.cuda.set_device(local_rank)
     dev = torch.device(f"cuda:{local_rank}")
-    cfg = opt_config(args.model, args.seq)
+    cfg = _config(args)
     B, T = args.batch, args.seq
     M = B * T
     hyper = zo.ZoHyper(EPS, LR)
@@ -380,7 +389,7 @@ def ours(args, rank, world, local_rank):
     if rank != 0:
         return
     hbm, tf_sus, tf_burst, peak_kind = _peaks()
-    traffic = _traffic() if (args.model, T, B) == (MODEL, SEQ, BATCH_PER_GROUP) else {}
+    traffic = _traffic() if (args.model, T, B, args.arch) == (MODEL, SEQ, BATCH_PER_GROUP, "zosim") else {}
     P = store.total_params
     bytes_per_param = 12 if world == 1 else 10
     pert_avg = statistics.mean(p_ms)
@@ -407,11 +416,12 @@ def ours(args, rank, world, local_rank):
     dominant = roof_gemm if gemm_share >= pert_share else roof_pert
     other = roof_pert if dominant is roof_gemm else roof_gemm
     line = {
-        "metric": "OPT ZO fine-tune tokens/s (zosim arch, OPT-1.3B shape)",
+        "metric": "OPT ZO fine-tune tokens/s (zosim arch, OPT-1.3B shape)" if args.arch == "zosim"
+        else "OPT ZO fine-tune tokens/s (real OPT arch, comparison row)",
         "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic tokens, random-init (Philox) weights",
-        "config": {"workload": f"{args.model} ZO-SGD step (zosim arch), seq {T}, batch {B} per PertP group",
+        "config": {"workload": f"{args.model} ZO-SGD step ({args.arch} arch), seq {T}, batch {B} per PertP group",
                    "global_batch": B * n_groups, "seq_len": T, "parallelism": strategy, "eps": EPS, "lr": LR,
                    "params": P, "l2": "inputs > L2 (fp32 master 4 B/param + bf16 shadows stream every step)",
                    "perturb_plan": args.overlap,
@@ -424,7 +434,7 @@ def ours(args, rank, world, local_rank):
                 "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
         "last_step": {"loss_pos": float(rec[0]), "loss_neg": float(rec[1]), "g": float(rec[2])},
     }
-    if world == 1 and not args.no_cpu_baseline:
+    if world == 1 and not args.no_cpu_baseline and args.arch == "zosim":
         s = cpu_reference_sample(cfg, B)
         line["cpu_baseline"] = {"value": s["tokens_per_s"], "unit": "tokens/s", "cores": s["cores"], "kind": "port",
                                 "sample": s["sample"]}

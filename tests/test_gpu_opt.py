@@ -6,7 +6,7 @@ Checker: tests/opt_ref.py, a plain-torch fp32 OPT forward pinned to HF
 transformers' OPTForCausalLM by tests/test_opt_cpu.py.  Tolerances (bf16
 operands, fp32 accumulate): logits |d| <= 2e-2 * max|ref| + 1e-3, losses
 |dL| <= 3e-3, projected gradient |dg| <= 3e-3 / eps; the update itself is
-exact fp32 arithmetic on the master (checked to <= 1 ulp)."""
+fp32 arithmetic on the master (checked to 1 ulp of the result + 1 ulp of the product)."""
 
 import numpy as np
 import pytest
@@ -69,7 +69,9 @@ def test_mezo_step_matches_reference_at_perturbed_weights(name):
     assert abs(rec.g - (lp - ln) / (2 * eps)) <= 3e-3 / eps
     want = (master.astype(np.float64) - (lr * rec.g) * z).astype(np.float32)
     got = store.theta.cpu().numpy()
-    assert np.all(np.abs(got - want) <= 1.5 * np.spacing(np.abs(want)))     # fp32 update, <= 1 ulp
+    # fp32 update: one rounding of the result plus the fp32 product (lr g) z
+    tol = 1.5 * np.spacing(np.abs(want)) + 2.4e-7 * np.abs(lr * rec.g * z)
+    assert np.all(np.abs(got - want) <= tol)
 
 
 def test_lazy_equals_eager_and_offloaded_equals_resident():
