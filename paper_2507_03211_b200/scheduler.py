@@ -326,6 +326,9 @@ class OffloadedZo:
     # -- byte movement --------------------------------------------------------------
     def _upload(self, bid, slot, stream):
         slot.bind(bid)
+        if getattr(self.host, "is_sharded", False):      # HBM-sharded master (sharded.py)
+            self.host.upload_into(bid, slot.theta, stream)
+            return
         hb = self.host.block_buf(bid)
         if self.fabric is None:
             with torch.cuda.stream(stream) if stream is not None else _null():
@@ -334,6 +337,9 @@ class OffloadedZo:
             sliced_upload(hb, slot.theta, self.host.slice_plan["layouts"][bid], self.fabric, self.rank, stream)
 
     def _offload(self, bid, slot, stream):
+        if getattr(self.host, "is_sharded", False):
+            self.host.offload_from(bid, slot.theta, stream)
+            return
         hb = self.host.block_buf(bid)
         if self.fabric is None:
             with torch.cuda.stream(stream):
@@ -502,6 +508,9 @@ class OffloadedZo:
         """Copy the persistent device blocks back to the host master."""
         cs = self.streams[COMPUTE]
         for bid, slot in self.persistent.items():
+            if getattr(self.host, "is_sharded", False):
+                self.host.offload_from(bid, slot.theta, cs)
+                continue
             hb = self.host.block_buf(bid)
             with torch.cuda.stream(cs):
                 hb.copy_(slot.theta[:hb.numel()], non_blocking=True)

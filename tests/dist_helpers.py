@@ -185,3 +185,36 @@ def gpu_strategy_worker_theta(rank, world, port, strategy, steps, q):
     theta = store.theta.cpu().numpy()
     dist.destroy_process_group()
     q.put((rank, recs, theta))
+
+
+def sharded_worker(rank, world, port, strategy, steps, init_kind, q):
+    """OffloadedZo over an HBM-sharded fp32 master (sharded.ShardStore):
+    upload = own shard slice + all-gather, offload = own slice back (gloo,
+    all ranks on one GPU)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2507_03211_b200.fabric import TorchFabric
+    from paper_2507_03211_b200.model import ModelConfig, make_batch
+    from paper_2507_03211_b200.rng import iteration_seeds
+    from paper_2507_03211_b200.scheduler import OffloadedZo
+    from paper_2507_03211_b200.sharded import ShardStore
+    from paper_2507_03211_b200.zo import ZoHyper
+
+    torch.cuda.set_device(0)
+    init(rank, world, port)
+    fab = TorchFabric()
+    cfg = ModelConfig(*DEEP, "f32")
+    shards = ShardStore(cfg, fab, 7, init=init_kind)
+    init_master = shards.gather_master()
+    rt = OffloadedZo(shards, ZoHyper(1e-3, 1e-2), batch=4 // world, fabric=fab, strategy=strategy)
+    recs = []
+    for j, s in enumerate(iteration_seeds(9, steps), 1):
+        r = rt.step(make_batch(cfg, 4, 40 + j).shard(world, rank), s)
+        recs.append((r.loss_pos, r.loss_neg, r.g))
+    rt.flush()
+    torch.cuda.synchronize()
+    theta = shards.gather_master()
+    nbytes = shards.shard_bytes
+    dist.destroy_process_group()
+    q.put((rank, recs, theta, init_master, nbytes))

@@ -77,3 +77,34 @@ def test_sliced_offload_two_ranks_equals_resident():
     ddp = H.run(H.gpu_strategy_worker_theta, 2, "ddp", 3)
     assert [r[2] for r in res[0][1]] == [r[2] for r in ddp[0][1]]
     assert np.array_equal(res[0][2], ddp[0][2])
+
+
+@pytest.mark.parametrize("init_kind", ["host", "philox"])
+def test_hbm_sharded_master_two_ranks_equals_resident(init_kind):
+    """the fp32 master sharded over 2 ranks' HBM (each rank
+    holds ceil(P_blk/2) of every block), blocks reassembled by all-gather,
+    own slice written back: records and the final master equal the resident
+    ZO-DDP(2) run bit for bit, and each rank holds half the master."""
+    res = H.run(H.sharded_worker, 2, "mezo", 3, init_kind)
+    want_init = DeviceStore(DEEP, 7, init=init_kind).theta.cpu().numpy()
+    for r in res:
+        assert np.array_equal(r[3], want_init)
+        assert r[4] <= (want_init.size // 2 + 8 * len(DeviceStore(DEEP, 7).layouts)) * 4
+    assert np.array_equal(res[0][2], res[1][2])
+    if init_kind == "host":
+        ddp = H.run(H.gpu_strategy_worker_theta, 2, "ddp", 3)
+        assert [r[2] for r in res[0][1]] == [r[2] for r in ddp[0][1]]
+        assert np.array_equal(res[0][2], ddp[0][2])
+
+
+def test_hbm_sharded_single_rank_equals_resident():
+    from paper_2507_03211_b200.sharded import ShardStore
+
+    recs, _, final = _resident(DEEP, 3)
+    shards = ShardStore(DEEP, None, 7)
+    rt = OffloadedZo(shards, zo.ZoHyper(EPS, LR), batch=2)
+    for j, s in enumerate(iteration_seeds(9, 3), 1):
+        r = rt.step(make_batch(DEEP, 2, 40 + j), s)
+        assert (r.loss_pos, r.loss_neg, r.g) == recs[j - 1]
+    rt.flush()
+    assert np.array_equal(shards.gather_master(), final)

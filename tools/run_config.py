@@ -3,6 +3,7 @@ for configs #3-#5; the bench line is config #2).
 
     python tools/run_config.py resident opt-13b 2048 1      # 13B, T=2048, B=1, both directions
     python tools/run_config.py offload  opt-66b 2048 1      # ZO2 schedule, host master, 3 slots
+    python tools/run_config.py sharded  opt-13b 2048 1      # same schedule, fp32 master in HBM (1 rank)
 """
 import json
 import sys
@@ -26,6 +27,11 @@ def main():
     if mode == "resident":
         store = DeviceStore(cfg, init_seed=7, init="philox")
         rt = zo.StreamingZo(store, hyper)
+    elif mode == "sharded":
+        from paper_2507_03211_b200.scheduler import OffloadedZo
+        from paper_2507_03211_b200.sharded import ShardStore
+        shards = ShardStore(cfg, None, 7, init="philox")
+        rt = OffloadedZo(shards, hyper, batch=B, trace=True)
     else:
         from paper_2507_03211_b200.scheduler import HostStore, OffloadedZo
         host = HostStore(cfg, 7, init="philox")
