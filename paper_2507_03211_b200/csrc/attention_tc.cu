@@ -3,7 +3,8 @@
 // head, batch) work items, heaviest (latest) query tiles first.
 //
 //   warp 0      TMA producer: Q tile (once per item), K/V blocks of 128 keys
-//               (2-stage ring) from the fused QKV activation
+//               (kKV-stage ring, so loads run ahead across short items) from
+//               the fused QKV activation
 //   warp 1      TMEM allocator + single-thread tcgen05.mma issuer:
 //                 S_j  = Q K_j^T      M=128 N=128 K=64   -> TMEM S[j%2]
 //                 PV_j = P_j V_j      M=128 N=64  K=128  -> TMEM PV[j%2]
@@ -30,14 +31,19 @@ namespace {
 constexpr int kAttnThreads = 320;   // producer, MMA, 8 softmax warps (2 per TMEM lane quarter)
 constexpr int kTileBytes = 128 * 64 * 2;     // 16 KB: 128 rows x 64 bf16 (Q, K, V tiles)
 constexpr int kPBytes = 128 * 128 * 2;       // 32 KB: P tile, two 64-key K-chunks
-// smem: Q[2] | K[2] | V[2] | P[2] | barriers
+#ifndef ZO_ATTN_KV_STAGES
+#define ZO_ATTN_KV_STAGES 4
+#endif
+constexpr int kKV = ZO_ATTN_KV_STAGES;       // K/V ring depth (4: 226 KB of smem in total)
+// smem: Q[2] | K[kKV] | V[kKV] | P[2] | barriers
 constexpr int kOffQ = 0;
 constexpr int kOffK = kOffQ + 2 * kTileBytes;
-constexpr int kOffV = kOffK + 2 * kTileBytes;
-constexpr int kOffP = kOffV + 2 * kTileBytes;
+constexpr int kOffV = kOffK + kKV * kTileBytes;
+constexpr int kOffP = kOffV + kKV * kTileBytes;
 constexpr int kOffBar = kOffP + 2 * kPBytes;
 constexpr int kOffRed = kOffBar + 256;                 // row-max / row-sum exchange [2][128] fp32
 constexpr int kAttnSmem = kOffRed + 2 * 128 * 4 + 1024;
+static_assert(kAttnSmem <= 232448, "attention smem");
 
 struct AttnArgs {
   int batch, seq, heads, ldc;
@@ -66,19 +72,23 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   uint8_t* gbase = smem_raw + (base - raw);
   const uint32_t sQ = base + kOffQ, sK = base + kOffK, sV = base + kOffV, sP = base + kOffP;
   const uint32_t bars = base + kOffBar;
-  // barriers: 0 q_full0, 1 q_empty0, 2-3 kv_full, 4-5 kv_empty, 6-7 s_full, 8-9 s_empty,
-  //           10-11 p_full, 12-13 p_empty, 14-15 pv_full, 16-17 pv_empty, 18 q_full1, 19 q_empty1
+  // barriers: 0 q_full0, 1 q_empty0, 6-7 s_full, 8-9 s_empty, 10-11 p_full, 12-13 p_empty,
+  //           14-15 pv_full, 16-17 pv_empty, 18 q_full1, 19 q_empty1,
+  //           20.. kv_full[kKV], 20+kKV.. kv_empty[kKV]
   auto bar = [&](int i) { return bars + 8u * i; };
   auto qfull = [&](uint32_t qb) { return bar(qb ? 18 : 0); };
   auto qempty = [&](uint32_t qb) { return bar(qb ? 19 : 1); };
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + kOffBar + 8 * 20);
+  auto kvfull = [&](uint32_t st) { return bar(20 + (int)st); };
+  auto kvempty = [&](uint32_t st) { return bar(20 + kKV + (int)st); };
+  static_assert(8 * (20 + 2 * kKV) + 4 <= 256, "barrier area");
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + kOffBar + 8 * (20 + 2 * kKV));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tm);
     mbar_init(bar(0), 1); mbar_init(bar(1), 1); mbar_init(bar(18), 1); mbar_init(bar(19), 1);
+    for (int i = 0; i < kKV; ++i) { mbar_init(kvfull(i), 1); mbar_init(kvempty(i), 1); }
     for (int i = 0; i < 2; ++i) {
-      mbar_init(bar(2 + i), 1); mbar_init(bar(4 + i), 1);
       mbar_init(bar(6 + i), 1); mbar_init(bar(8 + i), 8);
       mbar_init(bar(10 + i), 8); mbar_init(bar(12 + i), 1);
       mbar_init(bar(14 + i), 1); mbar_init(bar(16 + i), 8);
@@ -124,11 +134,11 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         tma_load_2d(sQ + qb * kTileBytes, &tm, qfull(qb), h * 64, row0 + qt * 128);
         const int nkb = n_blocks(qt);
         for (int j = 0; j < nkb; ++j, ++kvc) {
-          const uint32_t st = kvc & 1u, ph = (kvc >> 1) & 1u;
-          mbar_wait(bar(4 + st), ph ^ 1u);
-          mbar_expect_tx(bar(2 + st), 2 * kTileBytes);
-          tma_load_2d(sK + st * kTileBytes, &tm, bar(2 + st), (int)(a.d + h * 64), row0 + j * 128);
-          tma_load_2d(sV + st * kTileBytes, &tm, bar(2 + st), (int)(2 * a.d + h * 64), row0 + j * 128);
+          const uint32_t st = kvc % kKV, ph = (kvc / kKV) & 1u;
+          mbar_wait(kvempty(st), ph ^ 1u);
+          mbar_expect_tx(kvfull(st), 2 * kTileBytes);
+          tma_load_2d(sK + st * kTileBytes, &tm, kvfull(st), (int)(a.d + h * 64), row0 + j * 128);
+          tma_load_2d(sV + st * kTileBytes, &tm, kvfull(st), (int)(2 * a.d + h * 64), row0 + j * 128);
         }
       }
     }
@@ -142,7 +152,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
                               ((uint32_t)(128 >> 4) << 24);
     uint32_t kvc = 0, sc = 0, it_local = 0;
     auto issue_pv = [&](uint32_t c, uint32_t kv) {
-      const uint32_t pb = c & 1u, ph = (c >> 1) & 1u, st = kv & 1u;
+      const uint32_t pb = c & 1u, ph = (c >> 1) & 1u, st = kv % kKV;
       mbar_wait(bar(10 + pb), ph);               // P_c written
       mbar_wait(bar(16 + pb), ph ^ 1u);          // PV buffer drained by the softmax warps
       tc_fence_after();
@@ -154,7 +164,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
           tc_mma_f16(tmem + 256 + pb * 64, ad, bd, idesc_pv, kk != 0 ? 1u : 0u);
         }
         tc_commit(bar(14 + pb));                  // PV ready
-        tc_commit(bar(4 + st));                   // K/V stage free
+        tc_commit(kvempty(st));                   // K/V stage free
         tc_commit(bar(12 + pb));                  // P buffer free
       }
       __syncwarp();
@@ -168,14 +178,14 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       for (int j = 0; j < nkb; ++j) {
         const uint32_t c = sc + j, kv = kvc + j;
         const uint32_t sb = c & 1u, ph = (c >> 1) & 1u;
-        mbar_wait(bar(2 + (kv & 1u)), (kv >> 1) & 1u);   // K_j, V_j landed
+        mbar_wait(kvfull(kv % kKV), (kv / kKV) & 1u);    // K_j, V_j landed
         mbar_wait(bar(8 + sb), ph ^ 1u);                 // S buffer free
         tc_fence_after();
         if (lane == 0) {
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk) {
             const uint64_t ad = desc_sw128(sQ + qb * kTileBytes + kk * 32, 16, 1024);
-            const uint64_t bd = desc_sw128(sK + (kv & 1u) * kTileBytes + kk * 32, 16, 1024);
+            const uint64_t bd = desc_sw128(sK + (kv % kKV) * kTileBytes + kk * 32, 16, 1024);
             tc_mma_f16(tmem + sb * 128, ad, bd, idesc_s, kk != 0 ? 1u : 0u);
           }
           tc_commit(bar(6 + sb));                 // S ready

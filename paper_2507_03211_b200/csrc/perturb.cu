@@ -114,13 +114,14 @@ __device__ __forceinline__ void pu_load_fast(const PuParams& p, int64_t e0, int 
     if (full || lane + 32 * g < ngroups) th[g] = tp[32 * g];
 }
 
-// FULL: a whole 512-element tile with both shadows written (the common case,
-// no per-group guards or per-direction branches)
-template <bool PEND, bool BF16, int G, bool FULL = false>
+// FULL: a whole 512-element tile, no per-group guards; FULL_MASK says which
+// shadows it writes at compile time (3: both, the single-GPU step; 1 / 2: one,
+// a PertP / 2D rank's own direction) so the hot loop has no direction branches
+template <bool PEND, bool BF16, int G, bool FULL = false, int FULL_MASK = 3>
 __device__ __forceinline__ void pu_compute_fast(const PuParams& p, int64_t e0, int ngroups, int64_t dbase,
                                                 bool SA, bool SB, float sa, float sb, uint64_t seed_cur,
                                                 uint64_t seed_prev, float lrg32, int lane, float4 (&th)[G]) {
-  if constexpr (FULL) { SA = true; SB = true; }
+  if constexpr (FULL) { SA = (FULL_MASK & 1) != 0; SB = (FULL_MASK & 2) != 0; }
   float4* tp = reinterpret_cast<float4*>(p.theta + (e0 - p.theta_key0)) + lane;
   const uint64_t qa = (uint64_t)(e0 >> 2) + (uint64_t)lane;
   const bool full = FULL || ngroups >= 32 * G;
@@ -148,7 +149,11 @@ __device__ __forceinline__ void pu_compute_fast(const PuParams& p, int64_t e0, i
       const float4 t = th[g];
 #pragma unroll
       for (int d = 0; d < 2; ++d) {
-        if ((d == 0 && !SA) || (d == 1 && !SB)) continue;   // warp-uniform
+        if constexpr (FULL) {
+          if (!((FULL_MASK >> d) & 1)) continue;              // compile-time
+        } else if ((d == 0 && !SA) || (d == 1 && !SB)) {
+          continue;                                           // warp-uniform
+        }
         const float sc = d == 0 ? sa : sb;
         const float a = fmaf(sc, z.x, t.x), b = fmaf(sc, z.y, t.y);
         const float c = fmaf(sc, z.z, t.z), e = fmaf(sc, z.w, t.w);
@@ -220,15 +225,24 @@ __device__ __forceinline__ void pu_tile_fast(const PuParams& p, int64_t e0, int 
                                              float lrg32, int kind, int lane, float4 (&th)[kPuGroupsPerThread]) {
   constexpr int G = kPuGroupsPerThread;
   const bool sa = want_sh && sh[0], sb = want_sh && sh[1];
-  if (sa && sb && ngroups == 32 * G) {
-    if (kind == ZO_SHADOW_BF16) {
-      if (pending) pu_compute_fast<true, true, G, true>(p, e0, ngroups, dbase, sa, sb, sc32[0], sc32[1], seed_cur, seed_prev, lrg32, lane, th);
-      else pu_compute_fast<false, true, G, true>(p, e0, ngroups, dbase, sa, sb, sc32[0], sc32[1], seed_cur, seed_prev, lrg32, lane, th);
-    } else {
-      if (pending) pu_compute_fast<true, false, G, true>(p, e0, ngroups, dbase, sa, sb, sc32[0], sc32[1], seed_cur, seed_prev, lrg32, lane, th);
-      else pu_compute_fast<false, false, G, true>(p, e0, ngroups, dbase, sa, sb, sc32[0], sc32[1], seed_cur, seed_prev, lrg32, lane, th);
-    }
-  } else if (kind == ZO_SHADOW_BF16) {
+#define ZO_PU_FULL(M)                                                                                              \
+  {                                                                                                                \
+    if (kind == ZO_SHADOW_BF16) {                                                                                  \
+      if (pending) pu_compute_fast<true, true, G, true, M>(p, e0, ngroups, dbase, sa, sb, sc32[0], sc32[1], seed_cur, seed_prev, lrg32, lane, th); \
+      else pu_compute_fast<false, true, G, true, M>(p, e0, ngroups, dbase, sa, sb, sc32[0], sc32[1], seed_cur, seed_prev, lrg32, lane, th); \
+    } else {                                                                                                       \
+      if (pending) pu_compute_fast<true, false, G, true, M>(p, e0, ngroups, dbase, sa, sb, sc32[0], sc32[1], seed_cur, seed_prev, lrg32, lane, th); \
+      else pu_compute_fast<false, false, G, true, M>(p, e0, ngroups, dbase, sa, sb, sc32[0], sc32[1], seed_cur, seed_prev, lrg32, lane, th); \
+    }                                                                                                              \
+    return;                                                                                                        \
+  }
+  if (ngroups == 32 * G) {
+    if (sa && sb) ZO_PU_FULL(3)
+    if (sa) ZO_PU_FULL(1)
+    if (sb) ZO_PU_FULL(2)
+  }
+#undef ZO_PU_FULL
+  if (kind == ZO_SHADOW_BF16) {
     if (pending) pu_compute_fast<true, true, G>(p, e0, ngroups, dbase, sa, sb, sc32[0], sc32[1], seed_cur, seed_prev, lrg32, lane, th);
     else pu_compute_fast<false, true, G>(p, e0, ngroups, dbase, sa, sb, sc32[0], sc32[1], seed_cur, seed_prev, lrg32, lane, th);
   } else {
