@@ -169,6 +169,11 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       }
       __syncwarp();
     };
+    // PV of the previous block is issued after the next S, and that chain
+    // runs across item boundaries: the first S of item i+1 is already on the
+    // tensor core while the softmax warps finish item i (no per-item bubble)
+    bool have_prev = false;
+    uint32_t prev_c = 0, prev_kv = 0;
     for (int it = blockIdx.x; it < a.items; it += gridDim.x, ++it_local) {
       int qt, h, b;
       item_coords(it, qt, h, b);
@@ -192,12 +197,15 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
           if (j == nkb - 1) tc_commit(qempty(qb));  // Q buffer no longer needed
         }
         __syncwarp();
-        if (j >= 1) issue_pv(c - 1, kv - 1);
+        if (have_prev) issue_pv(prev_c, prev_kv);
+        prev_c = c;
+        prev_kv = kv;
+        have_prev = true;
       }
-      issue_pv(sc + nkb - 1, kvc + nkb - 1);
       sc += nkb;
       kvc += nkb;
     }
+    if (have_prev) issue_pv(prev_c, prev_kv);
   } else {
     // ================= softmax / output =================
     // warp pair (quarter q, half h): rows 32q..32q+31, key columns [64h, 64h+64)
