@@ -51,9 +51,10 @@ def _args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true", help="skip the public-API pass (profiling runs)")
     ap.add_argument("--no-graph", action="store_true", help="launch the step eagerly instead of replaying a CUDA graph")
-    ap.add_argument("--overlap", default="none", choices=["none", "blocks", "background"],
+    ap.add_argument("--overlap", default="none", choices=["none", "blocks", "background", "stacked"],
                     help="blocks: per-block perturb passes on a side stream ahead of the +eps forward; "
-                         "background: one co-resident perturb pass gated per block by device counters")
+                         "background: one co-resident perturb pass gated per block by device counters; "
+                         "stacked: both directions as one launch per layer over stacked activations")
     return ap.parse_args()
 
 
@@ -64,12 +65,14 @@ def _config(args):
 
 
 def _plan(args):
-    return {"none": False, "blocks": "blocks", "background": "background"}[args.overlap]
+    return {"none": False, "blocks": "blocks", "background": "background", "stacked": "stacked"}[args.overlap]
 
 
 def _plan_text(args, world):
     if world > 1 or args.overlap == "none":
         return "one launch; timed alone in a serialised replay"
+    if args.overlap == "stacked":
+        return "one launch; both directions' forwards stacked into one launch per layer"
     if args.overlap == "blocks":
         return "timed run: one launch per block on a side stream ahead of the +eps forward; timed alone in a serialised replay"
     return ("timed run: block 0 full-width, the rest as one co-resident background launch gating each block's "
@@ -259,7 +262,8 @@ def ours(args, rank, world, local_rank):
         runner = zo.StreamingZo(store, hyper, overlap=_plan(args))
         wss = [store.workspace(PLUS, B, T), store.workspace(MINUS, B, T)]
         step_calls = {"none": runner.step_calls, "blocks": runner.overlapped_step_calls,
-                      "background": runner.background_step_calls}[args.overlap](wss[0], wss[1])
+                      "background": runner.background_step_calls,
+                      "stacked": runner.stacked_step_calls}[args.overlap](wss[0], wss[1])
     else:
         from paper_2507_03211_b200.strategies import TwoDRunner
         runner = TwoDRunner(store, hyper, rank=rank, world=world, batch=B, seq=T)
@@ -277,7 +281,9 @@ def ours(args, rank, world, local_rank):
     if world > 1:
         n_launch += 0   # collectives are NCCL kernels, not ours
 
-    def gemm_flops(args_):
+    def gemm_flops(fn, args_):
+        if fn.__name__ == "zo_gemm_bf16_split":          # (A, lda, B, B2, ldb, M, N, K, ...)
+            return 2.0 * args_[5] * args_[6] * args_[7]
         return 2.0 * args_[4] * args_[5] * args_[6]
 
     pert_ev, gemm_ev = [], []
@@ -307,7 +313,7 @@ def ours(args, rank, world, local_rank):
                 if i in pert_set:
                     pert_ev.append((j, e0, e1))
                 else:
-                    gemm_ev.append((e0, e1, gemm_flops(a)))
+                    gemm_ev.append((e0, e1, gemm_flops(fn, a)))
         if hasattr(runner, "post_step"):
             runner.post_step()
 
@@ -346,7 +352,7 @@ def ours(args, rank, world, local_rank):
     # instrumented pass over the same steps: per-kernel CUDA-event durations.
     # Kernels of concurrent streams would overlap their event windows, so the
     # instrumented replay runs the two directional forwards serialised.
-    if world == 1:
+    if world == 1 and args.overlap != "stacked":      # the stacked plan is single-stream already
         runner.dual_stream = False
         step_calls[:] = runner.step_calls(wss[0], wss[1])
         pert_set.clear()

@@ -141,6 +141,12 @@ int zo_embed_fwd(const float* tok, int64_t tok_key0, const float* pos, int64_t p
 int zo_layernorm_fwd(const float* x, int64_t ldx, const float* gamma, const float* beta,
                      int64_t rows, int64_t d, void* out_bf16, int64_t ldo, void* stream);
 
+/* LayerNorm over stacked +eps / -eps rows: rows >= row_split use gamma2 /
+ * beta2 (each direction's perturbed LN parameters). */
+int zo_layernorm_fwd_split(const float* x, int64_t ldx, const float* gamma, const float* beta,
+                           const float* gamma2, const float* beta2, int64_t rows, int64_t row_split,
+                           int64_t d, void* out_bf16, int64_t ldo, void* stream);
+
 /*
  * C[M,N] = A[M,K] (bf16, K-major) x B[K,N] (bf16, N-major = the reference's
  * (d_in, d_out) weight layout, src/zosim/model.py:325) on tcgen05 tensor
@@ -156,6 +162,21 @@ int zo_gemm_bf16(const void* A, int64_t lda, const void* B, int64_t ldb,
                  const float* bias, void* out, int64_t ldo,
                  const int32_t* targets, float* ce_part, float* ce_tgt,
                  int32_t* err_flag, void* stream);
+/*
+ * The +eps and -eps forwards of one ZO step as ONE launch ("stacked"): the
+ * activations of both directions are stacked as A = [a+; a-] (M rows), rows
+ * [0, m_split) multiply B (the +eps shadow) and add bias, rows [m_split, M)
+ * multiply B2 / add bias2.  Same kernel, tile schedule and per-tile
+ * arithmetic as zo_gemm_bf16 on each half (results are bit-identical); one
+ * launch fills twice the tiles, so the partial last wave and the launch
+ * prologue / tail are paid once per layer instead of once per direction.
+ * m_split must be a multiple of 256 and M > 256 (CTA-pair kernel).
+ */
+int zo_gemm_bf16_split(const void* A, int64_t lda, const void* B, const void* B2, int64_t ldb,
+                       int64_t M, int64_t N, int64_t K, int64_t m_split, int32_t epilogue,
+                       const float* bias, const float* bias2, void* out, int64_t ldo,
+                       const int32_t* targets, float* ce_part, float* ce_tgt,
+                       int32_t* err_flag, void* stream);
 /* number of N tiles the ZO_EPI_CE epilogue writes per row for a given N */
 /* Same GEMM with a caller-owned workspace (zero-initialised once, reusable
  * by later calls on the same stream; not shared by concurrent calls): the

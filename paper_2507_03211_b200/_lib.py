@@ -53,6 +53,8 @@ SIGNATURES = {
     "zo_perturb_tile_elems": (I64, []),
     "zo_embed_fwd": (C.c_int, [P, I64, P, I64, P, I64, I64, I64, I64, D, P, I32, P, I64, P, I64, P, P]),
     "zo_layernorm_fwd": (C.c_int, [P, I64, P, P, I64, I64, P, I64, P]),
+    "zo_layernorm_fwd_split": (C.c_int, [P, I64, P, P, P, P, I64, I64, I64, P, I64, P]),
+    "zo_gemm_bf16_split": (C.c_int, [P, I64, P, P, I64, I64, I64, I64, I64, I32, P, P, P, I64, P, P, P, P, P]),
     "zo_gemm_bf16": (C.c_int, [P, I64, P, I64, I64, I64, I64, I32, P, P, I64, P, P, P, P, P]),
     "zo_gemm_bf16_ws": (C.c_int, [P, I64, P, I64, I64, I64, I64, I32, P, P, I64, P, P, P, P, P, I64, P]),
     "zo_gemm_workspace_bytes": (I64, [I64, I64, I64]),

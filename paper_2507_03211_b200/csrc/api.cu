@@ -49,7 +49,7 @@ int embed_launch(const float*, int64_t, const float*, int64_t, const int32_t*, i
                  double, const ZoStepScalars*, int32_t, const double*, int64_t, float*, int64_t, int32_t*,
                  cudaStream_t);
 int layernorm_launch(const float*, int64_t, const float*, const float*, int64_t, int64_t, __nv_bfloat16*, int64_t,
-                     cudaStream_t);
+                     cudaStream_t, const float*, const float*, int64_t);
 int attention_launch(const __nv_bfloat16*, int64_t, int64_t, int64_t, int64_t, int64_t, __nv_bfloat16*, int64_t,
                      cudaStream_t);
 int ce_finalize_launch(const float*, const float*, int64_t, int64_t, double*, double*, int32_t*, cudaStream_t);
@@ -58,7 +58,8 @@ int grad_groups_launch(const double*, int, int, int, int, int, int, double, doub
                        cudaStream_t);
 int hash_launch(const void*, int64_t, uint64_t*, uint64_t*, int, cudaStream_t);
 int gemm_launch(const void*, int64_t, const void*, int64_t, int64_t, int64_t, int64_t, int, const float*, void*,
-                int64_t, const int32_t*, float*, float*, int32_t*, void*, int64_t, cudaStream_t);
+                int64_t, const int32_t*, float*, float*, int32_t*, void*, int64_t, cudaStream_t, const void*,
+                const float*, int64_t);
 int64_t gemm_workspace_bytes(int64_t M, int64_t N, int64_t K);
 int64_t gemm_ce_tiles(int64_t N);
 
@@ -171,7 +172,18 @@ int zo_layernorm_fwd(const float* x, int64_t ldx, const float* gamma, const floa
   ZO_CHECK_ARG(x && gamma && beta && out_bf16, ZO_ERR_CONFIG, "zo_layernorm_fwd: null argument");
   ZO_CHECK_ARG(d > 0 && d <= 49152, ZO_ERR_CONFIG, "zo_layernorm_fwd: d=%lld out of range", (long long)d);
   return zo::layernorm_launch(x, ldx, gamma, beta, rows, d, static_cast<__nv_bfloat16*>(out_bf16), ldo,
-                              ZO_STREAM(stream));
+                              ZO_STREAM(stream), nullptr, nullptr, 0);
+}
+
+int zo_layernorm_fwd_split(const float* x, int64_t ldx, const float* gamma, const float* beta,
+                           const float* gamma2, const float* beta2, int64_t rows, int64_t row_split, int64_t d,
+                           void* out_bf16, int64_t ldo, void* stream) {
+  ZO_CHECK_ARG(x && gamma && beta && gamma2 && beta2 && out_bf16, ZO_ERR_CONFIG,
+               "zo_layernorm_fwd_split: null argument");
+  ZO_CHECK_ARG(d > 0 && d <= 49152, ZO_ERR_CONFIG, "zo_layernorm_fwd_split: d=%lld out of range", (long long)d);
+  ZO_CHECK_ARG(row_split >= 0 && row_split <= rows, ZO_ERR_CONFIG, "zo_layernorm_fwd_split: bad row_split");
+  return zo::layernorm_launch(x, ldx, gamma, beta, rows, d, static_cast<__nv_bfloat16*>(out_bf16), ldo,
+                              ZO_STREAM(stream), gamma2, beta2, row_split);
 }
 
 int zo_gemm_bf16(const void* A, int64_t lda, const void* B, int64_t ldb, int64_t M, int64_t N, int64_t K,
@@ -183,7 +195,22 @@ int zo_gemm_bf16(const void* A, int64_t lda, const void* B, int64_t ldb, int64_t
                ZO_ERR_CONFIG, "zo_gemm_bf16: missing epilogue buffers");
   ZO_CHECK_ARG(epi == ZO_EPI_F32 || epi == ZO_EPI_CE || bias, ZO_ERR_CONFIG, "zo_gemm_bf16: bias required");
   return zo::gemm_launch(A, lda, B, ldb, M, N, K, epilogue, bias, out, ldo, targets, ce_part, ce_tgt, err_flag,
-                         nullptr, 0, ZO_STREAM(stream));
+                         nullptr, 0, ZO_STREAM(stream), nullptr, nullptr, 0);
+}
+
+int zo_gemm_bf16_split(const void* A, int64_t lda, const void* B, const void* B2, int64_t ldb, int64_t M, int64_t N,
+                       int64_t K, int64_t m_split, int32_t epilogue, const float* bias, const float* bias2, void* out,
+                       int64_t ldo, const int32_t* targets, float* ce_part, float* ce_tgt, int32_t* err_flag,
+                       void* stream) {
+  ZO_CHECK_ARG(A && B && B2, ZO_ERR_CONFIG, "zo_gemm_bf16_split: null operand");
+  const int32_t epi = epilogue & ~ZO_GEMM_B_KMAJOR;
+  ZO_CHECK_ARG(epi == ZO_EPI_CE ? (targets && ce_part && ce_tgt && err_flag) : (out != nullptr),
+               ZO_ERR_CONFIG, "zo_gemm_bf16_split: missing epilogue buffers");
+  ZO_CHECK_ARG(epi == ZO_EPI_F32 || epi == ZO_EPI_CE || (bias && bias2), ZO_ERR_CONFIG,
+               "zo_gemm_bf16_split: bias required");
+  ZO_CHECK_ARG(m_split > 0, ZO_ERR_CONFIG, "zo_gemm_bf16_split: m_split must be positive");
+  return zo::gemm_launch(A, lda, B, ldb, M, N, K, epilogue, bias, out, ldo, targets, ce_part, ce_tgt, err_flag,
+                         nullptr, 0, ZO_STREAM(stream), B2, bias2, m_split);
 }
 
 int zo_gemm_bf16_ws(const void* A, int64_t lda, const void* B, int64_t ldb, int64_t M, int64_t N, int64_t K,
@@ -197,7 +224,7 @@ int zo_gemm_bf16_ws(const void* A, int64_t lda, const void* B, int64_t ldb, int6
   ZO_CHECK_ARG(epi == ZO_EPI_F32 || epi == ZO_EPI_CE || bias, ZO_ERR_CONFIG,
                "zo_gemm_bf16_ws: bias required");
   return zo::gemm_launch(A, lda, B, ldb, M, N, K, epilogue, bias, out, ldo, targets, ce_part, ce_tgt, err_flag,
-                         workspace, workspace_bytes, ZO_STREAM(stream));
+                         workspace, workspace_bytes, ZO_STREAM(stream), nullptr, nullptr, 0);
 }
 
 int64_t zo_gemm_workspace_bytes(int64_t M, int64_t N, int64_t K) { return zo::gemm_workspace_bytes(M, N, K); }

@@ -37,8 +37,16 @@ namespace zo {
 
 constexpr int kBM = 128;
 constexpr int kBK = 64;
-constexpr int kGemmThreads = 320;   // warp 0 TMA, warp 1 MMA/TMEM, warps 2..9 epilogue
-constexpr int kEpiWarps = 8;
+// Epilogue warps: 8 (each owns a TMEM lane quarter x one column half), or 4
+// (each walks both halves) -- the 6-warp CTA at <= 168 registers leaves half
+// of the SM's register file for a co-resident perturb pass.
+#ifndef ZO_GEMM_EPI_WARPS
+#define ZO_GEMM_EPI_WARPS 8
+#endif
+constexpr int kEpiWarps = ZO_GEMM_EPI_WARPS;
+static_assert(kEpiWarps == 8 || kEpiWarps == 4, "epilogue warps");
+constexpr int kGemmThreads = 64 + 32 * kEpiWarps;   // warp 0 TMA, warp 1 MMA/TMEM, warps 2.. epilogue
+constexpr int kGemmMinBlocks = kEpiWarps == 4 ? 2 : 1;   // 4 epilogue warps: cap registers at 170
 
 template <int BN>
 struct GemmCfg {
@@ -67,6 +75,11 @@ struct GemmArgs {
   int32_t sk_pieces;    // max pieces per split tile
   int32_t* sk_flags;    // [slot][16 epilogue warps], self-clearing
   float* sk_part;       // [slot][16][32 rows x 128 cols] fp32 partial accumulators
+  // row-split ("stacked") problem: rows >= m_split use the second B operand
+  // (tmB2) and bias2 -- the +eps / -eps forwards of one ZO step as ONE launch
+  // over [x+; x-] (0 = off; a multiple of 256 so every pair tile is one side)
+  int64_t m_split;
+  const float* bias2;
 };
 
 constexpr int kSkWarpFloats = 32 * 128;   // one epilogue warp's share of a pair tile
@@ -202,12 +215,14 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t tme
   };
   const int64_t row_base = m0 + quarter * 32;
   const int64_t row = row_base + lane;
+  const bool second = args.m_split && row_base >= args.m_split;
+  const float* __restrict__ bias = second ? args.bias2 : args.bias;
   const bool row_ok = row < args.M;
   float ce_m = -INFINITY, ce_s = 0.f;
   int32_t tgt = -1;
   bool bad = false;
   if constexpr (EPI == ZO_EPI_CE) {
-    if (row_ok) tgt = args.targets[row];
+    if (row_ok) tgt = args.targets[second ? row - args.m_split : row];   // stacked rows share the targets
   }
   constexpr int CH = BN / 64;   // 32-column chunks per half
 #pragma unroll 1
@@ -222,11 +237,11 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t tme
       if (!row_ok || col0 >= args.N) continue;
       const int lim = col0 + 32 <= args.N ? 32 : (int)(args.N - col0);
       float cm = -INFINITY;
-      const bool has_bias = args.bias != nullptr;   // a tied head has no bias (real OPT)
+      const bool has_bias = bias != nullptr;   // a tied head has no bias (real OPT)
 #pragma unroll
       for (int i = 0; i < 32; ++i) {
         if (i < lim) {
-          if (has_bias) v[i] += __ldg(args.bias + col0 + i);
+          if (has_bias) v[i] += __ldg(bias + col0 + i);
           bad |= !isfinite(v[i]);
           cm = fmaxf(cm, v[i]);
         }
@@ -249,15 +264,15 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t tme
       // bf16 out: each thread writes 64 contiguous bytes of its row (4 x 16 B)
       float4 bias4[8];
       const bool full = row_ok && col0 + 32 <= args.N;
-      if (full && ((reinterpret_cast<uintptr_t>(args.bias + col0) & 15) == 0)) {
+      if (full && ((reinterpret_cast<uintptr_t>(bias + col0) & 15) == 0)) {
 #pragma unroll
-        for (int i = 0; i < 8; ++i) bias4[i] = __ldg(reinterpret_cast<const float4*>(args.bias + col0) + i);
+        for (int i = 0; i < 8; ++i) bias4[i] = __ldg(reinterpret_cast<const float4*>(bias + col0) + i);
       } else {
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
           float t[4];
 #pragma unroll
-          for (int j = 0; j < 4; ++j) t[j] = (col0 + 4 * i + j < args.N) ? args.bias[col0 + 4 * i + j] : 0.f;
+          for (int j = 0; j < 4; ++j) t[j] = (col0 + 4 * i + j < args.N) ? bias[col0 + 4 * i + j] : 0.f;
           bias4[i] = make_float4(t[0], t[1], t[2], t[3]);
         }
       }
@@ -302,7 +317,7 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t tme
       float* o = static_cast<float*>(args.out) + row * args.ldo + col0;
       const bool full = row_ok && col0 + 32 <= args.N;
       const bool vec = full && ((reinterpret_cast<uintptr_t>(o) & 31) == 0) &&
-                       (EPI == ZO_EPI_F32 || (reinterpret_cast<uintptr_t>(args.bias + col0) & 15) == 0);
+                       (EPI == ZO_EPI_F32 || (reinterpret_cast<uintptr_t>(bias + col0) & 15) == 0);
       float res[32];
       if constexpr (EPI == ZO_EPI_BIAS_RESID_F32) {
         // residual (the previous contents of out) read before the TMEM load so
@@ -323,7 +338,7 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t tme
         if (vec) {
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
-            const float4 b4 = __ldg(reinterpret_cast<const float4*>(args.bias + col0) + i);
+            const float4 b4 = __ldg(reinterpret_cast<const float4*>(bias + col0) + i);
             v[4 * i] = res[4 * i] + (v[4 * i] + b4.x);
             v[4 * i + 1] = res[4 * i + 1] + (v[4 * i + 1] + b4.y);
             v[4 * i + 2] = res[4 * i + 2] + (v[4 * i + 2] + b4.z);
@@ -332,7 +347,7 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t tme
         } else {
 #pragma unroll
           for (int i = 0; i < 32; ++i)
-            if (col0 + i < args.N) v[i] = res[i] + (v[i] + args.bias[col0 + i]);
+            if (col0 + i < args.N) v[i] = res[i] + (v[i] + bias[col0 + i]);
         }
       }
       if (vec) {
@@ -361,7 +376,7 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t tme
 }
 
 template <int BN, int EPI, bool BKM>
-__global__ void __launch_bounds__(kGemmThreads, 1)
+__global__ void __launch_bounds__(kGemmThreads, kGemmMinBlocks)
     gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                         const GemmArgs args) {
   using C = GemmCfg<BN>;
@@ -462,7 +477,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   } else {
     // ============================ epilogue ================================
     const int quarter = warp & 3;   // TMEM lanes 32*quarter .. +31
-    const int half = (warp - 2) >> 2;
     int64_t local = 0;
     for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++local) {
       const int acc = (int)(local & 1);
@@ -471,7 +485,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const int64_t tn = tile / num_m;
       mbar_wait(tfull_bar(acc), acc_phase);
       tc_fence_after();
-      epilogue_tile<BN, EPI>(args, tmem_base, acc, quarter, half, lane, m0, tn * BN, tn);
+#pragma unroll 1
+      for (int e = warp - 2; e < 8; e += kEpiWarps)        // logical epilogue slot e: column half e / 4
+        epilogue_tile<BN, EPI>(args, tmem_base, acc, quarter, e >> 2, lane, m0, tn * BN, tn);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(tempty_bar(acc));
@@ -550,9 +566,9 @@ __device__ __forceinline__ void tc_mma_f16_pair(uint32_t d_tmem, uint64_t adesc,
 }
 
 template <int EPI, bool BKM>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, kGemmMinBlocks)
     gemm_tcgen05_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                             const GemmArgs args) {
+                             const __grid_constant__ CUtensorMap tmB2, const GemmArgs args) {
   constexpr int BN = 256;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
@@ -578,6 +594,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tmA);
     prefetch_tmap(&tmB);
+    if (args.m_split) prefetch_tmap(&tmB2);
     for (int s = 0; s < k2Stages; ++s) { mbar_init(full_bar(s), 1); mbar_init(empty_bar(s), 1); }
     for (int a = 0; a < 2; ++a) { mbar_init(tfull_bar(a), 1); mbar_init(tempty_bar(a), 2 * kEpiWarps); }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
@@ -604,16 +621,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
         const int64_t tile = it.tile;
         const int m0 = (int)((tile % num_m) * (2 * kBM) + rank * kBM);
         const int n0 = (int)((tile / num_m) * BN + rank * 128);
+        const CUtensorMap* mb = (args.m_split && (tile % num_m) * (2 * kBM) >= args.m_split) ? &tmB2 : &tmB;
         for (int kb = it.kb0; kb < it.kb1; ++kb) {
           mbar_wait(empty_bar(stage), phase ^ 1u);
           if (leader) mbar_expect_tx(full_bar(stage), (uint32_t)(2 * k2StageBytes));
           const uint32_t fb = mapa_shared(full_bar(stage), 0);
           tma_load_2d_cg2(sA + stage * k2ABytes, &tmA, fb, kb * kBK, m0);
           if constexpr (BKM) {
-            tma_load_2d_cg2(sB + stage * k2BBytes, &tmB, fb, kb * kBK, n0);    // 128 rows x 64 k
+            tma_load_2d_cg2(sB + stage * k2BBytes, mb, fb, kb * kBK, n0);    // 128 rows x 64 k
           } else {
-            tma_load_2d_cg2(sB + stage * k2BBytes, &tmB, fb, n0, kb * kBK);
-            tma_load_2d_cg2(sB + stage * k2BBytes + kBK * 128, &tmB, fb, n0 + 64, kb * kBK);
+            tma_load_2d_cg2(sB + stage * k2BBytes, mb, fb, n0, kb * kBK);
+            tma_load_2d_cg2(sB + stage * k2BBytes + kBK * 128, mb, fb, n0 + 64, kb * kBK);
           }
           if (++stage == k2Stages) { stage = 0; phase ^= 1u; }
         }
@@ -658,8 +676,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
   } else {
     // ====== epilogue (both CTAs): this CTA's 128 rows x 256 columns ======
     const int quarter = warp & 3;
-    const int half = (warp - 2) >> 2;
-    const int64_t wslot = (int64_t)rank * kEpiWarps + (warp - 2);   // this warp's share of a pair tile
     SkItem it;
     for (int64_t local = 0; sk_item(args, cluster_id, n_clusters, nk, local, it); ++local) {
       const int64_t tile = it.tile;
@@ -669,13 +685,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       const int64_t tn = tile / num_m;
       mbar_wait(tfull_bar(acc), acc_phase);
       tc_fence_after();
-      if (it.kind == 1) {
-        store_partial(tmem_base, acc, quarter, half, lane, args.sk_part + (it.slot * 16 + wslot) * kSkWarpFloats,
-                      args.sk_flags + it.slot * 16 + wslot);
-      } else {
-        epilogue_tile<BN, EPI>(args, tmem_base, acc, quarter, half, lane, m0, tn * BN, tn,
-                               args.sk_part + (it.slot * 16 + wslot) * kSkWarpFloats, it.npart,
-                               args.sk_flags + it.slot * 16 + wslot);
+#pragma unroll 1
+      for (int e = warp - 2; e < 8; e += kEpiWarps) {      // logical slot e: lane quarter, column half e / 4
+        const int half = e >> 2;
+        const int64_t wslot = (int64_t)rank * 8 + e;        // this slot's share of a pair tile (16 per pair)
+        if (it.kind == 1) {
+          store_partial(tmem_base, acc, quarter, half, lane, args.sk_part + (it.slot * 16 + wslot) * kSkWarpFloats,
+                        args.sk_flags + it.slot * 16 + wslot);
+        } else {
+          epilogue_tile<BN, EPI>(args, tmem_base, acc, quarter, half, lane, m0, tn * BN, tn,
+                                 args.sk_part + (it.slot * 16 + wslot) * kSkWarpFloats, it.npart,
+                                 args.sk_flags + it.slot * 16 + wslot);
+        }
       }
       tc_fence_before();
       __syncwarp();
@@ -794,7 +815,8 @@ int launch_bn(int epi, bool bkm, const CUtensorMap& ma, const CUtensorMap& mb, c
 
 
 template <int EPI, bool BKM = false>
-int launch_pair_t(const CUtensorMap& ma, const CUtensorMap& mb, const GemmArgs& a, cudaStream_t st) {
+int launch_pair_t(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mb2, const GemmArgs& a,
+                  cudaStream_t st) {
   static bool attr_done = false;
   if (!attr_done) {
     cudaError_t e = cudaFuncSetAttribute(gemm_tcgen05_pair_kernel<EPI, BKM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -805,27 +827,27 @@ int launch_pair_t(const CUtensorMap& ma, const CUtensorMap& mb, const GemmArgs& 
   const int64_t tiles = ((a.M + 255) / 256) * ((a.N + 255) / 256);
   const int64_t pairs = num_sms() / 2;
   const int grid = 2 * (int)(a.sk_units ? pairs : (tiles < pairs ? tiles : pairs));
-  launch_k(gemm_tcgen05_pair_kernel<EPI, BKM>, dim3(grid), dim3(kGemmThreads), k2Smem, st, ma, mb, a);
+  launch_k(gemm_tcgen05_pair_kernel<EPI, BKM>, dim3(grid), dim3(kGemmThreads), k2Smem, st, ma, mb, mb2, a);
   return launch_status("gemm_tcgen05_pair_kernel");
 }
 
-int launch_pair(int epi, bool bkm, const CUtensorMap& ma, const CUtensorMap& mb, const GemmArgs& a,
-                cudaStream_t st) {
+int launch_pair(int epi, bool bkm, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mb2,
+                const GemmArgs& a, cudaStream_t st) {
   if (bkm) {
     switch (epi) {
-      case ZO_EPI_F32: return launch_pair_t<ZO_EPI_F32, true>(ma, mb, a, st);
-      case ZO_EPI_CE: return launch_pair_t<ZO_EPI_CE, true>(ma, mb, a, st);
+      case ZO_EPI_F32: return launch_pair_t<ZO_EPI_F32, true>(ma, mb, mb2, a, st);
+      case ZO_EPI_CE: return launch_pair_t<ZO_EPI_CE, true>(ma, mb, mb2, a, st);
     }
     set_error("zo_gemm_bf16: ZO_GEMM_B_KMAJOR supports the F32 and CE epilogues only (got %d)", epi);
     return ZO_ERR_CONFIG;
   }
   switch (epi) {
-    case ZO_EPI_F32: return launch_pair_t<ZO_EPI_F32>(ma, mb, a, st);
-    case ZO_EPI_BIAS_BF16: return launch_pair_t<ZO_EPI_BIAS_BF16>(ma, mb, a, st);
-    case ZO_EPI_BIAS_GELU_BF16: return launch_pair_t<ZO_EPI_BIAS_GELU_BF16>(ma, mb, a, st);
-    case ZO_EPI_BIAS_RELU_BF16: return launch_pair_t<ZO_EPI_BIAS_RELU_BF16>(ma, mb, a, st);
-    case ZO_EPI_BIAS_RESID_F32: return launch_pair_t<ZO_EPI_BIAS_RESID_F32>(ma, mb, a, st);
-    case ZO_EPI_CE: return launch_pair_t<ZO_EPI_CE>(ma, mb, a, st);
+    case ZO_EPI_F32: return launch_pair_t<ZO_EPI_F32>(ma, mb, mb2, a, st);
+    case ZO_EPI_BIAS_BF16: return launch_pair_t<ZO_EPI_BIAS_BF16>(ma, mb, mb2, a, st);
+    case ZO_EPI_BIAS_GELU_BF16: return launch_pair_t<ZO_EPI_BIAS_GELU_BF16>(ma, mb, mb2, a, st);
+    case ZO_EPI_BIAS_RELU_BF16: return launch_pair_t<ZO_EPI_BIAS_RELU_BF16>(ma, mb, mb2, a, st);
+    case ZO_EPI_BIAS_RESID_F32: return launch_pair_t<ZO_EPI_BIAS_RESID_F32>(ma, mb, mb2, a, st);
+    case ZO_EPI_CE: return launch_pair_t<ZO_EPI_CE>(ma, mb, mb2, a, st);
   }
   set_error("zo_gemm_bf16: unknown epilogue %d", epi);
   return ZO_ERR_CONFIG;
@@ -876,7 +898,8 @@ int64_t gemm_workspace_bytes(int64_t M, int64_t N, int64_t K) { return sk_plan(M
 
 int gemm_launch(const void* A, int64_t lda, const void* B, int64_t ldb, int64_t M, int64_t N, int64_t K, int epi,
                 const float* bias, void* out, int64_t ldo, const int32_t* targets, float* ce_part, float* ce_tgt,
-                int32_t* err, void* ws, int64_t ws_bytes, cudaStream_t st) {
+                int32_t* err, void* ws, int64_t ws_bytes, cudaStream_t st, const void* B2, const float* bias2,
+                int64_t m_split) {
   const bool bkm = (epi & ZO_GEMM_B_KMAJOR) != 0;
   epi &= ~ZO_GEMM_B_KMAJOR;
   if (M == 0 || N == 0) return ZO_OK;
@@ -887,7 +910,8 @@ int gemm_launch(const void* A, int64_t lda, const void* B, int64_t ldb, int64_t 
               (long long)ldb);
     return ZO_ERR_CONFIG;
   }
-  if ((reinterpret_cast<uintptr_t>(A) & 15) || (reinterpret_cast<uintptr_t>(B) & 15)) {
+  if ((reinterpret_cast<uintptr_t>(A) & 15) || (reinterpret_cast<uintptr_t>(B) & 15) ||
+      (reinterpret_cast<uintptr_t>(B2) & 15)) {
     set_error("zo_gemm_bf16: operands must be 16-byte aligned");
     return ZO_ERR_CONFIG;
   }
@@ -911,7 +935,18 @@ int gemm_launch(const void* A, int64_t lda, const void* B, int64_t ldb, int64_t 
   // B tile: MN-major 64-column boxes, or K-major (rows = N) boxes of 128 (pair half) / BN rows
   rc = bkm ? get_map(B, K, N, ldb, kBK, pair ? 128 : bn, &mb) : get_map(B, N, K, ldb, 64, kBK, &mb);
   if (rc) return rc;
-  GemmArgs a{M, N, K, bias, out, ldo, targets, ce_part, ce_tgt, err, gemm_ce_tiles(N), 0, 0, 1, nullptr, nullptr};
+  CUtensorMap mb2 = mb;
+  if (m_split) {
+    if (!pair || m_split % 256 || m_split >= M || !B2) {
+      set_error("zo_gemm_bf16_split: m_split=%lld must be a multiple of 256 in (0, M=%lld) with M > 128",
+                (long long)m_split, (long long)M);
+      return ZO_ERR_CONFIG;
+    }
+    rc = bkm ? get_map(B2, K, N, ldb, kBK, 128, &mb2) : get_map(B2, N, K, ldb, 64, kBK, &mb2);
+    if (rc) return rc;
+  }
+  GemmArgs a{M, N, K, bias, out, ldo, targets, ce_part, ce_tgt, err, gemm_ce_tiles(N), 0, 0, 1, nullptr, nullptr,
+             m_split, bias2};
   a.dp_tiles = ((M + 255) / 256) * ((N + 255) / 256);
   if (ws && (reinterpret_cast<uintptr_t>(ws) & 255) == 0) {
     const SkPlan pl = sk_plan(M, N, K);
@@ -923,7 +958,7 @@ int gemm_launch(const void* A, int64_t lda, const void* B, int64_t ldb, int64_t 
       a.sk_part = reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + pl.flag_bytes);
     }
   }
-  if (pair) return launch_pair(epi, bkm, ma, mb, a, st);
+  if (pair) return launch_pair(epi, bkm, ma, mb, mb2, a, st);
   return bn == 256 ? launch_bn<256>(epi, bkm, ma, mb, a, st) : launch_bn<128>(epi, bkm, ma, mb, a, st);
 }
 

@@ -76,8 +76,10 @@ __device__ __forceinline__ float block_sum(float v, float* red) {
 
 __global__ void layernorm_kernel(const float* __restrict__ x, int64_t ldx, const float* __restrict__ g,
                                  const float* __restrict__ b, int64_t d, __nv_bfloat16* __restrict__ out,
-                                 int64_t ldo) {
+                                 int64_t ldo, const float* __restrict__ g2, const float* __restrict__ b2,
+                                 int64_t row_split) {
   extern __shared__ float srow[];
+  if (row_split && (int64_t)blockIdx.x >= row_split) { g = g2; b = b2; }   // stacked +eps / -eps rows
   __shared__ float red[32];
   pdl_trigger();
   pdl_wait();
@@ -107,7 +109,9 @@ template <int NV>
 __global__ void __launch_bounds__(256) layernorm_warp_kernel(const float* __restrict__ x, int64_t ldx,
                                                               const float* __restrict__ g,
                                                               const float* __restrict__ b, int64_t rows, int d,
-                                                              __nv_bfloat16* __restrict__ out, int64_t ldo) {
+                                                              __nv_bfloat16* __restrict__ out, int64_t ldo,
+                                                              const float* __restrict__ g2,
+                                                              const float* __restrict__ b2, int64_t row_split) {
   pdl_trigger();
   pdl_wait();
   const int lane = threadIdx.x & 31;
@@ -139,12 +143,15 @@ __global__ void __launch_bounds__(256) layernorm_warp_kernel(const float* __rest
     for (int o = 16; o > 0; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
     const float rstd = 1.0f / sqrtf(q / (float)d + 1e-5f);
     __nv_bfloat16* orow = out + r * ldo;
+    const bool second = row_split && r >= row_split;      // stacked +eps / -eps rows
+    const float* gr = second ? g2 : g;
+    const float* br = second ? b2 : b;
 #pragma unroll
     for (int i = 0; i < NV; ++i) {
       const int c = (i * 32 + lane) * 4;
       if (c < d) {
-        const float4 gg = *reinterpret_cast<const float4*>(g + c);
-        const float4 bb = *reinterpret_cast<const float4*>(b + c);
+        const float4 gg = *reinterpret_cast<const float4*>(gr + c);
+        const float4 bb = *reinterpret_cast<const float4*>(br + c);
         __nv_bfloat162 lo = __floats2bfloat162_rn(fmaf((v[i].x - mu) * rstd, gg.x, bb.x),
                                                   fmaf((v[i].y - mu) * rstd, gg.y, bb.y));
         __nv_bfloat162 hi = __floats2bfloat162_rn(fmaf((v[i].z - mu) * rstd, gg.z, bb.z),
@@ -159,18 +166,22 @@ __global__ void __launch_bounds__(256) layernorm_warp_kernel(const float* __rest
 }
 
 int layernorm_launch(const float* x, int64_t ldx, const float* g, const float* b, int64_t rows, int64_t d,
-                     __nv_bfloat16* out, int64_t ldo, cudaStream_t st) {
+                     __nv_bfloat16* out, int64_t ldo, cudaStream_t st, const float* g2, const float* b2,
+                     int64_t row_split) {
   if (rows == 0) return ZO_OK;
+  if (!row_split) { g2 = g; b2 = b; }
   const bool vec = (d % 4 == 0) && (ldx % 4 == 0) && (ldo % 4 == 0) &&
-                   ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(g) |
-                     reinterpret_cast<uintptr_t>(b)) & 15) == 0 && ((reinterpret_cast<uintptr_t>(out) & 7) == 0);
+                   ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(g) | reinterpret_cast<uintptr_t>(b) |
+                     reinterpret_cast<uintptr_t>(g2) | reinterpret_cast<uintptr_t>(b2)) & 15) == 0 &&
+                   ((reinterpret_cast<uintptr_t>(out) & 7) == 0);
   if (vec && d <= 4096) {
     const int64_t want = (rows + 7) / 8;
     const int grid = (int)(want < (int64_t)num_sms() * 8 ? want : (int64_t)num_sms() * 8);
     const int nv = (int)((d + 127) / 128);
 #define ZO_LN_CASE(N)                                                                                   \
   if (nv <= N) {                                                                                        \
-    launch_k(layernorm_warp_kernel<N>, dim3(grid), dim3(256), 0, st, x, ldx, g, b, rows, (int)d, out, ldo);    \
+    launch_k(layernorm_warp_kernel<N>, dim3(grid), dim3(256), 0, st, x, ldx, g, b, rows, (int)d, out, ldo,  \
+             g2, b2, row_split);                                                                        \
     return launch_status("layernorm_warp_kernel");                                                      \
   }
     ZO_LN_CASE(1) ZO_LN_CASE(2) ZO_LN_CASE(4) ZO_LN_CASE(8) ZO_LN_CASE(16) ZO_LN_CASE(32)
@@ -183,7 +194,8 @@ int layernorm_launch(const float* x, int64_t ldx, const float* g, const float* b
     big_smem = true;
   }
   const int threads = d >= 1024 ? 512 : (d >= 256 ? 256 : 64);
-  launch_k(layernorm_kernel, dim3((unsigned)rows), dim3(threads), smem, st, x, ldx, g, b, d, out, ldo);
+  launch_k(layernorm_kernel, dim3((unsigned)rows), dim3(threads), smem, st, x, ldx, g, b, d, out, ldo, g2, b2,
+           row_split);
   return launch_status("layernorm_kernel");
 }
 

@@ -434,11 +434,24 @@ int perturb_update_launch(const PuParams& p, int zmode, cudaStream_t stream, boo
   if (p.n_tiles <= 0) return ZO_OK;
   static const int occ = [] { const char* e = getenv("ZO_PU_OCC"); return e ? atoi(e) : 4; }();
   static const int waves = [] { const char* e = getenv("ZO_PU_WAVES"); return e ? atoi(e) : 2; }();
-  // two resident waves of chunks: late-starting CTAs even out the tail
-  const int64_t want = (int64_t)num_sms() * (background ? 1 : occ * waves);
+  static const int bg_ctas = [] { const char* e = getenv("ZO_PU_BG_CTAS"); return e ? atoi(e) : 1; }();
+  // two resident waves of chunks: late-starting CTAs even out the tail;
+  // the background pass keeps bg_ctas CTAs per SM beside the forward's kernels
+  const int64_t want = (int64_t)num_sms() * (background ? bg_ctas : occ * waves);
   const int grid = (int)(p.n_tiles < want ? p.n_tiles : want);
   const size_t smem = p.n_segs + 1 <= kPuMaxSmemSegs ? (size_t)(p.n_segs + 1) * sizeof(int64_t) : 0;
   if (background) {
+    static bool carve = false;
+    if (!carve) {
+      // configure the SM for maximum shared memory when these CTAs land first,
+      // so the forward's GEMM / attention CTAs (~200 KB of smem) can still be
+      // placed beside them (an SM's L1/smem split changes only when it is idle)
+      cudaFuncSetAttribute(perturb_update_bg_kernel<ZO_Z_PHILOX>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                           (int)cudaSharedmemCarveoutMaxShared);
+      cudaFuncSetAttribute(perturb_update_bg_kernel<ZO_Z_ORACLE>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                           (int)cudaSharedmemCarveoutMaxShared);
+      carve = true;
+    }
     if (zmode == ZO_Z_PHILOX)
       launch_k(perturb_update_bg_kernel<ZO_Z_PHILOX>, dim3(grid), dim3(kPuThreads), smem, stream, p);
     else

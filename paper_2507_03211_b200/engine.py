@@ -324,6 +324,26 @@ class DeviceStore:
             self._ws[key] = ws
         return self._ws[key]
 
+    def stacked_workspace(self, batch: int, seq: int) -> Workspace:
+        """Activations of BOTH directions stacked as [+eps rows; -eps rows]
+        (2 * batch * seq rows) for the one-launch-per-layer plan
+        (forward_calls_stacked); token ids / targets are the per-direction
+        workspaces' shared buffers."""
+        key = ("stacked", batch, seq)
+        if key not in self._ws:
+            ws = Workspace(self.config, 2 * batch, seq, self.device)
+            base = self.workspace(PLUS, batch, seq)
+            ws.ids, ws.tgt = base.ids, base.tgt
+            ws.half = batch * seq
+            ws.loss2 = torch.zeros(2, dtype=torch.float64, device=self.device)
+            self._ws[key] = ws
+        return self._ws[key]
+
+    @staticmethod
+    def stackable(batch: int, seq: int) -> bool:
+        """The stacked GEMMs split rows on a CTA-pair tile boundary."""
+        return (batch * seq) % 256 == 0
+
     # -- scalar state ----------------------------------------------------------
     def set_seed(self, seed: int, stream=None):
         self.scal[0:1].fill_(int(seed))
@@ -441,6 +461,80 @@ class DeviceStore:
                                                      L.ZO_EPI_F32 | bflag, 0, _ptr(logits), logits.stride(0), 0, 0,
                                                      0, 0, st)))
         return calls
+
+    def forward_calls_stacked(self, ws: Workspace, eps: float, zmode=L.ZO_Z_PHILOX, z_cur=None, stream=None):
+        """Both directional forwards as one launch per layer over the stacked
+        activations [x+; x-] (rows [0, h) use the +eps shadows, [h, 2h) the
+        -eps shadows): zo_layernorm_fwd_split / zo_gemm_bf16_split, attention
+        over 2B sequences, two embedding gathers and two CE finalizes.  The
+        per-row / per-tile arithmetic equals forward_calls on each direction,
+        so losses are bit-identical to the two-stream plan."""
+        cfg, lib = self.config, L.lib()
+        d, H, hd, V = cfg.d_model, cfg.n_heads, cfg.head_dim, cfg.vocab_size
+        M2, h, B2, T = ws.M, ws.half, ws.batch, ws.seq
+        opt = cfg.arch == "opt"
+        pos_off = 2 * d if opt else 0
+        ffn_epi = L.ZO_EPI_BIAS_RELU_BF16 if opt else L.ZO_EPI_BIAS_GELU_BF16
+        st = L.stream_ptr(stream)
+        ldx, ldh = ws.x.stride(0), ws.h.stride(0)
+        calls = []
+        for bid in range(len(self.layouts)):
+            bl = self.layouts[bid]
+            vp = lambda n: _ptr(self.vview(PLUS, bid, n))    # noqa: E731
+            vm = lambda n: _ptr(self.vview(MINUS, bid, n))   # noqa: E731
+
+            def wv(n, _bid=bid):
+                return self.wview(PLUS, _bid, n)[0], self.wview(MINUS, _bid, n)[0]
+
+            if bl.kind == EMBEDDING:
+                for k, sc in ((0, +eps), (1, -eps)):
+                    calls.append((lib.zo_embed_fwd, (
+                        self.theta_ptr(bl.key("tok_emb")), bl.key("tok_emb"),
+                        self.theta_ptr(bl.key("pos_emb") + pos_off), bl.key("pos_emb") + pos_off,
+                        _ptr(ws.ids), B2 // 2, T, d, V, float(sc), _ptr(self.scal), zmode, _ptr(z_cur), 0,
+                        _ptr(ws.x) + 4 * k * h * ldx, ldx, _ptr(ws.err), st)))
+            elif bl.kind == TRANSFORMER:
+                (qa, qb), (oa, ob), (f1a, f1b), (f2a, f2b) = wv("qkv"), wv("wo"), wv("w1"), wv("w2")
+                g = lib.zo_gemm_bf16_split
+                calls += [
+                    (lib.zo_layernorm_fwd_split, (_ptr(ws.x), ldx, vp("ln1_g"), vp("ln1_b"), vm("ln1_g"), vm("ln1_b"),
+                                                  M2, h, d, _ptr(ws.h), ldh, st)),
+                    (g, (_ptr(ws.h), ldh, _ptr(qa), _ptr(qb), qa.stride(0), M2, 3 * d, d, h, L.ZO_EPI_BIAS_BF16,
+                         vp("bqkv"), vm("bqkv"), _ptr(ws.qkv), ws.qkv.stride(0), 0, 0, 0, 0, st)),
+                    (lib.zo_attn_causal_fwd, (_ptr(ws.qkv), ws.qkv.stride(0), B2, T, H, hd, _ptr(ws.ctx),
+                                              ws.ctx.stride(0), st)),
+                    (g, (_ptr(ws.ctx), ws.ctx.stride(0), _ptr(oa), _ptr(ob), oa.stride(0), M2, d, d, h,
+                         L.ZO_EPI_BIAS_RESID_F32, vp("bo"), vm("bo"), _ptr(ws.x), ldx, 0, 0, 0, 0, st)),
+                    (lib.zo_layernorm_fwd_split, (_ptr(ws.x), ldx, vp("ln2_g"), vp("ln2_b"), vm("ln2_g"), vm("ln2_b"),
+                                                  M2, h, d, _ptr(ws.h), ldh, st)),
+                    (g, (_ptr(ws.h), ldh, _ptr(f1a), _ptr(f1b), f1a.stride(0), M2, 4 * d, d, h, ffn_epi,
+                         vp("b1"), vm("b1"), _ptr(ws.ff), ws.ff.stride(0), 0, 0, 0, 0, st)),
+                    (g, (_ptr(ws.ff), ws.ff.stride(0), _ptr(f2a), _ptr(f2b), f2a.stride(0), M2, d, 4 * d, h,
+                         L.ZO_EPI_BIAS_RESID_F32, vp("b2"), vm("b2"), _ptr(ws.x), ldx, 0, 0, 0, 0, st)),
+                ]
+            else:
+                if opt:
+                    wa, wb = self.wview(PLUS, 0, "tok_emb")[0], self.wview(MINUS, 0, "tok_emb")[0]
+                    ba = bb = 0
+                    flag = L.ZO_GEMM_B_KMAJOR
+                else:
+                    wa, wb = wv("w_out")
+                    ba, bb, flag = vp("b_out"), vm("b_out"), 0
+                calls.append((lib.zo_layernorm_fwd_split, (_ptr(ws.x), ldx, vp("lnf_g"), vp("lnf_b"), vm("lnf_g"),
+                                                           vm("lnf_b"), M2, h, d, _ptr(ws.h), ldh, st)))
+                calls.append((lib.zo_gemm_bf16_split, (_ptr(ws.h), ldh, _ptr(wa), _ptr(wb), wa.stride(0), M2, V, d, h,
+                                                       L.ZO_EPI_CE | flag, ba, bb, 0, 0, _ptr(ws.tgt),
+                                                       _ptr(ws.ce_part), _ptr(ws.ce_tgt), _ptr(ws.err), st)))
+                for k in (0, 1):
+                    calls.append((lib.zo_ce_finalize, (_ptr(ws.ce_part) + 4 * k * h * ws.n_ce * 2,
+                                                       _ptr(ws.ce_tgt) + 4 * k * h, h, ws.n_ce,
+                                                       _ptr(ws.loss2) + 8 * k, _ptr(ws.row_scratch) + 8 * k * h,
+                                                       _ptr(ws.err), st)))
+        return calls
+
+    def grad_call_stacked(self, ws: Workspace, eps: float, lr: float, stream=None):
+        return [(L.lib().zo_grad_finalize, (_ptr(ws.loss2), _ptr(ws.loss2) + 8, float(eps), float(lr),
+                                            _ptr(self.scal), _ptr(self.record), L.stream_ptr(stream)))]
 
     def grad_call(self, ws_pos: Workspace, ws_neg: Workspace, eps: float, lr: float, stream=None):
         return [(L.lib().zo_grad_finalize, (_ptr(ws_pos.loss), _ptr(ws_neg.loss), float(eps), float(lr),

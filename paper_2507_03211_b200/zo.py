@@ -157,7 +157,8 @@ class StreamingZo:
         # False: one fused pass, then the forwards; "blocks" (or True): per-block
         # passes on a side stream gated by events; "background": one co-resident
         # pass gated per block by device counters
-        plan = {False: None, True: "blocks", "blocks": "blocks", "background": "background"}[overlap]
+        plan = {False: None, True: "blocks", "blocks": "blocks", "background": "background",
+                "stacked": "stacked"}[overlap]
         self.overlap = plan if not self.mgr.oracle else None
         self.dual_stream = True
         # Philox steps replay one captured CUDA graph per batch shape (the
@@ -256,7 +257,28 @@ class StreamingZo:
         calls += s.grad_call(wsp, wsn, eps, self.hyper.lr)
         return calls
 
+    def stacked_step_calls(self, wsp, wsn):
+        """Same step with both directional forwards as ONE launch per layer
+        over stacked [+eps; -eps] activations (DeviceStore.forward_calls_stacked):
+        every GEMM fills twice the tiles, so the partial last wave and each
+        launch's prologue / tail are paid once per layer, not once per
+        direction.  Bit-identical to step_calls (same per-tile arithmetic)."""
+        if self.mgr.oracle:
+            raise ProtocolError("the stacked plan runs the Philox direction only")
+        s, eps = self.store, self.hyper.epsilon
+        ws = s.stacked_workspace(wsp.batch, wsp.seq)
+        flags = L.ZO_PU_UPDATE | L.ZO_PU_SHADOW_A | L.ZO_PU_SHADOW_B
+        calls = s.perturb_call(s.model_table, flags, +eps, -eps)
+        calls += s.forward_calls_stacked(ws, eps)
+        calls += s.grad_call_stacked(ws, eps, self.hyper.lr)
+        return calls
+
+    def _stacked_ok(self, wsp):
+        return self.overlap == "stacked" and self.store.stackable(wsp.batch, wsp.seq)
+
     def _plan(self, wsp, wsn, zc=None, zp=None, update=True):
+        if self._stacked_ok(wsp):
+            return self.stacked_step_calls(wsp, wsn)
         if self.overlap == "blocks":
             return self.overlapped_step_calls(wsp, wsn)
         if self.overlap == "background":
@@ -292,7 +314,10 @@ class StreamingZo:
         else:
             self.store.run(self._plan(wsp, wsn, zc, self._z_prev if apply_pending else None,
                                       update=apply_pending or not self.mgr.oracle))
-        st = _finish(self.store, wsp, wsn, self.iteration, seed)
+        wss = [wsp, wsn]
+        if self._stacked_ok(wsp):
+            wss.append(self.store.stacked_workspace(wsp.batch, wsp.seq))
+        st = _finish_record(self.store, wss, self.iteration, seed)
         self.g_prev, self.last_seed, self._pending, self._z_prev = st.g, seed, True, zc
         self.store.unflushed = True
         return st

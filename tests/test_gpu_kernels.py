@@ -117,6 +117,60 @@ def test_gemm_tied_head_ce(M, V, K):
     assert abs(loss.item() - torch.nn.functional.cross_entropy(logits, tg.long()).item()) < 1e-4
 
 
+@pytest.mark.parametrize("M,N,K", [(512, 768, 256), (4096, 6144, 2048), (1024, 1000, 200)])
+def test_gemm_split_equals_two_gemms(M, N, K):
+    """zo_gemm_bf16_split over stacked rows == zo_gemm_bf16 on each half with
+    its own B / bias, bit for bit, for every epilogue."""
+    h = M // 2
+    a = _rand(M, K, seed=41, scale=0.5)
+    b1, b2 = _rand(K, N, seed=42, scale=0.1), _rand(K, N, seed=43, scale=0.1)
+    c1, c2 = _rand(N, dtype=torch.float32, seed=44), _rand(N, dtype=torch.float32, seed=45)
+    lib = L.lib()
+    for epi, dt in ((L.ZO_EPI_BIAS_BF16, torch.bfloat16), (L.ZO_EPI_BIAS_GELU_BF16, torch.bfloat16),
+                    (L.ZO_EPI_BIAS_RELU_BF16, torch.bfloat16), (L.ZO_EPI_BIAS_RESID_F32, torch.float32)):
+        x0 = _rand(M, N, dtype=torch.float32, seed=46)
+        got = x0.clone() if dt == torch.float32 else torch.empty(M, N, device=DEV, dtype=dt)
+        want = x0.clone() if dt == torch.float32 else torch.empty(M, N, device=DEV, dtype=dt)
+        L.check(lib.zo_gemm_bf16_split(a.data_ptr(), K, b1.data_ptr(), b2.data_ptr(), N, M, N, K, h, epi,
+                                       c1.data_ptr(), c2.data_ptr(), got.data_ptr(), N, 0, 0, 0, 0, L.stream_ptr()))
+        ops.gemm(a[:h], b1, epi, out=want[:h], bias=c1)
+        ops.gemm(a[h:], b2, epi, out=want[h:], bias=c2)
+        torch.cuda.synchronize()
+        assert torch.equal(got, want), epi
+    # CE epilogue: stacked rows share one [M/2] target vector
+    tg = torch.randint(0, N, (h,), generator=torch.Generator().manual_seed(6)).to(DEV, torch.int32)
+    nt = ops.ce_tiles(N)
+    part, tl = torch.empty(M, nt, 2, device=DEV), torch.empty(M, device=DEV)
+    err = torch.zeros(1, dtype=torch.int32, device=DEV)
+    L.check(lib.zo_gemm_bf16_split(a.data_ptr(), K, b1.data_ptr(), b2.data_ptr(), N, M, N, K, h, L.ZO_EPI_CE,
+                                   c1.data_ptr(), c2.data_ptr(), 0, 0, tg.data_ptr(), part.data_ptr(), tl.data_ptr(),
+                                   err.data_ptr(), L.stream_ptr()))
+    p1, t1 = torch.empty(h, nt, 2, device=DEV), torch.empty(h, device=DEV)
+    p2, t2 = torch.empty(h, nt, 2, device=DEV), torch.empty(h, device=DEV)
+    ops.gemm(a[:h], b1, L.ZO_EPI_CE, bias=c1, targets=tg, ce_part=p1, ce_tgt=t1, err=err)
+    ops.gemm(a[h:], b2, L.ZO_EPI_CE, bias=c2, targets=tg, ce_part=p2, ce_tgt=t2, err=err)
+    torch.cuda.synchronize()
+    assert torch.equal(part, torch.cat([p1, p2])) and torch.equal(tl, torch.cat([t1, t2]))
+    with pytest.raises(Exception):      # the split must sit on a 256-row pair-tile boundary
+        L.check(lib.zo_gemm_bf16_split(a.data_ptr(), K, b1.data_ptr(), b2.data_ptr(), N, M, N, K, 100,
+                                       L.ZO_EPI_BIAS_BF16, c1.data_ptr(), c2.data_ptr(), got.data_ptr(), N,
+                                       0, 0, 0, 0, L.stream_ptr()))
+
+
+def test_layernorm_split_equals_two_layernorms():
+    rows, d = 512, 2048
+    x = _rand(rows, d, dtype=torch.float32, seed=47)
+    g1, b1, g2, b2 = (_rand(d, dtype=torch.float32, seed=s) for s in (48, 49, 50, 51))
+    got = torch.empty(rows, d, device=DEV, dtype=torch.bfloat16)
+    want = torch.empty_like(got)
+    L.check(L.lib().zo_layernorm_fwd_split(x.data_ptr(), d, g1.data_ptr(), b1.data_ptr(), g2.data_ptr(),
+                                           b2.data_ptr(), rows, 200, d, got.data_ptr(), d, L.stream_ptr()))
+    ops.layernorm(x[:200], g1, b1, want[:200])
+    ops.layernorm(x[200:], g2, b2, want[200:])
+    torch.cuda.synchronize()
+    assert torch.equal(got, want)
+
+
 # shapes whose last wave is split along K (stream-K tail): 64 / 192 / 1576
 # tiles of 256 x 256 over the pairs, and a K=8192 case with 3 pieces per tile
 SK_SHAPES = [(2048, 2048, 2048), (2048, 6144, 2048), (2048, 2048, 8192), (1024, 4000, 1000), (512, 50272, 256)]

@@ -340,3 +340,44 @@ def test_graph_replay_equals_eager(plan):
     sa.flush()
     sb.flush()
     assert torch.equal(a.theta, b.theta)
+
+
+@pytest.mark.parametrize("arch", ["zosim", "opt"])
+@pytest.mark.parametrize("graph", [False, True])
+def test_stacked_plan_is_bit_identical(arch, graph):
+    """Both directions as one launch per layer over stacked [+eps; -eps]
+    activations (zo_gemm_bf16_split / zo_layernorm_fwd_split, attention over
+    2B sequences) give exactly the two-stream plan's records and weights --
+    eager and graph-replayed, zosim and real-OPT (tied K-major head)."""
+    from paper_2507_03211_b200.model import OPTConfig
+
+    if arch == "opt":
+        cfg = OPTConfig(500, 128, 2, 2, 128, "f32", max_positions=130).validate()
+    else:
+        cfg = ModelConfig(500, 128, 2, 2, 128, "f32")
+    assert DeviceStore.stackable(2, 128)
+    a, b = DeviceStore(cfg, 7), DeviceStore(cfg, 7)
+    h = zo.ZoHyper(EPS, LR)
+    sa = zo.StreamingZo(a, h, graph=graph)
+    sb = zo.StreamingZo(b, h, overlap="stacked", graph=graph)
+    for j, s in enumerate(iteration_seeds(29, 4), 1):
+        batch = make_batch(cfg, 2, 900 + j)
+        ra, rb = sa.step(batch, s), sb.step(batch, s)
+        assert (ra.loss_pos, ra.loss_neg, ra.g) == (rb.loss_pos, rb.loss_neg, rb.g)
+    sa.flush()
+    sb.flush()
+    assert torch.equal(a.theta, b.theta)
+
+
+def test_stacked_plan_falls_back_when_rows_do_not_split():
+    """M = B*T not a multiple of 256: the stacked plan quietly runs the
+    two-stream plan (same results)."""
+    cfg, bsz, _ = _cfg("mid32")
+    assert not DeviceStore.stackable(bsz, cfg.seq_len)
+    a, b = DeviceStore(cfg, 7), DeviceStore(cfg, 7)
+    h = zo.ZoHyper(EPS, LR)
+    sa, sb = zo.StreamingZo(a, h), zo.StreamingZo(b, h, overlap="stacked")
+    for j, s in enumerate(iteration_seeds(31, 3), 1):
+        batch = _batch(cfg, bsz, 40 + j)
+        ra, rb = sa.step(batch, s), sb.step(batch, s)
+        assert (ra.loss_pos, ra.loss_neg, ra.g) == (rb.loss_pos, rb.loss_neg, rb.g)
