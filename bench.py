@@ -51,8 +51,8 @@ def _args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true", help="skip the public-API pass (profiling runs)")
     ap.add_argument("--no-graph", action="store_true", help="launch the step eagerly instead of replaying a CUDA graph")
-    ap.add_argument("--overlap", default="none", choices=["none", "blocks", "background", "stacked"],
-                    help="blocks: per-block perturb passes on a side stream ahead of the +eps forward; "
+    ap.add_argument("--overlap", default="stacked", choices=["none", "blocks", "background", "stacked"],
+                    help="none: the two forwards on two streams; blocks: per-block perturb passes on a side stream ahead of the +eps forward; "
                          "background: one co-resident perturb pass gated per block by device counters; "
                          "stacked: both directions as one launch per layer over stacked activations")
     return ap.parse_args()

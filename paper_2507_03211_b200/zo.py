@@ -150,13 +150,15 @@ class StreamingZo:
     one.  Numerically identical to repeated ``mezo_step`` after flush."""
 
     def __init__(self, store: DeviceStore, hyper: ZoHyper, mgr: RngStateManager | None = None,
-                 overlap: bool | str = False, graph: bool = True):
+                 overlap: bool | str = "stacked", graph: bool = True):
         self.store = store
         self.hyper = hyper.validate()
         self.mgr = mgr or RngStateManager()
-        # False: one fused pass, then the forwards; "blocks" (or True): per-block
-        # passes on a side stream gated by events; "background": one co-resident
-        # pass gated per block by device counters
+        # "stacked" (default): one fused pass, then both forwards as one launch
+        # per layer over stacked activations; False: the fused pass, then the
+        # two forwards on two streams; "blocks" (or True): per-block passes on a
+        # side stream gated by events; "background": one co-resident pass gated
+        # per block by device counters.  All plans give identical results.
         plan = {False: None, True: "blocks", "blocks": "blocks", "background": "background",
                 "stacked": "stacked"}[overlap]
         self.overlap = plan if not self.mgr.oracle else None

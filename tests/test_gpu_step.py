@@ -358,7 +358,7 @@ def test_stacked_plan_is_bit_identical(arch, graph):
     assert DeviceStore.stackable(2, 128)
     a, b = DeviceStore(cfg, 7), DeviceStore(cfg, 7)
     h = zo.ZoHyper(EPS, LR)
-    sa = zo.StreamingZo(a, h, graph=graph)
+    sa = zo.StreamingZo(a, h, overlap=False, graph=graph)
     sb = zo.StreamingZo(b, h, overlap="stacked", graph=graph)
     for j, s in enumerate(iteration_seeds(29, 4), 1):
         batch = make_batch(cfg, 2, 900 + j)
@@ -376,7 +376,7 @@ def test_stacked_plan_falls_back_when_rows_do_not_split():
     assert not DeviceStore.stackable(bsz, cfg.seq_len)
     a, b = DeviceStore(cfg, 7), DeviceStore(cfg, 7)
     h = zo.ZoHyper(EPS, LR)
-    sa, sb = zo.StreamingZo(a, h), zo.StreamingZo(b, h, overlap="stacked")
+    sa, sb = zo.StreamingZo(a, h, overlap=False), zo.StreamingZo(b, h, overlap="stacked")
     for j, s in enumerate(iteration_seeds(31, 3), 1):
         batch = _batch(cfg, bsz, 40 + j)
         ra, rb = sa.step(batch, s), sb.step(batch, s)

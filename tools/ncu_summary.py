@@ -22,9 +22,10 @@ def launches(path):
     hi = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
     h, data = rows[hi], rows[hi + 1:]
     ki, vi, ui = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
+    mi = h.index("Metric Name")
     agg = collections.defaultdict(lambda: [0, 0.0])
     for r in data:
-        if len(r) <= vi:
+        if len(r) <= vi or r[mi] != "gpu__time_duration.sum":    # launch lists may carry DRAM metrics too
             continue
         name = r[ki].split("(")[0].replace("void ", "")[:64]
         v = float(r[vi].replace(",", ""))
