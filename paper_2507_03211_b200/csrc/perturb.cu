@@ -17,8 +17,8 @@
 namespace zo {
 
 constexpr int kPuThreads = 128;   // small CTAs: one co-resides with a GEMM CTA per SM
-constexpr int kPuGroupsPerThread = 4;
-constexpr int64_t kPuTile = 32 * kPuGroupsPerThread * 4;  // elements per warp tile (512)
+constexpr int kPuGroupsPerThread = 4;   // 4-element groups per lane per tile
+constexpr int64_t kPuTile = 32 * kPuGroupsPerThread * 4;  // elements per warp tile (512 at G = 4)
 constexpr int kPuMaxSmemSegs = 4096;   // prefix entries staged in shared memory (32 KB)
 
 __device__ __forceinline__ void store_shadow(const ZoSegment& s, __nv_bfloat16* w, float* v,
