@@ -28,11 +28,22 @@ int tma_map_bf16(const void* ptr, int64_t inner, int64_t outer, int64_t ld, int 
 
 namespace {
 
-constexpr int kAttnThreads = 320;   // producer, MMA, 8 softmax warps (2 per TMEM lane quarter)
+// Softmax warps: 8 (2 per TMEM lane quarter, 64 key columns each) or 16 (4
+// per quarter, 32 key columns each: half the work per thread and twice the
+// warps per scheduler to hide the TMEM-load / exchange / MUFU latencies).
+#ifndef ZO_ATTN_SOFTMAX_WARPS
+#define ZO_ATTN_SOFTMAX_WARPS 8
+#endif
+constexpr int kSW = ZO_ATTN_SOFTMAX_WARPS;
+static_assert(kSW == 8 || kSW == 16, "softmax warps");
+constexpr int kNCG = kSW / 4;                // column groups per lane quarter
+constexpr int kKC = 128 / kNCG;              // key columns of S per softmax warp
+constexpr int kOC = 64 / kNCG;               // output (head-dim) columns per softmax warp
+constexpr int kAttnThreads = 64 + 32 * kSW;  // producer, MMA, softmax warps
 constexpr int kTileBytes = 128 * 64 * 2;     // 16 KB: 128 rows x 64 bf16 (Q, K, V tiles)
 constexpr int kPBytes = 128 * 128 * 2;       // 32 KB: P tile, two 64-key K-chunks
 #ifndef ZO_ATTN_KV_STAGES
-#define ZO_ATTN_KV_STAGES 4
+#define ZO_ATTN_KV_STAGES (kSW == 16 ? 3 : 4)
 #endif
 constexpr int kKV = ZO_ATTN_KV_STAGES;       // K/V ring depth (4: 226 KB of smem in total)
 // smem: Q[2] | K[kKV] | V[kKV] | P[2] | barriers
@@ -41,8 +52,12 @@ constexpr int kOffK = kOffQ + 2 * kTileBytes;
 constexpr int kOffV = kOffK + kKV * kTileBytes;
 constexpr int kOffP = kOffV + kKV * kTileBytes;
 constexpr int kOffBar = kOffP + 2 * kPBytes;
-constexpr int kOffRed = kOffBar + 256;                 // row-max / row-sum exchange [2][128] fp32
-constexpr int kAttnSmem = kOffRed + 2 * 128 * 4 + 1024;
+// row-max / row-sum exchange [kRedBufs][kNCG][128] fp32: parity-double-buffered
+// (one barrier per exchange) when it fits; 8 warps + 4 K/V stages use one
+// buffer and a second barrier
+constexpr int kRedBufs = (kOffBar + 256 + 2 * kNCG * 128 * 4 + 1024 <= 232448) ? 2 : 1;
+constexpr int kOffRed = kOffBar + 256;
+constexpr int kAttnSmem = kOffRed + kRedBufs * kNCG * 128 * 4 + 1024;
 static_assert(kAttnSmem <= 232448, "attention smem");
 
 struct AttnArgs {
@@ -89,9 +104,9 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     mbar_init(bar(0), 1); mbar_init(bar(1), 1); mbar_init(bar(18), 1); mbar_init(bar(19), 1);
     for (int i = 0; i < kKV; ++i) { mbar_init(kvfull(i), 1); mbar_init(kvempty(i), 1); }
     for (int i = 0; i < 2; ++i) {
-      mbar_init(bar(6 + i), 1); mbar_init(bar(8 + i), 8);
-      mbar_init(bar(10 + i), 8); mbar_init(bar(12 + i), 1);
-      mbar_init(bar(14 + i), 1); mbar_init(bar(16 + i), 8);
+      mbar_init(bar(6 + i), 1); mbar_init(bar(8 + i), kSW);
+      mbar_init(bar(10 + i), kSW); mbar_init(bar(12 + i), 1);
+      mbar_init(bar(14 + i), 1); mbar_init(bar(16 + i), kSW);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
@@ -208,13 +223,27 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     if (have_prev) issue_pv(prev_c, prev_kv);
   } else {
     // ================= softmax / output =================
-    // warp pair (quarter q, half h): rows 32q..32q+31, key columns [64h, 64h+64)
-    // of S, output columns [32h, 32h+32).  Only the row max is exchanged.
-    const int quarter = warp & 3, half = (warp - 2) >> 2;
+    // warp (quarter q, column group cg): rows 32q..32q+31, key columns
+    // [kKC*cg, +kKC) of S, output columns [kOC*cg, +kOC).  The row max and the
+    // final row sum are exchanged between the kNCG warps of a quarter through a
+    // parity-double-buffered shared array: one named barrier per exchange.
+    const int quarter = warp & 3, cg = (warp - 2) >> 2;
     const int r = quarter * 32 + lane;
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
-    float* red = reinterpret_cast<float*>(gbase + kOffRed);   // [2][128]
-    auto pair_sync = [&]() { asm volatile("bar.sync %0, 64;\n" ::"r"(1 + quarter) : "memory"); };
+    float* red = reinterpret_cast<float*>(gbase + kOffRed);   // [kRedBufs][kNCG][128]
+    auto group_sync = [&]() { asm volatile("bar.sync %0, %1;\n" ::"r"(1 + quarter), "r"(kNCG * 32) : "memory"); };
+    uint32_t par = 0;
+    auto exchange = [&](float v, bool is_max) {
+      float* rb = red + par * (kNCG * 128);
+      rb[cg * 128 + r] = v;
+      group_sync();
+      float t = rb[r];
+#pragma unroll
+      for (int g = 1; g < kNCG; ++g) t = is_max ? fmaxf(t, rb[g * 128 + r]) : t + rb[g * 128 + r];
+      if constexpr (kRedBufs == 2) par ^= 1u;
+      else group_sync();                        // all read before the next exchange overwrites
+      return t;
+    };
     uint32_t sc = 0;
     for (int it = blockIdx.x; it < a.items; it += gridDim.x) {
       int qt, h, b;
@@ -222,19 +251,19 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       const int nkb = n_blocks(qt);
       const int qi = qt * 128 + r;
       float m = -INFINITY, l = 0.f, alpha_prev = 0.f;
-      float o[32];
+      float o[kOC];
 #pragma unroll
-      for (int i = 0; i < 32; ++i) o[i] = 0.f;
+      for (int i = 0; i < kOC; ++i) o[i] = 0.f;
       // O <- O * alpha_c + PV_c  (alpha_c rescales O to block c's running max)
       auto accumulate_pv = [&](uint32_t cc, float al) {
         const uint32_t pb = cc & 1u, pph = (cc >> 1) & 1u;
         mbar_wait(bar(14 + pb), pph);
         tc_fence_after();
-        uint32_t pv[32];
-        tmem_ld_32x32b_x32_nw(tmem + 256 + pb * 64 + half * 32 + lane_off, pv);
+        uint32_t pv[kOC];
+        tmem_ld_nw(tmem + 256 + pb * 64 + cg * kOC + lane_off, pv);
         tmem_wait_ld();
 #pragma unroll
-        for (int i = 0; i < 32; ++i) o[i] = fmaf(o[i], al, __uint_as_float(pv[i]));
+        for (int i = 0; i < kOC; ++i) o[i] = fmaf(o[i], al, __uint_as_float(pv[i]));
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(bar(16 + pb));
@@ -244,39 +273,40 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         const bool need_mask = (j * 128 + 127 > qt * 128) || ((j + 1) * 128 > a.seq);
         mbar_wait(bar(6 + sb), ph);
         tc_fence_after();
-        uint32_t sv[2][32];
-        tmem_ld_32x32b_x32_nw(tmem + sb * 128 + half * 64 + lane_off, sv[0]);
-        tmem_ld_32x32b_x32_nw(tmem + sb * 128 + half * 64 + 32 + lane_off, sv[1]);
+        constexpr int NCH = kKC / 32;
+        uint32_t sv[NCH][32];
+#pragma unroll
+        for (int ch = 0; ch < NCH; ++ch)
+          tmem_ld_32x32b_x32_nw(tmem + sb * 128 + cg * kKC + ch * 32 + lane_off, sv[ch]);
         tmem_wait_ld();
         if (need_mask) {
 #pragma unroll
-          for (int ch = 0; ch < 2; ++ch)
+          for (int ch = 0; ch < NCH; ++ch)
 #pragma unroll
             for (int i = 0; i < 32; ++i) {
-              const int ki = j * 128 + half * 64 + ch * 32 + i;
+              const int ki = j * 128 + cg * kKC + ch * 32 + i;
               if (!(ki <= qi && ki < a.seq)) sv[ch][i] = __float_as_uint(-INFINITY);
             }
         }
         float mx0 = -INFINITY, mx1 = -INFINITY;
 #pragma unroll
-        for (int ch = 0; ch < 2; ++ch)
+        for (int ch = 0; ch < NCH; ++ch)
 #pragma unroll
           for (int i = 0; i < 32; i += 2) {
             mx0 = fmaxf(mx0, __uint_as_float(sv[ch][i]));
             mx1 = fmaxf(mx1, __uint_as_float(sv[ch][i + 1]));
           }
-        red[half * 128 + r] = fmaxf(mx0, mx1);
-        pair_sync();
-        const float mx = fmaxf(red[r], red[128 + r]);
-        pair_sync();                              // both read before the next block overwrites
+        const float mx = exchange(fmaxf(mx0, mx1), true);
         const float m_new = fmaxf(m, mx);
         const float mb = m_new == -INFINITY ? 0.f : m_new * a.sl2;
         const float alpha = m == -INFINITY ? 0.f : ex2_approx(fmaf(m, a.sl2, -mb));
         mbar_wait(bar(12 + sb), ph ^ 1u);         // P buffer free
         float sum0 = 0.f, sum1 = 0.f;
-        const uint32_t region = sP + sb * kPBytes + half * kTileBytes + r * 128;   // this half's K-chunk
+        // this warp's keys: 64-key K-chunk (cg * kKC) / 64, 16-B units from ((cg * kKC) % 64) / 8
+        const uint32_t region = sP + sb * kPBytes + ((cg * kKC) >> 6) * kTileBytes + r * 128;
+        const int unit0 = ((cg * kKC) & 63) >> 3;
 #pragma unroll
-        for (int ch = 0; ch < 2; ++ch) {
+        for (int ch = 0; ch < NCH; ++ch) {
           uint32_t pk[16];
 #pragma unroll
           for (int i = 0; i < 32; i += 2) {
@@ -289,8 +319,8 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
           }
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
-            const int chunk = ch * 4 + q;
-            const uint32_t addr = region + ((chunk ^ (r & 7)) << 4);
+            const int unit = unit0 + ch * 4 + q;
+            const uint32_t addr = region + ((unit ^ (r & 7)) << 4);
             asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};\n" ::"r"(addr), "r"(pk[4 * q]),
                          "r"(pk[4 * q + 1]), "r"(pk[4 * q + 2]), "r"(pk[4 * q + 3])
                          : "memory");
@@ -300,7 +330,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) { mbar_arrive(bar(8 + sb)); mbar_arrive(bar(10 + sb)); }   // S read, P written
-        l = fmaf(l, alpha, sum0 + sum1);          // this half's running sum
+        l = fmaf(l, alpha, sum0 + sum1);          // this warp's running sum over its key columns
         m = m_new;
         // deferred: fold PV of the PREVIOUS block (ready while we computed this one)
         if (j > 0) accumulate_pv(c - 1, alpha_prev);
@@ -308,15 +338,12 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       }
       accumulate_pv(sc + nkb - 1, alpha_prev);
       sc += nkb;
-      red[half * 128 + r] = l;
-      pair_sync();
-      const float lt = red[r] + red[128 + r];
-      pair_sync();
+      const float lt = exchange(l, false);
       if (qi < a.seq) {
         const float inv = lt > 0.f ? 1.f / lt : 0.f;
-        __nv_bfloat16* out = a.ctx + ((int64_t)b * a.seq + qi) * a.ldc + (int64_t)h * 64 + half * 32;
+        __nv_bfloat16* out = a.ctx + ((int64_t)b * a.seq + qi) * a.ldc + (int64_t)h * 64 + cg * kOC;
 #pragma unroll
-        for (int i = 0; i < 32; i += 8) {
+        for (int i = 0; i < kOC; i += 8) {
           uint32_t pk[4];
 #pragma unroll
           for (int k = 0; k < 4; ++k) {

@@ -433,9 +433,9 @@ __global__ void __maxnreg__(88) perturb_update_bg_kernel(const PuParams p) {
 int perturb_update_launch(const PuParams& p, int zmode, cudaStream_t stream, bool background) {
   if (p.n_tiles <= 0) return ZO_OK;
   static const int occ = [] { const char* e = getenv("ZO_PU_OCC"); return e ? atoi(e) : 4; }();
-  static const int waves = [] { const char* e = getenv("ZO_PU_WAVES"); return e ? atoi(e) : 2; }();
+  static const int waves = [] { const char* e = getenv("ZO_PU_WAVES"); return e ? atoi(e) : 4; }();
   static const int bg_ctas = [] { const char* e = getenv("ZO_PU_BG_CTAS"); return e ? atoi(e) : 1; }();
-  // two resident waves of chunks: late-starting CTAs even out the tail;
+  // four resident waves of chunks (measured best of 1/2/4): late-starting CTAs even out the tail;
   // the background pass keeps bg_ctas CTAs per SM beside the forward's kernels
   const int64_t want = (int64_t)num_sms() * (background ? bg_ctas : occ * waves);
   const int grid = (int)(p.n_tiles < want ? p.n_tiles : want);

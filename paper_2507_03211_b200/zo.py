@@ -330,7 +330,9 @@ class StreamingZo:
         self.mgr.pop_state()
         s = self.store
         zmode = L.ZO_Z_ORACLE if self.mgr.oracle else L.ZO_Z_PHILOX
-        s.scal[3:4].fill_(1)
+        # the update uses self.g_prev like zo.py:287-293 (equal to the device's
+        # lr*g unless the caller replaced it; both are the same f64 product)
+        s.set_pending(self.hyper.lr * self.g_prev, self.last_seed, True)
         s.run(s.perturb_call(s.model_table, L.ZO_PU_UPDATE, 0.0, 0.0, sa=None, sb=None, zmode=zmode,
                              z_prev=self._z_prev))
         s.scal[3:4].fill_(0)

@@ -84,3 +84,15 @@ def test_run_outputs_and_mezo_equals_zo2(tmp_path):
     a, b = reps["mezo"], reps["zo2"]
     assert [(s.loss_pos, s.loss_neg, s.g) for s in a.steps] == [(s.loss_pos, s.loss_neg, s.g) for s in b.steps]
     assert a.final_checksum == b.final_checksum
+
+
+def test_hyper_validation():
+    """pkg/tests/test_zo_core.py:328-334."""
+    from paper_2507_03211_b200.errors import NumericError
+
+    with pytest.raises(NumericError):
+        ZoHyper(epsilon=0.0, lr=1e-2).validate()
+    with pytest.raises(NumericError):
+        ZoHyper(epsilon=1e-3, lr=0.0).validate()
+    with pytest.raises(NumericError):
+        ZoHyper(epsilon=1e-3, lr=1e-2, steps=0).validate()
