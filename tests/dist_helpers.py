@@ -218,3 +218,59 @@ def sharded_worker(rank, world, port, strategy, steps, init_kind, q):
     nbytes = shards.shard_bytes
     dist.destroy_process_group()
     q.put((rank, recs, theta, init_master, nbytes))
+
+
+def gpu_strategy_edge_worker(rank, world, port, case, q):
+    """Edge contracts of the strategies (pkg/tests/test_strategies.py:114-232,
+    321-326) on the GPU path, all ranks on cuda:0 with gloo."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2507_03211_b200 import zo
+    from paper_2507_03211_b200.engine import DeviceStore
+    from paper_2507_03211_b200.errors import ConfigurationError, ConsistencyError
+    from paper_2507_03211_b200.fabric import TorchFabric
+    from paper_2507_03211_b200.model import ModelConfig, make_batch
+    from paper_2507_03211_b200.rng import RngStateManager, iteration_seeds
+    from paper_2507_03211_b200.strategies import ddp_step, mesh_assignments, pertp_step, twod_step
+
+    torch.cuda.set_device(0)
+    init(rank, world, port)
+    fab = TorchFabric()
+    cfg = ModelConfig(16, 16, 2, 2, 8, "f32")
+    hyper = zo.ZoHyper(1e-3, 1e-2)
+    store = DeviceStore(cfg, init_seed=7)
+    out = {}
+    try:
+        if case == "divergence":
+            pertp_step(fab, rank, store, make_batch(cfg, 4, 3), hyper, 11 if rank == 0 else None)
+            if rank == 1:
+                store.theta[5] += 1e-3          # silent corruption on one replica
+            try:
+                pertp_step(fab, rank, store, make_batch(cfg, 4, 4), hyper, 12 if rank == 0 else None, iteration=2)
+                out["raised"] = None
+            except ConsistencyError:
+                out["raised"] = "ConsistencyError"
+        elif case == "traffic":
+            for j, s in enumerate(iteration_seeds(1, 3), 1):
+                ddp_step(fab, rank, store, make_batch(cfg, 8, j).shard(world, rank), hyper,
+                         s if rank == 0 else None, RngStateManager(), iteration=j)
+            out["bytes"] = dict(fab.bytes_by_tag)
+        elif case == "k1":
+            batch = make_batch(cfg, 4, 3)
+            r = ddp_step(fab, rank, store, batch.shard(1, 0), hyper, 21)
+            ref = DeviceStore(cfg, init_seed=7)
+            rr = zo.mezo_step(ref, batch, hyper, 21)
+            out["same"] = (r.g == rr.g) and bool(torch.equal(store.theta, ref.theta))
+        elif case == "wrong_count":
+            for name, fn in (("pertp", lambda: pertp_step(fab, rank, store, make_batch(cfg, 4, 3), hyper, 1)),
+                             ("twod", lambda: twod_step(fab, rank, mesh_assignments(2)[0], store,
+                                                        make_batch(cfg, 4, 1), hyper, 1))):
+                try:
+                    fn()
+                    out[name] = None
+                except ConfigurationError:
+                    out[name] = "ConfigurationError"
+    finally:
+        dist.destroy_process_group()
+    q.put((rank, out))

@@ -70,3 +70,30 @@ def test_pertp_oracle_mode_against_reference_fixture(golden):
     zmax = max(float(np.abs(np.concatenate(O.z_stream(s, om.sizes))).max()) for s in O.iteration_seeds(5, 3))
     diff = np.abs(res[0][3].astype(np.float64) - np.concatenate(om.blocks)).max()
     assert diff <= 3 * 1e-2 * dg * zmax + 1e-6
+
+
+def test_replica_divergence_is_detected():
+    """test_strategies.py:121-140: a silently corrupted replica makes the
+    post-step replica check raise ConsistencyError on every rank."""
+    res = H.run(H.gpu_strategy_edge_worker, 2, "divergence")
+    assert [r[1]["raised"] for r in res] == ["ConsistencyError", "ConsistencyError"]
+
+
+def test_ddp_gradient_traffic_is_k_scalars_per_iteration():
+    """test_strategies.py:200-215: only 8 B of g per rank per iteration move
+    (plus the seed broadcast and the replica checksum); no parameter bytes."""
+    res = H.run(H.gpu_strategy_edge_worker, 4, "traffic")
+    assert sum(r[1]["bytes"]["grad"] for r in res) == 3 * 4 * 8
+    assert all(r[1]["bytes"].get("param", 0) == 0 for r in res)
+
+
+def test_ddp_k1_equals_eager():
+    """test_strategies.py:218-226."""
+    res = H.run(H.gpu_strategy_edge_worker, 1, "k1")
+    assert res[0][1]["same"]
+
+
+def test_wrong_worker_counts_are_configuration_errors():
+    """test_strategies.py:114-118 and 321-326 (3 ranks)."""
+    res = H.run(H.gpu_strategy_edge_worker, 3, "wrong_count")
+    assert all(r[1] == {"pertp": "ConfigurationError", "twod": "ConfigurationError"} for r in res)
