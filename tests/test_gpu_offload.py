@@ -108,3 +108,46 @@ def test_hbm_sharded_single_rank_equals_resident():
         assert (r.loss_pos, r.loss_neg, r.g) == recs[j - 1]
     rt.flush()
     assert np.array_equal(shards.gather_master(), final)
+
+
+def test_offload_flush_then_continue_and_single_block():
+    """test_offload.py: flush, keep stepping, flush again == resident; and a
+    one-transformer-block model degenerates to a valid schedule."""
+    for cfg in (DEEP, ModelConfig(64, 32, 4, 1, 16, "f32")):
+        recs, _, final = _resident(cfg, 4, flush=False)
+        st = DeviceStore(cfg, 7)
+        sz = zo.StreamingZo(st, zo.ZoHyper(EPS, LR))
+        host = HostStore(cfg, 7)
+        rt = OffloadedZo(host, zo.ZoHyper(EPS, LR), batch=2)
+        for j, s in enumerate(iteration_seeds(9, 4), 1):
+            batch = make_batch(cfg, 2, 40 + j)
+            a, b = sz.step(batch, s), rt.step(batch, s)
+            assert (a.loss_pos, a.loss_neg, a.g) == (b.loss_pos, b.loss_neg, b.g) == recs[j - 1]
+            if j == 2:
+                sz.flush()
+                rt.flush()
+                assert np.array_equal(host.theta.numpy(), st.theta.cpu().numpy())
+        sz.flush()
+        rt.flush()
+        assert np.array_equal(host.theta.numpy(), st.theta.cpu().numpy())
+
+
+def test_streamed_peak_is_independent_of_depth():
+    """test_offload.py:187-194 in bytes: the device footprint of the offload
+    runtime is the persistent embedding / head + 3 block slots, so doubling
+    the number of streamed blocks does not raise the allocation peak."""
+    peaks = []
+    for n in (4, 8):
+        cfg = ModelConfig(256, 128, 4, n, 32, "f32")
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
+        base = torch.cuda.memory_allocated()
+        torch.cuda.reset_peak_memory_stats()
+        rt = OffloadedZo(HostStore(cfg, 7), zo.ZoHyper(EPS, LR), batch=2)
+        for j, s in enumerate(iteration_seeds(3, 2), 1):
+            rt.step(make_batch(cfg, 2, j), s)
+        rt.flush()
+        peaks.append(torch.cuda.max_memory_allocated() - base)
+        del rt
+    blk = (12 * 128 * 128 + 13 * 128) * 4
+    assert abs(peaks[1] - peaks[0]) < blk          # no growth with depth
