@@ -1,5 +1,5 @@
 // Causal attention on the 5th-generation tensor cores (src/zosim/model.py:
-// 325-332), head_dim 64.  One CTA per SM, persistent over (query tile of 128,
+// 325-332), head_dim 64 or 128.  One CTA per SM, persistent over (query tile of 128,
 // head, batch) work items, heaviest (latest) query tiles first.
 //
 //   warp 0      TMA producer: Q tile (once per item), K/V blocks of 128 keys
@@ -38,31 +38,42 @@ constexpr int kSW = ZO_ATTN_SOFTMAX_WARPS;
 static_assert(kSW == 8 || kSW == 16, "softmax warps");
 constexpr int kNCG = kSW / 4;                // column groups per lane quarter
 constexpr int kKC = 128 / kNCG;              // key columns of S per softmax warp
-constexpr int kOC = 64 / kNCG;               // output (head-dim) columns per softmax warp
 constexpr int kAttnThreads = 64 + 32 * kSW;  // producer, MMA, softmax warps
-constexpr int kTileBytes = 128 * 64 * 2;     // 16 KB: 128 rows x 64 bf16 (Q, K, V tiles)
+constexpr int kChunkBytes = 128 * 64 * 2;    // 16 KB: 128 rows x 64 bf16, one SW128 K-chunk
 constexpr int kPBytes = 128 * 128 * 2;       // 32 KB: P tile, two 64-key K-chunks
-#ifndef ZO_ATTN_KV_STAGES
-#define ZO_ATTN_KV_STAGES (kSW == 16 ? 3 : 4)
+
+// Per-head-dim layout.  hd 64: Q[2] | K[kKV] | V[kKV] | P[2], 4 K/V stages
+// (3 with 16 softmax warps).  hd 128: every Q/K/V tile is two 64-column
+// chunks (32 KB); Q single-buffered, 2 K/V stages: 224 KB.  TMEM: S[2] in
+// columns [0, 256), PV[2] (hd columns each) from column 256.
+template <int HD>
+struct AttnCfg {
+  static constexpr int kTile = 128 * HD * 2;                 // Q / K / V tile bytes
+  static constexpr int kChunks = HD / 64;                    // 64-column SW128 chunks per tile
+  static constexpr int kQB = HD == 64 ? 2 : 1;               // Q buffers
+#ifdef ZO_ATTN_KV_STAGES
+  static constexpr int kKV = ZO_ATTN_KV_STAGES;
+#else
+  static constexpr int kKV = HD == 64 ? (kSW == 16 ? 3 : 4) : 2;
 #endif
-constexpr int kKV = ZO_ATTN_KV_STAGES;       // K/V ring depth (4: 226 KB of smem in total)
-// smem: Q[2] | K[kKV] | V[kKV] | P[2] | barriers
-constexpr int kOffQ = 0;
-constexpr int kOffK = kOffQ + 2 * kTileBytes;
-constexpr int kOffV = kOffK + kKV * kTileBytes;
-constexpr int kOffP = kOffV + kKV * kTileBytes;
-constexpr int kOffBar = kOffP + 2 * kPBytes;
-// row-max / row-sum exchange [kRedBufs][kNCG][128] fp32: parity-double-buffered
-// (one barrier per exchange) when it fits; 8 warps + 4 K/V stages use one
-// buffer and a second barrier
-constexpr int kRedBufs = (kOffBar + 256 + 2 * kNCG * 128 * 4 + 1024 <= 232448) ? 2 : 1;
-constexpr int kOffRed = kOffBar + 256;
-constexpr int kAttnSmem = kOffRed + kRedBufs * kNCG * 128 * 4 + 1024;
-static_assert(kAttnSmem <= 232448, "attention smem");
+  static constexpr int kOC = HD / kNCG;                      // output columns per softmax warp
+  static constexpr int kOffQ = 0;
+  static constexpr int kOffK = kOffQ + kQB * kTile;
+  static constexpr int kOffV = kOffK + kKV * kTile;
+  static constexpr int kOffP = kOffV + kKV * kTile;
+  static constexpr int kOffBar = kOffP + 2 * kPBytes;
+  // row-max / row-sum exchange [kRedBufs][kNCG][128] fp32: parity-double-buffered
+  // (one barrier per exchange) when it fits, else one buffer and a second barrier
+  static constexpr int kRedBufs = (kOffBar + 256 + 2 * kNCG * 128 * 4 + 1024 <= 232448) ? 2 : 1;
+  static constexpr int kOffRed = kOffBar + 256;
+  static constexpr int kSmem = kOffRed + kRedBufs * kNCG * 128 * 4 + 1024;
+  static_assert(kSmem <= 232448, "attention smem");
+  static_assert(8 * (20 + 2 * kKV) + 4 <= 256, "barrier area");
+};
 
 struct AttnArgs {
   int batch, seq, heads, ldc;
-  int64_t d;            // heads * 64
+  int64_t d;            // heads * head_dim
   int n_qt;             // query tiles per sequence
   int items;
   float sl2;            // log2(e) / sqrt(hd)
@@ -79,14 +90,17 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
 }
 
+template <int HD>
 __global__ void __launch_bounds__(kAttnThreads, 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tm, const AttnArgs a) {
+  using C = AttnCfg<HD>;
+  constexpr int kKV = C::kKV, kOC = C::kOC, kTile = C::kTile, kCh = C::kChunks;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;
   uint8_t* gbase = smem_raw + (base - raw);
-  const uint32_t sQ = base + kOffQ, sK = base + kOffK, sV = base + kOffV, sP = base + kOffP;
-  const uint32_t bars = base + kOffBar;
+  const uint32_t sQ = base + C::kOffQ, sK = base + C::kOffK, sV = base + C::kOffV, sP = base + C::kOffP;
+  const uint32_t bars = base + C::kOffBar;
   // barriers: 0 q_full0, 1 q_empty0, 6-7 s_full, 8-9 s_empty, 10-11 p_full, 12-13 p_empty,
   //           14-15 pv_full, 16-17 pv_empty, 18 q_full1, 19 q_empty1,
   //           20.. kv_full[kKV], 20+kKV.. kv_empty[kKV]
@@ -95,8 +109,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   auto qempty = [&](uint32_t qb) { return bar(qb ? 19 : 1); };
   auto kvfull = [&](uint32_t st) { return bar(20 + (int)st); };
   auto kvempty = [&](uint32_t st) { return bar(20 + kKV + (int)st); };
-  static_assert(8 * (20 + 2 * kKV) + 4 <= 256, "barrier area");
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + kOffBar + 8 * (20 + 2 * kKV));
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + C::kOffBar + 8 * (20 + 2 * kKV));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (warp == 0 && lane == 0) {
@@ -143,27 +156,35 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         int qt, h, b;
         item_coords(it, qt, h, b);
         const int row0 = b * a.seq;
-        const uint32_t qb = it_local & 1u, qph = (it_local >> 1) & 1u;
+        const uint32_t qb = it_local % C::kQB, qph = (it_local / C::kQB) & 1u;
         mbar_wait(qempty(qb), qph ^ 1u);
-        mbar_expect_tx(qfull(qb), kTileBytes);
-        tma_load_2d(sQ + qb * kTileBytes, &tm, qfull(qb), h * 64, row0 + qt * 128);
+        mbar_expect_tx(qfull(qb), kTile);
+#pragma unroll
+        for (int ch = 0; ch < kCh; ++ch)
+          tma_load_2d(sQ + qb * kTile + ch * kChunkBytes, &tm, qfull(qb), h * HD + ch * 64, row0 + qt * 128);
         const int nkb = n_blocks(qt);
         for (int j = 0; j < nkb; ++j, ++kvc) {
           const uint32_t st = kvc % kKV, ph = (kvc / kKV) & 1u;
           mbar_wait(kvempty(st), ph ^ 1u);
-          mbar_expect_tx(kvfull(st), 2 * kTileBytes);
-          tma_load_2d(sK + st * kTileBytes, &tm, kvfull(st), (int)(a.d + h * 64), row0 + j * 128);
-          tma_load_2d(sV + st * kTileBytes, &tm, kvfull(st), (int)(2 * a.d + h * 64), row0 + j * 128);
+          mbar_expect_tx(kvfull(st), 2 * kTile);
+#pragma unroll
+          for (int ch = 0; ch < kCh; ++ch) {
+            tma_load_2d(sK + st * kTile + ch * kChunkBytes, &tm, kvfull(st), (int)(a.d + h * HD + ch * 64),
+                        row0 + j * 128);
+            tma_load_2d(sV + st * kTile + ch * kChunkBytes, &tm, kvfull(st), (int)(2 * a.d + h * HD + ch * 64),
+                        row0 + j * 128);
+          }
         }
       }
     }
   } else if (warp == 1) {
     // ================= MMA issuer =================
-    // S: A = Q (K-major), B = K (K-major), M=N=128.  PV: A = P (K-major),
-    // B = V (MN-major: hd contiguous), M=128, N=64.
+    // S: A = Q (K-major), B = K (K-major), M=N=128, K = hd in 64-column chunks.
+    // PV: A = P (K-major), B = V (MN-major: hd contiguous, 64-wide N chunks
+    // 16 KB apart), M=128, N=hd.
     const uint32_t idesc_s = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(128 >> 3) << 17) |
                              ((uint32_t)(128 >> 4) << 24);
-    const uint32_t idesc_pv = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) | ((uint32_t)(64 >> 3) << 17) |
+    const uint32_t idesc_pv = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) | ((uint32_t)(HD >> 3) << 17) |
                               ((uint32_t)(128 >> 4) << 24);
     uint32_t kvc = 0, sc = 0, it_local = 0;
     auto issue_pv = [&](uint32_t c, uint32_t kv) {
@@ -174,9 +195,9 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       if (lane == 0) {
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {         // 128 keys = 8 x K16
-          const uint64_t ad = desc_sw128(sP + pb * kPBytes + (kk >> 2) * kTileBytes + (kk & 3) * 32, 16, 1024);
-          const uint64_t bd = desc_sw128(sV + st * kTileBytes + kk * 2048, 8192, 1024);
-          tc_mma_f16(tmem + 256 + pb * 64, ad, bd, idesc_pv, kk != 0 ? 1u : 0u);
+          const uint64_t ad = desc_sw128(sP + pb * kPBytes + (kk >> 2) * kChunkBytes + (kk & 3) * 32, 16, 1024);
+          const uint64_t bd = desc_sw128(sV + st * kTile + kk * 2048, kChunkBytes, 1024);
+          tc_mma_f16(tmem + 256 + pb * HD, ad, bd, idesc_pv, kk != 0 ? 1u : 0u);
         }
         tc_commit(bar(14 + pb));                  // PV ready
         tc_commit(kvempty(st));                   // K/V stage free
@@ -193,8 +214,8 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       int qt, h, b;
       item_coords(it, qt, h, b);
       const int nkb = n_blocks(qt);
-      const uint32_t qb = it_local & 1u;
-      mbar_wait(qfull(qb), (it_local >> 1) & 1u);
+      const uint32_t qb = it_local % C::kQB;
+      mbar_wait(qfull(qb), (it_local / C::kQB) & 1u);
       for (int j = 0; j < nkb; ++j) {
         const uint32_t c = sc + j, kv = kvc + j;
         const uint32_t sb = c & 1u, ph = (c >> 1) & 1u;
@@ -203,9 +224,10 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         tc_fence_after();
         if (lane == 0) {
 #pragma unroll
-          for (int kk = 0; kk < 4; ++kk) {
-            const uint64_t ad = desc_sw128(sQ + qb * kTileBytes + kk * 32, 16, 1024);
-            const uint64_t bd = desc_sw128(sK + (kv % kKV) * kTileBytes + kk * 32, 16, 1024);
+          for (int kk = 0; kk < HD / 16; ++kk) {     // K16 steps; 4 per 64-column chunk
+            const uint32_t off = (kk >> 2) * kChunkBytes + (kk & 3) * 32;
+            const uint64_t ad = desc_sw128(sQ + qb * kTile + off, 16, 1024);
+            const uint64_t bd = desc_sw128(sK + (kv % kKV) * kTile + off, 16, 1024);
             tc_mma_f16(tmem + sb * 128, ad, bd, idesc_s, kk != 0 ? 1u : 0u);
           }
           tc_commit(bar(6 + sb));                 // S ready
@@ -230,7 +252,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     const int quarter = warp & 3, cg = (warp - 2) >> 2;
     const int r = quarter * 32 + lane;
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
-    float* red = reinterpret_cast<float*>(gbase + kOffRed);   // [kRedBufs][kNCG][128]
+    float* red = reinterpret_cast<float*>(gbase + C::kOffRed);   // [kRedBufs][kNCG][128]
     auto group_sync = [&]() { asm volatile("bar.sync %0, %1;\n" ::"r"(1 + quarter), "r"(kNCG * 32) : "memory"); };
     uint32_t par = 0;
     auto exchange = [&](float v, bool is_max) {
@@ -240,7 +262,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       float t = rb[r];
 #pragma unroll
       for (int g = 1; g < kNCG; ++g) t = is_max ? fmaxf(t, rb[g * 128 + r]) : t + rb[g * 128 + r];
-      if constexpr (kRedBufs == 2) par ^= 1u;
+      if constexpr (C::kRedBufs == 2) par ^= 1u;
       else group_sync();                        // all read before the next exchange overwrites
       return t;
     };
@@ -259,11 +281,15 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         const uint32_t pb = cc & 1u, pph = (cc >> 1) & 1u;
         mbar_wait(bar(14 + pb), pph);
         tc_fence_after();
-        uint32_t pv[kOC];
-        tmem_ld_nw(tmem + 256 + pb * 64 + cg * kOC + lane_off, pv);
+        constexpr int W = kOC < 32 ? kOC : 32;     // TMEM load width
+        uint32_t pv[kOC / W][W];
+#pragma unroll
+        for (int q = 0; q < kOC / W; ++q) tmem_ld_nw(tmem + 256 + pb * HD + cg * kOC + q * W + lane_off, pv[q]);
         tmem_wait_ld();
 #pragma unroll
-        for (int i = 0; i < kOC; ++i) o[i] = fmaf(o[i], al, __uint_as_float(pv[i]));
+        for (int q = 0; q < kOC / W; ++q)
+#pragma unroll
+          for (int i = 0; i < W; ++i) o[q * W + i] = fmaf(o[q * W + i], al, __uint_as_float(pv[q][i]));
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(bar(16 + pb));
@@ -303,7 +329,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         mbar_wait(bar(12 + sb), ph ^ 1u);         // P buffer free
         float sum0 = 0.f, sum1 = 0.f;
         // this warp's keys: 64-key K-chunk (cg * kKC) / 64, 16-B units from ((cg * kKC) % 64) / 8
-        const uint32_t region = sP + sb * kPBytes + ((cg * kKC) >> 6) * kTileBytes + r * 128;
+        const uint32_t region = sP + sb * kPBytes + ((cg * kKC) >> 6) * kChunkBytes + r * 128;
         const int unit0 = ((cg * kKC) & 63) >> 3;
 #pragma unroll
         for (int ch = 0; ch < NCH; ++ch) {
@@ -341,7 +367,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       const float lt = exchange(l, false);
       if (qi < a.seq) {
         const float inv = lt > 0.f ? 1.f / lt : 0.f;
-        __nv_bfloat16* out = a.ctx + ((int64_t)b * a.seq + qi) * a.ldc + (int64_t)h * 64 + cg * kOC;
+        __nv_bfloat16* out = a.ctx + ((int64_t)b * a.seq + qi) * a.ldc + (int64_t)h * HD + cg * kOC;
 #pragma unroll
         for (int i = 0; i < kOC; i += 8) {
           uint32_t pk[4];
@@ -362,18 +388,17 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   }
 }
 
-}  // namespace
-
-// head_dim 64, qkv / ctx leading dims multiples of 8, 16-byte aligned.
-int attention_tc_launch(const __nv_bfloat16* qkv, int64_t ldq, int64_t batch, int64_t seq, int64_t heads,
-                        __nv_bfloat16* ctx, int64_t ldc, cudaStream_t st) {
+template <int HD>
+int attention_tc_launch_t(const __nv_bfloat16* qkv, int64_t ldq, int64_t batch, int64_t seq, int64_t heads,
+                          __nv_bfloat16* ctx, int64_t ldc, cudaStream_t st) {
+  using C = AttnCfg<HD>;
   CUtensorMap tm;
   const int64_t rows = batch * seq;
-  int rc = tma_map_bf16(qkv, 3 * heads * 64, rows, ldq, 64, 128, &tm);
+  int rc = tma_map_bf16(qkv, 3 * heads * HD, rows, ldq, 64, 128, &tm);
   if (rc) return rc;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kAttnSmem);
+    cudaError_t e = cudaFuncSetAttribute(attn_tc_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
     if (e != cudaSuccess) { set_error("attn_tc smem attribute: %s", cudaGetErrorString(e)); return ZO_ERR_CUDA; }
     attr = true;
   }
@@ -382,14 +407,23 @@ int attention_tc_launch(const __nv_bfloat16* qkv, int64_t ldq, int64_t batch, in
   a.seq = (int)seq;
   a.heads = (int)heads;
   a.ldc = (int)ldc;
-  a.d = heads * 64;
+  a.d = heads * HD;
   a.n_qt = (int)((seq + 127) / 128);
   a.items = a.n_qt * (int)(batch * heads);
-  a.sl2 = 1.4426950408889634f / 8.0f;   // log2(e) / sqrt(64)
+  a.sl2 = 1.4426950408889634f / sqrtf((float)HD);   // log2(e) / sqrt(hd)
   a.ctx = ctx;
   const int grid = a.items < num_sms() ? a.items : num_sms();
-  launch_k(attn_tc_kernel, dim3(grid), dim3(kAttnThreads), kAttnSmem, st, tm, a);
+  launch_k(attn_tc_kernel<HD>, dim3(grid), dim3(kAttnThreads), C::kSmem, st, tm, a);
   return launch_status("attn_tc_kernel");
+}
+
+}  // namespace
+
+// head_dim 64 or 128, qkv / ctx leading dims multiples of 8, 16-byte aligned.
+int attention_tc_launch(const __nv_bfloat16* qkv, int64_t ldq, int64_t batch, int64_t seq, int64_t heads,
+                        int64_t hd, __nv_bfloat16* ctx, int64_t ldc, cudaStream_t st) {
+  if (hd == 128) return attention_tc_launch_t<128>(qkv, ldq, batch, seq, heads, ctx, ldc, st);
+  return attention_tc_launch_t<64>(qkv, ldq, batch, seq, heads, ctx, ldc, st);
 }
 
 }  // namespace zo

@@ -236,7 +236,8 @@ def _attn_ref(qkv, B, T, H, hd):
 
 
 @pytest.mark.parametrize("B,T,H,hd", [(1, 64, 12, 64), (2, 512, 4, 64), (1, 100, 2, 64), (2, 256, 2, 128),
-                                      (4, 8, 2, 8), (2, 6, 2, 3), (1, 33, 3, 32)])
+                                      (1, 300, 3, 128), (1, 1024, 2, 128), (4, 8, 2, 8), (2, 6, 2, 3),
+                                      (1, 33, 3, 32)])
 def test_attention(B, T, H, hd):
     qkv = _rand(B * T, 3 * H * hd, seed=16)
     out = torch.empty(B * T, H * hd, dtype=torch.bfloat16, device=DEV)
