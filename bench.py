@@ -286,7 +286,7 @@ def ours(args, rank, world, local_rank):
             return 2.0 * args_[5] * args_[6] * args_[7]
         return 2.0 * args_[4] * args_[5] * args_[6]
 
-    pert_ev, gemm_ev = [], []
+    pert_ev, gemm_ev, all_ev = [], [], []   # all_ev: every library call of the instrumented replay
 
     def one_step(j, instrument=False):
         for ws in wss:
@@ -298,7 +298,7 @@ def ours(args, rank, world, local_rank):
             runner._replay(wss[0], wss[1])         # the captured step (same launches)
             return
         for i, (fn, a) in enumerate(step_calls):
-            timed = instrument and (i in pert_set or i in gemm_set)
+            timed = instrument and fn.__name__.startswith("zo_")
             if timed:
                 st_ = streams.get(int(a[-1]) if a and isinstance(a[-1], int) else -1,
                                   torch.cuda.current_stream())
@@ -312,8 +312,9 @@ def ours(args, rank, world, local_rank):
                 e1.record(st_)
                 if i in pert_set:
                     pert_ev.append((j, e0, e1))
-                else:
+                elif i in gemm_set:
                     gemm_ev.append((e0, e1, gemm_flops(fn, a)))
+                all_ev.append((fn.__name__, e0, e1))
         if hasattr(runner, "post_step"):
             runner.post_step()
 
@@ -369,6 +370,9 @@ def ours(args, rank, world, local_rank):
         per_step[jj] = per_step.get(jj, 0.0) + a.elapsed_time(b)
     p_ms = list(per_step.values())
     g_tot = sum(a.elapsed_time(b) for a, b, _ in gemm_ev)
+    breakdown = {}
+    for name, a, b in all_ev:
+        breakdown[name] = breakdown.get(name, 0.0) + a.elapsed_time(b) / args.steps
     g_flops = sum(f for _, _, f in gemm_ev)
     rec = store.record.cpu().numpy()
 
@@ -434,6 +438,7 @@ def ours(args, rank, world, local_rank):
                    "launch": "eager" if (args.no_graph or world > 1) else "CUDA graph replay per step"},
         "roofline": dominant, "roofline_other": other,
         "perturb_kernel_gbs": pert_gbs,
+        "breakdown_ms_per_step": {k: round(v, 4) for k, v in sorted(breakdown.items(), key=lambda kv: -kv[1])},
         "clocks": clk.summary(),
         "gpu_launches": n_launch * args.steps,
         "e2e": {"value": tokens / (e2e_ms * 1e-3), "unit": "tokens/s", "h2d_bytes_per_step": h2d,

@@ -21,7 +21,7 @@ def t(f, n=30):
     return s.elapsed_time(e) / n * 1e3
 
 
-for M, N, K in [(2048, 6144, 2048), (2048, 2048, 2048), (2048, 8192, 2048), (2048, 2048, 8192), (8192, 8192, 8192)]:
+for M, N, K in [(4096, 6144, 2048), (4096, 2048, 2048), (4096, 8192, 2048), (4096, 2048, 8192), (4096, 50272, 2048), (8192, 8192, 8192)]:
     a = torch.randn(M, K, device="cuda").bfloat16()
     b = torch.randn(K, N, device="cuda").bfloat16()
     bt = b.t().contiguous()
