@@ -879,8 +879,12 @@ SkPlan sk_plan(int64_t M, int64_t N, int64_t K) {
   const int64_t nk = (K + kBK - 1) / kBK;
   pl.dp_tiles = tiles;
   if (M <= kBM || tiles % W == 0 || tiles * nk < 8 * W) return pl;
+  static const int tail_only = [] {
+    const char* e = getenv("ZO_SK_POLICY");   // "tail": split only the partial last wave
+    return e && e[0] == 't' ? 1 : 0;
+  }();
   const int64_t full = tiles / W;
-  const int64_t dp = full >= 1 ? (full - 1) * W : 0;
+  const int64_t dp = tail_only ? full * W : (full >= 1 ? (full - 1) * W : 0);
   const int64_t units = (tiles - dp) * nk;
   const int64_t lmin = units / W;
   if (lmin < 4) return pl;                     // pieces too small to pay for the fixup

@@ -381,3 +381,27 @@ def test_stacked_plan_falls_back_when_rows_do_not_split():
         batch = _batch(cfg, bsz, 40 + j)
         ra, rb = sa.step(batch, s), sb.step(batch, s)
         assert (ra.loss_pos, ra.loss_neg, ra.g) == (rb.loss_pos, rb.loss_neg, rb.g)
+
+
+def test_config1_opt125m_shape_step_matches_oracle():
+    """BASELINE configs[0]: the OPT-125M-shaped MeZO step (V=50272, d=768,
+    12 heads, 12 blocks, T=64, B=1, f32) on the GPU with the reference's z
+    injected, against the oracle's eager step: losses within the bf16
+    tolerance, g within 2e-3/eps, and the updated 162M-parameter master within
+    lr*|dg|*max|z| of the reference's (the update arithmetic itself is exact)."""
+    from paper_2507_03211_b200.model import opt_config
+
+    cfg = opt_config("opt-125m", 64)
+    store = DeviceStore(cfg, init_seed=7)
+    om = O.Model(cfg.vocab_size, cfg.d_model, cfg.n_heads, cfg.n_blocks, cfg.seq_len, init_seed=7)
+    assert np.array_equal(store.theta.cpu().numpy(), np.concatenate(om.blocks))
+    seed = O.iteration_seeds(1234, 1)[0]
+    ids, tg = O.synthetic_batch(cfg.vocab_size, cfg.seq_len, 1, O.bench_batch_seed(99, 1))
+    zs = O.z_stream(seed, om.sizes)
+    lp, ln, g = O.mezo_step(om, ids, tg, EPS, LR, seed, zs=zs)
+    got = zo.mezo_step(store, Batch(ids, tg), zo.ZoHyper(EPS, LR), seed, mgr=RngStateManager("oracle"))
+    assert abs(got.loss_pos - lp) <= 2e-3 and abs(got.loss_neg - ln) <= 2e-3
+    assert abs(got.g - g) <= 2e-3 / EPS
+    zmax = max(float(np.abs(z).max()) for z in zs)
+    diff = np.abs(store.theta.cpu().numpy().astype(np.float64) - np.concatenate(om.blocks)).max()
+    assert diff <= LR * abs(got.g - g) * zmax + 1e-6
