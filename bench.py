@@ -51,7 +51,7 @@ def _args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true", help="skip the public-API pass (profiling runs)")
     ap.add_argument("--no-graph", action="store_true", help="launch the step eagerly instead of replaying a CUDA graph")
-    ap.add_argument("--overlap", default="stacked", choices=["none", "blocks", "background", "stacked"],
+    ap.add_argument("--overlap", default="stacked", choices=["none", "blocks", "background", "stacked", "stacked_bg"],
                     help="none: the two forwards on two streams; blocks: per-block perturb passes on a side stream ahead of the +eps forward; "
                          "background: one co-resident perturb pass gated per block by device counters; "
                          "stacked: both directions as one launch per layer over stacked activations")
@@ -65,7 +65,8 @@ def _config(args):
 
 
 def _plan(args):
-    return {"none": False, "blocks": "blocks", "background": "background", "stacked": "stacked"}[args.overlap]
+    return {"none": False, "blocks": "blocks", "background": "background", "stacked": "stacked",
+            "stacked_bg": "stacked_bg"}[args.overlap]
 
 
 def _plan_text(args, world):
@@ -263,7 +264,8 @@ def ours(args, rank, world, local_rank):
         wss = [store.workspace(PLUS, B, T), store.workspace(MINUS, B, T)]
         step_calls = {"none": runner.step_calls, "blocks": runner.overlapped_step_calls,
                       "background": runner.background_step_calls,
-                      "stacked": runner.stacked_step_calls}[args.overlap](wss[0], wss[1])
+                      "stacked": runner.stacked_step_calls,
+                      "stacked_bg": runner.stacked_bg_step_calls}[args.overlap](wss[0], wss[1])
     else:
         from paper_2507_03211_b200.strategies import TwoDRunner
         runner = TwoDRunner(store, hyper, rank=rank, world=world, batch=B, seq=T)
@@ -353,9 +355,13 @@ def ours(args, rank, world, local_rank):
     # instrumented pass over the same steps: per-kernel CUDA-event durations.
     # Kernels of concurrent streams would overlap their event windows, so the
     # instrumented replay runs the two directional forwards serialised.
-    if world == 1 and args.overlap != "stacked":      # the stacked plan is single-stream already
-        runner.dual_stream = False
-        step_calls[:] = runner.step_calls(wss[0], wss[1])
+    if world == 1 and args.overlap != "stacked":      # instrument a single-stream plan
+        if args.overlap == "stacked_bg":
+            runner.overlap = "stacked"
+            step_calls[:] = runner.stacked_step_calls(wss[0], wss[1])
+        else:
+            runner.dual_stream = False
+            step_calls[:] = runner.step_calls(wss[0], wss[1])
         pert_set.clear()
         pert_set.update(i for i, (fn, _) in enumerate(step_calls) if fn.__name__ == "zo_perturb_update")
         gemm_set.clear()
@@ -364,6 +370,7 @@ def ours(args, rank, world, local_rank):
         one_step(j, instrument=True)
     if world == 1:
         runner.dual_stream = True
+        runner.overlap = _plan(args) or None
     torch.cuda.synchronize()
     per_step = {}
     for jj, a, b in pert_ev:

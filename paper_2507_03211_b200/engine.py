@@ -462,7 +462,8 @@ class DeviceStore:
                                                      0, 0, st)))
         return calls
 
-    def forward_calls_stacked(self, ws: Workspace, eps: float, zmode=L.ZO_Z_PHILOX, z_cur=None, stream=None):
+    def forward_calls_stacked(self, ws: Workspace, eps: float, zmode=L.ZO_Z_PHILOX, z_cur=None, stream=None,
+                              blocks=None):
         """Both directional forwards as one launch per layer over the stacked
         activations [x+; x-] (rows [0, h) use the +eps shadows, [h, 2h) the
         -eps shadows): zo_layernorm_fwd_split / zo_gemm_bf16_split, attention
@@ -478,7 +479,7 @@ class DeviceStore:
         st = L.stream_ptr(stream)
         ldx, ldh = ws.x.stride(0), ws.h.stride(0)
         calls = []
-        for bid in range(len(self.layouts)):
+        for bid in (range(len(self.layouts)) if blocks is None else blocks):
             bl = self.layouts[bid]
             vp = lambda n: _ptr(self.vview(PLUS, bid, n))    # noqa: E731
             vm = lambda n: _ptr(self.vview(MINUS, bid, n))   # noqa: E731

@@ -160,7 +160,7 @@ class StreamingZo:
         # side stream gated by events; "background": one co-resident pass gated
         # per block by device counters.  All plans give identical results.
         plan = {False: None, True: "blocks", "blocks": "blocks", "background": "background",
-                "stacked": "stacked"}[overlap]
+                "stacked": "stacked", "stacked_bg": "stacked_bg"}[overlap]
         self.overlap = plan if not self.mgr.oracle else None
         self.dual_stream = True
         # Philox steps replay one captured CUDA graph per batch shape (the
@@ -275,11 +275,54 @@ class StreamingZo:
         calls += s.grad_call_stacked(ws, eps, self.hyper.lr)
         return calls
 
+    def stacked_bg_step_calls(self, wsp, wsn):
+        """The stacked step with the perturb pass split per block onto a
+        LOW-priority stream while the forward runs on a HIGH-priority one:
+        blocks 0-1 are perturbed up front (the forward starts at once), every
+        later block's pass is queued behind at low priority and the forward of
+        block b waits on its event.  The short perturb CTAs fill the SMs the
+        forward leaves idle (partial GEMM waves, LayerNorm / attention
+        tails, kernel boundaries) and the block scheduler hands freed SMs to the
+        forward's pending CTAs first.  Same kernels and per-element arithmetic
+        as stacked_step_calls, so results are bit-identical."""
+        if self.mgr.oracle:
+            raise ProtocolError("the stacked background plan runs the Philox direction only")
+        s, eps = self.store, self.hyper.epsilon
+        ws = s.stacked_workspace(wsp.batch, wsp.seq)
+        nb = len(s.layouts)
+        if not hasattr(s, "_prio_streams"):
+            lo, hi = torch.cuda.Stream.priority_range() if hasattr(torch.cuda.Stream, "priority_range") else (0, -1)
+            s._prio_streams = (torch.cuda.Stream(device=s.device, priority=hi),
+                               torch.cuda.Stream(device=s.device, priority=lo))
+            s._prio_events = [torch.cuda.Event() for _ in range(nb + 2)]
+        hi_s, lo_s = s._prio_streams
+        ev = s._prio_events
+        main = torch.cuda.current_stream()
+        flags = L.ZO_PU_UPDATE | L.ZO_PU_SHADOW_A | L.ZO_PU_SHADOW_B
+        calls = [(_record_and_wait, (ev[nb], main, hi_s)), (_wait, (lo_s, ev[nb]))]
+        head = min(2, nb)
+        for b in range(head):
+            calls += s.perturb_call(s.block_tables[b], flags, +eps, -eps, stream=hi_s)
+        calls.append((_record, (ev[0], hi_s)))
+        calls.append((_wait, (lo_s, ev[0])))        # the background pass starts behind the head blocks
+        for b in range(head, nb):
+            calls += s.perturb_call(s.block_tables[b], flags, +eps, -eps, stream=lo_s)
+            calls.append((_record, (ev[b], lo_s)))
+        for b in range(nb):
+            if b >= head:
+                calls.append((_wait, (hi_s, ev[b])))
+            calls += s.forward_calls_stacked(ws, eps, stream=hi_s, blocks=[b])
+        calls += s.grad_call_stacked(ws, eps, self.hyper.lr, stream=hi_s)
+        calls.append((_record_and_wait, (ev[nb + 1], hi_s, main)))
+        return calls
+
     def _stacked_ok(self, wsp):
-        return self.overlap == "stacked" and self.store.stackable(wsp.batch, wsp.seq)
+        return self.overlap in ("stacked", "stacked_bg") and self.store.stackable(wsp.batch, wsp.seq)
 
     def _plan(self, wsp, wsn, zc=None, zp=None, update=True):
         if self._stacked_ok(wsp):
+            if self.overlap == "stacked_bg":
+                return self.stacked_bg_step_calls(wsp, wsn)
             return self.stacked_step_calls(wsp, wsn)
         if self.overlap == "blocks":
             return self.overlapped_step_calls(wsp, wsn)

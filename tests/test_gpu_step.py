@@ -342,9 +342,10 @@ def test_graph_replay_equals_eager(plan):
     assert torch.equal(a.theta, b.theta)
 
 
+@pytest.mark.parametrize("plan", ["stacked", "stacked_bg"])
 @pytest.mark.parametrize("arch", ["zosim", "opt"])
 @pytest.mark.parametrize("graph", [False, True])
-def test_stacked_plan_is_bit_identical(arch, graph):
+def test_stacked_plan_is_bit_identical(arch, graph, plan):
     """Both directions as one launch per layer over stacked [+eps; -eps]
     activations (zo_gemm_bf16_split / zo_layernorm_fwd_split, attention over
     2B sequences) give exactly the two-stream plan's records and weights --
@@ -359,7 +360,7 @@ def test_stacked_plan_is_bit_identical(arch, graph):
     a, b = DeviceStore(cfg, 7), DeviceStore(cfg, 7)
     h = zo.ZoHyper(EPS, LR)
     sa = zo.StreamingZo(a, h, overlap=False, graph=graph)
-    sb = zo.StreamingZo(b, h, overlap="stacked", graph=graph)
+    sb = zo.StreamingZo(b, h, overlap=plan, graph=graph)
     for j, s in enumerate(iteration_seeds(29, 4), 1):
         batch = make_batch(cfg, 2, 900 + j)
         ra, rb = sa.step(batch, s), sb.step(batch, s)
