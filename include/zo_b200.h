@@ -193,6 +193,24 @@ int zo_gemm_bf16_ws(const void* A, int64_t lda, const void* B, int64_t ldb,
 int64_t zo_gemm_workspace_bytes(int64_t M, int64_t N, int64_t K);
 int64_t zo_gemm_ce_tiles(int64_t N);
 
+/*
+ * fp32 forward of the f32 parity mode (SURVEY.md 8c mode (i)): the same ops
+ * as the bf16 production path with every operand and activation in fp32 and
+ * accurate expf / tanhf (CUDA-core FFMA; checker-grade, not the hot path).
+ *   zo_gemm_f32: C = A[M,K] B[K,N] with ZO_EPI_F32 / BIAS_BF16 (here: fp32
+ *     out) / BIAS_GELU_BF16 (fp32 out) / BIAS_RELU_BF16 / BIAS_RESID_F32.
+ *   zo_ce_rows_f32: per-row (max, sum exp) and target logit of fp32 logits
+ *     written as the CE partials zo_ce_finalize combines (slot 0 of n_tiles).
+ */
+int zo_gemm_f32(const float* A, int64_t lda, const float* B, int64_t ldb, int64_t M, int64_t N, int64_t K,
+                int32_t epilogue, const float* bias, float* out, int64_t ldo, void* stream);
+int zo_attn_causal_fwd_f32(const float* qkv, int64_t ldqkv, int64_t batch, int64_t seq, int64_t heads,
+                           int64_t head_dim, float* ctx, int64_t ldc, void* stream);
+int zo_layernorm_fwd_f32(const float* x, int64_t ldx, const float* gamma, const float* beta, int64_t rows,
+                         int64_t d, float* out, int64_t ldo, void* stream);
+int zo_ce_rows_f32(const float* logits, int64_t ld, int64_t rows, int64_t vocab, const int32_t* targets,
+                   float* ce_part, float* ce_tgt, int64_t n_tiles, int32_t* err_flag, void* stream);
+
 /* Causal exact-softmax attention (src/zosim/model.py:325-332): qkv rows are
  * [q | k | v] (each H*hd wide), out ctx[B*T, H*hd] bf16. */
 int zo_attn_causal_fwd(const void* qkv, int64_t ldqkv, int64_t batch, int64_t seq,

@@ -60,6 +60,10 @@ SIGNATURES = {
     "zo_gemm_workspace_bytes": (I64, [I64, I64, I64]),
     "zo_gemm_ce_tiles": (I64, [I64]),
     "zo_attn_causal_fwd": (C.c_int, [P, I64, I64, I64, I64, I64, P, I64, P]),
+    "zo_gemm_f32": (C.c_int, [P, I64, P, I64, I64, I64, I64, I32, P, P, I64, P]),
+    "zo_attn_causal_fwd_f32": (C.c_int, [P, I64, I64, I64, I64, I64, P, I64, P]),
+    "zo_layernorm_fwd_f32": (C.c_int, [P, I64, P, P, I64, I64, P, I64, P]),
+    "zo_ce_rows_f32": (C.c_int, [P, I64, I64, I64, P, P, P, I64, P, P]),
     "zo_ce_finalize": (C.c_int, [P, P, I64, I64, P, P, P, P]),
     "zo_grad_finalize": (C.c_int, [P, P, D, D, P, P, P]),
     "zo_grad_finalize_groups": (C.c_int, [P, I32, I32, I32, I32, I32, I32, D, D, P, P, P]),

@@ -62,6 +62,13 @@ int gemm_launch(const void*, int64_t, const void*, int64_t, int64_t, int64_t, in
                 const float*, int64_t);
 int64_t gemm_workspace_bytes(int64_t M, int64_t N, int64_t K);
 int64_t gemm_ce_tiles(int64_t N);
+int gemm_f32_launch(const float*, int64_t, const float*, int64_t, int64_t, int64_t, int64_t, int, const float*,
+                    float*, int64_t, cudaStream_t);
+int attn_f32_launch(const float*, int64_t, int64_t, int64_t, int64_t, int64_t, float*, int64_t, cudaStream_t);
+int layernorm_f32_launch(const float*, int64_t, const float*, const float*, int64_t, int64_t, float*, int64_t,
+                         cudaStream_t);
+int ce_rows_f32_launch(const float*, int64_t, int64_t, int64_t, const int32_t*, float*, float*, int64_t, int32_t*,
+                       cudaStream_t);
 
 }  // namespace zo
 
@@ -228,6 +235,36 @@ int zo_gemm_bf16_ws(const void* A, int64_t lda, const void* B, int64_t ldb, int6
 }
 
 int64_t zo_gemm_workspace_bytes(int64_t M, int64_t N, int64_t K) { return zo::gemm_workspace_bytes(M, N, K); }
+
+int zo_gemm_f32(const float* A, int64_t lda, const float* B, int64_t ldb, int64_t M, int64_t N, int64_t K,
+                int32_t epilogue, const float* bias, float* out, int64_t ldo, void* stream) {
+  ZO_CHECK_ARG(A && B && out, ZO_ERR_CONFIG, "zo_gemm_f32: null operand");
+  ZO_CHECK_ARG(epilogue == ZO_EPI_F32 || bias, ZO_ERR_CONFIG, "zo_gemm_f32: bias required");
+  ZO_CHECK_ARG(lda >= K && ldb >= N && ldo >= N, ZO_ERR_CONFIG, "zo_gemm_f32: leading dimension too small");
+  return zo::gemm_f32_launch(A, lda, B, ldb, M, N, K, epilogue, bias, out, ldo, ZO_STREAM(stream));
+}
+
+int zo_attn_causal_fwd_f32(const float* qkv, int64_t ldqkv, int64_t batch, int64_t seq, int64_t heads,
+                           int64_t head_dim, float* ctx, int64_t ldc, void* stream) {
+  ZO_CHECK_ARG(qkv && ctx, ZO_ERR_CONFIG, "zo_attn_causal_fwd_f32: null argument");
+  ZO_CHECK_ARG(head_dim >= 1 && head_dim <= 128, ZO_ERR_CONFIG, "zo_attn_causal_fwd_f32: head_dim %lld > 128",
+               (long long)head_dim);
+  return zo::attn_f32_launch(qkv, ldqkv, batch, seq, heads, head_dim, ctx, ldc, ZO_STREAM(stream));
+}
+
+int zo_layernorm_fwd_f32(const float* x, int64_t ldx, const float* gamma, const float* beta, int64_t rows,
+                         int64_t d, float* out, int64_t ldo, void* stream) {
+  ZO_CHECK_ARG(x && gamma && beta && out, ZO_ERR_CONFIG, "zo_layernorm_fwd_f32: null argument");
+  return zo::layernorm_f32_launch(x, ldx, gamma, beta, rows, d, out, ldo, ZO_STREAM(stream));
+}
+
+int zo_ce_rows_f32(const float* logits, int64_t ld, int64_t rows, int64_t vocab, const int32_t* targets,
+                   float* ce_part, float* ce_tgt, int64_t n_tiles, int32_t* err_flag, void* stream) {
+  ZO_CHECK_ARG(logits && targets && ce_part && ce_tgt && err_flag, ZO_ERR_CONFIG, "zo_ce_rows_f32: null argument");
+  ZO_CHECK_ARG(n_tiles >= 1, ZO_ERR_CONFIG, "zo_ce_rows_f32: n_tiles must be >= 1");
+  return zo::ce_rows_f32_launch(logits, ld, rows, vocab, targets, ce_part, ce_tgt, n_tiles, err_flag,
+                                ZO_STREAM(stream));
+}
 
 int64_t zo_gemm_ce_tiles(int64_t N) { return zo::gemm_ce_tiles(N); }
 

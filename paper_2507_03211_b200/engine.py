@@ -47,9 +47,10 @@ class ShadowPlan:
     """Where each tensor's perturbed copy lives, and the perturb kernel's
     segment tables (per block and for the whole model)."""
 
-    def __init__(self, config: ModelConfig, layouts):
+    def __init__(self, config: ModelConfig, layouts, f32_weights: bool = False):
         d, v = config.d_model, config.vocab_size
         self.config = config
+        self.f32_weights = f32_weights       # f32 parity mode: weight shadows are fp32 too (in vsh)
         self.w_elems = 0
         self.v_elems = 0
         self.views = {}       # bid -> name -> (buffer 'w'|'v', offset, rows, cols, ld)
@@ -57,9 +58,16 @@ class ShadowPlan:
 
         def walloc(rows, cols):
             ld = _r8(cols)
+            if f32_weights:
+                off = _a64(self.v_elems)
+                self.v_elems = off + rows * ld
+                return off, ld
             off = _a64(self.w_elems)
             self.w_elems = off + rows * ld
             return off, ld
+
+        wbuf = "v" if f32_weights else "w"
+        wkind = L.ZO_SHADOW_F32 if f32_weights else L.ZO_SHADOW_BF16
 
         def valloc(n):
             off = (self.v_elems + 3) // 4 * 4
@@ -74,19 +82,19 @@ class ShadowPlan:
                     # bf16 shadow of tok_emb [V, d] = the head's K-major B operand;
                     # the gather still perturbs the fp32 rows it reads
                     o, ld = walloc(v, d)
-                    vw["tok_emb"] = ("w", o, v, d, ld)
+                    vw["tok_emb"] = (wbuf, o, v, d, ld)
                 for name in bl.names:
                     if tied and name == "tok_emb":
-                        segs.append((bl.key(name), v, d, o, ld, L.ZO_SHADOW_BF16) if ld != d else
-                                    (bl.key(name), 1, v * d, o, v * d, L.ZO_SHADOW_BF16))
+                        segs.append((bl.key(name), v, d, o, ld, wkind) if ld != d else
+                                    (bl.key(name), 1, v * d, o, v * d, wkind))
                     else:
                         segs.append((bl.key(name), 1, bl.size(name), 0, bl.size(name), L.ZO_SHADOW_NONE))
             elif bl.kind == TRANSFORMER:
                 qo, qld = walloc(d, 3 * d)
-                vw["qkv"] = ("w", qo, d, 3 * d, qld)
+                vw["qkv"] = (wbuf, qo, d, 3 * d, qld)
                 for name, (r, c) in (("wo", (d, d)), ("w1", (d, 4 * d)), ("w2", (4 * d, d))):
                     o, ld = walloc(r, c)
-                    vw[name] = ("w", o, r, c, ld)
+                    vw[name] = (wbuf, o, r, c, ld)
                 for name, n in (("ln1_g", d), ("ln1_b", d), ("bqkv", 3 * d), ("bo", d), ("ln2_g", d),
                                 ("ln2_b", d), ("b1", 4 * d), ("b2", d)):
                     vw[name] = ("v", valloc(n), 1, n, n)
@@ -94,16 +102,16 @@ class ShadowPlan:
                     k, n = bl.key(name), bl.size(name)
                     if name in ("wq", "wk", "wv"):
                         j = "qkv".index(name[1])
-                        segs.append((k, d, d, qo + j * d, qld, L.ZO_SHADOW_BF16))
+                        segs.append((k, d, d, qo + j * d, qld, wkind))
                     elif name in ("bq", "bk", "bv"):
                         j = "qkv".index(name[1])
                         segs.append((k, 1, d, vw["bqkv"][1] + j * d, d, L.ZO_SHADOW_F32))
                     elif name in ("wo", "w1", "w2"):
                         _, o, r, c, ld = vw[name]
                         if ld == c:
-                            segs.append((k, 1, r * c, o, r * c, L.ZO_SHADOW_BF16))
+                            segs.append((k, 1, r * c, o, r * c, wkind))
                         else:
-                            segs.append((k, r, c, o, ld, L.ZO_SHADOW_BF16))
+                            segs.append((k, r, c, o, ld, wkind))
                     else:
                         segs.append((k, 1, n, vw[name][1], n, L.ZO_SHADOW_F32))
             elif tied:  # real-OPT head: final LayerNorm only
@@ -112,16 +120,16 @@ class ShadowPlan:
                     segs.append((bl.key(name), 1, d, vw[name][1], d, L.ZO_SHADOW_F32))
             else:  # head
                 wo_, wld = walloc(d, v)
-                vw["w_out"] = ("w", wo_, d, v, wld)
+                vw["w_out"] = (wbuf, wo_, d, v, wld)
                 for name, n in (("lnf_g", d), ("lnf_b", d), ("b_out", v)):
                     vw[name] = ("v", valloc(n), 1, n, n)
                 for name in bl.names:
                     k, n = bl.key(name), bl.size(name)
                     if name == "w_out":
                         if wld == v:
-                            segs.append((k, 1, d * v, wo_, d * v, L.ZO_SHADOW_BF16))
+                            segs.append((k, 1, d * v, wo_, d * v, wkind))
                         else:
-                            segs.append((k, d, v, wo_, wld, L.ZO_SHADOW_BF16))
+                            segs.append((k, d, v, wo_, wld, wkind))
                     else:
                         segs.append((k, 1, n, vw[name][1], n, L.ZO_SHADOW_F32))
             self.views[bl.block_id] = vw
@@ -133,7 +141,7 @@ class ShadowPlan:
 def block_extent(plan: ShadowPlan, bid: int):
     """(w_lo, w_hi, v_lo, v_hi): the contiguous shadow ranges of one block."""
     ws = [(o, o + r * ld) for (b, o, r, c, ld) in plan.views[bid].values() if b == "w"] or [(0, 0)]
-    vs = [(o, o + c) for (b, o, r, c, ld) in plan.views[bid].values() if b == "v"] or [(0, 0)]
+    vs = [(o, o + r * ld) for (b, o, r, c, ld) in plan.views[bid].values() if b == "v"] or [(0, 0)]
     return (min(a for a, _ in ws), max(b for _, b in ws), min(a for a, _ in vs), max(b for _, b in vs))
 
 
@@ -162,16 +170,18 @@ class SegTable:
 class Workspace:
     """Activations of one directional forward at batch shape (B, T)."""
 
-    def __init__(self, config: ModelConfig, batch: int, seq: int, device):
+    def __init__(self, config: ModelConfig, batch: int, seq: int, device, f32: bool = False):
         d, v = config.d_model, config.vocab_size
         self.batch, self.seq, self.M = batch, seq, batch * seq
         M = self.M
         ld = _r8(d)
+        adt = torch.float32 if f32 else torch.bfloat16        # f32 parity mode: fp32 activations
         self.x = torch.zeros(M, ld, dtype=torch.float32, device=device)
-        self.h = torch.zeros(M, ld, dtype=torch.bfloat16, device=device)
-        self.ctx = torch.zeros(M, ld, dtype=torch.bfloat16, device=device)
-        self.qkv = torch.zeros(M, _r8(3 * d), dtype=torch.bfloat16, device=device)
-        self.ff = torch.zeros(M, _r8(4 * d), dtype=torch.bfloat16, device=device)
+        self.h = torch.zeros(M, ld, dtype=adt, device=device)
+        self.ctx = torch.zeros(M, ld, dtype=adt, device=device)
+        self.qkv = torch.zeros(M, _r8(3 * d), dtype=adt, device=device)
+        self.ff = torch.zeros(M, _r8(4 * d), dtype=adt, device=device)
+        self.logits = torch.zeros(M, _r8(v), dtype=torch.float32, device=device) if f32 else None
         self.n_ce = int(L.lib().zo_gemm_ce_tiles(v))
         self.ce_part = torch.zeros(M, self.n_ce, 2, dtype=torch.float32, device=device)
         self.ce_tgt = torch.zeros(M, dtype=torch.float32, device=device)
@@ -211,8 +221,16 @@ class DeviceStore:
     """
 
     def __init__(self, config: ModelConfig, init_seed: int = 7, device=None, init: str = "host",
-                 directions=(PLUS, MINUS)):
+                 directions=(PLUS, MINUS), precision: str = "bf16"):
+        """precision "bf16": the production path (bf16 GEMM operands, fp32
+        accumulate, tcgen05 kernels); "f32": the parity mode of SURVEY 8c (i),
+        fp32 operands and activations through the CUDA-core fp32 kernels."""
         config.validate()
+        if precision not in ("bf16", "f32"):
+            raise ConfigurationError(f"precision must be 'bf16' or 'f32', got {precision!r}")
+        if precision == "f32" and config.arch != "zosim":
+            raise ConfigurationError("the f32 parity mode covers the zosim architecture")
+        self.precision = precision
         self.config = config
         self.init_seed = init_seed
         self.device = torch.device(device or f"cuda:{torch.cuda.current_device()}")
@@ -228,12 +246,12 @@ class DeviceStore:
             self._init_philox(init_seed)
         elif init != "none":
             raise ConfigurationError(f"unknown init {init!r}")
-        self.plan = ShadowPlan(config, self.layouts)
+        self.plan = ShadowPlan(config, self.layouts, f32_weights=precision == "f32")
         self.directions = tuple(directions)
         self.wsh = [None, None]
         self.vsh = [None, None]
         for s in self.directions:
-            self.wsh[s] = torch.zeros(self.plan.w_elems, dtype=torch.bfloat16, device=self.device)
+            self.wsh[s] = torch.zeros(max(self.plan.w_elems, 64), dtype=torch.bfloat16, device=self.device)
             self.vsh[s] = torch.zeros(self.plan.v_elems, dtype=torch.float32, device=self.device)
         self.block_tables = {bid: SegTable(segs, self.device, [bid] * len(segs))
                              for bid, segs in self.plan.segments.items()}
@@ -304,8 +322,8 @@ class DeviceStore:
 
     def wview(self, s: int, bid: int, name: str):
         buf, off, rows, cols, ld = self.plan.views[bid][name]
-        assert buf == "w"
-        return self.wsh[s][off:off + rows * ld].view(rows, ld), rows, cols
+        src = self.wsh[s] if buf == "w" else self.vsh[s]       # "v": f32 parity-mode weights
+        return src[off:off + rows * ld].view(rows, ld), rows, cols
 
     def vview(self, s: int, bid: int, name: str) -> torch.Tensor:
         buf, off, rows, cols, ld = self.plan.views[bid][name]
@@ -317,7 +335,7 @@ class DeviceStore:
         the device token-id / target buffers (one H2D per step, not two)."""
         key = (s, batch, seq)
         if key not in self._ws:
-            ws = Workspace(self.config, batch, seq, self.device)
+            ws = Workspace(self.config, batch, seq, self.device, f32=self.precision == "f32")
             other = self._ws.get((1 - s, batch, seq))
             if other is not None:
                 ws.ids, ws.tgt = other.ids, other.tgt
@@ -339,10 +357,9 @@ class DeviceStore:
             self._ws[key] = ws
         return self._ws[key]
 
-    @staticmethod
-    def stackable(batch: int, seq: int) -> bool:
-        """The stacked GEMMs split rows on a CTA-pair tile boundary."""
-        return (batch * seq) % 256 == 0
+    def stackable(self, batch: int, seq: int) -> bool:
+        """The stacked GEMMs split rows on a CTA-pair tile boundary (bf16 path)."""
+        return self.precision == "bf16" and (batch * seq) % 256 == 0
 
     # -- scalar state ----------------------------------------------------------
     def set_seed(self, seed: int, stream=None):
@@ -398,6 +415,9 @@ class DeviceStore:
         (embedding -> N decoder blocks -> LN_f + LM head + CE).  ``slots``
         maps block ids to objects with the same wview / vview / theta_ptr
         interface when those blocks live outside this store (offload)."""
+        if self.precision == "f32":
+            return self.forward_calls_f32(s, ws, scale, zmode, z_cur, stream, blocks, head_mode, logits, loss_out,
+                                          scal)
         cfg, lib = self.config, L.lib()
         d, H, hd, V = cfg.d_model, cfg.n_heads, cfg.head_dim, cfg.vocab_size
         opt = cfg.arch == "opt"
@@ -460,6 +480,64 @@ class DeviceStore:
                     calls.append(ws.gemm(lib, *(_ptr(ws.h), ws.h.stride(0), _ptr(wout), wout.stride(0), M, V, d,
                                                      L.ZO_EPI_F32 | bflag, 0, _ptr(logits), logits.stride(0), 0, 0,
                                                      0, 0, st)))
+        return calls
+
+    def forward_calls_f32(self, s, ws, scale, zmode=L.ZO_Z_PHILOX, z_cur=None, stream=None, blocks=None,
+                          head_mode="ce", logits=None, loss_out=None, scal=None):
+        """forward_calls of the f32 parity mode: same block structure, fp32
+        operands / activations through zo_gemm_f32, zo_attn_causal_fwd_f32,
+        zo_layernorm_fwd_f32; the head materialises fp32 logits and
+        zo_ce_rows_f32 + zo_ce_finalize form the f64 loss."""
+        cfg, lib = self.config, L.lib()
+        d, H, hd, V = cfg.d_model, cfg.n_heads, cfg.head_dim, cfg.vocab_size
+        M, B, T = ws.M, ws.batch, ws.seq
+        st = L.stream_ptr(stream)
+        calls = []
+        blocks = range(len(self.layouts)) if blocks is None else blocks
+        scal_p = _ptr(scal) if scal is not None else _ptr(self.scal)
+        ldx, ldh = ws.x.stride(0), ws.h.stride(0)
+        for bid in blocks:
+            bl = self.layouts[bid]
+            if bl.kind == EMBEDDING:
+                calls.append((lib.zo_embed_fwd, (
+                    self.theta_ptr(bl.key("tok_emb")), bl.key("tok_emb"), self.theta_ptr(bl.key("pos_emb")),
+                    bl.key("pos_emb"), _ptr(ws.ids), B, T, d, V, float(scale), scal_p, zmode, _ptr(z_cur), 0,
+                    _ptr(ws.x), ldx, _ptr(ws.err), st)))
+            elif bl.kind == TRANSFORMER:
+                v = lambda n: _ptr(self.vview(s, bid, n))  # noqa: E731
+                w = {n: self.wview(s, bid, n)[0] for n in ("qkv", "wo", "w1", "w2")}
+                g = lib.zo_gemm_f32
+                calls += [
+                    (lib.zo_layernorm_fwd_f32, (_ptr(ws.x), ldx, v("ln1_g"), v("ln1_b"), M, d, _ptr(ws.h), ldh, st)),
+                    (g, (_ptr(ws.h), ldh, _ptr(w["qkv"]), w["qkv"].stride(0), M, 3 * d, d, L.ZO_EPI_BIAS_BF16,
+                         v("bqkv"), _ptr(ws.qkv), ws.qkv.stride(0), st)),
+                    (lib.zo_attn_causal_fwd_f32, (_ptr(ws.qkv), ws.qkv.stride(0), B, T, H, hd, _ptr(ws.ctx),
+                                                  ws.ctx.stride(0), st)),
+                    (g, (_ptr(ws.ctx), ws.ctx.stride(0), _ptr(w["wo"]), w["wo"].stride(0), M, d, d,
+                         L.ZO_EPI_BIAS_RESID_F32, v("bo"), _ptr(ws.x), ldx, st)),
+                    (lib.zo_layernorm_fwd_f32, (_ptr(ws.x), ldx, v("ln2_g"), v("ln2_b"), M, d, _ptr(ws.h), ldh, st)),
+                    (g, (_ptr(ws.h), ldh, _ptr(w["w1"]), w["w1"].stride(0), M, 4 * d, d, L.ZO_EPI_BIAS_GELU_BF16,
+                         v("b1"), _ptr(ws.ff), ws.ff.stride(0), st)),
+                    (g, (_ptr(ws.ff), ws.ff.stride(0), _ptr(w["w2"]), w["w2"].stride(0), M, d, 4 * d,
+                         L.ZO_EPI_BIAS_RESID_F32, v("b2"), _ptr(ws.x), ldx, st)),
+                ]
+            else:
+                wout = self.wview(s, bid, "w_out")[0]
+                calls.append((lib.zo_layernorm_fwd_f32, (_ptr(ws.x), ldx, _ptr(self.vview(s, bid, "lnf_g")),
+                                                         _ptr(self.vview(s, bid, "lnf_b")), M, d, _ptr(ws.h), ldh,
+                                                         st)))
+                if head_mode == "ce":
+                    calls.append((lib.zo_gemm_f32, (_ptr(ws.h), ldh, _ptr(wout), wout.stride(0), M, V, d,
+                                                    L.ZO_EPI_BIAS_BF16, _ptr(self.vview(s, bid, "b_out")),
+                                                    _ptr(ws.logits), ws.logits.stride(0), st)))
+                    calls.append((lib.zo_ce_rows_f32, (_ptr(ws.logits), ws.logits.stride(0), M, V, _ptr(ws.tgt),
+                                                       _ptr(ws.ce_part), _ptr(ws.ce_tgt), ws.n_ce, _ptr(ws.err), st)))
+                    calls.append((lib.zo_ce_finalize, (_ptr(ws.ce_part), _ptr(ws.ce_tgt), M, ws.n_ce,
+                                                       loss_out if loss_out is not None else _ptr(ws.loss),
+                                                       _ptr(ws.row_scratch), _ptr(ws.err), st)))
+                else:
+                    calls.append((lib.zo_gemm_f32, (_ptr(ws.h), ldh, _ptr(wout), wout.stride(0), M, V, d,
+                                                    L.ZO_EPI_F32, 0, _ptr(logits), logits.stride(0), st)))
         return calls
 
     def forward_calls_stacked(self, ws: Workspace, eps: float, zmode=L.ZO_Z_PHILOX, z_cur=None, stream=None,

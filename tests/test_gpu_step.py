@@ -356,8 +356,8 @@ def test_stacked_plan_is_bit_identical(arch, graph, plan):
         cfg = OPTConfig(500, 128, 2, 2, 128, "f32", max_positions=130).validate()
     else:
         cfg = ModelConfig(500, 128, 2, 2, 128, "f32")
-    assert DeviceStore.stackable(2, 128)
     a, b = DeviceStore(cfg, 7), DeviceStore(cfg, 7)
+    assert a.stackable(2, 128)
     h = zo.ZoHyper(EPS, LR)
     sa = zo.StreamingZo(a, h, overlap=False, graph=graph)
     sb = zo.StreamingZo(b, h, overlap=plan, graph=graph)
@@ -374,8 +374,8 @@ def test_stacked_plan_falls_back_when_rows_do_not_split():
     """M = B*T not a multiple of 256: the stacked plan quietly runs the
     two-stream plan (same results)."""
     cfg, bsz, _ = _cfg("mid32")
-    assert not DeviceStore.stackable(bsz, cfg.seq_len)
     a, b = DeviceStore(cfg, 7), DeviceStore(cfg, 7)
+    assert not a.stackable(bsz, cfg.seq_len)
     h = zo.ZoHyper(EPS, LR)
     sa, sb = zo.StreamingZo(a, h, overlap=False), zo.StreamingZo(b, h, overlap="stacked")
     for j, s in enumerate(iteration_seeds(31, 3), 1):
@@ -406,3 +406,47 @@ def test_config1_opt125m_shape_step_matches_oracle():
     zmax = max(float(np.abs(z).max()) for z in zs)
     diff = np.abs(store.theta.cpu().numpy().astype(np.float64) - np.concatenate(om.blocks)).max()
     assert diff <= LR * abs(got.g - g) * zmax + 1e-6
+
+
+@pytest.mark.parametrize("name", ["tiny32", "ragged32", "mid32", "wide32"])
+def test_f32_parity_mode_matches_reference_trajectory(name, golden):
+    """SURVEY 8c parity mode (i): reference z injected, fp32 forward. The
+    lazy trajectory's losses match the REAL reference's recorded ones
+    (tests/golden, zosim's StreamingZo) to 1e-6 and g to 1e-4 relative; the
+    flushed weights stay within lr * |dg| * max|z| per step of zosim's."""
+    cfg, bsz, steps = _cfg(name)
+    store = DeviceStore(cfg, init_seed=7, precision="f32")
+    sz = zo.StreamingZo(store, zo.ZoHyper(EPS, LR), mgr=RngStateManager("oracle"))
+    ref = golden[f"{name}/streaming"]
+    dg = []
+    for j, s in enumerate(golden[f"{name}/seeds"].tolist(), 1):
+        ids, tg = golden[f"{name}/ids/{j}"], golden[f"{name}/tgt/{j}"]
+        got = sz.step(Batch(ids, tg), int(np.uint64(s)))
+        lp, ln, g = ref[j - 1]
+        assert abs(got.loss_pos - lp) <= 1e-6 and abs(got.loss_neg - ln) <= 1e-6, (got, ref[j - 1])
+        assert abs(got.g - g) <= 1e-4 * max(1.0, abs(g)), (got.g, g)
+        dg.append(abs(got.g - g))
+    sz.flush()
+    om = _oracle_model(cfg)
+    zmax = max(float(np.abs(np.concatenate(O.z_stream(int(np.uint64(s)), om.sizes))).max())
+               for s in golden[f"{name}/seeds"].tolist())
+    bound = len(dg) * LR * max(dg) * zmax + 1e-6
+    final = [golden[f"{name}/final/{b}"] for b in range(cfg.n_blocks + 2)]
+    for a, b in zip(_theta_blocks(store), final):
+        assert float(np.abs(a.astype(np.float64) - b).max()) <= bound
+
+
+def test_f32_parity_mode_config1_opt125m_shape():
+    """BASELINE configs[0] shape in the f32 parity mode: |dL| <= 1e-6 and
+    |dg| <= 1e-4 relative against the oracle's eager step."""
+    from paper_2507_03211_b200.model import opt_config
+
+    cfg = opt_config("opt-125m", 64)
+    store = DeviceStore(cfg, init_seed=7, precision="f32")
+    om = O.Model(cfg.vocab_size, cfg.d_model, cfg.n_heads, cfg.n_blocks, cfg.seq_len, init_seed=7)
+    seed = O.iteration_seeds(1234, 1)[0]
+    ids, tg = O.synthetic_batch(cfg.vocab_size, cfg.seq_len, 1, O.bench_batch_seed(99, 1))
+    lp, ln, g = O.mezo_step(om, ids, tg, EPS, LR, seed)
+    got = zo.mezo_step(store, Batch(ids, tg), zo.ZoHyper(EPS, LR), seed, mgr=RngStateManager("oracle"))
+    assert abs(got.loss_pos - lp) <= 1e-6 and abs(got.loss_neg - ln) <= 1e-6, (got, lp, ln)
+    assert abs(got.g - g) <= 1e-4 * max(1.0, abs(g)), (got.g, g)
