@@ -415,7 +415,7 @@ class DeviceStore:
         (embedding -> N decoder blocks -> LN_f + LM head + CE).  ``slots``
         maps block ids to objects with the same wview / vview / theta_ptr
         interface when those blocks live outside this store (offload)."""
-        if self.precision == "f32":
+        if getattr(self, "precision", "bf16") == "f32":      # (offload slot views carry no precision)
             return self.forward_calls_f32(s, ws, scale, zmode, z_cur, stream, blocks, head_mode, logits, loss_out,
                                           scal)
         cfg, lib = self.config, L.lib()

@@ -541,6 +541,7 @@ class _StoreView:
 
         self.config, self.layouts, self.plan = rt.config, rt.layouts, rt.plan
         self.scal = rt.scal
+        self.precision = "bf16"
         self._fc = DeviceStore.forward_calls.__get__(self)
 
     def forward_calls(self, *a, **k):
