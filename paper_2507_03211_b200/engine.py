@@ -312,6 +312,30 @@ class DeviceStore:
     def equal(self, other) -> bool:
         return bool(torch.equal(self.theta, other.theta))
 
+    def block(self, block_id: int):
+        """ParamStore.block (model.py:181-182)."""
+        return self.blocks[block_id]
+
+    def transformer_blocks(self):
+        """ParamStore.transformer_blocks (model.py:184-185)."""
+        return [b for b in self.blocks if b.kind == TRANSFORMER]
+
+    def copy(self) -> "DeviceStore":
+        """ParamStore.copy (model.py:187-188): a new store with this master;
+        refused mid-perturbation (model.py:152-157) and with a deferred update
+        outstanding (the copy would silently lack it)."""
+        from .errors import ProtocolError
+
+        for b in getattr(self, "_blocks", []):
+            if b.pert_scale != 0.0:
+                raise ProtocolError(f"block {b.block_id} copied mid-perturbation")
+        if getattr(self, "unflushed", False):
+            raise ProtocolError("copy of a master with a deferred update: call flush() first")
+        out = DeviceStore(self.config, init_seed=self.init_seed, device=self.device, init="none",
+                          directions=self.directions, precision=self.precision)
+        out.theta.copy_(self.theta)
+        return out
+
     # -- views -----------------------------------------------------------------
     def block_buf(self, bid: int) -> torch.Tensor:
         bl = self.layouts[bid]

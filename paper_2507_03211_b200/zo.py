@@ -470,6 +470,20 @@ class DeviceBlock:
     def nbytes(self) -> int:
         return self.elem_count * 4
 
+    @property
+    def dtype(self):
+        return torch.float32
+
+    def spec(self):
+        return [(n, self.shapes[n]) for n in self.names]
+
+    def copy(self) -> torch.Tensor:
+        """ParamBlock.copy (model.py:152-157): the block's master values;
+        refused mid-perturbation."""
+        if self.pert_scale != 0.0:
+            raise ProtocolError(f"block {self.block_id} copied mid-perturbation")
+        return self.buf.clone()
+
 
 def store_blocks(store: DeviceStore):
     if not hasattr(store, "_blocks"):

@@ -4,10 +4,10 @@ direction source (oracle mode) the perturb / update arithmetic is the
 reference's bit for bit, so "bit-exact" assertions carry over unchanged; the
 forward is bf16 (tolerances as DESIGN.md states).
 
-Not mirrored: test_estimator_second_order_in_epsilon -- a finite-difference
-order estimate needs loss differences far below the bf16 operand rounding of
-the production forward (the oracle restatement checks it on CPU instead,
-tests/test_oracle_golden.py)."""
+Not mirrored here: test_estimator_second_order_in_epsilon -- a
+finite-difference order estimate needs f64 losses (the reference runs it on an
+f64 model); the oracle restatement checks it on CPU instead
+(tests/test_oracle_golden.py::test_estimator_second_order_in_epsilon)."""
 
 import numpy as np
 import pytest
@@ -257,3 +257,29 @@ def test_uniform_logits_loss_is_log_vocab():
     assert abs(st.loss_pos - np.log(TINY.vocab_size)) < 1e-3
     assert abs(st.loss_neg - np.log(TINY.vocab_size)) < 1e-3
     _ = PLUS
+
+
+def test_store_copy_and_block_views():
+    """model.py:140-200: copy equals the source, refuses mid-perturbation
+    and with a deferred update outstanding; block views share the master."""
+    store = _store()
+    c = store.copy()
+    assert c.equal(store) and c.checksum() == store.checksum()
+    assert store.block(1).kind == "transformer" and len(store.transformer_blocks()) == TINY.n_blocks
+    blk = store.block(1)
+    blk.buf[0] = 1.5                              # the view writes through to the master
+    assert float(store.theta[blk.key0]) == 1.5
+    mgr, gen = _oracle_gen(4)
+    zo.perturb_block(blk, 1e-3, gen)
+    with pytest.raises(ProtocolError):
+        store.copy()
+    with pytest.raises(ProtocolError):
+        blk.copy()
+    mgr.reset(4)
+    zo.perturb_block(blk, -1e-3, mgr.generator(4))
+    sz = zo.StreamingZo(store, HYPER)
+    sz.step(make_batch(TINY, 4, 1), 3)
+    with pytest.raises(ProtocolError):
+        store.copy()
+    sz.flush()
+    assert store.copy().equal(store)

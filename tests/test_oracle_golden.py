@@ -180,3 +180,42 @@ def test_perturb_restore_cycle_exact():
         assert np.array_equal(O.perturbed(b, 0.0, z), b)
         lo, hi = O.perturbed(b, -EPS, z), O.perturbed(b, +EPS, z)
         assert not np.array_equal(lo, hi)
+
+
+def test_estimator_second_order_in_epsilon():
+    """pkg/tests/test_zo_core.py:186-233 on the oracle (f64): the central
+    difference's error against z . grad shrinks as eps^2 (empirical order in
+    [1.8, 2.2])."""
+    m = O.Model(7, 6, 2, 1, 6, init_seed=3, dtype=np.float64)
+    ids, tg = O.synthetic_batch(7, 6, 2, 5)
+
+    def loss_at(blocks):
+        return O.cross_entropy(m.forward(ids, blocks), tg)
+
+    h = 1e-5
+    grad = []
+    for bi, blk in enumerate(m.blocks):
+        gb = np.empty(blk.size)
+        for i in range(blk.size):
+            orig = blk[i]
+            blk[i] = orig + h
+            lp = loss_at(m.blocks)
+            blk[i] = orig - h
+            lm = loss_at(m.blocks)
+            blk[i] = orig
+            gb[i] = (lp - lm) / (2 * h)
+        grad.append(gb)
+    grad = np.concatenate(grad)
+
+    def g_at(eps, seed):
+        zs = O.z_stream(seed, m.sizes)
+        return O.zo_grad(m.loss_at(+eps, zs, ids, tg), m.loss_at(-eps, zs, ids, tg), eps)
+
+    e_full, e_half = [], []
+    for seed in range(10):
+        zv = np.concatenate(O.z_stream(seed, m.sizes))
+        proj = float(zv @ grad)
+        e_full.append(abs(g_at(1e-3, seed) - proj))
+        e_half.append(abs(g_at(5e-4, seed) - proj))
+    order = math.log2(np.mean(e_full) / np.mean(e_half))
+    assert 1.8 <= order <= 2.2, order
