@@ -276,7 +276,13 @@ class OffloadedZo:
     """
 
     def __init__(self, host: HostStore, hyper: ZoHyper, batch: int, device=None, n_slots: int = 3,
-                 mode: str = "streams", fabric=None, strategy: str = "mezo", trace: bool = False):
+                 mode: str = "streams", fabric=None, strategy: str = "mezo", trace: bool = False,
+                 resident_blocks: int = 0):
+        """resident_blocks: keep the first k transformer blocks on the device
+        for the whole run (uploaded once, written back at flush / sync_host)
+        and stream only the rest -- use whatever HBM the model leaves free,
+        so only the blocks that do not fit cross PCIe every step.  The
+        results are bit-identical for every k (same kernels, same order)."""
         if mode not in ("streams", "serial"):
             raise ProtocolError(f"unknown scheduler mode {mode!r}")
         if n_slots < 2:
@@ -297,11 +303,17 @@ class OffloadedZo:
         if fabric is not None:
             apply_thread_aligned_layout(host, self.world)
         emb, head = self.layouts[0].block_id, self.layouts[-1].block_id
-        self.wids = [bl.block_id for bl in self.layouts if bl.kind == TRANSFORMER]
+        wids = [bl.block_id for bl in self.layouts if bl.kind == TRANSFORMER]
+        if not 0 <= resident_blocks <= len(wids):
+            raise ConfigurationError(f"resident_blocks must be in [0, {len(wids)}], got {resident_blocks}")
+        self.resident = wids[:resident_blocks]          # computed in place, never streamed
+        self.wids = wids[resident_blocks:]              # streamed through the slots
         pad = lambda bid: (-(-self.layouts[bid].elem_count // self.world)) * self.world  # noqa: E731
         self.persistent = {emb: BlockSlot(self.plan, self.layouts, emb, self.dirs, self.device, pad(emb)),
                            head: BlockSlot(self.plan, self.layouts, head, self.dirs, self.device, pad(head))}
-        tpl = self.wids[0] if self.wids else head
+        for bid in self.resident:
+            self.persistent[bid] = BlockSlot(self.plan, self.layouts, bid, self.dirs, self.device, pad(bid))
+        tpl = self.wids[0] if self.wids else (self.resident[0] if self.resident else head)
         self.slots = [BlockSlot(self.plan, self.layouts, tpl, self.dirs, self.device, pad(tpl))
                       for _ in range(n_slots)]
         self.tables = {bl.block_id: rebased_table(self.plan, bl.block_id, self.device) for bl in self.layouts}
@@ -424,29 +436,29 @@ class OffloadedZo:
         os_.wait_event(start)
         emb, head = self.layouts[0].block_id, self.layouts[-1].block_id
         n = len(self.slots)
-        if self.wids:
-            s0 = self.slots[0]
-            e0 = torch.cuda.Event(enable_timing=self.trace)
-            e0.record(us)
-            self._upload(self.wids[0], s0, us)
-            mark(UPLOAD, self.wids[0], us)
-            rec.append((UPLOAD, self.wids[0], e0))
+
+        def upload(k):                                         # U(wids[k]) into slot k % n
+            eu = torch.cuda.Event(enable_timing=self.trace)
+            eu.record(us)
+            self._upload(self.wids[k], self.slots[k % n], us)
+            mark(UPLOAD, self.wids[k], us)
+            rec.append((UPLOAD, self.wids[k], eu))
+
+        for k in range(min(n, len(self.wids))):                # fill every slot up front: the uploads
+            upload(k)                                          # run under the embedding / resident blocks
         e_c = torch.cuda.Event(enable_timing=self.trace)
         e_c.record(cs)
         self._compute(emb, self.persistent[emb], cs)
         mark(COMPUTE, emb, cs)
         rec.append((COMPUTE, emb, e_c))
+        for bid in self.resident:                              # resident blocks: no U / O
+            er = torch.cuda.Event(enable_timing=self.trace)
+            er.record(cs)
+            self._compute(bid, self.persistent[bid], cs)
+            mark(COMPUTE, bid, cs)
+            rec.append((COMPUTE, bid, er))
         for idx, i in enumerate(self.wids):
             slot = self.slots[idx % n]
-            if idx + 1 < len(self.wids):                       # U(i+1) into the next slot once it is free
-                nxt, nslot = self.wids[idx + 1], self.slots[(idx + 1) % n]
-                if idx + 1 - n >= 0:
-                    us.wait_event(ev[(OFFLOAD, self.wids[idx + 1 - n])])
-                eu = torch.cuda.Event(enable_timing=self.trace)
-                eu.record(us)
-                self._upload(nxt, nslot, us)
-                mark(UPLOAD, nxt, us)
-                rec.append((UPLOAD, nxt, eu))
             cs.wait_event(ev[(UPLOAD, i)])                        # C(i) after U(i) (and C(i-1): same stream)
             ec = torch.cuda.Event(enable_timing=self.trace)
             ec.record(cs)
@@ -459,6 +471,9 @@ class OffloadedZo:
             self._offload(i, slot, os_)
             mark(OFFLOAD, i, os_)
             rec.append((OFFLOAD, i, eo))
+            if idx + n < len(self.wids):                           # U(i+n) into this slot once O(i) freed it
+                us.wait_event(ev[(OFFLOAD, i)])
+                upload(idx + n)
         eh = torch.cuda.Event(enable_timing=self.trace)
         eh.record(cs)
         self._compute(head, self.persistent[head], cs)
@@ -523,6 +538,33 @@ class OffloadedZo:
     def makespan(self) -> float:
         tl = self.last_timeline
         return max(e["end"] for e in tl) if tl else float("nan")
+
+
+def plan_residency(config: ModelConfig, budget_bytes: int, n_dirs: int = 2, max_slots: int = 8):
+    """(resident_blocks, n_slots) for OffloadedZo under a device-memory budget
+    for the transformer blocks: a block costs 4 B/param of fp32 master + 2 B
+    per direction of bf16 shadow, resident or in a slot.  As many blocks as
+    fit stay resident (each one removes a block's H2D + D2H per step); the
+    slots only need to prefetch what PCIe can move while the resident blocks
+    compute (~1 upload per 8 resident blocks at the measured 49 GB/s and
+    ~3 ms of compute per OPT-13B block), so they get just that depth (>= 3,
+    or whatever fits).  The embedding / head / activations are outside the
+    budget."""
+    from .model import model_layout
+
+    blocks = [bl for bl in model_layout(config) if bl.kind == TRANSFORMER]
+    nb = len(blocks)
+    per = blocks[0].elem_count * (4 + 2 * n_dirs)
+    fit = int(budget_bytes // per)
+    if fit >= nb:
+        return nb, 0
+    if fit <= 3:
+        return 0, max(2, fit)
+    for slots in range(3, max_slots + 1):
+        k = fit - slots
+        if slots >= min(max_slots, max(3, k // 8 + 1)):
+            return k, slots
+    return fit - max_slots, max_slots
 
 
 def _load(ws: Workspace, batch: Batch):

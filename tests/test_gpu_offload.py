@@ -151,3 +151,19 @@ def test_streamed_peak_is_independent_of_depth():
         del rt
     blk = (12 * 128 * 128 + 13 * 128) * 4
     assert abs(peaks[1] - peaks[0]) < blk          # no growth with depth
+
+
+@pytest.mark.parametrize("k", [2, 5])
+def test_partially_resident_offload_equals_resident(k):
+    """OffloadedZo(resident_blocks=k): the first k transformer blocks stay in
+    HBM (uploaded once), only the rest stream -- records and the flushed host
+    master equal the resident path bit for bit, and the streamed bytes drop."""
+    recs, _, final = _resident(DEEP, 3)
+    host = HostStore(DEEP, 7)
+    rt = OffloadedZo(host, zo.ZoHyper(EPS, LR), batch=2, resident_blocks=k)
+    for j, s in enumerate(iteration_seeds(9, 3), 1):
+        r = rt.step(make_batch(DEEP, 2, 40 + j), s)
+        assert (r.loss_pos, r.loss_neg, r.g) == recs[j - 1]
+    assert rt.uploaded_params == 3 * sum(host.layouts[b].elem_count for b in rt.wids)
+    rt.flush()
+    assert np.array_equal(host.theta.numpy(), final)

@@ -30,3 +30,21 @@ def test_layout_fixed_at_init():
     assert p["layouts"][1].width == -(-s.layouts[1].elem_count // 4)
     with pytest.raises(ProtocolError):
         apply_thread_aligned_layout(s, 2)
+
+
+def test_plan_residency_fills_the_budget():
+    """plan_residency: resident blocks + slots never exceed the budget, all
+    blocks resident when they fit, at least 2 slots otherwise."""
+    from paper_2507_03211_b200.model import model_layout, opt_config
+    from paper_2507_03211_b200.scheduler import plan_residency
+
+    cfg = opt_config("opt-13b", 2048)
+    per = [bl for bl in model_layout(cfg) if bl.kind == "transformer"][0].elem_count * 8
+    nb = cfg.n_blocks
+    for gb in (5, 20, 40, 60, 80, 100, 101, 200):
+        k, slots = plan_residency(cfg, int(gb * 1e9))
+        if gb * 1e9 >= nb * per:
+            assert (k, slots) == (nb, 0)
+        else:
+            assert 0 <= k < nb and 2 <= slots <= nb - k
+            assert (k + slots) * per <= max(gb * 1e9, 2 * per)

@@ -1,0 +1,3 @@
+export PYTHONPATH=$PWD
+OUT=gpurun_out
+for m in offload:budget=40 offload:budget=60 offload:budget=80; do timeout 900 python tools/run_config.py $m opt-13b 2048 1 4 > "$OUT/cfg41_${m/:/_}.json" 2>> $OUT/cfg41.err; done

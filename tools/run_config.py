@@ -4,6 +4,7 @@ for configs #3-#5; the bench line is config #2).
     python tools/run_config.py resident opt-13b 2048 1      # 13B, T=2048, B=1, both directions
     python tools/run_config.py offload  opt-66b 2048 1      # ZO2 schedule, host master, 3 slots
     python tools/run_config.py sharded  opt-13b 2048 1      # same schedule, fp32 master in HBM (1 rank)
+    python tools/run_config.py offload:20 opt-13b 2048 1    # 20 of 40 blocks resident, the rest streamed
 """
 import json
 import sys
@@ -32,10 +33,15 @@ def main():
         from paper_2507_03211_b200.sharded import ShardStore
         shards = ShardStore(cfg, None, 7, init="philox")
         rt = OffloadedZo(shards, hyper, batch=B, trace=True)
-    else:
-        from paper_2507_03211_b200.scheduler import HostStore, OffloadedZo
+    else:   # "offload", "offload:K" (K blocks resident) or "offload:budget=GB" (plan_residency)
+        from paper_2507_03211_b200.scheduler import HostStore, OffloadedZo, plan_residency
+        arg = mode.split(":")[1] if ":" in mode else "0"
+        if arg.startswith("budget="):
+            k, slots = plan_residency(cfg, int(float(arg.split("=")[1]) * 1e9))
+        else:
+            k, slots = int(arg), (6 if int(arg) else 3)
         host = HostStore(cfg, 7, init="philox")
-        rt = OffloadedZo(host, hyper, batch=B, trace=True)
+        rt = OffloadedZo(host, hyper, batch=B, trace=True, resident_blocks=k, n_slots=max(slots, 2))
     torch.cuda.synchronize()
     init_s = time.time() - t0
     seeds = iteration_seeds(1234, steps)
