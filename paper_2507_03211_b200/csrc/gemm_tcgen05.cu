@@ -136,6 +136,12 @@ __device__ __forceinline__ uint32_t make_idesc() {
          ((uint32_t)(kBM >> 4) << 24);
 }
 
+__device__ __forceinline__ float ex2_fast(float x) {   // MUFU.EX2, ex2(-inf) = 0
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 // tanh-GELU (model.py:286-289).  tanh via MUFU.TANH (rel. error ~2^-11), far
 // below the bf16 rounding of the output that follows.
 __device__ __forceinline__ float tanh_fast(float x) {
@@ -236,8 +242,48 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t tme
       if (npart > 0) add_parts(c, v);
       if (!row_ok || col0 >= args.N) continue;
       const int lim = col0 + 32 <= args.N ? 32 : (int)(args.N - col0);
-      float cm = -INFINITY;
       const bool has_bias = bias != nullptr;   // a tied head has no bias (real OPT)
+      if (lim == 32) {
+        // full chunk (all but a row's last): float4 bias, 4-way max / min / sum
+        // chains, exp2 with the log2(e) scale folded into one FFMA; non-finite
+        // logits surface as an infinite max / min or a NaN sum
+        if (has_bias) {
+          if ((reinterpret_cast<uintptr_t>(bias + col0) & 15) == 0) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const float4 b4 = __ldg(reinterpret_cast<const float4*>(bias + col0) + i);
+              v[4 * i] += b4.x; v[4 * i + 1] += b4.y; v[4 * i + 2] += b4.z; v[4 * i + 3] += b4.w;
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] += __ldg(bias + col0 + i);
+          }
+        }
+        float mx[4], mn[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) { mx[k] = v[k]; mn[k] = v[k]; }
+#pragma unroll
+        for (int i = 4; i < 32; ++i) { mx[i & 3] = fmaxf(mx[i & 3], v[i]); mn[i & 3] = fminf(mn[i & 3], v[i]); }
+        const float cm = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3]));
+        const float cmin = fminf(fminf(mn[0], mn[1]), fminf(mn[2], mn[3]));
+        const float nm = fmaxf(ce_m, cm);
+        const float nl = nm * 1.4426950408889634f;
+        float sk[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int i = 0; i < 32; ++i) sk[i & 3] += ex2_fast(fmaf(v[i], 1.4426950408889634f, -nl));
+        const float prev = ce_m == -INFINITY ? 0.f : ce_s * ex2_fast((ce_m - nm) * 1.4426950408889634f);
+        ce_s = prev + ((sk[0] + sk[1]) + (sk[2] + sk[3]));
+        ce_m = nm;
+        bad |= !(isfinite(cm) && isfinite(cmin) && isfinite(ce_s));
+        if (tgt >= col0 && tgt < col0 + 32) {
+          const int ti = (int)(tgt - col0);
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            if (i == ti) args.ce_tgt[row] = v[i];
+        }
+        continue;
+      }
+      float cm = -INFINITY;
 #pragma unroll
       for (int i = 0; i < 32; ++i) {
         if (i < lim) {
