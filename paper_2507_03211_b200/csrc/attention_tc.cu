@@ -26,6 +26,20 @@ namespace zo {
 int tma_map_bf16(const void* ptr, int64_t inner, int64_t outer, int64_t ld, int box_in, int box_out,
                  CUtensorMap* out);
 
+// ZO_ATTN_TRACE (debug builds only): clock64 stamps of CTA 0's softmax warp 2
+// (TR), MMA warp (TRW) and producer (TRP), read back by zo_attn_trace_read;
+// tools/attn_trace.py prints the timeline.  Compiled out otherwise.
+#ifdef ZO_ATTN_TRACE
+__device__ long long g_attn_trace[4096];
+#define TR(slot) do { if (blockIdx.x == 0 && threadIdx.x == 64 && (slot) < 4096) g_attn_trace[(slot)] = clock64(); } while (0)
+#define TRW(slot) do { if (blockIdx.x == 0 && threadIdx.x == 32 && (slot) < 4096) g_attn_trace[(slot)] = clock64(); } while (0)
+#define TRP(slot) do { if (blockIdx.x == 0 && threadIdx.x == 0 && (slot) < 4096) g_attn_trace[(slot)] = clock64(); } while (0)
+#else
+#define TR(slot)
+#define TRW(slot)
+#define TRP(slot)
+#endif
+
 namespace {
 
 // Softmax warps: 8 (2 per TMEM lane quarter, 64 key columns each) or 16 (4
@@ -158,6 +172,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         const int row0 = b * a.seq;
         const uint32_t qb = it_local % C::kQB, qph = (it_local / C::kQB) & 1u;
         mbar_wait(qempty(qb), qph ^ 1u);
+        TRP(3072 + (int)it_local);
         mbar_expect_tx(qfull(qb), kTile);
 #pragma unroll
         for (int ch = 0; ch < kCh; ++ch)
@@ -166,6 +181,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         for (int j = 0; j < nkb; ++j, ++kvc) {
           const uint32_t st = kvc % kKV, ph = (kvc / kKV) & 1u;
           mbar_wait(kvempty(st), ph ^ 1u);
+          TRP(2048 + (int)kvc);
           mbar_expect_tx(kvfull(st), 2 * kTile);
 #pragma unroll
           for (int ch = 0; ch < kCh; ++ch) {
@@ -190,6 +206,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     auto issue_pv = [&](uint32_t c, uint32_t kv) {
       const uint32_t pb = c & 1u, ph = (c >> 1) & 1u, st = kv % kKV;
       mbar_wait(bar(10 + pb), ph);               // P_c written
+      TRW(1024 + 4 * (int)c + 3);
       mbar_wait(bar(16 + pb), ph ^ 1u);          // PV buffer drained by the softmax warps
       tc_fence_after();
       if (lane == 0) {
@@ -219,8 +236,11 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       for (int j = 0; j < nkb; ++j) {
         const uint32_t c = sc + j, kv = kvc + j;
         const uint32_t sb = c & 1u, ph = (c >> 1) & 1u;
+        TRW(1024 + 4 * (int)c + 0);
         mbar_wait(kvfull(kv % kKV), (kv / kKV) & 1u);    // K_j, V_j landed
+        TRW(1024 + 4 * (int)c + 1);
         mbar_wait(bar(8 + sb), ph ^ 1u);                 // S buffer free
+        TRW(1024 + 4 * (int)c + 2);
         tc_fence_after();
         if (lane == 0) {
 #pragma unroll
@@ -273,6 +293,9 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       const int nkb = n_blocks(qt);
       const int qi = qt * 128 + r;
       float m = -INFINITY, l = 0.f, alpha_prev = 0.f;
+      const int tr_item = (it - blockIdx.x) / gridDim.x;
+      TR(tr_item * 32 + 0);
+      (void)tr_item;
       float o[kOC];
 #pragma unroll
       for (int i = 0; i < kOC; ++i) o[i] = 0.f;
@@ -297,7 +320,9 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       for (int j = 0; j < nkb; ++j) {
         const uint32_t c = sc + j, sb = c & 1u, ph = (c >> 1) & 1u;
         const bool need_mask = (j * 128 + 127 > qt * 128) || ((j + 1) * 128 > a.seq);
+        TR(tr_item * 32 + 1 + 3 * j);
         mbar_wait(bar(6 + sb), ph);
+        TR(tr_item * 32 + 2 + 3 * j);
         tc_fence_after();
         constexpr int NCH = kKC / 32;
         uint32_t sv[NCH][32];
@@ -356,13 +381,16 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) { mbar_arrive(bar(8 + sb)); mbar_arrive(bar(10 + sb)); }   // S read, P written
+        TR(tr_item * 32 + 3 + 3 * j);
         l = fmaf(l, alpha, sum0 + sum1);          // this warp's running sum over its key columns
         m = m_new;
         // deferred: fold PV of the PREVIOUS block (ready while we computed this one)
         if (j > 0) accumulate_pv(c - 1, alpha_prev);
         alpha_prev = alpha;
       }
+      TR(tr_item * 32 + 20);
       accumulate_pv(sc + nkb - 1, alpha_prev);
+      TR(tr_item * 32 + 21);
       sc += nkb;
       const float lt = exchange(l, false);
       if (qi < a.seq) {
@@ -379,6 +407,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
           *reinterpret_cast<uint4*>(out + i) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
         }
       }
+      TR(tr_item * 32 + 22);
     }
   }
   __syncthreads();
@@ -427,3 +456,9 @@ int attention_tc_launch(const __nv_bfloat16* qkv, int64_t ldq, int64_t batch, in
 }
 
 }  // namespace zo
+
+#ifdef ZO_ATTN_TRACE
+extern "C" int zo_attn_trace_read(long long* host) {
+  return (int)cudaMemcpyFromSymbol(host, zo::g_attn_trace, sizeof(long long) * 4096);
+}
+#endif

@@ -4,9 +4,9 @@ softmax warp 2, MMA warp and producer), from a trace build:
     ZO_NVCC_EXTRA=-DZO_ATTN_TRACE python -c "from paper_2507_03211_b200 import build_lib as b; b.build(force=True)"
     cp paper_2507_03211_b200/lib/libzo_b200.so build/alt/libzo_trace.so   # then rebuild the normal library
 
-(the ZO_ATTN_TRACE instrumentation lives in the git history of
-csrc/attention_tc.cu next to this tool; profiles/r01_attn_trace_cta0.txt is
-its output at the stacked step's shape)."""
+(the TR / TRW / TRP stamps in csrc/attention_tc.cu compile to nothing
+without ZO_ATTN_TRACE; profiles/r01_attn_trace_cta0.txt is this tool's output
+at the stacked step's shape)."""
 import ctypes, os, sys
 import numpy as np
 import torch
