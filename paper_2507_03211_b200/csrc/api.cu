@@ -61,6 +61,7 @@ int gemm_launch(const void*, int64_t, const void*, int64_t, int64_t, int64_t, in
                 int64_t, const int32_t*, float*, float*, int32_t*, void*, int64_t, cudaStream_t, const void*,
                 const float*, int64_t);
 int64_t gemm_workspace_bytes(int64_t M, int64_t N, int64_t K);
+int64_t perturb_tile_elems();
 int64_t gemm_ce_tiles(int64_t N);
 int gemm_f32_launch(const float*, int64_t, const float*, int64_t, int64_t, int64_t, int64_t, int, const float*,
                     float*, int64_t, cudaStream_t);
@@ -94,7 +95,7 @@ int zo_device_check(int dev) {
   return ZO_OK;
 }
 
-int64_t zo_perturb_tile_elems(void) { return 512; }
+int64_t zo_perturb_tile_elems(void) { return zo::perturb_tile_elems(); }
 
 int zo_perturb_update(float* theta, int64_t theta_key0, const ZoSegment* segs, const int64_t* tile_prefix,
                       int32_t n_segs, int64_t n_tiles, void* wsh_a, float* vsh_a, void* wsh_b, float* vsh_b,

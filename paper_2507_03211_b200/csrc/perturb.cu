@@ -17,7 +17,10 @@
 namespace zo {
 
 constexpr int kPuThreads = 128;   // small CTAs: one co-resides with a GEMM CTA per SM
-constexpr int kPuGroupsPerThread = 4;   // 4-element groups per lane per tile
+#ifndef ZO_PU_G
+#define ZO_PU_G 4
+#endif
+constexpr int kPuGroupsPerThread = ZO_PU_G;   // 4-element groups per lane per tile
 constexpr int64_t kPuTile = 32 * kPuGroupsPerThread * 4;  // elements per warp tile (512 at G = 4)
 constexpr int kPuMaxSmemSegs = 4096;   // prefix entries staged in shared memory (32 KB)
 
@@ -430,6 +433,8 @@ __global__ void __maxnreg__(88) perturb_update_bg_kernel(const PuParams p) {
   perturb_update_body<ZMODE, true>(p);
 }
 
+int64_t perturb_tile_elems() { return kPuTile; }   // the host builds its tile prefixes with this
+
 int perturb_update_launch(const PuParams& p, int zmode, cudaStream_t stream, bool background) {
   if (p.n_tiles <= 0) return ZO_OK;
   static const int occ = [] { const char* e = getenv("ZO_PU_OCC"); return e ? atoi(e) : 4; }();
@@ -461,6 +466,8 @@ int perturb_update_launch(const PuParams& p, int zmode, cudaStream_t stream, boo
       launch_k(perturb_update_kernel<ZO_Z_PHILOX, 5>, dim3(grid), dim3(kPuThreads), smem, stream, p);
     else if (zmode == ZO_Z_PHILOX && occ == 6)
       launch_k(perturb_update_kernel<ZO_Z_PHILOX, 6>, dim3(grid), dim3(kPuThreads), smem, stream, p);
+    else if (zmode == ZO_Z_PHILOX && occ == 8)
+      launch_k(perturb_update_kernel<ZO_Z_PHILOX, 8>, dim3(grid), dim3(kPuThreads), smem, stream, p);
     else if (zmode == ZO_Z_PHILOX)
       launch_k(perturb_update_kernel<ZO_Z_PHILOX>, dim3(grid), dim3(kPuThreads), smem, stream, p);
     else
