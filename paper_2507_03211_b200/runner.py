@@ -57,8 +57,10 @@ class MeshConfig:
 
 @dataclass
 class RunConfig:
-    """bench.py:55-150 minus the simulator's topology / compute_time /
-    device_capacity_blocks knobs (real hardware replaces the cost model)."""
+    """bench.py:55-150 minus the simulator's topology / compute_time knobs
+    (real hardware replaces the cost model).  ``device_capacity_blocks`` keeps
+    the reference's meaning of a device capacity in block footprints, used as
+    the zo2 runtime's HBM budget: what fits stays resident, the rest streams."""
 
     model: ModelConfig
     hyper: object                  # zo.ZoHyper
@@ -69,6 +71,7 @@ class RunConfig:
     init_seed: int = 7
     data_seed: int = 99
     init: str = "host"             # "host" (zosim's numpy draws) or "philox" (random-init at scale)
+    device_capacity_blocks: float | None = None   # zo2: HBM budget in transformer-block footprints
     report_dir: str | None = None
 
     def validate(self) -> "RunConfig":
@@ -107,7 +110,7 @@ class RunConfig:
         from .zo import ZoHyper
 
         d = dict(d)
-        for k in ("topology", "compute_time", "device_capacity_blocks"):   # simulator-only knobs
+        for k in ("topology", "compute_time"):   # simulator-only knobs
             d.pop(k, None)
         try:
             cfg = cls(model=ModelConfig.from_dict(d.pop("model")), hyper=ZoHyper(**d.pop("hyper")),
@@ -139,6 +142,7 @@ class RunConfig:
             "init_seed": self.init_seed,
             "data_seed": self.data_seed,
             "init": self.init,
+            "device_capacity_blocks": self.device_capacity_blocks,
         }
 
 
@@ -254,7 +258,18 @@ def _run_zo2(config: RunConfig) -> RunReport:
     dev = _device()
     torch.cuda.reset_peak_memory_stats(dev)
     host = HostStore(config.model, init_seed=config.init_seed, init=config.init, device=dev)
-    rt = OffloadedZo(host, config.hyper, config.batch_size, device=dev, trace=True)
+    k, slots = 0, 3
+    if config.device_capacity_blocks is not None:
+        # the reference's capacity knob (bench.py:262-264) as a real HBM budget:
+        # keep what fits resident, stream the rest (scheduler.plan_residency)
+        from .model import model_layout
+        from .scheduler import plan_residency
+
+        per = [bl for bl in model_layout(config.model) if bl.kind == "transformer"][0].elem_count * 8
+        k, slots = plan_residency(config.model, int(config.device_capacity_blocks * per))
+        slots = max(slots, 2)
+    rt = OffloadedZo(host, config.hyper, config.batch_size, device=dev, trace=True, resident_blocks=k,
+                     n_slots=slots)
     steps, walls = [], []
     for j, seed in enumerate(iteration_seeds(config.seed, config.hyper.steps), 1):
         batch = batch_for(config, j)

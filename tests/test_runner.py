@@ -81,6 +81,11 @@ def test_run_outputs_and_mezo_equals_zo2(tmp_path):
         else:
             assert tl == []
         assert rep.peak_device_bytes > 0 and rep.tokens_per_sec > 0
+    # the capacity knob: part of the model resident, same trajectory
+    out = tmp_path / "zo2cap"
+    rep = run(_rc(strategy="zo2", report_dir=str(out), device_capacity_blocks=3.0))
+    reps["zo2cap"] = rep
+    assert rep.final_checksum == reps["zo2"].final_checksum
     a, b = reps["mezo"], reps["zo2"]
     assert [(s.loss_pos, s.loss_neg, s.g) for s in a.steps] == [(s.loss_pos, s.loss_neg, s.g) for s in b.steps]
     assert a.final_checksum == b.final_checksum
