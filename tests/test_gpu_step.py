@@ -450,3 +450,28 @@ def test_f32_parity_mode_config1_opt125m_shape():
     got = zo.mezo_step(store, Batch(ids, tg), zo.ZoHyper(EPS, LR), seed, mgr=RngStateManager("oracle"))
     assert abs(got.loss_pos - lp) <= 1e-6 and abs(got.loss_neg - ln) <= 1e-6, (got, lp, ln)
     assert abs(got.g - g) <= 1e-4 * max(1.0, abs(g)), (got.g, g)
+
+
+@pytest.mark.parametrize("shape", [(1, 1), (1, 3), (3, 5), (2, 17)])
+@pytest.mark.parametrize("precision", ["bf16", "f32"])
+def test_short_and_ragged_batches_match_oracle(shape, precision):
+    """Degenerate batch shapes (one token, sequences shorter than seq_len,
+    odd row counts) through one lazy step with the reference's z, both
+    precisions: positions read pos_emb[:T] like model.py:305-309; losses, g
+    and the flushed weights against the oracle.  (One step: with a 1-token
+    batch g is dominated by noise, so later steps of a trajectory diverge by
+    lr * dg * z and are compared with that bound elsewhere.)"""
+    cfg = ModelConfig(50, 32, 4, 2, 24, "f32")
+    bsz, t = shape
+    store = DeviceStore(cfg, init_seed=7, precision=precision)
+    om = _oracle_model(cfg)
+    seed = iteration_seeds(41, 1)[0]
+    ids, tg = O.synthetic_batch(cfg.vocab_size, t, bsz, 61)
+    lp, ln, g = O.mezo_step(om, ids, tg, EPS, LR, seed)
+    got = zo.mezo_step(store, Batch(ids, tg), zo.ZoHyper(EPS, LR), seed, mgr=RngStateManager("oracle"))
+    tol = 1e-6 if precision == "f32" else 2e-3
+    assert abs(got.loss_pos - lp) <= tol and abs(got.loss_neg - ln) <= tol, (shape, got, lp, ln)
+    assert abs(got.g - g) <= tol / EPS
+    zmax = float(np.abs(np.concatenate(O.z_stream(seed, om.sizes))).max())
+    diff = np.abs(store.theta.cpu().numpy().astype(np.float64) - np.concatenate(om.blocks)).max()
+    assert diff <= LR * abs(got.g - g) * zmax + 1e-6
