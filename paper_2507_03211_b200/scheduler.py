@@ -21,6 +21,15 @@ waits O(i) (slot reuse), so in steady state O(i-1) / C(i) / U(i+1) overlap.
 The update of iteration j is applied to each block on the device right before
 it is perturbed in iteration j+1 (the host master lags one update,
 test_offload.py:130-150); ``flush`` applies the last one.
+
+With one direction per rank (PertP / 2D) and ``redistribute="bf16"`` the
+exchange is the direction-aware one of SURVEY 8e: U(i) is the own fp32 slice
+only; C(i) updates that slice and writes both directions' perturbed values
+for it (bf16 weights in key order, fp32 vectors), every rank receives only
+its own direction's bf16 slices from the peers (half the NVLink bytes of the
+fp32 all-gather), and a strided copy lays them out as the GEMM operands.
+The perturbed values still come from the fp32 master, so the result is
+bit-identical to the fp32 redistribution.
 """
 
 from __future__ import annotations
@@ -158,6 +167,10 @@ class BlockSlot:
 
 def rebased_table(plan: ShadowPlan, bid: int, device) -> SegTable:
     """The block's perturb segments with shadow offsets relative to its slot."""
+    return SegTable(rebased_segments(plan, bid), device)
+
+
+def rebased_segments(plan: ShadowPlan, bid: int) -> list:
     if plan.views[bid]:
         wlo, _, vlo, _ = block_extent(plan, bid)
     else:
@@ -169,7 +182,7 @@ def rebased_table(plan: ShadowPlan, bid: int, device) -> SegTable:
         elif kind == L.ZO_SHADOW_F32:
             dst -= vlo
         segs.append((src, rows, cols, dst, ld, kind))
-    return SegTable(segs, device)
+    return segs
 
 
 # -----------------------------------------------------------------------------
@@ -220,7 +233,7 @@ def apply_thread_aligned_layout(store, n: int) -> dict:
 
 
 def sliced_upload(host_block: torch.Tensor, slot_theta: torch.Tensor, layout: SliceLayout, fabric, rank: int,
-                  stream=None):
+                  stream=None, gather: bool = True):
     """Phase 1: this rank's slice host -> device over its PCIe link; phase 2:
     the peers' slices arrive by an all-gather of the slot (NVLink), never
     from the host (comm.py:314-328).  slot_theta is padded to n * width."""
@@ -229,7 +242,7 @@ def sliced_upload(host_block: torch.Tensor, slot_theta: torch.Tensor, layout: Sl
     with torch.cuda.stream(stream) if stream is not None else _null():
         if ln:
             slot_theta[rank * w:rank * w + ln].copy_(host_block[off:off + ln], non_blocking=True)
-        if layout.n > 1:
+        if layout.n > 1 and gather:
             fabric.all_gather_tensor(slot_theta[:layout.n * w], slot_theta[rank * w:(rank + 1) * w], tag="param")
 
 
@@ -277,12 +290,16 @@ class OffloadedZo:
 
     def __init__(self, host: HostStore, hyper: ZoHyper, batch: int, device=None, n_slots: int = 3,
                  mode: str = "streams", fabric=None, strategy: str = "mezo", trace: bool = False,
-                 resident_blocks: int = 0):
+                 resident_blocks: int = 0, redistribute: str = "fp32"):
         """resident_blocks: keep the first k transformer blocks on the device
         for the whole run (uploaded once, written back at flush / sync_host)
         and stream only the rest -- use whatever HBM the model leaves free,
         so only the blocks that do not fit cross PCIe every step.  The
-        results are bit-identical for every k (same kernels, same order)."""
+        results are bit-identical for every k (same kernels, same order).
+
+        redistribute: "fp32" (all-gather the fp32 slices; every rank updates
+        and perturbs the whole block) or "bf16" (one direction per rank only:
+        the direction-aware bf16 exchange described in the module docstring)."""
         if mode not in ("streams", "serial"):
             raise ProtocolError(f"unknown scheduler mode {mode!r}")
         if n_slots < 2:
@@ -300,6 +317,12 @@ class OffloadedZo:
         self.mesh = MeshLayout("ddp" if strategy == "mezo" else strategy, self.world, self.rank) \
             if fabric is not None else None
         self.dirs = self.mesh.dirs if self.mesh is not None else (PLUS, MINUS)
+        if redistribute not in ("fp32", "bf16"):
+            raise ConfigurationError(f"redistribute must be 'fp32' or 'bf16', got {redistribute!r}")
+        if redistribute == "bf16" and (fabric is None or len(self.dirs) != 1):
+            raise ConfigurationError("bf16 redistribution needs a mesh with one direction per rank "
+                                     "(strategy 'pertp' or '2d')")
+        self.redistribute = redistribute
         if fabric is not None:
             apply_thread_aligned_layout(host, self.world)
         emb, head = self.layouts[0].block_id, self.layouts[-1].block_id
@@ -316,6 +339,17 @@ class OffloadedZo:
         tpl = self.wids[0] if self.wids else (self.resident[0] if self.resident else head)
         self.slots = [BlockSlot(self.plan, self.layouts, tpl, self.dirs, self.device, pad(tpl))
                       for _ in range(n_slots)]
+        self._bf16 = {}
+        if redistribute == "bf16" and self.wids:
+            me = self.dirs[0]
+            for slot in self.slots:                   # both directions' vectors, for the peers
+                slot.vsh[1 - me] = torch.zeros_like(slot.vsh[me])
+            # key-ordered bf16 staging of both directions, shared by the slots
+            # (C(i) runs on one stream)
+            self._stage = {d: torch.zeros(pad(tpl), dtype=torch.bfloat16, device=self.device) for d in (PLUS, MINUS)}
+            self._vgather = torch.zeros(self.world * 2 * self.slots[0].vsh[me].numel(), dtype=torch.float32,
+                                        device=self.device)
+            self._dir_of = [PLUS if q % 2 == 0 else MINUS for q in range(self.world)]
         self.tables = {bl.block_id: rebased_table(self.plan, bl.block_id, self.device) for bl in self.layouts}
         for bid, slot in self.persistent.items():      # embedding + head stay on the device
             self._upload(bid, slot, None)
@@ -336,17 +370,20 @@ class OffloadedZo:
         self.uploaded_params = self.offloaded_params = 0
 
     # -- byte movement --------------------------------------------------------------
-    def _upload(self, bid, slot, stream):
+    def _upload(self, bid, slot, stream, gather=None):
         slot.bind(bid)
+        if gather is None:      # the bf16 exchange replaces the fp32 all-gather of streamed blocks
+            gather = not (self.redistribute == "bf16" and bid in self.wids)
         if getattr(self.host, "is_sharded", False):      # HBM-sharded master (sharded.py)
-            self.host.upload_into(bid, slot.theta, stream)
+            self.host.upload_into(bid, slot.theta, stream, gather=gather)
             return
         hb = self.host.block_buf(bid)
         if self.fabric is None:
             with torch.cuda.stream(stream) if stream is not None else _null():
                 slot.theta[:hb.numel()].copy_(hb, non_blocking=True)
         else:
-            sliced_upload(hb, slot.theta, self.host.slice_plan["layouts"][bid], self.fabric, self.rank, stream)
+            sliced_upload(hb, slot.theta, self.host.slice_plan["layouts"][bid], self.fabric, self.rank, stream,
+                          gather=gather)
 
     def _offload(self, bid, slot, stream):
         if getattr(self.host, "is_sharded", False):
@@ -372,6 +409,71 @@ class OffloadedZo:
                                           t.n_segs, t.n_tiles, wa, va, wb, vb, +eps, -eps, flags,
                                           self.scal.data_ptr(), L.ZO_Z_PHILOX, 0, 0, 0, int(stream.cuda_stream)))
 
+    def _bf16_plan(self, bid):
+        """Per streamed block, built once: this rank's slice of the perturb
+        segments (bf16 weights -> key-ordered staging, fp32 vectors -> their
+        shadow slots), the strided re-layout of the staging into the GEMM
+        operands, and the owning rank of every vector shadow element."""
+        if bid in self._bf16:
+            return self._bf16[bid]
+        lay = self.host.slice_plan["layouts"][bid]
+        key0, total, w = self.layouts[bid].key0, lay.total, lay.width
+        rng = [(key0 + q * w, key0 + min((q + 1) * w, total)) for q in range(self.world)]
+        lo, hi = rng[self.rank]
+        me = self.dirs[0]
+        owner = torch.zeros(self.slots[0].vsh[me].numel(), dtype=torch.int64)
+        clipped, relayout = [], []
+        for (src, rows, cols, dst, ld, kind) in rebased_segments(self.plan, bid):
+            end = src + rows * cols
+            if kind == L.ZO_SHADOW_BF16:
+                relayout.append((src - key0, rows, cols, dst, ld))
+            elif kind == L.ZO_SHADOW_F32:
+                if rows > 1 and ld != cols:
+                    raise ConfigurationError("bf16 redistribution needs contiguous vector shadows")
+                for q, (a, b) in enumerate(rng):
+                    a, b = max(src, a), min(end, b)
+                    if a < b:
+                        owner[dst + a - src:dst + b - src] = q
+            a, b = max(src, lo), min(end, hi)
+            if a >= b:
+                continue
+            if kind == L.ZO_SHADOW_BF16:
+                clipped.append((a, 1, b - a, a - key0, b - a, kind))
+            elif kind == L.ZO_SHADOW_F32:
+                clipped.append((a, 1, b - a, dst + a - src, b - a, kind))
+            else:
+                clipped.append((a, 1, b - a, 0, b - a, kind))
+        plan = (SegTable(clipped, self.device), relayout, owner.to(self.device), w)
+        self._bf16[bid] = plan
+        return plan
+
+    def _perturb_slice(self, bid, slot, flags, stream):
+        """Update this rank's slice of the block's master and (with the shadow
+        flags) write both directions' perturbed values for it."""
+        t = self._bf16_plan(bid)[0]
+        eps = self.hyper.epsilon
+        L.check(L.lib().zo_perturb_update(slot.theta.data_ptr(), slot.key0, t.segs.data_ptr(), t.prefix.data_ptr(),
+                                          t.n_segs, t.n_tiles, self._stage[PLUS].data_ptr(),
+                                          slot.vsh[PLUS].data_ptr(), self._stage[MINUS].data_ptr(),
+                                          slot.vsh[MINUS].data_ptr(), +eps, -eps, flags, self.scal.data_ptr(),
+                                          L.ZO_Z_PHILOX, 0, 0, 0, int(stream.cuda_stream)))
+
+    def _redistribute_bf16(self, bid, slot, stream):
+        """C(i) prologue of the bf16 exchange: own slice -> both directions,
+        peers' slices of this rank's direction in, laid out as GEMM operands."""
+        _, relayout, owner, w = self._bf16_plan(bid)
+        me = self.dirs[0]
+        self._perturb_slice(bid, slot, L.ZO_PU_UPDATE | L.ZO_PU_SHADOW_A | L.ZO_PU_SHADOW_B, stream)
+        with torch.cuda.stream(stream):
+            self.fabric.exchange_slices(self._stage, me, self._dir_of, w, tag="param")
+            nv = slot.vsh[me].numel()
+            vg = self._vgather[:self.world * 2 * nv]
+            self.fabric.all_gather_tensor(vg, torch.cat([slot.vsh[PLUS], slot.vsh[MINUS]]), tag="param_vec")
+            slot.vsh[me].copy_(vg.view(self.world, 2, nv)[:, me].gather(0, owner[None])[0])
+            stage, wsh = self._stage[me], slot.wsh[me]
+            for (s0, rows, cols, d0, ld) in relayout:
+                torch.as_strided(wsh, (rows, cols), (ld, 1), d0).copy_(stage[s0:s0 + rows * cols].view(rows, cols))
+
     def _shadow_flags(self):
         f = 0
         if PLUS in self.dirs:
@@ -382,7 +484,10 @@ class OffloadedZo:
 
     def _compute(self, bid, slot, stream):
         """C(i): fused update+perturb of the block, then each direction's forward."""
-        self._perturb(bid, slot, L.ZO_PU_UPDATE | self._shadow_flags(), stream)
+        if self.redistribute == "bf16" and bid in self.wids:
+            self._redistribute_bf16(bid, slot, stream)
+        else:
+            self._perturb(bid, slot, L.ZO_PU_UPDATE | self._shadow_flags(), stream)
         eps = self.hyper.epsilon
         for s in self.dirs:
             loss_out = self.local.data_ptr() + 8 * s
@@ -509,7 +614,10 @@ class OffloadedZo:
         for i in self.wids:
             slot = self.slots[0]
             self._upload(i, slot, cs)
-            self._perturb(i, slot, L.ZO_PU_UPDATE, cs)
+            if self.redistribute == "bf16":
+                self._perturb_slice(i, slot, L.ZO_PU_UPDATE, cs)     # own slice only
+            else:
+                self._perturb(i, slot, L.ZO_PU_UPDATE, cs)
             self._offload(i, slot, cs)
             cs.synchronize()
         for bid, slot in self.persistent.items():

@@ -104,7 +104,7 @@ class ShardStore:
                     seg.mul_(0.02)
 
     # -- the two byte movements of the streaming schedule ----------------------------
-    def upload_into(self, bid: int, slot_theta: torch.Tensor, stream=None) -> None:
+    def upload_into(self, bid: int, slot_theta: torch.Tensor, stream=None, gather: bool = True) -> None:
         """Own slice -> its place in the (n * width padded) slot, then the
         peers' slices by an all-gather over NVLink (comm.py:314-328 with the
         host leg replaced by a device copy)."""
@@ -115,7 +115,7 @@ class ShardStore:
         with ctx:
             if ln:
                 slot_theta[self.rank * w:self.rank * w + ln].copy_(self.slice_of(bid), non_blocking=True)
-            if self.n > 1:
+            if self.n > 1 and gather:
                 self.fabric.all_gather_tensor(slot_theta[:self.n * w],
                                               slot_theta[self.rank * w:(self.rank + 1) * w], tag="param")
 

@@ -52,6 +52,27 @@ def fabric_worker(rank, world, port, q):
     q.put((rank, out))
 
 
+def exchange_worker(rank, world, port, width, q):
+    """CPU: the direction-aware slice exchange -- rank q ends up with slice k
+    of direction dir_of[q] from every rank k (gloo path)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2507_03211_b200.fabric import TorchFabric
+
+    init(rank, world, port)
+    fab = TorchFabric()
+    dir_of = [q % 2 for q in range(world)]
+    bufs = {d: torch.full((world * width,), float("nan"), dtype=torch.bfloat16) for d in (0, 1)}
+    for d in (0, 1):      # this rank's slice of each direction: value = 100 d + rank + i / 64
+        bufs[d][rank * width:(rank + 1) * width] = (100 * d + rank + torch.arange(width) / 64).bfloat16()
+    fab.exchange_slices(bufs, dir_of[rank], dir_of, width, tag="param")
+    out = bufs[dir_of[rank]].float().tolist()
+    nbytes = dict(fab.bytes_by_tag)
+    dist.destroy_process_group()
+    q.put((rank, out, nbytes))
+
+
 def gpu_strategy_worker(rank, world, port, strategy, name, steps, oracle, q):
     """GPU (all ranks on cuda:0, gloo collectives): run the eager strategy
     step of the drop-in API and report records + the master hash."""
@@ -185,6 +206,57 @@ def gpu_strategy_worker_theta(rank, world, port, strategy, steps, q):
     theta = store.theta.cpu().numpy()
     dist.destroy_process_group()
     q.put((rank, recs, theta))
+
+
+def sliced_dir_worker(rank, world, port, redistribute, steps, sharded, q):
+    """OffloadedZo on the 2D mesh (one direction per rank) with the fp32
+    all-gather or the direction-aware bf16 exchange, over a
+    shared host master or an HBM-sharded one (gloo, one GPU)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2507_03211_b200.fabric import TorchFabric
+    from paper_2507_03211_b200.model import ModelConfig, make_batch
+    from paper_2507_03211_b200.rng import iteration_seeds
+    from paper_2507_03211_b200.scheduler import HostStore, OffloadedZo
+    from paper_2507_03211_b200.sharded import ShardStore
+    from paper_2507_03211_b200.zo import ZoHyper
+
+    torch.cuda.set_device(0)
+    init(rank, world, port)
+    fab = TorchFabric()
+    cfg = ModelConfig(*DEEP, "f32")
+    path = f"/dev/shm/zo_b200_test_{port}"
+    if sharded:
+        host = ShardStore(cfg, fab, 7)
+    else:
+        if rank == 0:
+            host = HostStore(cfg, 7, shared=path)
+        fab.barrier()
+        if rank != 0:
+            host = HostStore(cfg, 7, init="attach", shared=path)
+    groups = world // 2
+    rt = OffloadedZo(host, ZoHyper(1e-3, 1e-2), batch=4 // groups, fabric=fab, strategy="2d",
+                     redistribute=redistribute)
+    fab.bytes_by_tag.clear()
+    recs = []
+    for j, s in enumerate(iteration_seeds(9, steps), 1):
+        r = rt.step(make_batch(cfg, 4, 40 + j).shard(groups, rank // 2), s)
+        recs.append((r.loss_pos, r.loss_neg, r.g))
+    nbytes = dict(fab.bytes_by_tag)
+    rt.flush()
+    torch.cuda.synchronize()
+    fab.barrier()
+    if sharded:
+        theta = host.gather_master()
+    else:
+        theta = host.theta.numpy().copy()
+        host.close()
+        fab.barrier()
+        if rank == 0:
+            os.unlink(path)
+    dist.destroy_process_group()
+    q.put((rank, recs, theta, nbytes))
 
 
 def sharded_worker(rank, world, port, strategy, steps, init_kind, q):

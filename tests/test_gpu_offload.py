@@ -97,6 +97,36 @@ def test_hbm_sharded_master_two_ranks_equals_resident(init_kind):
         assert np.array_equal(res[0][2], ddp[0][2])
 
 
+@pytest.mark.parametrize("world,sharded", [(2, False), (4, False), (4, True)])
+def test_direction_aware_bf16_redistribution_equals_fp32(world, sharded):
+    """SURVEY 8e direction-aware exchange: each rank updates and perturbs its
+    own slice for both directions and receives only its direction's bf16
+    slices.  Records and the final master equal the fp32 all-gather
+    redistribution bit for bit (2D mesh, host or HBM-sharded master, slices
+    that are not multiples of 4 and vectors split across ranks), with half
+    the per-step parameter bytes received."""
+    fp = H.run(H.sliced_dir_worker, world, "fp32", 3, sharded)
+    bf = H.run(H.sliced_dir_worker, world, "bf16", 3, sharded)
+    for a, b in zip(fp, bf):
+        assert a[1] == b[1]
+        assert np.array_equal(a[2], b[2])
+    for r in range(world):
+        assert [x[2] for x in fp[r][1]] == [x[2] for x in fp[0][1]]      # one g (losses are per group)
+        assert np.array_equal(fp[r][2], fp[0][2])
+        p32, p16 = fp[r][3]["param"], bf[r][3]["param"]
+        assert p16 * 2 <= p32 * 1.01, (p16, p32)
+
+
+def test_bf16_redistribution_needs_one_direction_per_rank():
+    from paper_2507_03211_b200.errors import ConfigurationError
+
+    host = HostStore(DEEP, 7)
+    with pytest.raises(ConfigurationError):
+        OffloadedZo(host, zo.ZoHyper(EPS, LR), batch=2, redistribute="bf16")
+    with pytest.raises(ConfigurationError):
+        OffloadedZo(host, zo.ZoHyper(EPS, LR), batch=2, redistribute="fp16")
+
+
 def test_hbm_sharded_single_rank_equals_resident():
     from paper_2507_03211_b200.sharded import ShardStore
 

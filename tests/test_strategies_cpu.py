@@ -30,6 +30,21 @@ def test_fabric_ordered_collectives_and_mesh_layout(world):
     assert set(outs[0]["bytes"]) <= {"seed", "loss", "grad", "checksum"}
 
 
+@pytest.mark.parametrize("world", [2, 4])
+def test_direction_aware_slice_exchange(world):
+    """rank q holds slice k of its own direction's buffer from
+    every rank k after the exchange; each rank contributes one bf16 slice."""
+    import torch
+
+    w = 5
+    res = H.run(H.exchange_worker, world, w)
+    for r, out, nbytes in res:
+        d = r % 2
+        want = [float(torch.tensor(100 * d + k + i / 64).bfloat16()) for k in range(world) for i in range(w)]
+        assert out == want
+        assert nbytes == {"param": w * 2}
+
+
 def test_mesh_layout_rejects_bad_meshes():
     from paper_2507_03211_b200.errors import ConfigurationError
     from paper_2507_03211_b200.strategies import MeshLayout, mesh_assignments
