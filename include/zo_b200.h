@@ -244,6 +244,14 @@ int zo_grad_finalize_groups(const double* losses, int32_t n_groups, int32_t plus
 int zo_hash_u64(const void* data, int64_t nbytes, uint64_t* out_dev,
                 uint64_t* scratch_dev /* >= 256 words */, void* stream);
 
+/* 16-bit planes of the fp32 master for transfer-compressed offload (SURVEY
+ * 8f row 4; no reference counterpart: it replaces the fp32 H2D / D2H of
+ * src/zosim/comm.py:314-342 with half the bytes): bits(theta[i]) =
+ * hi[i] << 16 | lo[i], exact both ways.  hi (the bf16 truncation) crosses
+ * PCIe, lo stays in device memory. */
+int zo_planes_join(const uint16_t* hi, const uint16_t* lo, float* theta, int64_t n, void* stream);
+int zo_planes_split(const float* theta, uint16_t* hi, uint16_t* lo, int64_t n, void* stream);
+
 /* Debug/test: the Philox direction itself, z[i] for keys e0 .. e0+n-1. */
 int zo_philox_normals(uint64_t seed, int64_t e0, int64_t n, float* out, void* stream);
 

@@ -68,6 +68,8 @@ SIGNATURES = {
     "zo_grad_finalize": (C.c_int, [P, P, D, D, P, P, P]),
     "zo_grad_finalize_groups": (C.c_int, [P, I32, I32, I32, I32, I32, I32, D, D, P, P, P]),
     "zo_hash_u64": (C.c_int, [P, I64, P, P, P]),
+    "zo_planes_join": (C.c_int, [P, P, P, I64, P]),
+    "zo_planes_split": (C.c_int, [P, P, P, I64, P]),
     "zo_philox_normals": (C.c_int, [U64, I64, I64, P, P]),
 }
 

@@ -57,6 +57,8 @@ int grad_finalize_launch(const double*, const double*, double, double, ZoStepSca
 int grad_groups_launch(const double*, int, int, int, int, int, int, double, double, ZoStepScalars*, double*,
                        cudaStream_t);
 int hash_launch(const void*, int64_t, uint64_t*, uint64_t*, int, cudaStream_t);
+int planes_join_launch(const uint16_t*, const uint16_t*, float*, int64_t, cudaStream_t);
+int planes_split_launch(const float*, uint16_t*, uint16_t*, int64_t, cudaStream_t);
 int gemm_launch(const void*, int64_t, const void*, int64_t, int64_t, int64_t, int64_t, int, const float*, void*,
                 int64_t, const int32_t*, float*, float*, int32_t*, void*, int64_t, cudaStream_t, const void*,
                 const float*, int64_t);
@@ -305,6 +307,16 @@ int zo_grad_finalize_groups(const double* losses, int32_t n_groups, int32_t plus
 int zo_hash_u64(const void* data, int64_t nbytes, uint64_t* out_dev, uint64_t* scratch_dev, void* stream) {
   ZO_CHECK_ARG(data && out_dev && scratch_dev && nbytes >= 0, ZO_ERR_CONFIG, "zo_hash_u64: bad argument");
   return zo::hash_launch(data, nbytes, out_dev, scratch_dev, 256, ZO_STREAM(stream));
+}
+
+int zo_planes_join(const uint16_t* hi, const uint16_t* lo, float* theta, int64_t n, void* stream) {
+  ZO_CHECK_ARG(n >= 0 && (n == 0 || (hi && lo && theta)), ZO_ERR_CONFIG, "zo_planes_join: bad argument");
+  return zo::planes_join_launch(hi, lo, theta, n, ZO_STREAM(stream));
+}
+
+int zo_planes_split(const float* theta, uint16_t* hi, uint16_t* lo, int64_t n, void* stream) {
+  ZO_CHECK_ARG(n >= 0 && (n == 0 || (hi && lo && theta)), ZO_ERR_CONFIG, "zo_planes_split: bad argument");
+  return zo::planes_split_launch(theta, hi, lo, n, ZO_STREAM(stream));
 }
 
 int zo_philox_normals(uint64_t seed, int64_t e0, int64_t n, float* out, void* stream) {

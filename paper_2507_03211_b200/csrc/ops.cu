@@ -343,6 +343,89 @@ __global__ void hash_final_kernel(const uint64_t* partial, int n, uint64_t* out)
   *out = acc;
 }
 
+// ---------------------------------------------------------------------------
+// 16-bit planes of the fp32 master (transfer compression):
+// bits(theta) = hi << 16 | lo.  The hi plane (the bf16 truncation of theta)
+// crosses PCIe; the lo plane stays in HBM; join / split are exact.  HBM-bound
+// elementwise passes, 8 elements per thread when all three pointers are
+// 16-byte aligned, a scalar grid-stride loop otherwise.
+// ---------------------------------------------------------------------------
+__global__ void planes_join_kernel(const uint16_t* __restrict__ hi, const uint16_t* __restrict__ lo,
+                                   uint32_t* __restrict__ out, int64_t n, bool vec) {
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+  int64_t done = 0;
+  if (vec) {
+    const int64_t n8 = n >> 3;
+    for (int64_t i = tid; i < n8; i += nth) {
+      const uint4 h = reinterpret_cast<const uint4*>(hi)[i];
+      const uint4 l = reinterpret_cast<const uint4*>(lo)[i];
+      const uint32_t hw[4] = {h.x, h.y, h.z, h.w}, lw[4] = {l.x, l.y, l.z, l.w};
+      uint32_t o[8];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        o[2 * j] = (hw[j] << 16) | (lw[j] & 0xFFFFu);
+        o[2 * j + 1] = (hw[j] & 0xFFFF0000u) | (lw[j] >> 16);
+      }
+      reinterpret_cast<uint4*>(out)[2 * i] = make_uint4(o[0], o[1], o[2], o[3]);
+      reinterpret_cast<uint4*>(out)[2 * i + 1] = make_uint4(o[4], o[5], o[6], o[7]);
+    }
+    done = n8 << 3;
+  }
+  for (int64_t i = done + tid; i < n; i += nth) out[i] = ((uint32_t)hi[i] << 16) | lo[i];
+}
+
+__global__ void planes_split_kernel(const uint32_t* __restrict__ in, uint16_t* __restrict__ hi,
+                                    uint16_t* __restrict__ lo, int64_t n, bool vec) {
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+  int64_t done = 0;
+  if (vec) {
+    const int64_t n8 = n >> 3;
+    for (int64_t i = tid; i < n8; i += nth) {
+      const uint4 a = reinterpret_cast<const uint4*>(in)[2 * i];
+      const uint4 b = reinterpret_cast<const uint4*>(in)[2 * i + 1];
+      const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+      uint32_t h[4], l[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        h[j] = (w[2 * j] >> 16) | (w[2 * j + 1] & 0xFFFF0000u);
+        l[j] = (w[2 * j] & 0xFFFFu) | (w[2 * j + 1] << 16);
+      }
+      reinterpret_cast<uint4*>(hi)[i] = make_uint4(h[0], h[1], h[2], h[3]);
+      reinterpret_cast<uint4*>(lo)[i] = make_uint4(l[0], l[1], l[2], l[3]);
+    }
+    done = n8 << 3;
+  }
+  for (int64_t i = done + tid; i < n; i += nth) {
+    const uint32_t w = in[i];
+    hi[i] = (uint16_t)(w >> 16);
+    lo[i] = (uint16_t)(w & 0xFFFFu);
+  }
+}
+
+static int planes_grid(int64_t n) {
+  const int64_t want = (n / 8 + 255) / 256;
+  const int64_t cap = (int64_t)num_sms() * 8;
+  return (int)(want < 1 ? 1 : (want < cap ? want : cap));
+}
+
+int planes_join_launch(const uint16_t* hi, const uint16_t* lo, float* out, int64_t n, cudaStream_t st) {
+  if (n == 0) return ZO_OK;
+  const bool vec = ((reinterpret_cast<uintptr_t>(hi) | reinterpret_cast<uintptr_t>(lo) |
+                     reinterpret_cast<uintptr_t>(out)) & 15) == 0;
+  planes_join_kernel<<<planes_grid(n), 256, 0, st>>>(hi, lo, reinterpret_cast<uint32_t*>(out), n, vec);
+  return launch_status("planes_join");
+}
+
+int planes_split_launch(const float* in, uint16_t* hi, uint16_t* lo, int64_t n, cudaStream_t st) {
+  if (n == 0) return ZO_OK;
+  const bool vec = ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(hi) |
+                     reinterpret_cast<uintptr_t>(lo)) & 15) == 0;
+  planes_split_kernel<<<planes_grid(n), 256, 0, st>>>(reinterpret_cast<const uint32_t*>(in), hi, lo, n, vec);
+  return launch_status("planes_split");
+}
+
 int hash_launch(const void* data, int64_t nbytes, uint64_t* out, uint64_t* scratch, int nblk, cudaStream_t st) {
   const bool aligned = (reinterpret_cast<uintptr_t>(data) & 7) == 0;
   if (!aligned) { set_error("zo_hash_u64: buffer must be 8-byte aligned"); return ZO_ERR_CONFIG; }

@@ -110,3 +110,20 @@ def hash_u64(t: torch.Tensor, stream=None) -> torch.Tensor:
     scratch = torch.empty(256, dtype=torch.int64, device=t.device)
     L.call("zo_hash_u64", _p(t), t.numel() * t.element_size(), _p(out), _p(scratch), L.stream_ptr(stream))
     return out
+
+
+def planes_join(hi: torch.Tensor, lo: torch.Tensor, out: torch.Tensor, stream=None) -> torch.Tensor:
+    """out (fp32) = the float whose bits are hi << 16 | lo (int16 planes)."""
+    n = out.numel()
+    if hi.numel() != n or lo.numel() != n or out.dtype != torch.float32:
+        raise ValueError("planes_join: hi / lo / out sizes or dtype mismatch")
+    L.call("zo_planes_join", _p(hi), _p(lo), _p(out), n, L.stream_ptr(stream))
+    return out
+
+
+def planes_split(theta: torch.Tensor, hi: torch.Tensor, lo: torch.Tensor, stream=None) -> None:
+    """hi / lo (int16) = the upper / lower 16 bits of each fp32 of theta."""
+    n = theta.numel()
+    if hi.numel() != n or lo.numel() != n or theta.dtype != torch.float32:
+        raise ValueError("planes_split: theta / hi / lo sizes or dtype mismatch")
+    L.call("zo_planes_split", _p(theta), _p(hi), _p(lo), n, L.stream_ptr(stream))

@@ -30,6 +30,16 @@ its own direction's bf16 slices from the peers (half the NVLink bytes of the
 fp32 all-gather), and a strided copy lays them out as the GEMM operands.
 The perturbed values still come from the fp32 master, so the result is
 bit-identical to the fp32 redistribution.
+
+``compress="split16"`` (transfer compression) halves the
+PCIe bytes of every streamed block: the fp32 master is kept as two exact
+16-bit planes, bits(theta) = hi << 16 | lo.  The hi plane (the bf16
+truncation) lives in pinned host memory and is what U(i) / O(i) move; the lo
+plane stays in HBM (2 B/param of the streamed blocks, or of this rank's
+slices); ``zo_planes_join`` / ``zo_planes_split`` rebuild / split the fp32
+block on the device, so every kernel sees the same fp32 values and the run
+is bit-identical to the uncompressed one.  The host fp32 master of streamed
+blocks is rebuilt by ``sync_host`` / ``flush``.
 """
 
 from __future__ import annotations
@@ -41,6 +51,7 @@ import numpy as np
 import torch
 
 from . import _lib as L
+from . import ops
 from .engine import MINUS, PLUS, SegTable, ShadowPlan, Workspace, block_extent
 from .errors import ConfigurationError, ConsistencyError, ProtocolError
 from .model import EMBEDDING, HEAD, TRANSFORMER, Batch, ModelConfig, init_block_host, model_layout
@@ -290,7 +301,7 @@ class OffloadedZo:
 
     def __init__(self, host: HostStore, hyper: ZoHyper, batch: int, device=None, n_slots: int = 3,
                  mode: str = "streams", fabric=None, strategy: str = "mezo", trace: bool = False,
-                 resident_blocks: int = 0, redistribute: str = "fp32"):
+                 resident_blocks: int = 0, redistribute: str = "fp32", compress: str = "none"):
         """resident_blocks: keep the first k transformer blocks on the device
         for the whole run (uploaded once, written back at flush / sync_host)
         and stream only the rest -- use whatever HBM the model leaves free,
@@ -299,7 +310,10 @@ class OffloadedZo:
 
         redistribute: "fp32" (all-gather the fp32 slices; every rank updates
         and perturbs the whole block) or "bf16" (one direction per rank only:
-        the direction-aware bf16 exchange described in the module docstring)."""
+        the direction-aware bf16 exchange described in the module docstring).
+
+        compress: "none" or "split16" (hi / lo 16-bit planes: half the PCIe
+        bytes per streamed block, lo kept in device memory; module docstring)."""
         if mode not in ("streams", "serial"):
             raise ProtocolError(f"unknown scheduler mode {mode!r}")
         if n_slots < 2:
@@ -323,6 +337,12 @@ class OffloadedZo:
             raise ConfigurationError("bf16 redistribution needs a mesh with one direction per rank "
                                      "(strategy 'pertp' or '2d')")
         self.redistribute = redistribute
+        if compress not in ("none", "split16"):
+            raise ConfigurationError(f"compress must be 'none' or 'split16', got {compress!r}")
+        if compress == "split16" and getattr(host, "is_sharded", False):
+            raise ConfigurationError("transfer compression applies to a host master (the HBM-sharded master "
+                                     "has no PCIe leg)")
+        self.compress = compress
         if fabric is not None:
             apply_thread_aligned_layout(host, self.world)
         emb, head = self.layouts[0].block_id, self.layouts[-1].block_id
@@ -350,6 +370,9 @@ class OffloadedZo:
             self._vgather = torch.zeros(self.world * 2 * self.slots[0].vsh[me].numel(), dtype=torch.float32,
                                         device=self.device)
             self._dir_of = [PLUS if q % 2 == 0 else MINUS for q in range(self.world)]
+        self._hi, self._lo = {}, {}
+        if compress == "split16" and self.wids:
+            self._init_planes()
         self.tables = {bl.block_id: rebased_table(self.plan, bl.block_id, self.device) for bl in self.layouts}
         for bid, slot in self.persistent.items():      # embedding + head stay on the device
             self._upload(bid, slot, None)
@@ -370,10 +393,55 @@ class OffloadedZo:
         self.uploaded_params = self.offloaded_params = 0
 
     # -- byte movement --------------------------------------------------------------
+    def _own(self, bid):
+        """(offset, length) of the part of block bid this rank moves over PCIe."""
+        if self.fabric is None:
+            return 0, self.layouts[bid].elem_count
+        _, off, ln = self.host.slice_plan["layouts"][bid].slices[self.rank]
+        return off, ln
+
+    def _init_planes(self):
+        """Split this rank's part of every streamed block once: lo into HBM,
+        hi into pinned host memory."""
+        own = {bid: self._own(bid) for bid in self.wids}
+        total = sum(ln for _, ln in own.values())
+        wmax = max(ln for _, ln in own.values())
+        self._hi_pool = torch.empty(total, dtype=torch.int16, pin_memory=True)
+        self._lo_pool = torch.empty(total, dtype=torch.int16, device=self.device)
+        for slot in self.slots:
+            slot.hi_stage = torch.empty(wmax, dtype=torch.int16, device=self.device)
+        tmp = torch.empty(wmax, dtype=torch.float32, device=self.device)
+        pos = 0
+        for bid in self.wids:
+            off, ln = own[bid]
+            self._hi[bid] = self._hi_pool[pos:pos + ln]
+            self._lo[bid] = self._lo_pool[pos:pos + ln]
+            pos += ln
+            tmp[:ln].copy_(self.host.block_buf(bid)[off:off + ln])
+            ops.planes_split(tmp[:ln], self.slots[0].hi_stage[:ln], self._lo[bid])
+            self._hi[bid].copy_(self.slots[0].hi_stage[:ln])
+        torch.cuda.synchronize(self.device)
+
+    def pcie_bytes_per_step(self):
+        """(H2D, D2H) bytes this rank moves per step for the streamed blocks."""
+        per = 2 if self.compress == "split16" else 4
+        n = sum(self._own(bid)[1] for bid in self.wids)
+        return per * n, per * n
+
     def _upload(self, bid, slot, stream, gather=None):
         slot.bind(bid)
         if gather is None:      # the bf16 exchange replaces the fp32 all-gather of streamed blocks
             gather = not (self.redistribute == "bf16" and bid in self.wids)
+        if bid in self._lo:                              # hi plane over PCIe, joined with the resident lo
+            off, ln = self._own(bid)
+            with torch.cuda.stream(stream) if stream is not None else _null():
+                slot.hi_stage[:ln].copy_(self._hi[bid], non_blocking=True)
+                ops.planes_join(slot.hi_stage[:ln], self._lo[bid], slot.theta[off:off + ln])
+                if self.fabric is not None and self.world > 1 and gather:
+                    w = self.host.slice_plan["layouts"][bid].width
+                    self.fabric.all_gather_tensor(slot.theta[:self.world * w],
+                                                  slot.theta[self.rank * w:(self.rank + 1) * w], tag="param")
+            return
         if getattr(self.host, "is_sharded", False):      # HBM-sharded master (sharded.py)
             self.host.upload_into(bid, slot.theta, stream, gather=gather)
             return
@@ -386,6 +454,12 @@ class OffloadedZo:
                           gather=gather)
 
     def _offload(self, bid, slot, stream):
+        if bid in self._lo:                              # split: lo stays, hi goes to the host
+            off, ln = self._own(bid)
+            with torch.cuda.stream(stream) if stream is not None else _null():
+                ops.planes_split(slot.theta[off:off + ln], slot.hi_stage[:ln], self._lo[bid])
+                self._hi[bid].copy_(slot.hi_stage[:ln], non_blocking=True)
+            return
         if getattr(self.host, "is_sharded", False):
             self.host.offload_from(bid, slot.theta, stream)
             return
@@ -628,8 +702,20 @@ class OffloadedZo:
         self.host.unflushed = False
 
     def sync_host(self) -> None:
-        """Copy the persistent device blocks back to the host master."""
+        """Copy the persistent device blocks back to the host master (and,
+        with split16 compression, rebuild the streamed blocks' fp32 master
+        from the hi / lo planes)."""
         cs = self.streams[COMPUTE]
+        if self._lo:
+            stage = self.slots[0].hi_stage
+            tmp = torch.empty(stage.numel(), dtype=torch.float32, device=self.device)
+            for bid in self.wids:
+                off, ln = self._own(bid)
+                with torch.cuda.stream(cs):
+                    stage[:ln].copy_(self._hi[bid], non_blocking=True)
+                    ops.planes_join(stage[:ln], self._lo[bid], tmp[:ln])
+                    self.host.block_buf(bid)[off:off + ln].copy_(tmp[:ln], non_blocking=True)
+                cs.synchronize()
         for bid, slot in self.persistent.items():
             if getattr(self.host, "is_sharded", False):
                 self.host.offload_from(bid, slot.theta, cs)

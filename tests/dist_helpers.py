@@ -208,7 +208,7 @@ def gpu_strategy_worker_theta(rank, world, port, strategy, steps, q):
     q.put((rank, recs, theta))
 
 
-def sliced_dir_worker(rank, world, port, redistribute, steps, sharded, q):
+def sliced_dir_worker(rank, world, port, redistribute, steps, sharded, compress, strategy, q):
     """OffloadedZo on the 2D mesh (one direction per rank) with the fp32
     all-gather or the direction-aware bf16 exchange, over a
     shared host master or an HBM-sharded one (gloo, one GPU)."""
@@ -235,15 +235,16 @@ def sliced_dir_worker(rank, world, port, redistribute, steps, sharded, q):
         fab.barrier()
         if rank != 0:
             host = HostStore(cfg, 7, init="attach", shared=path)
-    groups = world // 2
-    rt = OffloadedZo(host, ZoHyper(1e-3, 1e-2), batch=4 // groups, fabric=fab, strategy="2d",
-                     redistribute=redistribute)
+    groups = world // 2 if strategy == "2d" else world
+    rt = OffloadedZo(host, ZoHyper(1e-3, 1e-2), batch=4 // groups, fabric=fab, strategy=strategy,
+                     redistribute=redistribute, compress=compress)
     fab.bytes_by_tag.clear()
     recs = []
     for j, s in enumerate(iteration_seeds(9, steps), 1):
-        r = rt.step(make_batch(cfg, 4, 40 + j).shard(groups, rank // 2), s)
+        r = rt.step(make_batch(cfg, 4, 40 + j).shard(groups, rank // (world // groups)), s)
         recs.append((r.loss_pos, r.loss_neg, r.g))
     nbytes = dict(fab.bytes_by_tag)
+    nbytes["pcie"] = rt.pcie_bytes_per_step()
     rt.flush()
     torch.cuda.synchronize()
     fab.barrier()

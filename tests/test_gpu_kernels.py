@@ -271,3 +271,23 @@ def test_philox_normals_finite_over_a_large_window():
         assert bool(torch.isfinite(z).all())
         assert float(z.abs().max()) < 6.5
         del z
+
+
+@pytest.mark.parametrize("n,off", [(1, 0), (7, 1), (4096, 0), (100003, 3), (1 << 22, 8)])
+def test_planes_split_join_roundtrip(n, off):
+    """hi / lo 16-bit planes of fp32 (transfer compression): split then join
+    is the identity on the bits (incl. +-0, inf, NaN payloads, subnormals),
+    hi equals the upper half-word, for aligned and unaligned buffers."""
+    g = torch.Generator().manual_seed(n)
+    bits = torch.randint(-2**31, 2**31 - 1, (n + off,), generator=g, dtype=torch.int64).to(torch.int32)
+    special = torch.tensor([0, -2**31, 0x7F800000, -8388608, 0x7FC00001, 1, 0x00400000], dtype=torch.int32)
+    bits[off:off + min(n, special.numel())] = special[:min(n, special.numel())]
+    x = bits.view(torch.float32).to(DEV)[off:]
+    hi = torch.empty(n + off, dtype=torch.int16, device=DEV)[off:]
+    lo = torch.empty(n + off, dtype=torch.int16, device=DEV)[off:]
+    ops.planes_split(x, hi, lo)
+    y = torch.empty(n + off, dtype=torch.float32, device=DEV)[off:]
+    ops.planes_join(hi, lo, y)
+    torch.cuda.synchronize()
+    assert torch.equal(y.view(torch.int32).cpu(), bits[off:])
+    assert torch.equal(hi.cpu().to(torch.int32) & 0xFFFF, (bits[off:] >> 16) & 0xFFFF)

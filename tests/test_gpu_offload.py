@@ -105,8 +105,8 @@ def test_direction_aware_bf16_redistribution_equals_fp32(world, sharded):
     redistribution bit for bit (2D mesh, host or HBM-sharded master, slices
     that are not multiples of 4 and vectors split across ranks), with half
     the per-step parameter bytes received."""
-    fp = H.run(H.sliced_dir_worker, world, "fp32", 3, sharded)
-    bf = H.run(H.sliced_dir_worker, world, "bf16", 3, sharded)
+    fp = H.run(H.sliced_dir_worker, world, "fp32", 3, sharded, "none", "2d")
+    bf = H.run(H.sliced_dir_worker, world, "bf16", 3, sharded, "none", "2d")
     for a, b in zip(fp, bf):
         assert a[1] == b[1]
         assert np.array_equal(a[2], b[2])
@@ -125,6 +125,50 @@ def test_bf16_redistribution_needs_one_direction_per_rank():
         OffloadedZo(host, zo.ZoHyper(EPS, LR), batch=2, redistribute="bf16")
     with pytest.raises(ConfigurationError):
         OffloadedZo(host, zo.ZoHyper(EPS, LR), batch=2, redistribute="fp16")
+
+
+@pytest.mark.parametrize("mode", ["streams", "serial"])
+def test_split16_compressed_offload_equals_resident(mode):
+    """the fp32 master of streamed blocks as hi / lo 16-bit
+    planes (hi over PCIe, lo in HBM).  Records every step, the host master
+    rebuilt by sync_host (lagging one update, like the uncompressed path) and
+    the flushed master equal the resident run bit for bit; PCIe bytes halve."""
+    recs, thetas, final = _resident(DEEP, 4)
+    host = HostStore(DEEP, 7)
+    rt = OffloadedZo(host, zo.ZoHyper(EPS, LR), batch=2, mode=mode, compress="split16")
+    plain = OffloadedZo(HostStore(DEEP, 7), zo.ZoHyper(EPS, LR), batch=2, mode=mode)
+    assert [2 * b for b in rt.pcie_bytes_per_step()] == list(plain.pcie_bytes_per_step())
+    for j, s in enumerate(iteration_seeds(9, 4), 1):
+        r = rt.step(make_batch(DEEP, 2, 40 + j), s)
+        assert (r.loss_pos, r.loss_neg, r.g) == recs[j - 1]
+        rt.sync_host()
+        for bl in host.layouts[1:-1]:
+            assert np.array_equal(host.block_buf(bl.block_id).numpy(),
+                                  thetas[j - 1][bl.key0:bl.key0 + bl.elem_count])
+    rt.flush()
+    assert np.array_equal(host.theta.numpy(), final)
+
+
+@pytest.mark.parametrize("world,redistribute,strategy", [(2, "fp32", "ddp"), (4, "bf16", "2d")])
+def test_split16_sliced_offload_equals_uncompressed(world, redistribute, strategy):
+    """Compression composes with the sliced schedule (each rank keeps the lo
+    plane of its own slices) and with the bf16 exchange: bit-identical."""
+    a = H.run(H.sliced_dir_worker, world, redistribute, 3, False, "none", strategy)
+    b = H.run(H.sliced_dir_worker, world, redistribute, 3, False, "split16", strategy)
+    for x, y in zip(a, b):
+        assert x[1] == y[1]
+        assert np.array_equal(x[2], y[2])
+        assert [2 * v for v in y[3]["pcie"]] == list(x[3]["pcie"])
+
+
+def test_split16_rejects_sharded_master_and_unknown_modes():
+    from paper_2507_03211_b200.errors import ConfigurationError
+    from paper_2507_03211_b200.sharded import ShardStore
+
+    with pytest.raises(ConfigurationError):
+        OffloadedZo(ShardStore(DEEP, None, 7), zo.ZoHyper(EPS, LR), batch=2, compress="split16")
+    with pytest.raises(ConfigurationError):
+        OffloadedZo(HostStore(DEEP, 7), zo.ZoHyper(EPS, LR), batch=2, compress="fp8")
 
 
 def test_hbm_sharded_single_rank_equals_resident():
