@@ -33,15 +33,20 @@ def main():
         from paper_2507_03211_b200.sharded import ShardStore
         shards = ShardStore(cfg, None, 7, init="philox")
         rt = OffloadedZo(shards, hyper, batch=B, trace=True)
-    else:   # "offload", "offload:K" (K blocks resident) or "offload:budget=GB" (plan_residency)
+    else:   # "offload", "offload:K" (K blocks resident) or "offload:budget=GB" (plan_residency),
+        # optionally ":split16" (hi / lo plane transfer compression)
         from paper_2507_03211_b200.scheduler import HostStore, OffloadedZo, plan_residency
-        arg = mode.split(":")[1] if ":" in mode else "0"
+        parts = mode.split(":")
+        compress = "split16" if "split16" in parts[1:] else "none"
+        rest = [p for p in parts[1:] if p != "split16"]
+        arg = rest[0] if rest else "0"
         if arg.startswith("budget="):
             k, slots = plan_residency(cfg, int(float(arg.split("=")[1]) * 1e9))
         else:
             k, slots = int(arg), (6 if int(arg) else 3)
         host = HostStore(cfg, 7, init="philox")
-        rt = OffloadedZo(host, hyper, batch=B, trace=True, resident_blocks=k, n_slots=max(slots, 2))
+        rt = OffloadedZo(host, hyper, batch=B, trace=True, resident_blocks=k, n_slots=max(slots, 2),
+                         compress=compress)
     torch.cuda.synchronize()
     init_s = time.time() - t0
     seeds = iteration_seeds(1234, steps)
@@ -63,6 +68,8 @@ def main():
         busy = {k: sum(e["end"] - e["start"] for e in tl if e["op"] == k) for k in ("upload", "compute", "offload")}
         out["stream_busy_ms"] = {k: round(v, 2) for k, v in busy.items()}
         out["makespan_ms"] = round(rt.makespan(), 2)
+        if hasattr(rt, "pcie_bytes_per_step"):
+            out["pcie_gb_per_step"] = [round(b / 1e9, 2) for b in rt.pcie_bytes_per_step()]
     print(json.dumps(out))
 
 
