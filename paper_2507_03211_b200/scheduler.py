@@ -734,31 +734,40 @@ class OffloadedZo:
         return max(e["end"] for e in tl) if tl else float("nan")
 
 
-def plan_residency(config: ModelConfig, budget_bytes: int, n_dirs: int = 2, max_slots: int = 8):
+def plan_residency(config: ModelConfig, budget_bytes: int, n_dirs: int = 2, max_slots: int = 8,
+                   compress: str = "none"):
     """(resident_blocks, n_slots) for OffloadedZo under a device-memory budget
     for the transformer blocks: a block costs 4 B/param of fp32 master + 2 B
-    per direction of bf16 shadow, resident or in a slot.  As many blocks as
-    fit stay resident (each one removes a block's H2D + D2H per step); the
-    slots only need to prefetch what PCIe can move while the resident blocks
-    compute (~1 upload per 8 resident blocks at the measured 49 GB/s and
-    ~3 ms of compute per OPT-13B block), so they get just that depth (>= 3,
-    or whatever fits).  The embedding / head / activations are outside the
-    budget."""
+    per direction of bf16 shadow, resident or in a slot, and with
+    compress="split16" every streamed block also keeps its 2 B/param lo plane
+    on the device.  As many blocks as fit stay resident (each one removes a
+    block's H2D + D2H per step); the slots only need to prefetch what PCIe
+    can move while the resident blocks compute (~1 upload per 8 resident
+    blocks at the measured 49 GB/s and ~3 ms of compute per OPT-13B block), so
+    they get just that depth (>= 3, or whatever fits).  The embedding / head /
+    activations are outside the budget."""
     from .model import model_layout
 
+    if compress not in ("none", "split16"):
+        raise ConfigurationError(f"compress must be 'none' or 'split16', got {compress!r}")
     blocks = [bl for bl in model_layout(config) if bl.kind == TRANSFORMER]
     nb = len(blocks)
-    per = blocks[0].elem_count * (4 + 2 * n_dirs)
-    fit = int(budget_bytes // per)
-    if fit >= nb:
+    P = blocks[0].elem_count
+    per = P * (4 + 2 * n_dirs)
+    lo = P * (2 if compress == "split16" else 0)          # per streamed block
+    if nb * per <= budget_bytes:
         return nb, 0
-    if fit <= 3:
-        return 0, max(2, fit)
+
+    def kmax(slots):          # resident blocks that fit beside `slots` slots
+        return int((budget_bytes - slots * per - nb * lo) // (per - lo))
+
+    if kmax(0) <= 3:
+        return 0, max(2, min(3, int((budget_bytes - nb * lo) // per)))
     for slots in range(3, max_slots + 1):
-        k = fit - slots
+        k = kmax(slots)
         if slots >= min(max_slots, max(3, k // 8 + 1)):
-            return k, slots
-    return fit - max_slots, max_slots
+            return max(k, 0), slots
+    return max(kmax(max_slots), 0), max_slots
 
 
 def _load(ws: Workspace, batch: Batch):

@@ -48,3 +48,28 @@ def test_plan_residency_fills_the_budget():
         else:
             assert 0 <= k < nb and 2 <= slots <= nb - k
             assert (k + slots) * per <= max(gb * 1e9, 2 * per)
+
+
+def test_plan_residency_counts_split16_lo_planes():
+    """With compress="split16" the streamed blocks' 2 B/param lo planes sit in
+    the same budget: fewer resident blocks, never over budget (when the
+    planes + 3 slots fit at all), and the uncompressed plan is unchanged."""
+    from paper_2507_03211_b200.errors import ConfigurationError
+    from paper_2507_03211_b200.model import model_layout, opt_config
+    from paper_2507_03211_b200.scheduler import plan_residency
+
+    cfg = opt_config("opt-13b", 2048)
+    P = [bl for bl in model_layout(cfg) if bl.kind == "transformer"][0].elem_count
+    per, lo, nb = 8 * P, 2 * P, cfg.n_blocks
+    for gb in (40, 60, 80, 100, 120):
+        b = int(gb * 1e9)
+        k0, s0 = plan_residency(cfg, b)
+        k, slots = plan_residency(cfg, b, compress="split16")
+        if nb * per <= b:
+            assert (k, slots) == (k0, s0) == (nb, 0)
+            continue
+        assert k <= k0 and slots >= 2
+        if nb * lo + 3 * per <= b:
+            assert (k + slots) * per + (nb - k) * lo <= b
+    with pytest.raises(ConfigurationError):
+        plan_residency(cfg, int(60e9), compress="fp8")

@@ -41,7 +41,7 @@ def main():
         rest = [p for p in parts[1:] if p != "split16"]
         arg = rest[0] if rest else "0"
         if arg.startswith("budget="):
-            k, slots = plan_residency(cfg, int(float(arg.split("=")[1]) * 1e9))
+            k, slots = plan_residency(cfg, int(float(arg.split("=")[1]) * 1e9), compress=compress)
         else:
             k, slots = int(arg), (6 if int(arg) else 3)
         host = HostStore(cfg, 7, init="philox")
