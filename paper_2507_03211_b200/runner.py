@@ -72,6 +72,7 @@ class RunConfig:
     data_seed: int = 99
     init: str = "host"             # "host" (zosim's numpy draws) or "philox" (random-init at scale)
     device_capacity_blocks: float | None = None   # zo2: HBM budget in transformer-block footprints
+    offload_compress: str = "none"                 # zo2: "split16" = hi plane over PCIe, lo plane in HBM
     report_dir: str | None = None
 
     def validate(self) -> "RunConfig":
@@ -103,6 +104,8 @@ class RunConfig:
             raise ConfigurationError("batch_size must be >= 1")
         if self.init not in ("host", "philox"):
             raise ConfigurationError(f"init must be 'host' or 'philox', got {self.init!r}")
+        if self.offload_compress not in ("none", "split16"):
+            raise ConfigurationError(f"offload_compress must be 'none' or 'split16', got {self.offload_compress!r}")
         return self
 
     @classmethod
@@ -143,6 +146,7 @@ class RunConfig:
             "data_seed": self.data_seed,
             "init": self.init,
             "device_capacity_blocks": self.device_capacity_blocks,
+            "offload_compress": self.offload_compress,
         }
 
 
@@ -266,10 +270,11 @@ def _run_zo2(config: RunConfig) -> RunReport:
         from .scheduler import plan_residency
 
         per = [bl for bl in model_layout(config.model) if bl.kind == "transformer"][0].elem_count * 8
-        k, slots = plan_residency(config.model, int(config.device_capacity_blocks * per))
+        k, slots = plan_residency(config.model, int(config.device_capacity_blocks * per),
+                                  compress=config.offload_compress)
         slots = max(slots, 2)
     rt = OffloadedZo(host, config.hyper, config.batch_size, device=dev, trace=True, resident_blocks=k,
-                     n_slots=slots)
+                     n_slots=slots, compress=config.offload_compress)
     steps, walls = [], []
     for j, seed in enumerate(iteration_seeds(config.seed, config.hyper.steps), 1):
         batch = batch_for(config, j)
@@ -277,7 +282,8 @@ def _run_zo2(config: RunConfig) -> RunReport:
         steps.append(rt.step(batch, seed))
         walls.append(time.perf_counter() - t)
     rt.flush()
-    comm = {"host_upload_bytes": rt.uploaded_params * 4, "host_offload_bytes": rt.offloaded_params * 4}
+    bpp = 2 if config.offload_compress == "split16" else 4      # PCIe bytes per streamed parameter
+    comm = {"host_upload_bytes": rt.uploaded_params * bpp, "host_offload_bytes": rt.offloaded_params * bpp}
     tps = _tokens_per_step(config)
     peak = int(torch.cuda.max_memory_allocated(dev))
     return RunReport("zo2", 1, steps, throughput(walls, tps), tps * len(steps) / sum(walls), sum(walls),

@@ -86,6 +86,10 @@ def test_run_outputs_and_mezo_equals_zo2(tmp_path):
     rep = run(_rc(strategy="zo2", report_dir=str(out), device_capacity_blocks=3.0))
     reps["zo2cap"] = rep
     assert rep.final_checksum == reps["zo2"].final_checksum
+    # transfer compression: same trajectory, half the PCIe bytes
+    rep = run(_rc(strategy="zo2", report_dir=str(tmp_path / "zo2c"), offload_compress="split16"))
+    assert rep.final_checksum == reps["zo2"].final_checksum
+    assert 2 * rep.comm_bytes["host_upload_bytes"] == reps["zo2"].comm_bytes["host_upload_bytes"]
     a, b = reps["mezo"], reps["zo2"]
     assert [(s.loss_pos, s.loss_neg, s.g) for s in a.steps] == [(s.loss_pos, s.loss_neg, s.g) for s in b.steps]
     assert a.final_checksum == b.final_checksum
