@@ -289,6 +289,7 @@ def ours(args, rank, world, local_rank):
         return 2.0 * args_[4] * args_[5] * args_[6]
 
     pert_ev, gemm_ev, all_ev = [], [], []   # all_ev: every library call of the instrumented replay
+    gemm_shape_ev = []
 
     def one_step(j, instrument=False):
         for ws in wss:
@@ -317,6 +318,8 @@ def ours(args, rank, world, local_rank):
                 elif i in gemm_set:
                     gemm_ev.append((e0, e1, gemm_flops(fn, a)))
                 all_ev.append((fn.__name__, e0, e1))
+                if i in gemm_set and fn.__name__ == "zo_gemm_bf16_split":      # per-shape split of the GEMM time
+                    gemm_shape_ev.append((f"{a[5]}x{a[6]}x{a[7]}", e0, e1))
         if hasattr(runner, "post_step"):
             runner.post_step()
 
@@ -381,6 +384,11 @@ def ours(args, rank, world, local_rank):
     for name, a, b in all_ev:
         breakdown[name] = breakdown.get(name, 0.0) + a.elapsed_time(b) / args.steps
     g_flops = sum(f for _, _, f in gemm_ev)
+    gemm_shapes = {}
+    for name, a, b in gemm_shape_ev:
+        gemm_shapes.setdefault(name, []).append(a.elapsed_time(b) * 1e3)
+    gemm_shapes = {k: {"n_per_step": len(v) // args.steps, "median_us": round(statistics.median(v), 1)}
+                   for k, v in gemm_shapes.items()}
     rec = store.record.cpu().numpy()
 
     # e2e through the public API: host batch -> device, record -> host, every step
@@ -446,6 +454,7 @@ def ours(args, rank, world, local_rank):
         "roofline": dominant, "roofline_other": other,
         "perturb_kernel_gbs": pert_gbs,
         "breakdown_ms_per_step": {k: round(v, 4) for k, v in sorted(breakdown.items(), key=lambda kv: -kv[1])},
+        "gemm_us_by_shape": gemm_shapes,
         "clocks": clk.summary(),
         "gpu_launches": n_launch * args.steps,
         "e2e": {"value": tokens / (e2e_ms * 1e-3), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
