@@ -61,11 +61,17 @@ __host__ __device__ __forceinline__ uint32_t mulhi32(uint32_t a, uint32_t b) {
 #endif
 }
 
+// Philox4x32 round count: 10 (Random123's recommended default; the value
+// every test and measurement uses).  Overridable at build time only for
+// experiments (-DZO_PHILOX_ROUNDS=7, the smallest count that passes BigCrush).
+#ifndef ZO_PHILOX_ROUNDS
+#define ZO_PHILOX_ROUNDS 10
+#endif
 __host__ __device__ __forceinline__ u32x4 philox4x32_10(uint64_t ctr, uint64_t seed) {
   uint32_t c0 = (uint32_t)ctr, c1 = (uint32_t)(ctr >> 32), c2 = 0u, c3 = 0u;
   uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
 #pragma unroll
-  for (int r = 0; r < 10; ++r) {
+  for (int r = 0; r < ZO_PHILOX_ROUNDS; ++r) {
     const uint64_t p0 = (uint64_t)0xD2511F53u * c0;   // one IMAD.WIDE.U32: hi and lo
     const uint64_t p1 = (uint64_t)0xCD9E8D57u * c2;
     const uint32_t n0 = (uint32_t)(p1 >> 32) ^ c1 ^ k0, n2 = (uint32_t)(p0 >> 32) ^ c3 ^ k1;
@@ -99,20 +105,20 @@ __device__ __forceinline__ void box_muller(uint32_t a, uint32_t b, float& z0, fl
 // computed once per thread (PhiloxKeys) and each round is 2 IMAD.WIDE.U32 +
 // 2 LOP3.  Produces exactly the words of philox4x32_10 (same z everywhere).
 // ---------------------------------------------------------------------------
-struct PhiloxKeys { uint32_t k0[10], k1[10]; };
+struct PhiloxKeys { uint32_t k0[ZO_PHILOX_ROUNDS], k1[ZO_PHILOX_ROUNDS]; };
 
 __host__ __device__ __forceinline__ PhiloxKeys philox_keys(uint64_t seed) {
   PhiloxKeys k;
   uint32_t a = (uint32_t)seed, b = (uint32_t)(seed >> 32);
 #pragma unroll
-  for (int r = 0; r < 10; ++r) { k.k0[r] = a; k.k1[r] = b; a += 0x9E3779B9u; b += 0xBB67AE85u; }
+  for (int r = 0; r < ZO_PHILOX_ROUNDS; ++r) { k.k0[r] = a; k.k1[r] = b; a += 0x9E3779B9u; b += 0xBB67AE85u; }
   return k;
 }
 
 __device__ __forceinline__ u32x4 philox4x32_10_k(uint64_t ctr, const PhiloxKeys& k) {
   uint32_t c0 = (uint32_t)ctr, c1 = (uint32_t)(ctr >> 32), c2 = 0u, c3 = 0u;
 #pragma unroll
-  for (int r = 0; r < 10; ++r) {
+  for (int r = 0; r < ZO_PHILOX_ROUNDS; ++r) {
     const uint64_t p0 = (uint64_t)0xD2511F53u * c0;
     const uint64_t p1 = (uint64_t)0xCD9E8D57u * c2;
     const uint32_t n0 = (uint32_t)(p1 >> 32) ^ c1 ^ k.k0[r];
@@ -146,7 +152,7 @@ __device__ __forceinline__ void philox4x32_10_xn(const uint64_t (&ctr)[N], uint6
   for (int i = 0; i < N; ++i) { c0[i] = (uint32_t)ctr[i]; c1[i] = (uint32_t)(ctr[i] >> 32); c2[i] = 0u; c3[i] = 0u; }
   uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
 #pragma unroll
-  for (int r = 0; r < 10; ++r) {
+  for (int r = 0; r < ZO_PHILOX_ROUNDS; ++r) {
 #pragma unroll
     for (int i = 0; i < N; ++i) {
       const uint64_t p0 = (uint64_t)0xD2511F53u * c0[i];
