@@ -15,7 +15,7 @@ __global__ void embed_kernel(const float* __restrict__ tok, int64_t tok_key0,
                              const float* __restrict__ pos, int64_t pos_key0,
                              const int32_t* __restrict__ ids, int64_t seq, int64_t d, int64_t vocab,
                              double scale, const ZoStepScalars* scal, const double* z, int64_t z_key0,
-                             float* __restrict__ x, int64_t ldx, int32_t* err) {
+                             float* __restrict__ x, int64_t ldx, int32_t* err, bool vec) {
   pdl_trigger();
   pdl_wait();
   const int64_t m = blockIdx.x;
@@ -27,6 +27,27 @@ __global__ void embed_kernel(const float* __restrict__ tok, int64_t tok_key0,
   }
   const uint64_t seed = scal ? scal->seed_cur : 0ull;
   const float s32 = (float)scale;
+  if constexpr (ZMODE == ZO_Z_PHILOX) {
+    if (vec) {
+      // 4 consecutive elements per thread = one Philox4x32 counter (keys
+      // 4-aligned): one generator call per 4 outputs instead of per output,
+      // the same z values and arithmetic as the scalar loop below
+      const int64_t kt0 = tok_key0 + id * d, kp0 = pos_key0 + t * d;
+      for (int64_t c = 4 * (int64_t)threadIdx.x; c < d; c += 4 * (int64_t)blockDim.x) {
+        float4 a = *reinterpret_cast<const float4*>(tok + id * d + c);
+        float4 b = *reinterpret_cast<const float4*>(pos + t * d + c);
+        if (scale != 0.0) {
+          const f32x4 za = philox_normal4(seed, (uint64_t)(kt0 + c) >> 2);
+          const f32x4 zb = philox_normal4(seed, (uint64_t)(kp0 + c) >> 2);
+          a.x = fmaf(s32, za.x, a.x); a.y = fmaf(s32, za.y, a.y); a.z = fmaf(s32, za.z, a.z); a.w = fmaf(s32, za.w, a.w);
+          b.x = fmaf(s32, zb.x, b.x); b.y = fmaf(s32, zb.y, b.y); b.z = fmaf(s32, zb.z, b.z); b.w = fmaf(s32, zb.w, b.w);
+        }
+        *reinterpret_cast<float4*>(x + m * ldx + c) =
+            make_float4(__fadd_rn(a.x, b.x), __fadd_rn(a.y, b.y), __fadd_rn(a.z, b.z), __fadd_rn(a.w, b.w));
+      }
+      return;
+    }
+  }
   for (int64_t c = threadIdx.x; c < d; c += blockDim.x) {
     const int64_t kt = tok_key0 + id * d + c, kp = pos_key0 + t * d + c;
     float a = tok[id * d + c], b = pos[t * d + c];
@@ -49,13 +70,17 @@ int embed_launch(const float* tok, int64_t tok_key0, const float* pos, int64_t p
                  int64_t z_key0, float* x, int64_t ldx, int32_t* err, cudaStream_t st) {
   const int64_t rows = batch * seq;
   if (rows == 0) return ZO_OK;
-  const int threads = d >= 256 ? 256 : (int)((d + 31) / 32 * 32);
+  const bool vec = zmode == ZO_Z_PHILOX && d % 4 == 0 && tok_key0 % 4 == 0 && pos_key0 % 4 == 0 && ldx % 4 == 0 &&
+                   ((reinterpret_cast<uintptr_t>(tok) | reinterpret_cast<uintptr_t>(pos) |
+                     reinterpret_cast<uintptr_t>(x)) & 15) == 0;
+  const int64_t lanes = vec ? d / 4 : d;
+  const int threads = lanes >= 256 ? 256 : (int)((lanes + 31) / 32 * 32);
   if (zmode == ZO_Z_PHILOX)
     launch_k(embed_kernel<ZO_Z_PHILOX>, dim3((unsigned)rows), dim3(threads), 0, st, tok, tok_key0, pos, pos_key0, ids,
-             seq, d, vocab, scale, scal, z, z_key0, x, ldx, err);
+             seq, d, vocab, scale, scal, z, z_key0, x, ldx, err, vec);
   else
     launch_k(embed_kernel<ZO_Z_ORACLE>, dim3((unsigned)rows), dim3(threads), 0, st, tok, tok_key0, pos, pos_key0, ids,
-             seq, d, vocab, scale, scal, z, z_key0, x, ldx, err);
+             seq, d, vocab, scale, scal, z, z_key0, x, ldx, err, false);
   return launch_status("embed_kernel");
 }
 

@@ -291,3 +291,38 @@ def test_planes_split_join_roundtrip(n, off):
     torch.cuda.synchronize()
     assert torch.equal(y.view(torch.int32).cpu(), bits[off:])
     assert torch.equal(hi.cpu().to(torch.int32) & 0xFFFF, (bits[off:] >> 16) & 0xFFFF)
+
+
+@pytest.mark.parametrize("tok_key0,d", [(0, 2048), (4096, 64), (2, 64), (0, 30)])
+def test_embed_perturb_on_gather_matches_philox(tok_key0, d):
+    """zo_embed_fwd (Philox mode): the 4-element vector path (4-aligned keys
+    and buffers) gives the same bits as the scalar path at the same keys
+    (forced by a misaligned output row), and both equal
+    f32(tok[id] + eps z) + f32(pos[t] + eps z) with z from zo_philox_normals
+    (reference in float64, one fused rounding)."""
+    V, T, B, eps, seed = 97, 16, 3, 1e-3, 0x1234_5678_9ABC
+    pos_key0 = tok_key0 + V * d
+    g = torch.Generator().manual_seed(d)
+    tok = torch.randn(V * d, generator=g).to(DEV)
+    pos = torch.randn(T * d, generator=g).to(DEV)
+    ids = torch.randint(0, V, (B * T,), generator=g, dtype=torch.int32).to(DEV)
+    scal = torch.zeros(4, dtype=torch.int64, device=DEV)
+    scal[0] = seed
+    err = torch.zeros(1, dtype=torch.int32, device=DEV)
+    outs = []
+    for off in (0, 1):                 # off = 1: output not 16-byte aligned -> scalar path
+        buf = torch.full((B * T * d + 4,), float("nan"), device=DEV)
+        x = buf[off:off + B * T * d]
+        L.check(L.lib().zo_embed_fwd(tok.data_ptr(), tok_key0, pos.data_ptr(), pos_key0, ids.data_ptr(), B, T, d,
+                                     V, eps, scal.data_ptr(), L.ZO_Z_PHILOX, 0, 0, x.data_ptr(), d, err.data_ptr(),
+                                     L.stream_ptr()))
+        outs.append(x.view(B * T, d).clone())
+    torch.cuda.synchronize()
+    assert err.item() == 0
+    assert torch.equal(outs[0], outs[1])
+    zt = ops.philox_normals(seed, tok_key0, V * d).view(V, d).double()
+    zp = ops.philox_normals(seed, pos_key0, T * d).view(T, d).double()
+    e32 = float(torch.tensor(eps, dtype=torch.float32))
+    a = (tok.view(V, d).double() + e32 * zt).float()[ids.long()]
+    b = (pos.view(T, d).double() + e32 * zp).float().repeat(B, 1)
+    torch.testing.assert_close(outs[0], a + b, rtol=0, atol=0)
