@@ -46,6 +46,7 @@ from __future__ import annotations
 
 import hashlib
 import time
+from typing import NamedTuple
 
 import numpy as np
 import torch
@@ -200,6 +201,13 @@ def rebased_segments(plan: ShadowPlan, bid: int) -> list:
 # slicing (comm.py:106-119, 314-358)
 # -----------------------------------------------------------------------------
 
+class Slice(NamedTuple):
+    """One contiguous slice of a block (comm.py's Slice: owner, offset, length)."""
+    owner: int
+    offset: int
+    length: int
+
+
 class SliceLayout:
     """Ceil-width slices, owner i = rank i, last one may be short
     (comm.py:106-119)."""
@@ -213,8 +221,14 @@ class SliceLayout:
         off = 0
         for owner in range(n):
             length = max(min(self.width, total - off), 0)
-            self.slices.append((owner, off, length))
+            self.slices.append(Slice(owner, off, length))
             off += length
+
+    def __eq__(self, other):
+        return isinstance(other, SliceLayout) and (self.block_id, self.total, self.n, self.slices) == (
+            other.block_id, other.total, other.n, other.slices)
+
+    __hash__ = None
 
     @classmethod
     def build(cls, block_id: int, total: int, n: int) -> "SliceLayout":
@@ -255,6 +269,50 @@ def sliced_upload(host_block: torch.Tensor, slot_theta: torch.Tensor, layout: Sl
             slot_theta[rank * w:rank * w + ln].copy_(host_block[off:off + ln], non_blocking=True)
         if layout.n > 1 and gather:
             fabric.all_gather_tensor(slot_theta[:layout.n * w], slot_theta[rank * w:(rank + 1) * w], tag="param")
+
+
+def execute_sliced_upload(host_buf, layout: SliceLayout, devices=None) -> list:
+    """comm.py:314-328 for one process driving ``layout.n`` device replicas
+    (``devices``: one CUDA device per owner; default: all on the current
+    GPU).  Phase 1: each replica pulls its own slice from the host; phase 2:
+    the rest comes from the owning replica (device to device -- NVLink peer
+    copies between GPUs), never from the host.  ``host_buf``: numpy array or
+    tensor (shared, not copied).  Returns the replicas (device tensors)."""
+    host = torch.as_tensor(host_buf)
+    if host.numel() != layout.total:
+        raise ConfigurationError("layout does not match buffer size")
+    devs = list(devices) if devices is not None else [torch.device("cuda", torch.cuda.current_device())] * layout.n
+    if len(devs) != layout.n:
+        raise ConfigurationError(f"need {layout.n} devices, got {len(devs)}")
+    reps = [torch.empty(layout.total, dtype=host.dtype, device=d) for d in devs]
+    for s in layout.slices:
+        if s.length:
+            reps[s.owner][s.offset:s.offset + s.length].copy_(host[s.offset:s.offset + s.length])
+    for s in layout.slices:
+        for dst in range(layout.n):
+            if dst != s.owner and s.length:
+                reps[dst][s.offset:s.offset + s.length].copy_(reps[s.owner][s.offset:s.offset + s.length])
+    for d in set(devs):
+        torch.cuda.synchronize(d)
+    return reps
+
+
+def execute_sliced_offload(replicas: list, layout: SliceLayout, host_buf) -> None:
+    """comm.py:331-342: each replica writes only its owned slice back, after
+    checking that the replicas are bit-identical (ConsistencyError otherwise:
+    a diverged replica would reassemble a corrupt block)."""
+    from .ops import hash_u64
+
+    ref = replicas[0]
+    for r in replicas[1:]:
+        same = torch.equal(r, ref) if r.device == ref.device else \
+            int(hash_u64(r).item()) == int(hash_u64(ref).item())
+        if not same:
+            raise ConsistencyError("device replicas diverged; offload would reassemble a corrupt block")
+    host = torch.as_tensor(host_buf)
+    for s in layout.slices:
+        if s.length:
+            host[s.offset:s.offset + s.length].copy_(replicas[s.owner][s.offset:s.offset + s.length])
 
 
 def sliced_offload(slot_theta: torch.Tensor, host_block: torch.Tensor, layout: SliceLayout, rank: int,

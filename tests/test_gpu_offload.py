@@ -241,3 +241,41 @@ def test_partially_resident_offload_equals_resident(k):
     assert rt.uploaded_params == 3 * sum(host.layouts[b].elem_count for b in rt.wids)
     rt.flush()
     assert np.array_equal(host.theta.numpy(), final)
+
+
+def test_execute_sliced_upload_offload_bytes_and_divergence_guard():
+    """pkg/tests/test_comm.py:188-207 on device replicas: every replica equals
+    the host buffer after the two-phase upload, the offload reassembles it
+    exactly, a diverged replica raises ConsistencyError, and a layout of the
+    wrong size is a ConfigurationError."""
+    from paper_2507_03211_b200.errors import ConfigurationError, ConsistencyError
+    from paper_2507_03211_b200.scheduler import SliceLayout, execute_sliced_offload, execute_sliced_upload
+
+    buf = np.random.default_rng(0).normal(size=1000)
+    lay = SliceLayout.build(0, 1000, 4)
+    replicas = execute_sliced_upload(buf, lay)
+    assert all(np.array_equal(r.cpu().numpy(), buf) for r in replicas)
+    out = np.empty_like(buf)
+    execute_sliced_offload(replicas, lay, out)
+    assert np.array_equal(out, buf)
+    replicas[1][3] += 1e-12
+    with pytest.raises(ConsistencyError):
+        execute_sliced_offload(replicas, lay, out)
+    with pytest.raises(ConfigurationError):
+        execute_sliced_upload(buf[:999], lay)
+
+
+def test_execute_sliced_transfer_through_store_layouts():
+    """pkg/tests/test_comm.py:233-241: every block of a store round-trips
+    through its fixed thread-aligned layout unchanged."""
+    from paper_2507_03211_b200.scheduler import apply_thread_aligned_layout, execute_sliced_offload, \
+        execute_sliced_upload
+
+    host = HostStore(DEEP, 7)
+    before = host.theta.clone()
+    apply_thread_aligned_layout(host, 4)
+    for bl in host.layouts:
+        lay = host.slice_plan["layouts"][bl.block_id]
+        replicas = execute_sliced_upload(host.block_buf(bl.block_id), lay)
+        execute_sliced_offload(replicas, lay, host.block_buf(bl.block_id))
+    assert torch.equal(host.theta, before)

@@ -73,3 +73,15 @@ def test_plan_residency_counts_split16_lo_planes():
             assert (k + slots) * per + (nb - k) * lo <= b
     with pytest.raises(ConfigurationError):
         plan_residency(cfg, int(60e9), compress="fp8")
+
+
+def test_slice_fields_and_layout_equality():
+    """comm.py's Slice has owner / offset / length (pkg/tests/test_comm.py:47-53)
+    and layouts compare by value (test_comm.py:210-218)."""
+    from paper_2507_03211_b200.scheduler import SliceLayout
+
+    lay = SliceLayout.build(0, 10, 4)
+    assert [s.length for s in lay.slices] == [3, 3, 3, 1]
+    assert [s.offset for s in lay.slices] == [0, 3, 6, 9]
+    assert sorted(s.owner for s in lay.slices) == [0, 1, 2, 3]
+    assert lay == SliceLayout.build(0, 10, 4) and lay != SliceLayout.build(0, 10, 2)
