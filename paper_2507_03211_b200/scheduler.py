@@ -357,9 +357,10 @@ class OffloadedZo:
     directions per rank (ZO-DDP when N > 1), "2d" for one direction per rank).
     """
 
-    def __init__(self, host: HostStore, hyper: ZoHyper, batch: int, device=None, n_slots: int = 3,
+    def __init__(self, host: HostStore, hyper: ZoHyper, batch: int | None = None, device=None, n_slots: int = 3,
                  mode: str = "streams", fabric=None, strategy: str = "mezo", trace: bool = False,
-                 resident_blocks: int = 0, redistribute: str = "fp32", compress: str = "none"):
+                 resident_blocks: int = 0, redistribute: str = "fp32", compress: str = "none",
+                 capacity: int | None = None, cost=None):
         """resident_blocks: keep the first k transformer blocks on the device
         for the whole run (uploaded once, written back at flush / sync_host)
         and stream only the rest -- use whatever HBM the model leaves free,
@@ -371,9 +372,21 @@ class OffloadedZo:
         the direction-aware bf16 exchange described in the module docstring).
 
         compress: "none" or "split16" (hi / lo 16-bit planes: half the PCIe
-        bytes per streamed block, lo kept in device memory; module docstring)."""
+        bytes per streamed block, lo kept in device memory; module docstring).
+
+        The reference's constructor form ``OffloadedZo(store, hyper,
+        capacity=None, cost=None, mode="events")`` (scheduler.py:209-216) is
+        accepted as is: ``batch`` may be omitted (activations are sized by the
+        first step's batch); ``capacity`` is the device-memory budget in bytes
+        (the reference's MemoryPool capacity) and picks ``resident_blocks`` /
+        ``n_slots`` through ``plan_residency`` after the persistent embedding
+        and head; ``cost`` is accepted and unused (real streams replace the
+        simulated cost model); the simulated executors "events" / "threads"
+        map to the real concurrent "streams"."""
+        mode = {"events": "streams", "threads": "streams"}.get(mode, mode)
         if mode not in ("streams", "serial"):
             raise ProtocolError(f"unknown scheduler mode {mode!r}")
+        self.cost = cost
         if n_slots < 2:
             raise ConfigurationError("need at least 2 block slots")
         self.host, self.hyper, self.mode, self.trace = host, hyper.validate(), mode, trace
@@ -405,6 +418,16 @@ class OffloadedZo:
             apply_thread_aligned_layout(host, self.world)
         emb, head = self.layouts[0].block_id, self.layouts[-1].block_id
         wids = [bl.block_id for bl in self.layouts if bl.kind == TRANSFORMER]
+        if capacity is not None:
+            nd = len(self.dirs)
+            persistent = sum(self.layouts[b].elem_count for b in (emb, head)) * (4 + 2 * nd)
+            per = self.layouts[wids[0]].elem_count * (4 + 2 * nd) if wids else 0
+            if wids and capacity - persistent < 2 * per:
+                raise ConfigurationError(f"device capacity {capacity} B cannot hold the persistent blocks "
+                                         f"({persistent} B) and two streamed block slots ({2 * per} B)")
+            if wids:
+                resident_blocks, n_slots = plan_residency(cfg, capacity - persistent, n_dirs=nd, compress=compress)
+                n_slots = max(n_slots, 2)
         if not 0 <= resident_blocks <= len(wids):
             raise ConfigurationError(f"resident_blocks must be in [0, {len(wids)}], got {resident_blocks}")
         self.resident = wids[:resident_blocks]          # computed in place, never streamed
@@ -439,7 +462,7 @@ class OffloadedZo:
         self.record = torch.zeros(3, dtype=torch.float64, device=self.device)
         self.local = torch.zeros(2, dtype=torch.float64, device=self.device)
         self.gathered = torch.zeros(2 * self.world, dtype=torch.float64, device=self.device)
-        self.ws = {s: Workspace(cfg, batch, cfg.seq_len, self.device) for s in self.dirs}
+        self.ws = {s: Workspace(cfg, batch, cfg.seq_len, self.device) for s in self.dirs} if batch else None
         self.streams = {COMPUTE: torch.cuda.current_stream(self.device)}
         if mode == "streams":
             self.streams[UPLOAD] = torch.cuda.Stream(self.device)
@@ -650,6 +673,8 @@ class OffloadedZo:
         self.iteration += 1
         batch.validate(self.config)
         B, T = batch.token_ids.shape
+        if self.ws is None:                      # reference constructor form: sized by the first batch
+            self.ws = {s: Workspace(self.config, B, T, self.device) for s in self.dirs}
         for ws in self.ws.values():
             if ws.batch != B or ws.seq != T:
                 raise ConfigurationError("batch shape differs from the runtime's workspace")

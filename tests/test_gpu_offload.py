@@ -279,3 +279,46 @@ def test_execute_sliced_transfer_through_store_layouts():
         replicas = execute_sliced_upload(host.block_buf(bl.block_id), lay)
         execute_sliced_offload(replicas, lay, host.block_buf(bl.block_id))
     assert torch.equal(host.theta, before)
+
+
+@pytest.mark.parametrize("mode", ["events", "threads", "serial"])
+def test_reference_constructor_form(mode):
+    """OffloadedZo(store, hyper, capacity=None, cost=None, mode=...) exactly as
+    the reference's tests call it (pkg/tests/test_offload.py:118-241): no batch
+    argument (sized by the first step), simulated executors mapped to real
+    streams, the cost model accepted and unused; same records as resident."""
+    recs, _, final = _resident(DEEP, 3)
+    host = HostStore(DEEP, 7)
+    rt = OffloadedZo(host, zo.ZoHyper(EPS, LR), cost=object(), mode=mode)
+    for j, s in enumerate(iteration_seeds(9, 3), 1):
+        r = rt.step(make_batch(DEEP, 2, 40 + j), s)
+        assert (r.loss_pos, r.loss_neg, r.g) == recs[j - 1]
+    rt.flush()
+    assert np.array_equal(host.theta.numpy(), final)
+    with pytest.raises(ProtocolError):
+        OffloadedZo(HostStore(DEEP, 7), zo.ZoHyper(EPS, LR), mode="bogus")
+
+
+def test_capacity_bound_run_and_too_small_capacity():
+    """pkg/tests/test_offload.py:208-215: a byte capacity that holds the
+    persistent blocks + 3 streamed blocks runs (and equals resident); one that
+    cannot hold two streamed slots is a ConfigurationError, not a crash."""
+    from paper_2507_03211_b200.errors import ConfigurationError
+    from paper_2507_03211_b200.model import model_layout
+
+    recs, _, final = _resident(DEEP, 2)
+    lay = model_layout(DEEP)
+    per = lay[1].elem_count * 8
+    persistent = (lay[0].elem_count + lay[-1].elem_count) * 8
+    host = HostStore(DEEP, 7)
+    rt = OffloadedZo(host, zo.ZoHyper(EPS, LR), capacity=persistent + 3 * per)
+    assert len(rt.wids) >= 2 and len(rt.slots) >= 2
+    for j, s in enumerate(iteration_seeds(9, 2), 1):
+        r = rt.step(make_batch(DEEP, 2, 40 + j), s)
+        assert (r.loss_pos, r.loss_neg, r.g) == recs[j - 1]
+    rt.flush()
+    assert np.array_equal(host.theta.numpy(), final)
+    big = OffloadedZo(HostStore(DEEP, 7), zo.ZoHyper(EPS, LR), capacity=persistent + 10 * per)
+    assert big.wids == []                      # everything fits: nothing streams
+    with pytest.raises(ConfigurationError):
+        OffloadedZo(HostStore(DEEP, 7), zo.ZoHyper(EPS, LR), capacity=persistent + per)
