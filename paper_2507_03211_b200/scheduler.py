@@ -360,7 +360,7 @@ class OffloadedZo:
     def __init__(self, host: HostStore, hyper: ZoHyper, batch: int | None = None, device=None, n_slots: int = 3,
                  mode: str = "streams", fabric=None, strategy: str = "mezo", trace: bool = False,
                  resident_blocks: int = 0, redistribute: str = "fp32", compress: str = "none",
-                 capacity: int | None = None, cost=None):
+                 capacity: int | None = None, cost=None, verify: bool = False):
         """resident_blocks: keep the first k transformer blocks on the device
         for the whole run (uploaded once, written back at flush / sync_host)
         and stream only the rest -- use whatever HBM the model leaves free,
@@ -382,7 +382,14 @@ class OffloadedZo:
         ``n_slots`` through ``plan_residency`` after the persistent embedding
         and head; ``cost`` is accepted and unused (real streams replace the
         simulated cost model); the simulated executors "events" / "threads"
-        map to the real concurrent "streams"."""
+        map to the real concurrent "streams".
+
+        verify (sliced schedule over a fabric, fp32 redistribution): before a
+        rank writes its slice of a streamed block back, the ranks compare a
+        64-bit hash of their whole block copy and refuse to offload diverged
+        replicas (ConsistencyError; comm.py:336-340).  A host-synchronising
+        collective per block, so off by default (a debug guard, like the
+        strategies' ``verify``)."""
         mode = {"events": "streams", "threads": "streams"}.get(mode, mode)
         if mode not in ("streams", "serial"):
             raise ProtocolError(f"unknown scheduler mode {mode!r}")
@@ -408,6 +415,10 @@ class OffloadedZo:
             raise ConfigurationError("bf16 redistribution needs a mesh with one direction per rank "
                                      "(strategy 'pertp' or '2d')")
         self.redistribute = redistribute
+        if verify and (fabric is None or redistribute == "bf16"):
+            raise ConfigurationError("verify compares full block replicas: it needs a fabric and the fp32 "
+                                     "redistribution (with bf16 only the own slice is materialised)")
+        self.verify = verify
         if compress not in ("none", "split16"):
             raise ConfigurationError(f"compress must be 'none' or 'split16', got {compress!r}")
         if compress == "split16" and getattr(host, "is_sharded", False):
@@ -535,6 +546,9 @@ class OffloadedZo:
                           gather=gather)
 
     def _offload(self, bid, slot, stream):
+        if self.verify and bid in self.wids:
+            with torch.cuda.stream(stream) if stream is not None else _null():
+                check_slices_identical(self.fabric, self.rank, slot.theta, self.layouts[bid].elem_count)
         if bid in self._lo:                              # split: lo stays, hi goes to the host
             off, ln = self._own(bid)
             with torch.cuda.stream(stream) if stream is not None else _null():

@@ -260,6 +260,49 @@ def sliced_dir_worker(rank, world, port, redistribute, steps, sharded, compress,
     q.put((rank, recs, theta, nbytes))
 
 
+def verify_offload_worker(rank, world, port, q):
+    """Sliced offload with the divergence guard: a clean step passes; a step
+    in which rank 1's copy of a block is corrupted after its update raises
+    ConsistencyError on every rank before anything is written back."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2507_03211_b200.errors import ConsistencyError
+    from paper_2507_03211_b200.fabric import TorchFabric
+    from paper_2507_03211_b200.model import ModelConfig, make_batch
+    from paper_2507_03211_b200.rng import iteration_seeds
+    from paper_2507_03211_b200.scheduler import OffloadedZo
+    from paper_2507_03211_b200.sharded import ShardStore
+    from paper_2507_03211_b200.zo import ZoHyper
+
+    torch.cuda.set_device(0)
+    init(rank, world, port)
+    fab = TorchFabric()
+    cfg = ModelConfig(*DEEP, "f32")
+    shards = ShardStore(cfg, fab, 7)
+    rt = OffloadedZo(shards, ZoHyper(1e-3, 1e-2), batch=4 // world, fabric=fab, strategy="mezo", verify=True,
+                     mode="serial")
+    seeds = iteration_seeds(9, 2)
+    rt.step(make_batch(cfg, 4, 41).shard(world, rank), seeds[0])
+    clean = True
+    if rank == 1:
+        orig = rt._perturb
+
+        def corrupt(bid, slot, flags, stream):
+            orig(bid, slot, flags, stream)
+            if bid in rt.wids:
+                with torch.cuda.stream(stream):
+                    slot.theta[0:1].add_(1e-3)
+        rt._perturb = corrupt
+    raised = False
+    try:
+        rt.step(make_batch(cfg, 4, 42).shard(world, rank), seeds[1])
+    except ConsistencyError:
+        raised = True
+    dist.destroy_process_group()
+    q.put((rank, clean, raised))
+
+
 def sharded_worker(rank, world, port, strategy, steps, init_kind, q):
     """OffloadedZo over an HBM-sharded fp32 master (sharded.ShardStore):
     upload = own shard slice + all-gather, offload = own slice back (gloo,

@@ -322,3 +322,15 @@ def test_capacity_bound_run_and_too_small_capacity():
     assert big.wids == []                      # everything fits: nothing streams
     with pytest.raises(ConfigurationError):
         OffloadedZo(HostStore(DEEP, 7), zo.ZoHyper(EPS, LR), capacity=persistent + per)
+
+
+def test_sliced_offload_divergence_guard():
+    """comm.py:336-340 in the distributed schedule (OffloadedZo(verify=True)):
+    diverged block replicas are refused before their slices are written
+    back, on every rank; verify is rejected where full replicas do not exist."""
+    from paper_2507_03211_b200.errors import ConfigurationError
+
+    res = H.run(H.verify_offload_worker, 2)
+    assert all(r[1] for r in res) and all(r[2] for r in res)
+    with pytest.raises(ConfigurationError):
+        OffloadedZo(HostStore(DEEP, 7), zo.ZoHyper(EPS, LR), batch=2, verify=True)
