@@ -1,21 +1,33 @@
-"""Exception hierarchy of the drop-in, mirroring src/zosim/errors.py:8-56.
+"""Exceptions of the drop-in (the class names and the tree are zosim's,
+src/zosim/errors.py:8-56, so ``except`` clauses written for the reference
+keep working).
 
-The C ABI returns ZO_ERR_* status codes (include/zo_b200.h); ``raise_for``
-maps them onto these classes so callers catch exactly what they caught with
-the reference.  Exit codes follow src/zosim/cli.py:176-192.
+Status codes returned by the C ABI (ZO_ERR_*, include/zo_b200.h) become
+these classes in ``raise_for``; ``exit_code`` is the process status the
+reference's CLI uses for each family (src/zosim/cli.py:176-192).
+
+    ZosimError                     exit 1
+    +-- ConfigurationError         exit 2   ABI status 2
+    |   +-- DimensionError
+    |   +-- MemoryCapacityError    (.block_id)
+    +-- NumericError               exit 3   ABI status 3
+    +-- FabricFault                exit 4
+    |   +-- ConsistencyError
+    +-- ProtocolError              exit 1   ABI status 1
+    +-- SimulationError            exit 1
+    +-- CudaError                  exit 1   ABI status 5 (native runtime failure; no reference analogue)
 """
 
 
-class ZosimError(Exception):
-    """Base class (errors.py:8)."""
-
-
-class ConfigurationError(ZosimError):
-    exit_code = 2
-
-
-class DimensionError(ConfigurationError):
-    """Shape mismatch (errors.py:18-20)."""
+class ZosimError(Exception): exit_code = 1                      # noqa: E701
+class ConfigurationError(ZosimError): exit_code = 2             # noqa: E701
+class DimensionError(ConfigurationError): pass                  # noqa: E701
+class NumericError(ZosimError): exit_code = 3                   # noqa: E701
+class FabricFault(ZosimError): exit_code = 4                    # noqa: E701
+class ConsistencyError(FabricFault): pass                       # noqa: E701
+class ProtocolError(ZosimError): pass                           # noqa: E701
+class SimulationError(ZosimError): pass                         # noqa: E701
+class CudaError(ZosimError): pass                               # noqa: E701
 
 
 class MemoryCapacityError(ConfigurationError):
@@ -24,35 +36,10 @@ class MemoryCapacityError(ConfigurationError):
         self.block_id = block_id
 
 
-class NumericError(ZosimError):
-    exit_code = 3
-
-
-class FabricFault(ZosimError):
-    exit_code = 4
-
-
-class ConsistencyError(FabricFault):
-    """Replicas diverged (errors.py:43-44)."""
-
-
-class ProtocolError(ZosimError):
-    exit_code = 1
-
-
-class SimulationError(ZosimError):
-    exit_code = 1
-
-
-class CudaError(ZosimError):
-    """CUDA runtime failure inside the native library (no reference analogue)."""
-
-    exit_code = 1
-
-
-_BY_CODE = {1: ProtocolError, 2: ConfigurationError, 3: NumericError, 4: FabricFault, 5: CudaError}
+_BY_STATUS = {1: ProtocolError, 2: ConfigurationError, 3: NumericError, 4: FabricFault, 5: CudaError}
 
 
 def raise_for(code: int, message: str) -> None:
+    """Raise the class mapped to a nonzero ABI status (no-op for 0)."""
     if code:
-        raise _BY_CODE.get(code, ZosimError)(message)
+        raise _BY_STATUS.get(code, ZosimError)(message)
