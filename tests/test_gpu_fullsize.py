@@ -89,3 +89,26 @@ def test_fullsize_long_run_is_finite_and_reproducible():
         del st, sz
         torch.cuda.empty_cache()
     assert hashes[0] == hashes[1] and finals[0] == finals[1]
+
+
+def test_fullsize_real_opt_lazy_graph_equals_eager_bit_exact():
+    """The same lattice at the real OPT-1.3B architecture (ReLU FFN, tied
+    bias-free LM head through the K-major B operand, positions + 2)."""
+    from paper_2507_03211_b200.model import real_opt_config
+
+    cfg = real_opt_config("opt-1.3b", 512)
+    steps = 2
+    seeds = iteration_seeds(99, steps)
+    batches = [make_batch(cfg, B, 5 + j) for j in range(steps)]
+    a = DeviceStore(cfg, 7, init="philox")
+    recs = [zo.mezo_step(a, batches[j], zo.ZoHyper(EPS, LR), s, iteration=j + 1) for j, s in enumerate(seeds)]
+    ha = int(ops.hash_u64(a.theta).item())
+    del a
+    torch.cuda.empty_cache()
+    b = DeviceStore(cfg, 7, init="philox")
+    sz = zo.StreamingZo(b, zo.ZoHyper(EPS, LR))
+    for j, s in enumerate(seeds):
+        r = sz.step(batches[j], s)
+        assert (r.loss_pos, r.loss_neg, r.g) == (recs[j].loss_pos, recs[j].loss_neg, recs[j].g)
+    sz.flush()
+    assert int(ops.hash_u64(b.theta).item()) == ha
