@@ -208,6 +208,37 @@ def gpu_strategy_worker_theta(rank, world, port, strategy, steps, q):
     q.put((rank, recs, theta))
 
 
+def fullsize_mesh_worker(rank, world, port, steps, q):
+    """The lazy 2D-mesh step (MeshZo, what bench.py runs at N > 1) at the
+    OPT-1.3B headline size, one direction per rank, all ranks on cuda:0."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2507_03211_b200 import ops
+    from paper_2507_03211_b200.engine import MINUS, PLUS, DeviceStore
+    from paper_2507_03211_b200.fabric import TorchFabric
+    from paper_2507_03211_b200.model import make_batch, opt_config
+    from paper_2507_03211_b200.rng import iteration_seeds
+    from paper_2507_03211_b200.strategies import MeshZo
+    from paper_2507_03211_b200.zo import ZoHyper
+
+    torch.cuda.set_device(0)
+    init(rank, world, port)
+    fab = TorchFabric()
+    cfg = opt_config("opt-1.3b", 512)
+    store = DeviceStore(cfg, 7, init="philox", directions=(PLUS,) if rank % 2 == 0 else (MINUS,))
+    groups = world // 2
+    mz = MeshZo(store, ZoHyper(1e-3, 1e-7), fab, "2d", 4, 512)
+    recs = []
+    for j, s in enumerate(iteration_seeds(1234, steps)):
+        r = mz.step(make_batch(cfg, 4 * groups, 99 * 1_000_003 + j + 1).shard(groups, rank // 2), s)
+        recs.append((r.loss_pos, r.loss_neg, r.g))
+    mz.flush()
+    h = int(ops.hash_u64(store.theta).item())
+    dist.destroy_process_group()
+    q.put((rank, recs, h))
+
+
 def sliced_dir_worker(rank, world, port, redistribute, steps, sharded, compress, strategy, q):
     """OffloadedZo on the 2D mesh (one direction per rank) with the fp32
     all-gather or the direction-aware bf16 exchange, over a

@@ -112,3 +112,28 @@ def test_fullsize_real_opt_lazy_graph_equals_eager_bit_exact():
         assert (r.loss_pos, r.loss_neg, r.g) == (recs[j].loss_pos, recs[j].loss_neg, recs[j].g)
     sz.flush()
     assert int(ops.hash_u64(b.theta).item()) == ha
+
+
+def test_fullsize_pertp_mesh_equals_single_gpu_mezo():
+    """PertP (the 2D mesh with one group, two ranks sharing cuda:0 over gloo)
+    at 1.42 G parameters: both ranks report the single-GPU lazy step's
+    records and end on the single-GPU master bits (SPEC lattice PertP ==
+    MeZO)."""
+    from tests import dist_helpers as H
+
+    steps = 2
+    seeds = iteration_seeds(1234, steps)
+    st = DeviceStore(CFG, 7, init="philox")
+    sz = zo.StreamingZo(st, zo.ZoHyper(EPS, LR))
+    want = []
+    for j, s in enumerate(seeds):
+        r = sz.step(make_batch(CFG, B, 99 * 1_000_003 + j + 1), s)
+        want.append((r.loss_pos, r.loss_neg, r.g))
+    sz.flush()
+    h = int(ops.hash_u64(st.theta).item())
+    del st, sz
+    torch.cuda.empty_cache()
+    res = H.run(H.fullsize_mesh_worker, 2, steps, timeout=600)
+    for rank, recs, hr in res:
+        assert recs == want, rank
+        assert hr == h, rank
