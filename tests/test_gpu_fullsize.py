@@ -137,3 +137,27 @@ def test_fullsize_pertp_mesh_equals_single_gpu_mezo():
     for rank, recs, hr in res:
         assert recs == want, rank
         assert hr == h, rank
+
+
+def test_13b_lazy_graph_equals_eager_bit_exact():
+    """BASELINE config #3's model (OPT-13B shape, hd 128, T = 2048, B = 1;
+    13.1 G parameters, ~105 GB on the device): lazy + graph == eager, one
+    store at a time."""
+    cfg = opt_config("opt-13b", 2048)
+    seeds = iteration_seeds(5, 2)
+    batches = [make_batch(cfg, 1, 11 + j) for j in range(2)]
+    a = DeviceStore(cfg, 7, init="philox")
+    recs = [zo.mezo_step(a, batches[j], zo.ZoHyper(EPS, LR), s, iteration=j + 1) for j, s in enumerate(seeds)]
+    ha = int(ops.hash_u64(a.theta).item())
+    del a
+    torch.cuda.empty_cache()
+    b = DeviceStore(cfg, 7, init="philox")
+    sz = zo.StreamingZo(b, zo.ZoHyper(EPS, LR))
+    for j, s in enumerate(seeds):
+        r = sz.step(batches[j], s)
+        assert (r.loss_pos, r.loss_neg, r.g) == (recs[j].loss_pos, recs[j].loss_neg, recs[j].g)
+        assert np.isfinite([r.loss_pos, r.loss_neg, r.g]).all()
+    sz.flush()
+    assert int(ops.hash_u64(b.theta).item()) == ha
+    del b, sz
+    torch.cuda.empty_cache()
