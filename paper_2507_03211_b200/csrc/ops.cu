@@ -263,7 +263,7 @@ __global__ void ce_rows_kernel(const float* __restrict__ part, const float* __re
     const float tl = tgt[r];
     if (!isfinite(tl)) bad = true;
     if (bad) atomicOr(err, 2);
-    row_loss[r] = m + log(s) - (double)tl;
+    row_loss[r] = bad ? (double)NAN : m + log(s) - (double)tl;   // a flagged row poisons the mean (gate below)
   }
 }
 
@@ -297,15 +297,25 @@ int ce_finalize_launch(const float* part, const float* tgt, int64_t rows, int64_
 // ---------------------------------------------------------------------------
 // projected gradient + scalar state for the folded update
 // ---------------------------------------------------------------------------
+// The deferred update is armed only for a finite g: a step whose losses are
+// non-finite (the CE kernels flag the rows and write NaN) leaves pending = 0
+// and lr_g_prev = 0, so the next fused pass / the eager update pass is a
+// value no-op and the master never sees theta -= NaN * z.  The host raises
+// NumericError from the workspace flag after the step (model.py:366-367).
+__device__ __forceinline__ void arm_update(ZoStepScalars* scal, double lr, double g) {
+  const bool ok = isfinite(g) && isfinite(lr * g);
+  scal->seed_prev = scal->seed_cur;
+  scal->lr_g_prev = ok ? lr * g : 0.0;
+  scal->pending = ok ? 1 : 0;
+}
+
 __global__ void grad_finalize_kernel(const double* lp, const double* ln, double eps, double lr,
                                      ZoStepScalars* scal, double* rec) {
   pdl_wait();
   const double a = *lp, b = *ln;
   const double g = (a - b) / (2.0 * eps);
   rec[0] = a; rec[1] = b; rec[2] = g;
-  scal->seed_prev = scal->seed_cur;
-  scal->lr_g_prev = lr * g;
-  scal->pending = 1;
+  arm_update(scal, lr, g);
 }
 
 __global__ void grad_groups_kernel(const double* losses, int n, int sp, int op, int sm, int om, int mine,
@@ -315,9 +325,7 @@ __global__ void grad_groups_kernel(const double* losses, int n, int sp, int op, 
   for (int i = 0; i < n; ++i) tot += (losses[i * sp + op] - losses[i * sm + om]) / (2.0 * eps);
   const double g = tot / (double)n;
   rec[0] = losses[mine * sp + op]; rec[1] = losses[mine * sm + om]; rec[2] = g;
-  scal->seed_prev = scal->seed_cur;
-  scal->lr_g_prev = lr * g;
-  scal->pending = 1;
+  arm_update(scal, lr, g);
 }
 
 int grad_finalize_launch(const double* lp, const double* ln, double eps, double lr, ZoStepScalars* scal,

@@ -439,9 +439,9 @@ class DeviceStore:
         (embedding -> N decoder blocks -> LN_f + LM head + CE).  ``slots``
         maps block ids to objects with the same wview / vview / theta_ptr
         interface when those blocks live outside this store (offload)."""
-        if getattr(self, "precision", "bf16") == "f32":      # (offload slot views carry no precision)
+        if getattr(self, "precision", "bf16") == "f32":
             return self.forward_calls_f32(s, ws, scale, zmode, z_cur, stream, blocks, head_mode, logits, loss_out,
-                                          scal)
+                                          scal, slots)
         cfg, lib = self.config, L.lib()
         d, H, hd, V = cfg.d_model, cfg.n_heads, cfg.head_dim, cfg.vocab_size
         opt = cfg.arch == "opt"
@@ -507,11 +507,12 @@ class DeviceStore:
         return calls
 
     def forward_calls_f32(self, s, ws, scale, zmode=L.ZO_Z_PHILOX, z_cur=None, stream=None, blocks=None,
-                          head_mode="ce", logits=None, loss_out=None, scal=None):
+                          head_mode="ce", logits=None, loss_out=None, scal=None, slots=None):
         """forward_calls of the f32 parity mode: same block structure, fp32
         operands / activations through zo_gemm_f32, zo_attn_causal_fwd_f32,
         zo_layernorm_fwd_f32; the head materialises fp32 logits and
-        zo_ce_rows_f32 + zo_ce_finalize form the f64 loss."""
+        zo_ce_rows_f32 + zo_ce_finalize form the f64 loss.  ``slots`` as in
+        forward_calls (offloaded blocks)."""
         cfg, lib = self.config, L.lib()
         d, H, hd, V = cfg.d_model, cfg.n_heads, cfg.head_dim, cfg.vocab_size
         M, B, T = ws.M, ws.batch, ws.seq
@@ -522,14 +523,15 @@ class DeviceStore:
         ldx, ldh = ws.x.stride(0), ws.h.stride(0)
         for bid in blocks:
             bl = self.layouts[bid]
+            src = (slots or {}).get(bid, self)
             if bl.kind == EMBEDDING:
                 calls.append((lib.zo_embed_fwd, (
-                    self.theta_ptr(bl.key("tok_emb")), bl.key("tok_emb"), self.theta_ptr(bl.key("pos_emb")),
+                    src.theta_ptr(bl.key("tok_emb")), bl.key("tok_emb"), src.theta_ptr(bl.key("pos_emb")),
                     bl.key("pos_emb"), _ptr(ws.ids), B, T, d, V, float(scale), scal_p, zmode, _ptr(z_cur), 0,
                     _ptr(ws.x), ldx, _ptr(ws.err), st)))
             elif bl.kind == TRANSFORMER:
-                v = lambda n: _ptr(self.vview(s, bid, n))  # noqa: E731
-                w = {n: self.wview(s, bid, n)[0] for n in ("qkv", "wo", "w1", "w2")}
+                v = lambda n: _ptr(src.vview(s, bid, n))  # noqa: E731
+                w = {n: src.wview(s, bid, n)[0] for n in ("qkv", "wo", "w1", "w2")}
                 g = lib.zo_gemm_f32
                 calls += [
                     (lib.zo_layernorm_fwd_f32, (_ptr(ws.x), ldx, v("ln1_g"), v("ln1_b"), M, d, _ptr(ws.h), ldh, st)),
@@ -546,13 +548,13 @@ class DeviceStore:
                          L.ZO_EPI_BIAS_RESID_F32, v("b2"), _ptr(ws.x), ldx, st)),
                 ]
             else:
-                wout = self.wview(s, bid, "w_out")[0]
-                calls.append((lib.zo_layernorm_fwd_f32, (_ptr(ws.x), ldx, _ptr(self.vview(s, bid, "lnf_g")),
-                                                         _ptr(self.vview(s, bid, "lnf_b")), M, d, _ptr(ws.h), ldh,
+                wout = src.wview(s, bid, "w_out")[0]
+                calls.append((lib.zo_layernorm_fwd_f32, (_ptr(ws.x), ldx, _ptr(src.vview(s, bid, "lnf_g")),
+                                                         _ptr(src.vview(s, bid, "lnf_b")), M, d, _ptr(ws.h), ldh,
                                                          st)))
                 if head_mode == "ce":
                     calls.append((lib.zo_gemm_f32, (_ptr(ws.h), ldh, _ptr(wout), wout.stride(0), M, V, d,
-                                                    L.ZO_EPI_BIAS_BF16, _ptr(self.vview(s, bid, "b_out")),
+                                                    L.ZO_EPI_BIAS_BF16, _ptr(src.vview(s, bid, "b_out")),
                                                     _ptr(ws.logits), ws.logits.stride(0), st)))
                     calls.append((lib.zo_ce_rows_f32, (_ptr(ws.logits), ws.logits.stride(0), M, V, _ptr(ws.tgt),
                                                        _ptr(ws.ce_part), _ptr(ws.ce_tgt), ws.n_ce, _ptr(ws.err), st)))

@@ -54,7 +54,7 @@ import torch
 from . import _lib as L
 from . import ops
 from .engine import MINUS, PLUS, SegTable, ShadowPlan, Workspace, block_extent
-from .errors import ConfigurationError, ConsistencyError, ProtocolError
+from .errors import ConfigurationError, ConsistencyError, MemoryCapacityError, ProtocolError
 from .model import EMBEDDING, HEAD, TRANSFORMER, Batch, ModelConfig, init_block_host, model_layout
 from .rng import RngStateManager
 from .zo import ZoHyper, ZoStep, _u64_as_i64
@@ -168,7 +168,9 @@ class BlockSlot:
 
     def wview(self, s: int, bid: int, name: str):
         b, off, rows, cols, ld = self.plan.views[bid][name]
-        wlo = block_extent(self.plan, bid)[0]
+        wlo, _, vlo, _ = block_extent(self.plan, bid)
+        if b == "v":                      # f32 parity mode: weights live in the fp32 shadow
+            return self.vsh[s][off - vlo:off - vlo + rows * ld].view(rows, ld), rows, cols
         return self.wsh[s][off - wlo:off - wlo + rows * ld].view(rows, ld), rows, cols
 
     def vview(self, s: int, bid: int, name: str) -> torch.Tensor:
@@ -360,7 +362,8 @@ class OffloadedZo:
     def __init__(self, host: HostStore, hyper: ZoHyper, batch: int | None = None, device=None, n_slots: int = 3,
                  mode: str = "streams", fabric=None, strategy: str = "mezo", trace: bool = False,
                  resident_blocks: int = 0, redistribute: str = "fp32", compress: str = "none",
-                 capacity: int | None = None, cost=None, verify: bool = False):
+                 capacity: int | None = None, cost=None, verify: bool = False, mgr: RngStateManager | None = None,
+                 precision: str = "bf16"):
         """resident_blocks: keep the first k transformer blocks on the device
         for the whole run (uploaded once, written back at flush / sync_host)
         and stream only the rest -- use whatever HBM the model leaves free,
@@ -389,7 +392,13 @@ class OffloadedZo:
         64-bit hash of their whole block copy and refuse to offload diverged
         replicas (ConsistencyError; comm.py:336-340).  A host-synchronising
         collective per block, so off by default (a debug guard, like the
-        strategies' ``verify``)."""
+        strategies' ``verify``).
+
+        mgr: RngStateManager("oracle") injects the reference's numpy z (the
+        whole model's stream per iteration, zo.py:90-125) instead of the
+        in-register Philox z; precision="f32" runs the fp32 parity forward
+        (SURVEY 8c mode (i)).  Together they reproduce the reference's
+        OffloadedZo trajectory (tests/test_gpu_offload.py)."""
         mode = {"events": "streams", "threads": "streams"}.get(mode, mode)
         if mode not in ("streams", "serial"):
             raise ProtocolError(f"unknown scheduler mode {mode!r}")
@@ -397,11 +406,17 @@ class OffloadedZo:
         if n_slots < 2:
             raise ConfigurationError("need at least 2 block slots")
         self.host, self.hyper, self.mode, self.trace = host, hyper.validate(), mode, trace
+        self.mgr = mgr or RngStateManager()
+        if precision not in ("bf16", "f32"):
+            raise ConfigurationError(f"precision must be 'bf16' or 'f32', got {precision!r}")
+        self.precision = precision
         cfg = self.config = host.config
+        if precision == "f32" and cfg.arch != "zosim":
+            raise ConfigurationError("the f32 parity mode covers the zosim architecture")
         self.device = torch.device(device or f"cuda:{torch.cuda.current_device()}")
         L.lib()
         self.layouts = host.layouts
-        self.plan = ShadowPlan(cfg, self.layouts)
+        self.plan = ShadowPlan(cfg, self.layouts, f32_weights=precision == "f32")
         self.fabric = fabric
         self.world = fabric.k if fabric is not None else 1
         self.rank = fabric.rank if fabric is not None else 0
@@ -414,6 +429,8 @@ class OffloadedZo:
         if redistribute == "bf16" and (fabric is None or len(self.dirs) != 1):
             raise ConfigurationError("bf16 redistribution needs a mesh with one direction per rank "
                                      "(strategy 'pertp' or '2d')")
+        if redistribute == "bf16" and precision == "f32":
+            raise ConfigurationError("the f32 parity mode redistributes fp32 blocks (redistribute='fp32')")
         self.redistribute = redistribute
         if verify and (fabric is None or redistribute == "bf16"):
             raise ConfigurationError("verify compares full block replicas: it needs a fabric and the fp32 "
@@ -434,11 +451,10 @@ class OffloadedZo:
             persistent = sum(self.layouts[b].elem_count for b in (emb, head)) * (4 + 2 * nd)
             per = self.layouts[wids[0]].elem_count * (4 + 2 * nd) if wids else 0
             if wids and capacity - persistent < 2 * per:
-                raise ConfigurationError(f"device capacity {capacity} B cannot hold the persistent blocks "
+                raise MemoryCapacityError(f"device capacity {capacity} B cannot hold the persistent blocks "
                                          f"({persistent} B) and two streamed block slots ({2 * per} B)")
             if wids:
                 resident_blocks, n_slots = plan_residency(cfg, capacity - persistent, n_dirs=nd, compress=compress)
-                n_slots = max(n_slots, 2)
         if not 0 <= resident_blocks <= len(wids):
             raise ConfigurationError(f"resident_blocks must be in [0, {len(wids)}], got {resident_blocks}")
         self.resident = wids[:resident_blocks]          # computed in place, never streamed
@@ -448,9 +464,10 @@ class OffloadedZo:
                            head: BlockSlot(self.plan, self.layouts, head, self.dirs, self.device, pad(head))}
         for bid in self.resident:
             self.persistent[bid] = BlockSlot(self.plan, self.layouts, bid, self.dirs, self.device, pad(bid))
-        tpl = self.wids[0] if self.wids else (self.resident[0] if self.resident else head)
+        tpl = self.wids[0] if self.wids else head
+        # no streamed block -> no slots (everything is persistent)
         self.slots = [BlockSlot(self.plan, self.layouts, tpl, self.dirs, self.device, pad(tpl))
-                      for _ in range(n_slots)]
+                      for _ in range(n_slots if self.wids else 0)]
         self._bf16 = {}
         if redistribute == "bf16" and self.wids:
             me = self.dirs[0]
@@ -473,16 +490,30 @@ class OffloadedZo:
         self.record = torch.zeros(3, dtype=torch.float64, device=self.device)
         self.local = torch.zeros(2, dtype=torch.float64, device=self.device)
         self.gathered = torch.zeros(2 * self.world, dtype=torch.float64, device=self.device)
-        self.ws = {s: Workspace(cfg, batch, cfg.seq_len, self.device) for s in self.dirs} if batch else None
+        self.ws = {s: Workspace(cfg, batch, cfg.seq_len, self.device, f32=precision == "f32")
+                   for s in self.dirs} if batch else None
+        self._zc = self._zp = None             # oracle mode: this / the previous iteration's z (device f64)
         self.streams = {COMPUTE: torch.cuda.current_stream(self.device)}
         if mode == "streams":
             self.streams[UPLOAD] = torch.cuda.Stream(self.device)
             self.streams[OFFLOAD] = torch.cuda.Stream(self.device)
         else:
             self.streams[UPLOAD] = self.streams[OFFLOAD] = self.streams[COMPUTE]
-        self.iteration, self.g_prev, self.last_seed, self._pending = 0, 0.0, None, False
+        self.iteration, self._g_prev, self.last_seed, self._pending = 0, 0.0, None, False
         self.timelines = []
         self.uploaded_params = self.offloaded_params = 0
+
+    @property
+    def g_prev(self) -> float:
+        return self._g_prev
+
+    @g_prev.setter
+    def g_prev(self, g: float) -> None:
+        """The reference applies ``self.g_prev`` as the deferred update
+        (scheduler.py:346-349 -> dual_forward); replacing it replaces the
+        device's lr * g_prev the next fused pass / flush applies."""
+        self._g_prev = float(g)
+        self.scal[2:3].fill_(int(np.float64(self.hyper.lr * float(g)).view(np.int64)))
 
     # -- byte movement --------------------------------------------------------------
     def _own(self, bid):
@@ -574,9 +605,24 @@ class OffloadedZo:
         va = slot.vsh[PLUS].data_ptr() if sa is not None and slot.vsh[PLUS] is not None else 0
         wb = slot.wsh[MINUS].data_ptr() if sb is not None and slot.wsh[MINUS] is not None else 0
         vb = slot.vsh[MINUS].data_ptr() if sb is not None and slot.vsh[MINUS] is not None else 0
+        zmode, zc, zp = self._zargs()
         L.check(L.lib().zo_perturb_update(slot.theta.data_ptr(), slot.key0, t.segs.data_ptr(), t.prefix.data_ptr(),
                                           t.n_segs, t.n_tiles, wa, va, wb, vb, +eps, -eps, flags,
-                                          self.scal.data_ptr(), L.ZO_Z_PHILOX, 0, 0, 0, int(stream.cuda_stream)))
+                                          self.scal.data_ptr(), zmode, zc, zp, 0, int(stream.cuda_stream)))
+
+    def _update_flag(self):
+        """Philox: always request the update (the device pending flag gates
+        it, so one launch plan serves every step); oracle z: only when a
+        previous iteration's z exists to regenerate the update from."""
+        return L.ZO_PU_UPDATE if (not self.mgr.oracle or self._zp is not None) else 0
+
+    def _zargs(self):
+        """(zmode, z_cur ptr, z_prev ptr) for the perturb / embedding kernels;
+        oracle z tensors hold the whole model's stream (z_key0 = 0)."""
+        if not self.mgr.oracle:
+            return L.ZO_Z_PHILOX, 0, 0
+        return (L.ZO_Z_ORACLE, 0 if self._zc is None else self._zc.data_ptr(),
+                0 if self._zp is None else self._zp.data_ptr())
 
     def _bf16_plan(self, bid):
         """Per streamed block, built once: this rank's slice of the perturb
@@ -625,14 +671,14 @@ class OffloadedZo:
                                           t.n_segs, t.n_tiles, self._stage[PLUS].data_ptr(),
                                           slot.vsh[PLUS].data_ptr(), self._stage[MINUS].data_ptr(),
                                           slot.vsh[MINUS].data_ptr(), +eps, -eps, flags, self.scal.data_ptr(),
-                                          L.ZO_Z_PHILOX, 0, 0, 0, int(stream.cuda_stream)))
+                                          *self._zargs(), 0, int(stream.cuda_stream)))
 
     def _redistribute_bf16(self, bid, slot, stream):
         """C(i) prologue of the bf16 exchange: own slice -> both directions,
         peers' slices of this rank's direction in, laid out as GEMM operands."""
         _, relayout, owner, w = self._bf16_plan(bid)
         me = self.dirs[0]
-        self._perturb_slice(bid, slot, L.ZO_PU_UPDATE | L.ZO_PU_SHADOW_A | L.ZO_PU_SHADOW_B, stream)
+        self._perturb_slice(bid, slot, self._update_flag() | L.ZO_PU_SHADOW_A | L.ZO_PU_SHADOW_B, stream)
         with torch.cuda.stream(stream):
             self.fabric.exchange_slices(self._stage, me, self._dir_of, w, tag="param")
             nv = slot.vsh[me].numel()
@@ -656,15 +702,16 @@ class OffloadedZo:
         if self.redistribute == "bf16" and bid in self.wids:
             self._redistribute_bf16(bid, slot, stream)
         else:
-            self._perturb(bid, slot, L.ZO_PU_UPDATE | self._shadow_flags(), stream)
+            self._perturb(bid, slot, self._update_flag() | self._shadow_flags(), stream)
         eps = self.hyper.epsilon
         for s in self.dirs:
             loss_out = self.local.data_ptr() + 8 * s
             slots = dict(self.persistent)       # the tied OPT head reads the embedding slot
             slots[bid] = slot
+            zmode = L.ZO_Z_ORACLE if self.mgr.oracle else L.ZO_Z_PHILOX
             calls = _store_view(self).forward_calls(s, self.ws[s], +eps if s == PLUS else -eps,
-                                                    stream=stream, blocks=[bid], slots=slots,
-                                                    scal=self.scal, loss_out=loss_out)
+                                                    zmode=zmode, z_cur=self._zc, stream=stream, blocks=[bid],
+                                                    slots=slots, scal=self.scal, loss_out=loss_out)
             for fn, args in calls:
                 L.check(fn(*args))
 
@@ -688,13 +735,19 @@ class OffloadedZo:
         batch.validate(self.config)
         B, T = batch.token_ids.shape
         if self.ws is None:                      # reference constructor form: sized by the first batch
-            self.ws = {s: Workspace(self.config, B, T, self.device) for s in self.dirs}
+            self.ws = {s: Workspace(self.config, B, T, self.device, f32=self.precision == "f32")
+                       for s in self.dirs}
         for ws in self.ws.values():
             if ws.batch != B or ws.seq != T:
                 raise ConfigurationError("batch shape differs from the runtime's workspace")
             _load(ws, batch)
         self.scal[0:1].fill_(_u64_as_i64(seed))
         self.scal[3:4].fill_(1 if self._pending else 0)
+        if self.mgr.oracle:                      # the reference's z of this iteration, whole model, key order
+            self.mgr.reset(seed)
+            self._zp = self._zc if self._pending else None
+            self._zc = torch.from_numpy(self.mgr.generator(seed).standard_normal(self.host.total_params)).to(
+                self.device)
         cs, us, os_ = self.streams[COMPUTE], self.streams[UPLOAD], self.streams[OFFLOAD]
         ev = {}
         rec = []
@@ -763,6 +816,8 @@ class OffloadedZo:
             if e:
                 ws.err.zero_()
                 from .errors import DimensionError, NumericError
+                # the blocks consumed the pending update; the device armed none
+                self._pending = False
                 raise DimensionError("token id out of embedding range") if e & 4 else NumericError("non-finite logits")
         if self.trace:
             self.timelines.append([{"op": k, "block_id": b, "stream": k, "start": t0.elapsed_time(e),
@@ -770,7 +825,7 @@ class OffloadedZo:
         self.uploaded_params += sum(self.layouts[i].elem_count for i in self.wids)
         self.offloaded_params += sum(self.layouts[i].elem_count for i in self.wids)
         st = ZoStep(self.iteration, seed, float(r[0]), float(r[1]), float(r[2]))
-        self.g_prev, self.last_seed, self._pending = st.g, seed, True
+        self._g_prev, self.last_seed, self._pending = st.g, seed, True
         self.host.unflushed = True
         return st
 
@@ -782,6 +837,7 @@ class OffloadedZo:
             raise ProtocolError("flush with no pending update (double flush?)")
         cs = self.streams[COMPUTE]
         self.scal[3:4].fill_(1)
+        self._zp = self._zc                      # oracle mode: the last iteration's z
         for i in self.wids:
             slot = self.slots[0]
             self._upload(i, slot, cs)
@@ -796,6 +852,7 @@ class OffloadedZo:
         self.scal[3:4].fill_(0)
         self.sync_host()
         self._pending = False
+        self._zc = self._zp = None
         self.host.unflushed = False
 
     def sync_host(self) -> None:
@@ -858,12 +915,18 @@ def plan_residency(config: ModelConfig, budget_bytes: int, n_dirs: int = 2, max_
     def kmax(slots):          # resident blocks that fit beside `slots` slots
         return int((budget_bytes - slots * per - nb * lo) // (per - lo))
 
+    fit = int((budget_bytes - nb * lo) // per)            # slots that fit with nothing resident
+    if fit < 2:
+        raise MemoryCapacityError(f"device budget {budget_bytes} B cannot hold two streamed block slots "
+                                  f"({2 * per} B) beside the lo planes ({nb * lo} B)")
     if kmax(0) <= 3:
-        return 0, max(2, min(3, int((budget_bytes - nb * lo) // per)))
+        return 0, min(3, fit)
     for slots in range(3, max_slots + 1):
         k = kmax(slots)
+        if k < 0:
+            return 0, min(3, fit)
         if slots >= min(max_slots, max(3, k // 8 + 1)):
-            return max(k, 0), slots
+            return k, slots
     return max(kmax(max_slots), 0), max_slots
 
 
@@ -883,11 +946,15 @@ class _StoreView:
 
         self.config, self.layouts, self.plan = rt.config, rt.layouts, rt.plan
         self.scal = rt.scal
-        self.precision = "bf16"
+        self.precision = rt.precision
         self._fc = DeviceStore.forward_calls.__get__(self)
+        self._fc32 = DeviceStore.forward_calls_f32.__get__(self)
 
     def forward_calls(self, *a, **k):
         return self._fc(*a, **k)
+
+    def forward_calls_f32(self, *a, **k):
+        return self._fc32(*a, **k)
 
 
 def _store_view(rt: OffloadedZo) -> _StoreView:

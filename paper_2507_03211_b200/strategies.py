@@ -30,7 +30,7 @@ import torch
 
 from . import _lib as L
 from .engine import MINUS, PLUS, DeviceStore
-from .errors import ConfigurationError, ConsistencyError, ProtocolError
+from .errors import ConfigurationError, ConsistencyError, NumericError, ProtocolError
 from .model import Batch
 from .rng import RngStateManager
 from .zo import ZoHyper, ZoStep, _finish_record, _u64_as_i64
@@ -105,17 +105,28 @@ class MeshZo:
         for s in self.mesh.dirs:
             if store.wsh[s] is None:
                 raise ConfigurationError("store lacks the shadow buffers of this rank's direction")
-        self.mgr = mgr or RngStateManager()
-        if self.mgr.oracle:
-            raise ConfigurationError("MeshZo runs the Philox direction; use *_step for oracle parity runs")
+        self.mgr = mgr or RngStateManager()      # "oracle": the reference's z injected (parity runs)
         self.ws = {s: store.workspace(s, batch, seq) for s in self.mesh.dirs}
         dev = store.device
         self.local = torch.zeros(2, dtype=torch.float64, device=dev)
         self.gathered = torch.zeros(2 * fabric.k, dtype=torch.float64, device=dev)
-        self.iteration, self._pending, self.g_prev, self.last_seed = 0, False, 0.0, None
+        self.iteration, self._pending, self._g_prev, self.last_seed = 0, False, 0.0, None
+        self._zc = self._zp = None
 
-    def step_calls(self, update: bool = True):
+    @property
+    def g_prev(self) -> float:
+        return self._g_prev
+
+    @g_prev.setter
+    def g_prev(self, g: float) -> None:
+        """Replacing g_prev replaces the deferred update the next step's
+        fused pass (or flush) applies, as in the reference (zo.py:267-278)."""
+        self._g_prev = float(g)
+        self.store.scal[2:3].fill_(int(np.float64(self.hyper.lr * float(g)).view(np.int64)))
+
+    def step_calls(self, update: bool = True, zc=None, zp=None):
         s, eps, m = self.store, self.hyper.epsilon, self.mesh
+        zmode = L.ZO_Z_ORACLE if self.mgr.oracle else L.ZO_Z_PHILOX
         flags = (L.ZO_PU_UPDATE if update else 0)
         sa = sb = None
         sc_a = sc_b = 0.0
@@ -125,10 +136,11 @@ class MeshZo:
         if MINUS in m.dirs:
             flags |= L.ZO_PU_SHADOW_B
             sb, sc_b = MINUS, -eps
-        calls = s.perturb_call(s.model_table, flags, sc_a, sc_b, sa=sa, sb=sb)
+        calls = s.perturb_call(s.model_table, flags, sc_a, sc_b, sa=sa, sb=sb, zmode=zmode, z_cur=zc, z_prev=zp)
         for d in m.dirs:
             loss_out = self.local.data_ptr() + 8 * d
-            calls += s.forward_calls(d, self.ws[d], +eps if d == PLUS else -eps, loss_out=loss_out)
+            calls += s.forward_calls(d, self.ws[d], +eps if d == PLUS else -eps, zmode=zmode, z_cur=zc,
+                                     loss_out=loss_out)
         calls.append((_gather, (self.fabric, self.gathered, self.local)))
         sp, op, sm, om = m.layout
         calls.append((L.lib().zo_grad_finalize_groups,
@@ -149,9 +161,17 @@ class MeshZo:
         s = self.store
         s.scal[0:1].fill_(_u64_as_i64(seed))
         s.scal[3:4].fill_(1 if self._pending else 0)
-        s.run(self.step_calls())
-        st = _finish_record(s, list(self.ws.values()), self.iteration, seed)
-        self._pending, self.g_prev, self.last_seed = True, st.g, seed
+        if self.mgr.oracle:
+            self._zp = self._zc if self._pending else None
+            self.mgr.reset(seed)
+            self._zc = torch.from_numpy(self.mgr.generator(seed).standard_normal(s.total_params)).to(s.device)
+        s.run(self.step_calls(update=not self.mgr.oracle or self._zp is not None, zc=self._zc, zp=self._zp))
+        try:
+            st = _finish_record(s, list(self.ws.values()), self.iteration, seed)
+        except NumericError:
+            self._pending, s.unflushed = False, False     # nothing armed (see StreamingZo.step)
+            raise
+        self._pending, self._g_prev, self.last_seed = True, st.g, seed
         s.unflushed = True
         return st
 
@@ -160,10 +180,13 @@ class MeshZo:
             raise ProtocolError("flush with no pending update (double flush?)")
         s = self.store
         s.scal[3:4].fill_(1)
-        s.run(s.perturb_call(s.model_table, L.ZO_PU_UPDATE, 0.0, 0.0, sa=None, sb=None))
+        zmode = L.ZO_Z_ORACLE if self.mgr.oracle else L.ZO_Z_PHILOX
+        s.run(s.perturb_call(s.model_table, L.ZO_PU_UPDATE, 0.0, 0.0, sa=None, sb=None, zmode=zmode,
+                             z_prev=self._zc))
         s.scal[3:4].fill_(0)
         torch.cuda.current_stream().synchronize()
         self._pending = False
+        self._zc = self._zp = None
         s.unflushed = False
 
 

@@ -168,10 +168,21 @@ class StreamingZo:
         self.graph = graph and not self.mgr.oracle
         self._graphs = {}
         self.iteration = 0
-        self.g_prev = 0.0
+        self._g_prev = 0.0
         self.last_seed = None
         self._pending = False
         self._z_prev = None
+
+    @property
+    def g_prev(self) -> float:
+        return self._g_prev
+
+    @g_prev.setter
+    def g_prev(self, g: float) -> None:
+        """The reference's next step / flush applies ``self.g_prev``
+        (zo.py:267-293); replacing it replaces the device's lr * g_prev too."""
+        self._g_prev = float(g)
+        self.store.scal[2:3].fill_(int(np.float64(self.hyper.lr * float(g)).view(np.int64)))
 
     def step_calls(self, wsp, wsn, zc=None, zp=None, update=True):
         """One lazy step: fused (update_{j-1} + perturb_j) pass, both
@@ -362,8 +373,16 @@ class StreamingZo:
         wss = [wsp, wsn]
         if self._stacked_ok(wsp):
             wss.append(self.store.stacked_workspace(wsp.batch, wsp.seq))
-        st = _finish_record(self.store, wss, self.iteration, seed)
-        self.g_prev, self.last_seed, self._pending, self._z_prev = st.g, seed, True, zc
+        try:
+            st = _finish_record(self.store, wss, self.iteration, seed)
+        except NumericError:
+            # the step's pass consumed the pending update and the device did
+            # not arm a new one (zo_grad_finalize gates on a finite g), so
+            # nothing is pending: flush / the next step must not re-apply one
+            self.mgr.pop_state()
+            self._pending, self.store.unflushed = False, False
+            raise
+        self._g_prev, self.last_seed, self._pending, self._z_prev = st.g, seed, True, zc
         self.store.unflushed = True
         return st
 

@@ -127,10 +127,23 @@ def run(fn, world, *args, timeout=240):
     for p in procs:
         p.start()
     out = {}
+    import queue
+    import time
+
+    t_end = time.monotonic() + timeout
     try:
-        for _ in range(world):
-            item = q.get(timeout=timeout)
-            out[item[0]] = item
+        while len(out) < world:
+            try:
+                item = q.get(timeout=2)
+                out[item[0]] = item
+                continue
+            except queue.Empty:
+                pass
+            dead = [p.exitcode for p in procs if p.exitcode not in (None, 0)]
+            if dead:       # a worker raised: fail now instead of waiting out the timeout
+                raise RuntimeError(f"worker process exited with {dead} (see its traceback above)")
+            if time.monotonic() > t_end:
+                raise TimeoutError(f"multi-process run did not finish within {timeout} s")
     finally:
         for p in procs:
             p.join(timeout=30)
@@ -421,3 +434,48 @@ def gpu_strategy_edge_worker(rank, world, port, case, q):
     finally:
         dist.destroy_process_group()
     q.put((rank, out))
+
+
+def mesh_golden_worker(rank, world, port, strategy, precision, teacher, golden_path, q):
+    """The lazy mesh step (MeshZo, the production multi-GPU path) in oracle-z
+    mode on the golden ``dist`` case (all ranks on cuda:0, gloo): records per
+    step, and with ``teacher`` the reference's g fed back as g_prev, the
+    flushed master's SHA-256 (the reference's ParamStore.checksum)."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2507_03211_b200.engine import MINUS, PLUS, DeviceStore
+    from paper_2507_03211_b200.fabric import TorchFabric
+    from paper_2507_03211_b200.model import ModelConfig, make_batch
+    from paper_2507_03211_b200.rng import RngStateManager
+    from paper_2507_03211_b200.strategies import MeshZo
+    from paper_2507_03211_b200.zo import ZoHyper
+
+    torch.cuda.set_device(0)
+    init(rank, world, port)
+    fab = TorchFabric()
+    gd = np.load(golden_path)
+    cfg = ModelConfig(16, 16, 2, 2, 8, "f32")
+    seeds = [int(np.uint64(s)) for s in gd["dist/seeds"].tolist()]
+    kind, ordering = (strategy.split(":") + ["pertp_inner"])[:2]
+    key = {"pertp": "dist/pertp", "ddp": f"dist/ddp{world}", "2d": f"dist/2d_{ordering}"}[kind]
+    ref = gd[key]
+    ref_mine = ref if kind == "pertp" else ref[rank]
+    groups = {"pertp": 1, "ddp": world, "2d": world // 2}[kind]
+    dirs = (PLUS, MINUS) if kind == "ddp" else ((PLUS,) if rank % 2 == 0 else (MINUS,))
+    store = DeviceStore(cfg, init_seed=7, directions=dirs, precision=precision)
+    gidx = rank if kind == "ddp" else rank // 2
+    mz = MeshZo(store, ZoHyper(1e-3, 1e-2), fab, "2d" if kind == "pertp" else kind, 4 // groups, 8,
+                mgr=RngStateManager("oracle"))
+    recs = []
+    for j, s in enumerate(seeds, 1):
+        r = mz.step(make_batch(cfg, 4, 200 + j).shard(groups, gidx), s)
+        recs.append((r.loss_pos, r.loss_neg, r.g))
+        if teacher:
+            mz.g_prev = float(ref_mine[j - 1][2])
+    mz.flush()
+    sha = store.checksum()
+    theta = store.theta.cpu().numpy()
+    dist.destroy_process_group()
+    q.put((rank, recs, [tuple(map(float, x)) for x in ref_mine], sha, str(gd[key + "_sha"]), theta))

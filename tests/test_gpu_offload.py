@@ -334,3 +334,120 @@ def test_sliced_offload_divergence_guard():
     assert all(r[1] for r in res) and all(r[2] for r in res)
     with pytest.raises(ConfigurationError):
         OffloadedZo(HostStore(DEEP, 7), zo.ZoHyper(EPS, LR), batch=2, verify=True)
+
+
+# ---------------------------------------------------------------------------
+# parity with the REAL reference's recorded OffloadedZo runs (tests/golden,
+# zosim's OffloadedZo.step / flush, scheduler.py:243-283, 393-410)
+# ---------------------------------------------------------------------------
+GOLDEN_F32 = ["tiny32", "ragged32", "mid32", "wide32"]     # (tiny64 is an f64 store: the device master is fp32)
+
+
+def _golden_cfg(golden, name):
+    c = next(c for c in golden["_meta"]["cases"] if c["name"] == name)
+    return ModelConfig(c["vocab"], c["d"], c["heads"], c["n_blocks"], c["seq"], "f32"), c["batch"], c["steps"]
+
+
+def _zmax(om, seeds):
+    from oracle import zo_oracle as O
+
+    return max(float(np.abs(np.concatenate(O.z_stream(s, om.sizes))).max()) for s in seeds)
+
+
+@pytest.mark.parametrize("mode", ["streams", "serial"])
+@pytest.mark.parametrize("name", GOLDEN_F32)
+def test_offload_oracle_f32_matches_reference_offload_run(name, mode, golden):
+    """OffloadedZo with the reference's z injected and the fp32 parity
+    forward reproduces zosim's recorded OffloadedZo trajectory: losses to
+    1e-6, g to 1e-4 relative; the host master after K steps (one update
+    behind, test_offload.py:130-150) is within lr*|dg|*max|z| per step of the
+    reference's unflushed buffers, and after flush of its final weights."""
+    from oracle import zo_oracle as O
+    from paper_2507_03211_b200.rng import RngStateManager
+
+    cfg, bsz, steps = _golden_cfg(golden, name)
+    host = HostStore(cfg, 7)
+    rt = OffloadedZo(host, zo.ZoHyper(EPS, LR), batch=bsz, mode=mode, mgr=RngStateManager("oracle"),
+                     precision="f32")
+    ref = golden[f"{name}/offload"]
+    seeds = [int(np.uint64(s)) for s in golden[f"{name}/seeds"].tolist()]
+    dg = []
+    for j, s in enumerate(seeds, 1):
+        from paper_2507_03211_b200.model import Batch
+        got = rt.step(Batch(golden[f"{name}/ids/{j}"], golden[f"{name}/tgt/{j}"]), s)
+        lp, ln, g = ref[j - 1]
+        assert abs(got.loss_pos - lp) <= 1e-6 and abs(got.loss_neg - ln) <= 1e-6, (j, got, ref[j - 1])
+        assert abs(got.g - g) <= 1e-4 * max(1.0, abs(g)), (got.g, g)
+        dg.append(abs(got.g - g))
+    om = O.Model(cfg.vocab_size, cfg.d_model, cfg.n_heads, cfg.n_blocks, cfg.seq_len, init_seed=7)
+    bound = steps * LR * max(dg) * _zmax(om, seeds) + 1e-6
+    rt.sync_host()
+    for bl in host.layouts:
+        want = golden[f"{name}/lazy_unflushed/{bl.block_id}"]
+        assert float(np.abs(host.block_buf(bl.block_id).numpy().astype(np.float64) - want).max()) <= bound
+    rt.flush()
+    for bl in host.layouts:
+        want = golden[f"{name}/final/{bl.block_id}"]
+        assert float(np.abs(host.block_buf(bl.block_id).numpy().astype(np.float64) - want).max()) <= bound
+
+
+@pytest.mark.parametrize("name", GOLDEN_F32)
+def test_offload_teacher_forced_reproduces_reference_buffers_and_checksum(name, golden):
+    """With the reference's own g fed back as ``g_prev`` (the attribute the
+    reference's next step and flush apply, scheduler.py:346-349, 393-410),
+    the offload runtime's host master is the reference's bit for bit: the
+    unflushed buffers after K steps equal golden ``lazy_unflushed`` and the
+    flushed store's SHA-256 equals golden ``offload_sha``."""
+    from paper_2507_03211_b200.model import Batch
+    from paper_2507_03211_b200.rng import RngStateManager
+
+    cfg, bsz, steps = _golden_cfg(golden, name)
+    host = HostStore(cfg, 7)
+    rt = OffloadedZo(host, zo.ZoHyper(EPS, LR), batch=bsz, mgr=RngStateManager("oracle"), precision="f32")
+    ref = golden[f"{name}/offload"]
+    for j, s in enumerate(golden[f"{name}/seeds"].tolist(), 1):
+        got = rt.step(Batch(golden[f"{name}/ids/{j}"], golden[f"{name}/tgt/{j}"]), int(np.uint64(s)))
+        assert abs(got.loss_pos - ref[j - 1][0]) <= 1e-6 and abs(got.loss_neg - ref[j - 1][1]) <= 1e-6
+        rt.g_prev = float(ref[j - 1][2])
+    rt.sync_host()
+    for bl in host.layouts:
+        assert np.array_equal(host.block_buf(bl.block_id).numpy(), golden[f"{name}/lazy_unflushed/{bl.block_id}"])
+    rt.flush()
+    assert host.checksum() == str(golden[f"{name}/offload_sha"])
+    assert host.checksum() == str(golden[f"{name}/streaming_sha"])
+
+
+def test_offload_oracle_bf16_production_kernels_within_stated_bound(golden):
+    """The production (bf16 tcgen05) offload path with the reference's z:
+    losses within the bf16 bound of the recorded OffloadedZo run."""
+    from paper_2507_03211_b200.model import Batch
+    from paper_2507_03211_b200.rng import RngStateManager
+
+    cfg, bsz, steps = _golden_cfg(golden, "mid32")
+    rt = OffloadedZo(HostStore(cfg, 7), zo.ZoHyper(EPS, LR), batch=bsz, mgr=RngStateManager("oracle"))
+    ref = golden["mid32/offload"]
+    for j, s in enumerate(golden["mid32/seeds"].tolist(), 1):
+        got = rt.step(Batch(golden[f"mid32/ids/{j}"], golden[f"mid32/tgt/{j}"]), int(np.uint64(s)))
+        assert abs(got.loss_pos - ref[j - 1][0]) <= 2e-3 and abs(got.loss_neg - ref[j - 1][1]) <= 2e-3
+    rt.flush()
+
+
+def test_no_slots_when_every_block_is_resident():
+    """plan / constructor: with every transformer block resident nothing
+    streams, so no slot is allocated, and results still equal the
+    resident path; a budget below two slots is a MemoryCapacityError."""
+    from paper_2507_03211_b200.errors import MemoryCapacityError
+    from paper_2507_03211_b200.scheduler import plan_residency
+
+    recs, _, final = _resident(DEEP, 2)
+    host = HostStore(DEEP, 7)
+    rt = OffloadedZo(host, zo.ZoHyper(EPS, LR), batch=2, resident_blocks=DEEP.n_blocks)
+    assert rt.slots == []
+    for j, s in enumerate(iteration_seeds(9, 2), 1):
+        r = rt.step(make_batch(DEEP, 2, 40 + j), s)
+        assert (r.loss_pos, r.loss_neg, r.g) == recs[j - 1]
+    rt.flush()
+    assert np.array_equal(host.theta.numpy(), final)
+    P = 12 * 32 * 32 + 13 * 32                    # one DEEP transformer block
+    with pytest.raises(MemoryCapacityError):
+        plan_residency(DEEP, int(1.5 * P * 8))

@@ -169,7 +169,14 @@ def test_forward_matches_torch_emulation_of_same_roundings(name):
     wsp, wsn = store.workspace(PLUS, bsz, cfg.seq_len), store.workspace(MINUS, bsz, cfg.seq_len)
     lp = _emulated_loss(store, PLUS, wsp, cfg, +EPS, emb_z)
     ln = _emulated_loss(store, MINUS, wsn, cfg, -EPS, emb_z)
-    assert abs(rec.loss_pos - lp) < 1e-3 and abs(rec.loss_neg - ln) < 1e-3
+    # same operands and roundings: what remains is accumulation order, the
+    # tcgen05 softmax's ex2.approx / bf16 P, and tanh.approx in the GELU
+    # epilogue: measured |dL| <= 4e-5, |dg| <= 4.4e-3 over these cases
+    dlp, dln = abs(rec.loss_pos - lp), abs(rec.loss_neg - ln)
+    dg = abs(rec.g - (lp - ln) / (2 * EPS))
+    print(f"emulation {name}: |dL+| {dlp:.2e} |dL-| {dln:.2e} |dg| {dg:.2e} (g {rec.g:.4f})")
+    assert dlp <= 1e-4 and dln <= 1e-4, (dlp, dln)
+    assert dg <= 0.015, dg               # measured <= 4.4e-3 (hd64); eps = 1e-3
 
 
 @pytest.mark.parametrize("name", ["tiny32", "ragged32", "mid32", "wide32"])
@@ -475,3 +482,26 @@ def test_short_and_ragged_batches_match_oracle(shape, precision):
     zmax = float(np.abs(np.concatenate(O.z_stream(seed, om.sizes))).max())
     diff = np.abs(store.theta.cpu().numpy().astype(np.float64) - np.concatenate(om.blocks)).max()
     assert diff <= LR * abs(got.g - g) * zmax + 1e-6
+
+
+@pytest.mark.parametrize("name", ["mid32", "wide32", "hd64"])
+def test_bf16_production_g_relative_bound_at_eps_1e2(name):
+    """The shipped bf16 / tcgen05 path with the reference's z at eps = 1e-2
+    (where the loss difference dominates bf16 rounding): g within a RELATIVE
+    bound of the oracle's f32 g, and of the same sign (SURVEY 8c mode (ii)
+    measured 0.1-7 % relative at this eps for a bf16 emulation)."""
+    cfg, bsz, _ = _cfg(name)
+    store = DeviceStore(cfg, init_seed=7)
+    om = _oracle_model(cfg)
+    eps = 1e-2
+    worst = 0.0
+    for j, s in enumerate(iteration_seeds(47, 3), 1):
+        ids, tg = O.synthetic_batch(cfg.vocab_size, cfg.seq_len, bsz, 300 + j)
+        lp, ln, g = O.mezo_step(om, ids, tg, eps, LR, s)
+        got = zo.mezo_step(store, Batch(ids, tg), zo.ZoHyper(eps, LR), s, mgr=RngStateManager("oracle"))
+        rel = abs(got.g - g) / max(abs(g), 1e-12)
+        worst = max(worst, rel)
+        assert np.sign(got.g) == np.sign(g), (j, got.g, g)
+        assert abs(got.loss_pos - lp) <= 2e-3 and abs(got.loss_neg - ln) <= 2e-3
+    print(f"eps=1e-2 {name}: worst relative g error {worst:.3%}")
+    assert worst <= 0.10, worst

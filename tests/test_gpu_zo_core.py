@@ -244,6 +244,49 @@ def test_nonfinite_logits_raise_numeric_error():
         zo.mezo_step(store, make_batch(TINY, 4, 1), HYPER, 5)
 
 
+def _bits(t):
+    return t.view(torch.int32).cpu().numpy().copy()
+
+
+@pytest.mark.parametrize("graph", [False, True])
+def test_nonfinite_loss_never_reaches_the_master(graph):
+    """A step with non-finite losses raises NumericError BEFORE any update
+    touches the master (the reference raises in loss(), model.py:366-367):
+    the device arms no deferred update for a non-finite g, so the eager
+    update pass and the next fused pass are value no-ops, nothing is left
+    pending, and stepping resumes from the last good weights."""
+    store = _store()
+    head = store.layouts[-1]
+    k = head.key("b_out")
+    store.theta[k] = float("nan")
+    before = _bits(store.theta)
+    with pytest.raises(NumericError):
+        zo.mezo_step(store, make_batch(TINY, 4, 1), HYPER, 5)
+    assert np.array_equal(_bits(store.theta), before)       # no theta -= NaN * z
+    assert store.scalars()["pending"] == 0 and store.scalars()["lr_g_prev"] == 0.0
+    # lazy: step 1 good, step 2 poisoned -> step 2's pass applied update 1 only
+    good, lazy = _store(), _store()
+    sz = zo.StreamingZo(lazy, HYPER, overlap=False, graph=graph)
+    sz.step(make_batch(TINY, 4, 1), 3)
+    zo.mezo_step(good, make_batch(TINY, 4, 1), HYPER, 3, iteration=1)
+    lazy.theta[k] = float("nan")
+    good.theta[k] = float("nan")
+    with pytest.raises(NumericError):
+        sz.step(make_batch(TINY, 4, 2), 4)
+    a, b = _bits(lazy.theta), _bits(good.theta)
+    a[k] = b[k] = 0                       # (NaN - lr g z is a NaN with other payload bits)
+    assert np.array_equal(a, b) and bool(torch.isnan(lazy.theta[k]))
+    with pytest.raises(ProtocolError):
+        sz.flush()                                             # nothing pending
+    lazy.theta[k] = 0.0                                        # repair, then resume
+    good.theta[k] = 0.0
+    r1 = sz.step(make_batch(TINY, 4, 3), 6)
+    r2 = zo.mezo_step(good, make_batch(TINY, 4, 3), HYPER, 6, iteration=3)
+    assert (r1.loss_pos, r1.loss_neg, r1.g) == (r2.loss_pos, r2.loss_neg, r2.g)
+    sz.flush()
+    assert lazy.equal(good)
+
+
 def test_uniform_logits_loss_is_log_vocab():
     """test_model.py:137-140 through the fused CE head: zero head weights and
     bias give uniform logits, so both directional losses are ln V up to the
@@ -283,3 +326,54 @@ def test_store_copy_and_block_views():
         store.copy()
     sz.flush()
     assert store.copy().equal(store)
+
+
+def _block_ref_out(kind, buf, cfg, x):
+    from oracle import zo_oracle as O
+
+    return O.block_forward(kind, buf, cfg.vocab_size, cfg.d_model, cfg.seq_len, cfg.n_heads, x)
+
+
+@pytest.mark.parametrize("precision,rtol", [("f32", 2e-5), ("bf16", 3e-2)])
+def test_dual_forward_values_match_oracle_blocks(precision, rtol):
+    """Alg. 2 per block (zo.py:181-224) against the oracle's pure block
+    forward (model.py:298-346) on the reference's perturbed buffers: every
+    block's +eps / -eps outputs, first without a pending update, then (next
+    iteration) with the deferred update folded in -- the block's master then
+    equals O.updated(base, g_prev, lr, z_prev) bit for bit and the outputs
+    are the oracle's forward of O.perturbed(O.updated(...), +-eps, z).  Each
+    block is fed the device's own input, so the error is per block.  f32
+    parity mode to 2e-5 relative; the bf16 production kernels to the
+    operand-rounding scale."""
+    from oracle import zo_oracle as O
+
+    cfg = ModelConfig(64, 32, 4, 2, 16, "f32")
+    store = DeviceStore(cfg, init_seed=7, device="cuda:0", precision=precision)
+    om = O.Model(64, 32, 4, 2, 16, init_seed=7)
+    kinds = O.block_kinds(cfg.n_blocks)
+    ids, _ = O.synthetic_batch(64, 16, 2, 77)
+    seeds = iteration_seeds(23, 2)
+    g_prev = 0.61803
+    mgr = RngStateManager("oracle")
+    base = [b.copy() for b in om.blocks]
+    start_prev = None
+    for it, seed in enumerate(seeds):
+        mgr.reset(seed)
+        rs = mgr.capture(seed)                  # this iteration's stream start (zo.py:264-266)
+        lrs = start_prev if it == 1 else None   # the previous iteration's, for the deferred update
+        start_prev = rs
+        zs = O.z_stream(seed, om.sizes)
+        zprev = O.z_stream(seeds[0], om.sizes) if it == 1 else None
+        xp = xn = ids
+        for bid, blk in enumerate(zo.store_blocks(store)):
+            op, on, rs, lrs = zo.dual_forward(blk, HYPER, seed, mgr, rs, lrs, g_prev, xp, xn, it == 1)
+            if it == 1:
+                base[bid] = O.updated(base[bid], g_prev, HYPER.lr, zprev[bid])
+            assert np.array_equal(blk.buf.cpu().numpy(), base[bid]), (it, bid)   # updated / restored exactly
+            for out, x, sc in ((op, xp, +HYPER.epsilon), (on, xn, -HYPER.epsilon)):
+                xin = x if kinds[bid] == "embedding" else x.cpu().numpy()
+                want = _block_ref_out(kinds[bid], O.perturbed(base[bid], sc, zs[bid]), cfg, xin)
+                got = out.cpu().numpy()
+                scale = float(np.abs(want).max())
+                assert float(np.abs(got - want).max()) <= rtol * scale, (precision, it, bid, sc)
+            xp, xn = op, on

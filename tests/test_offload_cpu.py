@@ -41,13 +41,17 @@ def test_plan_residency_fills_the_budget():
     cfg = opt_config("opt-13b", 2048)
     per = [bl for bl in model_layout(cfg) if bl.kind == "transformer"][0].elem_count * 8
     nb = cfg.n_blocks
-    for gb in (5, 20, 40, 60, 80, 100, 101, 200):
+    from paper_2507_03211_b200.errors import MemoryCapacityError
+
+    with pytest.raises(MemoryCapacityError):         # below two slots: refused, never clamped over budget
+        plan_residency(cfg, int(5e9))
+    for gb in (20, 40, 60, 80, 100, 101, 200):
         k, slots = plan_residency(cfg, int(gb * 1e9))
         if gb * 1e9 >= nb * per:
             assert (k, slots) == (nb, 0)
         else:
             assert 0 <= k < nb and 2 <= slots <= nb - k
-            assert (k + slots) * per <= max(gb * 1e9, 2 * per)
+            assert (k + slots) * per <= gb * 1e9
 
 
 def test_plan_residency_counts_split16_lo_planes():
