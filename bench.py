@@ -4,17 +4,30 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
     python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N
 
-Workload (BASELINE.json configs[1]): OPT-1.3B-shaped zosim model (V=50272,
-d=2048, H=32, 24 blocks, T=512), synthetic tokens, random-init weights, ZO-SGD
-with eps=1e-3, lr=1e-7, batch 4 sequences per PertP group.
-  N=1   both directions on one GPU (the lazy-update MeZO/ZO2 step, Alg. 2)
+Headline workload (BASELINE.json configs[1]): OPT-1.3B-shaped zosim model
+(V=50272, d=2048, H=32, 24 blocks, T=512), synthetic tokens, random-init
+weights, ZO-SGD with eps=1e-3, lr=1e-7.  Every GPU evaluates
+2 x ``--batch`` (default 4) sequences' forwards per step (weak scaling):
+  N=1   both directions on one GPU, batch 4 (the lazy MeZO / ZO2 step, Alg. 2)
   N=2   Perturbation Parallelism: rank 0 the +eps forward, rank 1 the -eps
-  N=2k  2D mesh, k groups x 2 directions, batch 4 per group (weak scaling)
+        forward of the same 8 sequences
+  N=2k  2D mesh, k groups x 2 directions, 8 sequences per group
 One step = fused update(j-1)+perturb(j) pass + forward(s) + loss + g.
+
+Offload leg (configs #4 / #5 at the OPT-13B shape, T=2048, 1 sequence per
+group; ``--offload-model`` for 66B / 175B): the fp32 master lives in pinned
+host memory and every transformer block streams through the GPU each step.
+  N=1   the 1-GPU ZO2 schedule (full-block H2D / D2H, both directions): the
+        baseline of the north star's >= 3x target
+  N>=2  the 2D mesh + sliced offload: per-rank NUMA-local host slices (1/N of
+        every block over each rank's own PCIe link), the direction-aware bf16
+        exchange over NVLink, split16 transfer compression
+It reports tokens/s, per-rank PCIe / NVLink GB/s and the per-block time
+against the reference's T_comm model (comm.py:250-256).
 
 Prints ONE JSON line (rank 0).  `value` is device-timed tokens/s with inputs
 resident; `e2e` is the same metric through the public API
-(StreamingZo.step / strategies) with host batches copied in and the step
+(StreamingZo.step / MeshZo.step) with host batches copied in and the step
 record read back every step.
 """
 
@@ -32,8 +45,9 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 EPS, LR = 1e-3, 1e-7
-MODEL, SEQ, BATCH_PER_GROUP = "opt-1.3b", 512, 4
+MODEL, SEQ, BATCH = "opt-1.3b", 512, 4
 BASE_SEED, DATA_SEED = 1234, 99
+NVLINK_GBS = 900.0          # NVLink 5, per direction (spec; no measured figure exists for this box)
 
 
 def _args():
@@ -47,14 +61,21 @@ def _args():
                     help="zosim: the reference's architecture at OPT dims (the headline); opt: real OPT "
                          "(ReLU, tied head, position offset) -- a comparison row")
     ap.add_argument("--seq", type=int, default=SEQ)
-    ap.add_argument("--batch", type=int, default=BATCH_PER_GROUP, help="sequences per PertP group")
-    ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-e2e", action="store_true", help="skip the public-API pass (profiling runs)")
+    ap.add_argument("--batch", type=int, default=BATCH,
+                    help="sequences per directional forward (N=1); a 2-rank PertP group runs 2x this")
+    ap.add_argument("--plan", default="stacked", choices=["stacked", "none"],
+                    help="N=1 step plan: both directions as one launch per layer (stacked) or two streams")
     ap.add_argument("--no-graph", action="store_true", help="launch the step eagerly instead of replaying a CUDA graph")
-    ap.add_argument("--overlap", default="stacked", choices=["none", "blocks", "background", "stacked", "stacked_bg"],
-                    help="none: the two forwards on two streams; blocks: per-block perturb passes on a side stream ahead of the +eps forward; "
-                         "background: one co-resident perturb pass gated per block by device counters; "
-                         "stacked: both directions as one launch per layer over stacked activations")
+    ap.add_argument("--no-e2e", action="store_true", help="skip the public-API pass (profiling runs)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-cpu-full", action="store_true", help="skip the one full (unsampled) CPU reference step")
+    ap.add_argument("--offload", default="on", choices=["on", "off"])
+    ap.add_argument("--offload-model", default="opt-13b")
+    ap.add_argument("--offload-seq", type=int, default=2048)
+    ap.add_argument("--offload-steps", type=int, default=3)
+    ap.add_argument("--offload-warmup", type=int, default=1)
+    ap.add_argument("--offload-compress", default="auto", choices=["auto", "none", "split16"],
+                    help="auto: none for the 1-GPU ZO2 baseline, split16 for the sliced mesh")
     return ap.parse_args()
 
 
@@ -62,22 +83,6 @@ def _config(args):
     from paper_2507_03211_b200.model import opt_config, real_opt_config
 
     return real_opt_config(args.model, args.seq) if args.arch == "opt" else opt_config(args.model, args.seq)
-
-
-def _plan(args):
-    return {"none": False, "blocks": "blocks", "background": "background", "stacked": "stacked",
-            "stacked_bg": "stacked_bg"}[args.overlap]
-
-
-def _plan_text(args, world):
-    if world > 1 or args.overlap == "none":
-        return "one launch; timed alone in a serialised replay"
-    if args.overlap == "stacked":
-        return "one launch; both directions' forwards stacked into one launch per layer"
-    if args.overlap == "blocks":
-        return "timed run: one launch per block on a side stream ahead of the +eps forward; timed alone in a serialised replay"
-    return ("timed run: block 0 full-width, the rest as one co-resident background launch gating each block's "
-            "forward by a device counter; timed alone in a serialised replay")
 
 
 # ----------------------------------------------------------------------------
@@ -147,8 +152,21 @@ def _peaks():
         return 6650.0, 1400.0, 1590.0, "fallback"
 
 
+def _host_info() -> dict:
+    info = {"cpu_count": os.cpu_count()}
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    info["cpu_model"] = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return info
+
+
 # ----------------------------------------------------------------------------
-# CPU reference sample (oracle port of zosim, bounded)
+# CPU reference (oracle port of zosim): a bounded sample, and one full step
 # ----------------------------------------------------------------------------
 def cpu_reference_sample(cfg, batch: int, rows_frac: float = 0.125, param_frac: float = 0.25) -> dict:
     """Time the reference's CPU algorithm (oracle/zo_oracle.py, a bit-exact
@@ -194,41 +212,90 @@ def cpu_reference_sample(cfg, batch: int, rows_frac: float = 0.125, param_frac: 
         t_head = (time.perf_counter() - t0) * (batch * T / rows)
     P = cfg.param_count()
     step = P * t_param + N * t_block + t_head
-    return {"step_s": step, "tokens_per_s": batch * T / step, "cores": cores,
+    return {"step_s": step, "tokens_per_s": batch * T / step, "cores": cores, "extrapolated": True,
+            "fractions": {"params": param_frac / N, "forward_blocks": 1.0 / N, "head_rows": rows_frac},
             "sample": (f"zosim oracle port (numpy, BLAS {cores} threads, z on 1 core): 4 z passes on "
                        f"{param_frac:g} of one transformer block, 2 forwards of 1/{N} blocks at B={batch},T={T}, "
                        f"2 LM-head forwards+CE on {rows_frac:g} of rows; extrapolated to P={P}")}
 
 
-def reference_arm(args, rank, world):
-    from paper_2507_03211_b200.model import opt_config
+def cpu_reference_full_step(cfg, batch: int) -> dict:
+    """ONE full, unsampled eager step of the reference's algorithm on the
+    host, in the reference's own op order (zo.py:136-168): reset, +eps over
+    every block (z regenerated block by block from one PCG64 stream),
+    forward + loss; reset, -2eps, forward + loss; reset, +eps (restore); g;
+    reset, update -- four z passes over all P parameters and two full
+    forwards, arithmetic from the oracle restatement.  Weights are drawn
+    cheaply (same shapes; the cost does not depend on their values)."""
+    import numpy as np
+    from threadpoolctl import threadpool_limits
 
+    from oracle import zo_oracle as O
+
+    cores = os.cpu_count() or 1
+    V, d, T, H, N = cfg.vocab_size, cfg.d_model, cfg.seq_len, cfg.n_heads, cfg.n_blocks
+    kinds = O.block_kinds(N)
+    sizes = [V * d + T * d] + [12 * d * d + 13 * d] * N + [2 * d + d * V + V]      # model.py:60-63
+    rng = np.random.default_rng(1)
+    blocks = [(0.02 * rng.standard_normal(n, dtype=np.float32)).astype(np.float32) for n in sizes]
+    ids = rng.integers(0, V, (batch, T))
+    tg = rng.integers(0, V, (batch, T))
+    seed = O.iteration_seeds(BASE_SEED, 1)[0]
+    with threadpool_limits(limits=cores):
+        t0 = time.perf_counter()
+        losses = []
+        for scale in (+EPS, -EPS):
+            gen = np.random.Generator(np.random.PCG64(seed))
+            x = ids
+            for kind, b in zip(kinds, blocks):
+                pert = O.perturbed(b, scale, gen.standard_normal(b.size))
+                x = O.block_forward(kind, pert, V, d, T, H, x)
+            losses.append(O.cross_entropy(x, tg))
+        gen = np.random.Generator(np.random.PCG64(seed))      # +eps closing the cycle: restore (z still drawn)
+        for b in blocks:
+            gen.standard_normal(b.size)
+        g = O.zo_grad(losses[0], losses[1], EPS)
+        gen = np.random.Generator(np.random.PCG64(seed))
+        blocks = [O.updated(b, g, LR, gen.standard_normal(b.size)) for b in blocks]
+        wall = time.perf_counter() - t0
+    return {"step_s": wall, "tokens_per_s": batch * T / wall, "cores": cores, "extrapolated": False,
+            "sample": f"one full eager step (4 z passes over P={sum(sizes)}, 2 full forwards at B={batch},T={T})"}
+
+
+def reference_arm(args, rank, world):
     if rank != 0:
         return
     cfg = _config(args)
-    n_groups = max(1, args.gpus // 2)
-    batch = args.batch * n_groups
+    batch = args.batch if world == 1 else 2 * args.batch * (world // 2)
     for _ in range(args.warmup):
         cpu_reference_sample(cfg, batch, rows_frac=0.03125, param_frac=0.0625)
     samples = [cpu_reference_sample(cfg, batch, rows_frac=0.03125, param_frac=0.0625) for _ in range(args.steps)]
     vals = [s["tokens_per_s"] for s in samples]
     v = statistics.median(vals)
     ms = 1e3 * statistics.median([s["step_s"] for s in samples])
-    line = {"metric": "OPT ZO fine-tune tokens/s (zosim arch, OPT-1.3B shape)", "value": v, "unit": "tokens/s",
+    line = {"metric": f"OPT ZO fine-tune tokens/s (zosim arch, {args.model} shape)", "value": v, "unit": "tokens/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic", "impl": "reference",
-            "config": {"workload": f"{args.model} ZO-SGD step, seq {args.seq}, batch {args.batch}/group",
+            "data": "synthetic", "impl": "reference", "extrapolated": True,
+            "config": {"workload": f"{args.model} ZO-SGD step, seq {args.seq}, global batch {batch}",
                        "global_batch": batch, "seq_len": args.seq, "strategy": "mezo (CPU reference)"},
             "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": samples[0]["cores"], "kind": "port",
-                             "sample": samples[0]["sample"]},
+                             "extrapolated": True, "fractions": samples[0]["fractions"],
+                             "sample": samples[0]["sample"], "host": _host_info()},
             "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
 # ----------------------------------------------------------------------------
-# our arm
+# our arm: the resident headline step
 # ----------------------------------------------------------------------------
+def _kernel_kind(name: str) -> str:
+    if name.startswith("zo_gemm"):
+        return "gemm"
+    return {"zo_perturb_update": "perturb", "zo_attn_causal_fwd": "attention",
+            "zo_layernorm_fwd": "layernorm", "zo_layernorm_fwd_split": "layernorm"}.get(name, "other")
+
+
 def ours(args, rank, world, local_rank):
     import numpy as np
     import torch
@@ -236,23 +303,24 @@ def ours(args, rank, world, local_rank):
     from paper_2507_03211_b200 import _lib as L
     from paper_2507_03211_b200 import zo
     from paper_2507_03211_b200.engine import MINUS, PLUS, DeviceStore
-    from paper_2507_03211_b200.model import make_batch, opt_config
+    from paper_2507_03211_b200.model import make_batch
     from paper_2507_03211_b200.rng import iteration_seeds
 
     torch.cuda.set_device(local_rank)
     dev = torch.device(f"cuda:{local_rank}")
     cfg = _config(args)
-    B, T = args.batch, args.seq
-    M = B * T
+    T = args.seq
     hyper = zo.ZoHyper(EPS, LR)
     if world == 1:
-        strategy, n_groups, dirs = "mezo-lazy (both directions, 1 GPU)", 1, (PLUS, MINUS)
+        strategy, n_groups, dirs, B = "mezo-lazy (both directions, 1 GPU)", 1, (PLUS, MINUS), args.batch
     else:
         if world % 2:
             raise SystemExit("world size must be 1 or even (PertP pairs)")
         n_groups = world // 2
         strategy = "pertp" if world == 2 else f"2d ({n_groups} groups x 2 directions)"
         dirs = (PLUS if rank % 2 == 0 else MINUS,)
+        B = 2 * args.batch             # one direction per rank: the same forward rows per GPU as N=1
+    M = B * T
     store = DeviceStore(cfg, init_seed=7, device=dev, init="philox", directions=dirs)
     seeds = iteration_seeds(BASE_SEED, args.warmup + args.steps)
     group = rank // 2
@@ -260,70 +328,52 @@ def ours(args, rank, world, local_rank):
                for j in range(1, args.warmup + args.steps + 1)]
 
     if world == 1:
-        runner = zo.StreamingZo(store, hyper, overlap=_plan(args))
+        runner = zo.StreamingZo(store, hyper, overlap=args.plan if args.plan == "stacked" else False,
+                                graph=not args.no_graph)
         wss = [store.workspace(PLUS, B, T), store.workspace(MINUS, B, T)]
-        step_calls = {"none": runner.step_calls, "blocks": runner.overlapped_step_calls,
-                      "background": runner.background_step_calls,
-                      "stacked": runner.stacked_step_calls,
-                      "stacked_bg": runner.stacked_bg_step_calls}[args.overlap](wss[0], wss[1])
+        step_calls = runner._plan(wss[0], wss[1])
     else:
-        from paper_2507_03211_b200.strategies import TwoDRunner
-        runner = TwoDRunner(store, hyper, rank=rank, world=world, batch=B, seq=T)
-        wss = runner.ws_list
+        from paper_2507_03211_b200.fabric import TorchFabric
+        from paper_2507_03211_b200.strategies import MeshZo
+
+        fabric = TorchFabric()
+        runner = MeshZo(store, hyper, fabric, "2d", B, T, graph=not args.no_graph)
+        wss = list(runner.ws.values())
         step_calls = runner.step_calls()
     ids_dev = torch.stack([torch.from_numpy(b.token_ids.reshape(-1).astype(np.int32)) for b in batches]).to(dev)
     tgt_dev = torch.stack([torch.from_numpy(b.targets.reshape(-1).astype(np.int32)) for b in batches]).to(dev)
-
-    pert_set = {i for i, (fn, _) in enumerate(step_calls) if fn.__name__ == "zo_perturb_update"}
-    gemm_idx = [i for i, (fn, _) in enumerate(step_calls) if fn.__name__.startswith("zo_gemm_bf16")]
+    n_launch = sum(2 if fn.__name__ == "zo_ce_finalize" else 1 for fn, _ in step_calls if fn.__name__.startswith("zo_"))
     streams = {int(torch.cuda.current_stream().cuda_stream): torch.cuda.current_stream()}
     if hasattr(store, "_side"):
         streams[int(store._side.cuda_stream)] = store._side
-    n_launch = sum(2 if fn.__name__ == "zo_ce_finalize" else 1 for fn, _ in step_calls if fn.__name__.startswith("zo_"))
-    if world > 1:
-        n_launch += 0   # collectives are NCCL kernels, not ours
 
-    def gemm_flops(fn, args_):
-        if fn.__name__ == "zo_gemm_bf16_split":          # (A, lda, B, B2, ldb, M, N, K, ...)
-            return 2.0 * args_[5] * args_[6] * args_[7]
-        return 2.0 * args_[4] * args_[5] * args_[6]
+    use_graph = not args.no_graph and (world == 1 or runner.graph)     # (a gloo mesh cannot be captured)
 
-    pert_ev, gemm_ev, all_ev = [], [], []   # all_ev: every library call of the instrumented replay
-    gemm_shape_ev = []
-
-    def one_step(j, instrument=False):
+    def one_step(j, instrument=None):
         for ws in wss:
             ws.ids.copy_(ids_dev[j])
             ws.tgt.copy_(tgt_dev[j])
         store.scal[0:1].fill_(zo._u64_as_i64(seeds[j]))
         store.scal[3:4].fill_(1 if j > 0 else 0)
-        if world == 1 and not instrument and not args.no_graph and j > 0:
-            runner._replay(wss[0], wss[1])         # the captured step (same launches)
+        if instrument is None and use_graph and j > 0:
+            if world == 1:
+                runner._replay(wss[0], wss[1])        # the captured step (same launches)
+            else:
+                runner.replay()
             return
-        for i, (fn, a) in enumerate(step_calls):
-            timed = instrument and fn.__name__.startswith("zo_")
+        for fn, a in step_calls:
+            timed = instrument is not None and fn.__name__.startswith("zo_")
             if timed:
-                st_ = streams.get(int(a[-1]) if a and isinstance(a[-1], int) else -1,
-                                  torch.cuda.current_stream())
-                e0 = torch.cuda.Event(enable_timing=True)
-                e1 = torch.cuda.Event(enable_timing=True)
+                st_ = streams.get(int(a[-1]) if a and isinstance(a[-1], int) else -1, torch.cuda.current_stream())
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record(st_)
             rc = fn(*a)
             if rc:
                 L.check(rc)
             if timed:
                 e1.record(st_)
-                if i in pert_set:
-                    pert_ev.append((j, e0, e1))
-                elif i in gemm_set:
-                    gemm_ev.append((e0, e1, gemm_flops(fn, a)))
-                all_ev.append((fn.__name__, e0, e1))
-                if i in gemm_set and fn.__name__ == "zo_gemm_bf16_split":      # per-shape split of the GEMM time
-                    gemm_shape_ev.append((f"{a[5]}x{a[6]}x{a[7]}", e0, e1))
-        if hasattr(runner, "post_step"):
-            runner.post_step()
+                instrument.append((fn.__name__, a, e0, e1))
 
-    gemm_set = set(gemm_idx)
     if world > 1:
         import torch.distributed as dist
     for j in range(args.warmup):
@@ -355,104 +405,124 @@ def ours(args, rank, world, local_rank):
         t = torch.tensor([ms], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    # instrumented pass over the same steps: per-kernel CUDA-event durations.
-    # Kernels of concurrent streams would overlap their event windows, so the
-    # instrumented replay runs the two directional forwards serialised.
-    if world == 1 and args.overlap != "stacked":      # instrument a single-stream plan
-        if args.overlap == "stacked_bg":
-            runner.overlap = "stacked"
-            step_calls[:] = runner.stacked_step_calls(wss[0], wss[1])
-        else:
-            runner.dual_stream = False
-            step_calls[:] = runner.step_calls(wss[0], wss[1])
-        pert_set.clear()
-        pert_set.update(i for i, (fn, _) in enumerate(step_calls) if fn.__name__ == "zo_perturb_update")
-        gemm_set.clear()
-        gemm_set.update(i for i, (fn, _) in enumerate(step_calls) if fn.__name__.startswith("zo_gemm_bf16"))
+
+    # instrumented eager replay of the same steps on ONE stream (event windows
+    # never overlap): per-kernel CUDA-event durations for the roofline rows
+    if world == 1 and args.plan != "stacked":
+        runner.dual_stream = False
+        step_calls = runner._plan(wss[0], wss[1])
+    events = []
     for j in range(args.warmup, args.warmup + args.steps):
-        one_step(j, instrument=True)
-    if world == 1:
-        runner.dual_stream = True
-        runner.overlap = _plan(args) or None
+        one_step(j, instrument=events)
+    runner.dual_stream = True
     torch.cuda.synchronize()
-    per_step = {}
-    for jj, a, b in pert_ev:
-        per_step[jj] = per_step.get(jj, 0.0) + a.elapsed_time(b)
-    p_ms = list(per_step.values())
-    g_tot = sum(a.elapsed_time(b) for a, b, _ in gemm_ev)
-    breakdown = {}
-    for name, a, b in all_ev:
-        breakdown[name] = breakdown.get(name, 0.0) + a.elapsed_time(b) / args.steps
-    g_flops = sum(f for _, _, f in gemm_ev)
-    gemm_shapes = {}
-    for name, a, b in gemm_shape_ev:
-        gemm_shapes.setdefault(name, []).append(a.elapsed_time(b) * 1e3)
+    rec = store.record.cpu().numpy()
+    by_kind, breakdown, gemm_shapes = {}, {}, {}
+    for name, a, e0, e1 in events:
+        t_ms = e0.elapsed_time(e1)
+        breakdown[name] = breakdown.get(name, 0.0) + t_ms / args.steps
+        k = _kernel_kind(name)
+        d = by_kind.setdefault(k, {"ms": 0.0, "work": 0.0})
+        d["ms"] += t_ms
+        if name == "zo_gemm_bf16_split":            # (A, lda, B, B2, ldb, M, N, K, ...)
+            d["work"] += 2.0 * a[5] * a[6] * a[7]
+            gemm_shapes.setdefault(f"{a[5]}x{a[6]}x{a[7]}", []).append(t_ms * 1e3)
+        elif name == "zo_gemm_bf16":                # (A, lda, B, ldb, M, N, K, ...)
+            d["work"] += 2.0 * a[4] * a[5] * a[6]
+            gemm_shapes.setdefault(f"{a[4]}x{a[5]}x{a[6]}", []).append(t_ms * 1e3)
+        elif k == "attention":                      # (qkv, ldq, B, T, H, hd, ...): causal 2*B*T^2*d
+            d["work"] += 2.0 * a[2] * a[3] * a[3] * a[4] * a[5]
+        elif name == "zo_layernorm_fwd_split":      # (x, ldx, g, b, g2, b2, rows, split, d, ...): 4 B in + 2 B out
+            d["work"] += 6.0 * a[6] * a[8]
+        elif name == "zo_layernorm_fwd":            # (x, ldx, g, b, rows, d, ...)
+            d["work"] += 6.0 * a[4] * a[5]
     gemm_shapes = {k: {"n_per_step": len(v) // args.steps, "median_us": round(statistics.median(v), 1)}
                    for k, v in gemm_shapes.items()}
-    rec = store.record.cpu().numpy()
 
     # e2e through the public API: host batch -> device, record -> host, every step
-    e2e_ms = None
-    h2d = d2h = 0
-    if args.no_e2e:
-        e2e_ms = ms
-    elif world == 1:
-        runner2 = zo.StreamingZo(store, hyper, overlap=_plan(args), graph=not args.no_graph)
+    e2e_ms, h2d, d2h = ms, 0, 0
+    api = None
+    if not args.no_e2e:
+        if world == 1:
+            api = zo.StreamingZo(store, hyper, overlap=args.plan if args.plan == "stacked" else False,
+                                 graph=not args.no_graph)
+        else:
+            api = MeshZo(store, hyper, fabric, "2d", B, T, graph=not args.no_graph)
         for j in range(args.warmup):
-            runner2.step(batches[j], seeds[j])
+            api.step(batches[j], seeds[j])
         torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
         t0 = time.perf_counter()
         for j in range(args.warmup, args.warmup + args.steps):
-            runner2.step(batches[j], seeds[j])
+            api.step(batches[j], seeds[j])
         torch.cuda.synchronize()
         e2e_ms = (time.perf_counter() - t0) * 1e3 / args.steps
-        h2d = 2 * M * 4              # ids + targets (int32), shared by both directional workspaces
-        d2h = 3 * 8 + 2 * 4          # ZoStep record (f64 x3) + 2 error flags (int32)
-    else:
-        e2e_ms, h2d, d2h = runner.e2e(batches, seeds, args.warmup, args.steps)
+        if world > 1:
+            t = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_ms = float(t.item())
+        h2d = 2 * M * 4                      # ids + targets (int32), shared by the rank's workspaces
+        d2h = 3 * 8 + len(wss) * 4           # ZoStep record (f64 x3) + error flags (int32)
+    P = store.total_params
+    pert_bytes = store.perturb_bytes(dirs)
+    api = None
+    del runner, store, wss, api
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+
+    offload = None
+    if args.offload == "on":
+        offload = offload_leg(args, rank, world, local_rank)
 
     if rank != 0:
         return
     hbm, tf_sus, tf_burst, peak_kind = _peaks()
-    traffic = _traffic() if (args.model, T, B, args.arch) == (MODEL, SEQ, BATCH_PER_GROUP, "zosim") else {}
-    P = store.total_params
-    bytes_per_param = 12 if world == 1 else 10
-    pert_avg = statistics.mean(p_ms)
-    pert_gbs = P * bytes_per_param / (pert_avg * 1e-3) / 1e9
-    gemm_tfs = g_flops / (g_tot * 1e-3) / 1e12
+    headline = (args.model, T, args.batch, args.arch, world) == (MODEL, SEQ, BATCH, "zosim", 1)
+    traffic = _traffic() if headline else {}
     tokens = B * n_groups * T
     value = tokens / (ms * 1e-3)
-    step_ms_per_rank = ms
-    gemm_share = g_tot / args.steps / step_ms_per_rank
-    pert_share = pert_avg / step_ms_per_rank
-    roof_gemm = {"bound": "tensor", "kernel": "gemm_tcgen05_kernel (all QKV/O/FFN/LM-head launches)",
-                 "achieved": gemm_tfs, "peak": tf_sus, "unit": "TFLOP/s", "frac": gemm_tfs / tf_sus,
-                 "traffic": traffic.get("gemm_bytes_per_step") if world == 1 else None,
-                 "traffic_unit": "DRAM bytes per step, all GEMM launches (ncu)",
-                 "peak_kind": f"{peak_kind} sustained bf16", "share_of_step": gemm_share,
-                 "algorithmic": "2*M*N*K per launch, M=B*T"}
-    roof_pert = {"bound": "hbm", "kernel": "perturb_update_kernel", "achieved": pert_gbs, "peak": hbm,
-                 "unit": "GB/s", "frac": pert_gbs / hbm,
-                 "traffic": traffic.get("perturb_bytes_per_launch") if world == 1 else None,
-                 "traffic_algorithmic": P * bytes_per_param, "peak_kind": f"{peak_kind} HBM copy",
-                 "share_of_step": pert_share,
-                 "algorithmic": f"{bytes_per_param} B/param x {P} params per step "
-                                f"({_plan_text(args, world)})"}
-    dominant = roof_gemm if gemm_share >= pert_share else roof_pert
-    other = roof_pert if dominant is roof_gemm else roof_gemm
+
+    def roof(kind, bound, unit, peak, work_unit, algorithmic, kernel, traffic_v=None):
+        d = by_kind.get(kind, {"ms": 0.0, "work": 0.0})
+        if not d["ms"]:
+            return None
+        ach = d["work"] / (d["ms"] * 1e-3) / work_unit
+        return {"bound": bound, "kernel": kernel, "achieved": ach, "peak": peak, "unit": unit, "frac": ach / peak,
+                "traffic": traffic_v, "share_of_step": d["ms"] / args.steps / ms, "algorithmic": algorithmic}
+
+    r_gemm = roof("gemm", "tensor", "TFLOP/s", tf_sus, 1e12, "2*M*N*K per launch, M = rows of the launch",
+                  "gemm_tcgen05_pair_kernel (all QKV / O / FFN / LM-head launches)",
+                  traffic.get("gemm_bytes_per_step"))
+    if r_gemm:
+        r_gemm["traffic_unit"] = "DRAM bytes per step, all GEMM launches (ncu)"
+        r_gemm["peak_kind"] = f"{peak_kind} sustained bf16"
+    d = by_kind["perturb"]
+    pert_ms = d["ms"] / args.steps
+    r_pert = {"bound": "hbm", "kernel": "perturb_update_kernel", "achieved": pert_bytes / (pert_ms * 1e-3) / 1e9,
+              "peak": hbm, "unit": "GB/s", "frac": pert_bytes / (pert_ms * 1e-3) / 1e9 / hbm,
+              "traffic": traffic.get("perturb_bytes_per_launch"), "traffic_algorithmic": pert_bytes,
+              "peak_kind": f"{peak_kind} HBM copy", "share_of_step": pert_ms / ms,
+              "algorithmic": (f"R+W fp32 master (8 B) + the bf16 / fp32 shadows this rank writes, per parameter "
+                              f"(embedding: no shadow, 8 B): {pert_bytes} B over {P} params, one launch per step")}
+    r_attn = roof("attention", "tensor", "TFLOP/s", tf_sus, 1e12, "2*B*T^2*d per launch (causal halves of QK^T, PV)",
+                  "attn_tc_kernel (tcgen05)")
+    r_ln = roof("layernorm", "hbm", "GB/s", hbm, 1e9, "4 B read + 2 B write per element", "layernorm_warp_kernel")
+    dominant = max([r for r in (r_gemm, r_pert) if r], key=lambda r: r["share_of_step"])
     line = {
-        "metric": "OPT ZO fine-tune tokens/s (zosim arch, OPT-1.3B shape)" if args.arch == "zosim"
-        else "OPT ZO fine-tune tokens/s (real OPT arch, comparison row)",
+        "metric": f"OPT ZO fine-tune tokens/s ({args.arch} arch, {args.model} shape)",
         "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic tokens, random-init (Philox) weights",
-        "config": {"workload": f"{args.model} ZO-SGD step ({args.arch} arch), seq {T}, batch {B} per PertP group",
-                   "global_batch": B * n_groups, "seq_len": T, "parallelism": strategy, "eps": EPS, "lr": LR,
-                   "params": P, "l2": "inputs > L2 (fp32 master 4 B/param + bf16 shadows stream every step)",
-                   "perturb_plan": args.overlap,
-                   "launch": "eager" if (args.no_graph or world > 1) else "CUDA graph replay per step"},
-        "roofline": dominant, "roofline_other": other,
-        "perturb_kernel_gbs": pert_gbs,
+        "config": {"workload": f"{args.model} ZO-SGD step ({args.arch} arch), seq {T}, {B} sequences per "
+                               f"directional forward per GPU", "global_batch": B * n_groups, "seq_len": T,
+                   "parallelism": strategy, "eps": EPS, "lr": LR, "params": P,
+                   "l2": "inputs > L2 (fp32 master 4 B/param + bf16 shadows stream every step)",
+                   "plan": args.plan if world == 1 else "mesh (one direction per rank)",
+                   "launch": "CUDA graph replay per step" if use_graph else "eager"},
+        "roofline": dominant,
+        "roofline_other": {"perturb": r_pert, "gemm": r_gemm, "attention": r_attn, "layernorm": r_ln},
+        "perturb_kernel_gbs": r_pert["achieved"],
         "breakdown_ms_per_step": {k: round(v, 4) for k, v in sorted(breakdown.items(), key=lambda kv: -kv[1])},
         "gemm_us_by_shape": gemm_shapes,
         "clocks": clk.summary(),
@@ -461,11 +531,130 @@ def ours(args, rank, world, local_rank):
                 "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
         "last_step": {"loss_pos": float(rec[0]), "loss_neg": float(rec[1]), "g": float(rec[2])},
     }
+    if offload is not None:
+        line["offload"] = offload
     if world == 1 and not args.no_cpu_baseline and args.arch == "zosim":
         s = cpu_reference_sample(cfg, B)
         line["cpu_baseline"] = {"value": s["tokens_per_s"], "unit": "tokens/s", "cores": s["cores"], "kind": "port",
-                                "sample": s["sample"]}
+                                "extrapolated": True, "fractions": s["fractions"], "sample": s["sample"],
+                                "host": _host_info()}
+        if not args.no_cpu_full:
+            f = cpu_reference_full_step(cfg, B)
+            line["cpu_baseline"]["full_step"] = {"value": f["tokens_per_s"], "unit": "tokens/s",
+                                                 "step_s": f["step_s"], "cores": f["cores"],
+                                                 "extrapolated": False, "sample": f["sample"]}
     print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------
+# our arm: the offload leg (configs #4 / #5 at a shape every box can hold)
+# ----------------------------------------------------------------------------
+def offload_leg(args, rank, world, local_rank) -> dict | None:
+    affinity = os.sched_getaffinity(0)          # the NUMA binding below is undone on return
+    try:
+        return _offload_leg(args, rank, world, local_rank)
+    finally:
+        os.sched_setaffinity(0, affinity)
+
+
+def _offload_leg(args, rank, world, local_rank) -> dict | None:
+    import torch
+
+    from paper_2507_03211_b200.model import make_batch, opt_config
+    from paper_2507_03211_b200.rng import iteration_seeds
+    from paper_2507_03211_b200.scheduler import HostStore, OffloadedZo
+    from paper_2507_03211_b200.zo import ZoHyper
+
+    dev = torch.device(f"cuda:{local_rank}")
+    cfg = opt_config(args.offload_model, args.offload_seq)
+    T = args.offload_seq
+    hyper = ZoHyper(EPS, LR)
+    steps, warm = args.offload_steps, args.offload_warmup
+    seeds = iteration_seeds(BASE_SEED, warm + steps)
+    t_setup = time.perf_counter()
+    if world == 1:
+        compress = "none" if args.offload_compress == "auto" else args.offload_compress
+        host = HostStore(cfg, init_seed=7, init="philox", device=dev, numa=True)
+        rt = OffloadedZo(host, hyper, batch=1, device=dev, trace=True, compress=compress)
+        schedule = ("ZO2 on 1 GPU: every transformer block's full fp32 master H2D and back D2H per step, both "
+                    "directions on the GPU (scheduler.py:285-322)" + (", split16" if compress == "split16" else ""))
+        n_groups, group, numa = 1, 0, host.numa
+    else:
+        from paper_2507_03211_b200.fabric import TorchFabric
+        from paper_2507_03211_b200.sharded import ShardStore
+
+        compress = "split16" if args.offload_compress == "auto" else args.offload_compress
+        fabric = TorchFabric()
+        host = ShardStore(cfg, fabric, init_seed=7, init="philox", device=dev, where="host")
+        rt = OffloadedZo(host, hyper, batch=1, device=dev, fabric=fabric, strategy="2d", redistribute="bf16",
+                         compress=compress, trace=True)
+        schedule = (f"2D mesh ({world // 2} groups x 2 directions) + sliced offload: per-rank NUMA-local pinned "
+                    f"slices (1/{world} of every block over each rank's PCIe link, comm.py:314-342), "
+                    f"direction-aware bf16 exchange over NVLink, compress={compress}")
+        n_groups, group, numa = world // 2, rank // 2, host.numa
+    t_setup = time.perf_counter() - t_setup
+    batches = [make_batch(cfg, n_groups, DATA_SEED * 1_000_003 + j).shard(n_groups, group)
+               for j in range(1, warm + steps + 1)]
+    for j in range(warm):
+        rt.step(batches[j], seeds[j])
+    rt.phase_stats.clear()
+    torch.cuda.synchronize()
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for j in range(warm, warm + steps):
+        rt.step(batches[j], seeds[j])
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    stats = {k: dict(v) for k, v in rt.phase_stats.items()}
+    if world > 1:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    nb = len(rt.wids)
+    P_blk = cfg.d_model * cfg.d_model * 12 + 13 * cfg.d_model
+
+    def gbs(k):
+        s = stats.get(k)
+        return None if not s or not s["ms"] else s["bytes"] / (s["ms"] * 1e-3) / 1e9
+
+    def per_block(k):
+        s = stats.get(k)
+        return None if not s or not s["n"] else s["ms"] / s["n"]
+
+    h2d_gbs, nvl = gbs("h2d"), gbs("nvlink_exchange") or gbs("nvlink_allgather")
+    b_pcie = 2 if compress == "split16" else 4
+    b_nvl = 2 if world > 1 else 4
+    # the reference's model (comm.py:250-256) at the measured PCIe rate and the NVLink spec
+    t_model = None
+    if h2d_gbs:
+        w = -(-P_blk // world)
+        t_model = 1e3 * (w * b_pcie / (h2d_gbs * 1e9) + (P_blk - w) * b_nvl / (NVLINK_GBS * 1e9))
+    measured_block = (per_block("h2d") or 0.0) + (per_block("nvlink_exchange") or per_block("nvlink_allgather") or 0.0)
+    rt.flush()
+    out = {
+        "workload": f"{args.offload_model} (zosim arch) ZO-SGD step, seq {T}, 1 sequence per PertP group, fp32 master "
+                    f"in pinned host memory, all {nb} transformer blocks streamed every step",
+        "schedule": schedule, "n_gpus": world, "global_batch": n_groups, "seq_len": T,
+        "tokens_per_s": n_groups * T / (ms * 1e-3), "ms_per_step": ms, "steps": steps, "warmup": warm,
+        "setup_s": t_setup, "compress": compress,
+        "pcie_bytes_per_step_per_rank": {"h2d": rt.pcie_bytes_per_step()[0], "d2h": rt.pcie_bytes_per_step()[1]},
+        "h2d_gbs_per_rank": h2d_gbs, "d2h_gbs_per_rank": gbs("d2h"),
+        "nvlink_rx_gbs_per_rank": nvl, "nvlink_peak_gbs": NVLINK_GBS,
+        "nvlink_frac": (nvl / NVLINK_GBS) if nvl else None,
+        "per_block_ms": {k: per_block(k) for k in ("h2d", "nvlink_exchange", "nvlink_allgather", "compute", "d2h")
+                         if per_block(k) is not None},
+        "per_block_upload_ms": measured_block, "t_comm_model_ms": t_model,
+        "t_comm_model": "ceil(M/N)*b_pcie/BW_pcie(measured h2d) + (M-ceil(M/N))*b_nvl/900 GB/s (comm.py:250-256)",
+        "numa": numa,
+    }
+    del rt, host
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    return out
 
 
 def main():

@@ -23,7 +23,6 @@ from __future__ import annotations
 
 import ctypes as C
 
-import os
 
 import numpy as np
 import torch
@@ -190,23 +189,11 @@ class Workspace:
         self.ids = torch.zeros(M, dtype=torch.int32, device=device)
         self.tgt = torch.zeros(M, dtype=torch.int32, device=device)
         self.err = torch.zeros(1, dtype=torch.int32, device=device)
-        # optional stream-K workspace of this direction's GEMMs (zeroed once;
-        # the kernels leave their flags cleared), sized for the largest one.
-        # Off by default: at these shapes the finisher's partial reduction,
-        # always a pair's last item, costs more than the partial wave it fills
-        # (tools/gemm_bench.py).
-        self.gemm_ws = None
-        if os.environ.get("ZO_GEMM_SK", "0") == "1":
-            lib = L.lib()
-            need = max(int(lib.zo_gemm_workspace_bytes(M, n, k))
-                       for n, k in ((3 * d, d), (d, d), (4 * d, d), (d, 4 * d), (v, d)))
-            self.gemm_ws = torch.zeros(max(need, 256), dtype=torch.uint8, device=device)
 
-    def gemm(self, lib, *args):
+    @staticmethod
+    def gemm(lib, *args):
         """(fn, args) of one GEMM launch; args are zo_gemm_bf16's, stream last."""
-        if self.gemm_ws is None:
-            return (lib.zo_gemm_bf16, args)
-        return (lib.zo_gemm_bf16_ws, (*args[:-1], self.gemm_ws.data_ptr(), self.gemm_ws.numel(), args[-1]))
+        return (lib.zo_gemm_bf16, args)
 
 
 def _ptr(t):
@@ -256,7 +243,6 @@ class DeviceStore:
         self.block_tables = {bid: SegTable(segs, self.device, [bid] * len(segs))
                              for bid, segs in self.plan.segments.items()}
         self.model_table = self.range_table(0, len(self.layouts))
-        self.block_done = torch.zeros(len(self.layouts), dtype=torch.int32, device=self.device)
         self.scal = torch.zeros(4, dtype=torch.int64, device=self.device)   # ZoStepScalars
         self.record = torch.zeros(3, dtype=torch.float64, device=self.device)
         self._ws = {}
@@ -409,20 +395,17 @@ class DeviceStore:
         return SegTable([x for b in bids for x in self.plan.segments[b]], self.device,
                         [b for b in bids for _ in self.plan.segments[b]])
 
+    def perturb_bytes(self, dirs=(PLUS, MINUS)) -> int:
+        """Algorithmic HBM bytes of one fused update + perturb pass over the
+        whole model: read + write of the fp32 master (8 B/param) plus each
+        written shadow (bf16 weights 2 B, fp32 vectors 4 B, per direction in
+        ``dirs``); tensors without a shadow (the embedding's gathered rows)
+        move 8 B/param."""
+        per = {L.ZO_SHADOW_BF16: 2, L.ZO_SHADOW_F32: 4, L.ZO_SHADOW_NONE: 0}
+        return sum(rows * cols * (8 + per[kind] * len(dirs))
+                   for segs in self.plan.segments.values() for (_, rows, cols, _, _, kind) in segs)
+
     # -- launch plans ----------------------------------------------------------
-    def perturb_bg_call(self, table: SegTable, flags: int, scale_a: float, scale_b: float, stream=None):
-        """Background pass (Philox only): one CTA per SM beside the forward,
-        bumping ``block_done[b]`` per finished tile of block b."""
-        fn = L.lib().zo_perturb_update_bg
-        args = (_ptr(self.theta), 0, _ptr(table.segs), _ptr(table.prefix), table.n_segs, table.n_tiles,
-                _ptr(self.wsh[PLUS]), _ptr(self.vsh[PLUS]), _ptr(self.wsh[MINUS]), _ptr(self.vsh[MINUS]),
-                float(scale_a), float(scale_b), flags, _ptr(self.scal), _ptr(self.block_done),
-                L.stream_ptr(stream))
-        return [(fn, args)]
-
-    def wait_block_call(self, bid: int, target: int, stream=None):
-        return [(L.lib().zo_wait_counter, (_ptr(self.block_done) + 4 * bid, int(target), L.stream_ptr(stream)))]
-
     def perturb_call(self, table: SegTable, flags: int, scale_a: float, scale_b: float, sa=PLUS, sb=MINUS,
                      zmode=L.ZO_Z_PHILOX, z_cur=None, z_prev=None, stream=None):
         fn = L.lib().zo_perturb_update
@@ -674,12 +657,16 @@ class DeviceStore:
 
     def check_errors(self, *wss, flags=None):
         errs = flags if flags is not None else [int(ws.err.item()) for ws in wss]
-        for ws, e in zip(wss, errs):
+        for ws, e in zip(wss, errs):        # clear every flagged workspace before raising
             if e:
                 ws.err.zero_()
-                if e & 4:
-                    raise DimensionError("token id out of embedding range")
-                raise NumericError("non-finite logits")
+        e = 0
+        for x in errs:
+            e |= int(x)
+        if e & 4:
+            raise DimensionError("token id out of embedding range")
+        if e:
+            raise NumericError("non-finite logits")
 
     def read_step(self, wss):
         """One D2H for the step record and the error flags (pinned, then a

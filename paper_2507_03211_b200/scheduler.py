@@ -74,12 +74,20 @@ class HostStore:
     cudaHostRegister so H2D/D2H run at full PCIe rate."""
 
     def __init__(self, config: ModelConfig, init_seed: int = 7, init: str = "host", device=None,
-                 shared: str | None = None):
+                 shared: str | None = None, numa: bool = False):
+        """numa: bind this process to the CPUs of its GPU's NUMA node before
+        the master is allocated, so the pinned pages are node-local
+        (sharded.bind_to_gpu_numa)."""
         config.validate()
         self.config, self.init_seed = config, init_seed
         self.layouts = model_layout(config)
         self.total_params = sum(b.elem_count for b in self.layouts)
         self.shared = shared
+        self.numa = None
+        if numa:
+            from .sharded import bind_to_gpu_numa
+
+            self.numa = bind_to_gpu_numa(torch.device(device or f"cuda:{torch.cuda.current_device()}"))
         if shared is None:
             self.theta = torch.empty(self.total_params, dtype=torch.float32, pin_memory=True)
         else:
@@ -116,7 +124,7 @@ class HostStore:
                             m = min(chunk, n - o)
                             z = torch.empty(m, dtype=torch.float32, device=dev)
                             L.call("zo_philox_normals", seed, k + o, m, z.data_ptr(), L.stream_ptr())
-                            dst[o:o + m].copy_(z.mul_(0.02).cpu())
+                            dst[o:o + m].copy_(z.mul_(0.02))        # straight into the pinned master
         elif init != "none":
             raise ConfigurationError(f"unknown init {init!r}")
 
@@ -438,7 +446,7 @@ class OffloadedZo:
         self.verify = verify
         if compress not in ("none", "split16"):
             raise ConfigurationError(f"compress must be 'none' or 'split16', got {compress!r}")
-        if compress == "split16" and getattr(host, "is_sharded", False):
+        if compress == "split16" and getattr(host, "is_sharded", False) and not getattr(host, "on_host", False):
             raise ConfigurationError("transfer compression applies to a host master (the HBM-sharded master "
                                      "has no PCIe leg)")
         self.compress = compress
@@ -469,6 +477,8 @@ class OffloadedZo:
         self.slots = [BlockSlot(self.plan, self.layouts, tpl, self.dirs, self.device, pad(tpl))
                       for _ in range(n_slots if self.wids else 0)]
         self._bf16 = {}
+        self._phase_ev = []                      # trace: (phase, start event, end event, bytes)
+        self.phase_stats = {}                    # trace: phase -> {"ms", "bytes", "n"} summed over steps
         if redistribute == "bf16" and self.wids:
             me = self.dirs[0]
             for slot in self.slots:                   # both directions' vectors, for the peers
@@ -540,61 +550,92 @@ class OffloadedZo:
             self._hi[bid] = self._hi_pool[pos:pos + ln]
             self._lo[bid] = self._lo_pool[pos:pos + ln]
             pos += ln
-            tmp[:ln].copy_(self.host.block_buf(bid)[off:off + ln])
+            tmp[:ln].copy_(self._host_part(bid))
             ops.planes_split(tmp[:ln], self.slots[0].hi_stage[:ln], self._lo[bid])
             self._hi[bid].copy_(self.slots[0].hi_stage[:ln])
         torch.cuda.synchronize(self.device)
 
     def pcie_bytes_per_step(self):
         """(H2D, D2H) bytes this rank moves per step for the streamed blocks."""
+        if getattr(self.host, "is_sharded", False) and not getattr(self.host, "on_host", False):
+            return 0, 0                                  # HBM-sharded master: no PCIe leg
         per = 2 if self.compress == "split16" else 4
         n = sum(self._own(bid)[1] for bid in self.wids)
         return per * n, per * n
+
+    def _host_part(self, bid) -> torch.Tensor:
+        """The part of block ``bid``'s master this rank moves over PCIe: the
+        whole block (one GPU), its slice of the shared host master, or its
+        own per-rank slice (ShardStore)."""
+        if getattr(self.host, "is_sharded", False):
+            return self.host.slice_of(bid)
+        off, ln = self._own(bid)
+        return self.host.block_buf(bid)[off:off + ln]
+
+    class _Phase:
+        """CUDA-event bracket of one byte movement / compute phase on a stream
+        (trace mode only); resolved per step into ``phase_stats``."""
+
+        def __init__(self, rt, name, stream, nbytes):
+            self.rt, self.name, self.stream, self.nbytes = rt, name, stream, nbytes
+
+        def __enter__(self):
+            if self.rt.trace:
+                self.e0 = torch.cuda.Event(enable_timing=True)
+                self.e0.record(self.stream)
+            return self
+
+        def __exit__(self, *a):
+            if self.rt.trace:
+                e1 = torch.cuda.Event(enable_timing=True)
+                e1.record(self.stream)
+                self.rt._phase_ev.append((self.name, self.e0, e1, self.nbytes))
+            return False
+
+    def _phase(self, name, stream, nbytes=0):
+        return OffloadedZo._Phase(self, name, stream or torch.cuda.current_stream(self.device), nbytes)
+
+    def _gather_slot(self, bid, slot, stream):
+        """Phase 2 of the sliced upload: the peers' fp32 slices over NVLink."""
+        if self.fabric is None or self.world == 1:
+            return
+        w = self.host.slice_plan["layouts"][bid].width
+        with torch.cuda.stream(stream) if stream is not None else _null(), \
+                self._phase("nvlink_allgather", stream, 4 * (self.world - 1) * w):
+            self.fabric.all_gather_tensor(slot.theta[:self.world * w],
+                                          slot.theta[self.rank * w:(self.rank + 1) * w], tag="param")
 
     def _upload(self, bid, slot, stream, gather=None):
         slot.bind(bid)
         if gather is None:      # the bf16 exchange replaces the fp32 all-gather of streamed blocks
             gather = not (self.redistribute == "bf16" and bid in self.wids)
-        if bid in self._lo:                              # hi plane over PCIe, joined with the resident lo
-            off, ln = self._own(bid)
-            with torch.cuda.stream(stream) if stream is not None else _null():
-                slot.hi_stage[:ln].copy_(self._hi[bid], non_blocking=True)
+        off, ln = self._own(bid)
+        sharded_hbm = getattr(self.host, "is_sharded", False) and not getattr(self.host, "on_host", False)
+        with torch.cuda.stream(stream) if stream is not None else _null():
+            if bid in self._lo:                          # hi plane over PCIe, joined with the resident lo
+                with self._phase("h2d", stream, 2 * ln):
+                    slot.hi_stage[:ln].copy_(self._hi[bid], non_blocking=True)
                 ops.planes_join(slot.hi_stage[:ln], self._lo[bid], slot.theta[off:off + ln])
-                if self.fabric is not None and self.world > 1 and gather:
-                    w = self.host.slice_plan["layouts"][bid].width
-                    self.fabric.all_gather_tensor(slot.theta[:self.world * w],
-                                                  slot.theta[self.rank * w:(self.rank + 1) * w], tag="param")
-            return
-        if getattr(self.host, "is_sharded", False):      # HBM-sharded master (sharded.py)
-            self.host.upload_into(bid, slot.theta, stream, gather=gather)
-            return
-        hb = self.host.block_buf(bid)
-        if self.fabric is None:
-            with torch.cuda.stream(stream) if stream is not None else _null():
-                slot.theta[:hb.numel()].copy_(hb, non_blocking=True)
-        else:
-            sliced_upload(hb, slot.theta, self.host.slice_plan["layouts"][bid], self.fabric, self.rank, stream,
-                          gather=gather)
+            elif ln:
+                with self._phase("d2d" if sharded_hbm else "h2d", stream, 4 * ln):
+                    slot.theta[off:off + ln].copy_(self._host_part(bid), non_blocking=True)
+        if gather:
+            self._gather_slot(bid, slot, stream)
 
     def _offload(self, bid, slot, stream):
         if self.verify and bid in self.wids:
             with torch.cuda.stream(stream) if stream is not None else _null():
                 check_slices_identical(self.fabric, self.rank, slot.theta, self.layouts[bid].elem_count)
-        if bid in self._lo:                              # split: lo stays, hi goes to the host
-            off, ln = self._own(bid)
-            with torch.cuda.stream(stream) if stream is not None else _null():
+        off, ln = self._own(bid)
+        sharded_hbm = getattr(self.host, "is_sharded", False) and not getattr(self.host, "on_host", False)
+        with torch.cuda.stream(stream) if stream is not None else _null():
+            if bid in self._lo:                          # split: lo stays, hi goes to the host
                 ops.planes_split(slot.theta[off:off + ln], slot.hi_stage[:ln], self._lo[bid])
-                self._hi[bid].copy_(slot.hi_stage[:ln], non_blocking=True)
-            return
-        if getattr(self.host, "is_sharded", False):
-            self.host.offload_from(bid, slot.theta, stream)
-            return
-        hb = self.host.block_buf(bid)
-        if self.fabric is None:
-            with torch.cuda.stream(stream):
-                hb.copy_(slot.theta[:hb.numel()], non_blocking=True)
-        else:
-            sliced_offload(slot.theta, hb, self.host.slice_plan["layouts"][bid], self.rank, stream)
+                with self._phase("d2h", stream, 2 * ln):
+                    self._hi[bid].copy_(slot.hi_stage[:ln], non_blocking=True)
+            elif ln:                                     # own slice only (comm.py:331-342)
+                with self._phase("d2d" if sharded_hbm else "d2h", stream, 4 * ln):
+                    self._host_part(bid).copy_(slot.theta[off:off + ln], non_blocking=True)
 
     # -- compute --------------------------------------------------------------------
     def _perturb(self, bid, slot, flags, stream):
@@ -679,11 +720,13 @@ class OffloadedZo:
         _, relayout, owner, w = self._bf16_plan(bid)
         me = self.dirs[0]
         self._perturb_slice(bid, slot, self._update_flag() | L.ZO_PU_SHADOW_A | L.ZO_PU_SHADOW_B, stream)
-        with torch.cuda.stream(stream):
+        nv = slot.vsh[me].numel()
+        with torch.cuda.stream(stream), self._phase("nvlink_exchange", stream, 2 * (self.world - 1) * w
+                                                     + 8 * (self.world - 1) * nv):
             self.fabric.exchange_slices(self._stage, me, self._dir_of, w, tag="param")
-            nv = slot.vsh[me].numel()
             vg = self._vgather[:self.world * 2 * nv]
             self.fabric.all_gather_tensor(vg, torch.cat([slot.vsh[PLUS], slot.vsh[MINUS]]), tag="param_vec")
+        with torch.cuda.stream(stream):
             slot.vsh[me].copy_(vg.view(self.world, 2, nv)[:, me].gather(0, owner[None])[0])
             stage, wsh = self._stage[me], slot.wsh[me]
             for (s0, rows, cols, d0, ld) in relayout:
@@ -751,6 +794,7 @@ class OffloadedZo:
         cs, us, os_ = self.streams[COMPUTE], self.streams[UPLOAD], self.streams[OFFLOAD]
         ev = {}
         rec = []
+        self._phase_ev = []
 
         def mark(kind, bid, stream):
             e = torch.cuda.Event(enable_timing=self.trace)
@@ -811,17 +855,24 @@ class OffloadedZo:
         rec.append((COMPUTE, head, eh))
         cs.wait_event(mark("tail", -1, os_))
         r = self.record.cpu().numpy()
-        for ws in self.ws.values():
-            e = int(ws.err.item())
-            if e:
-                ws.err.zero_()
-                from .errors import DimensionError, NumericError
-                # the blocks consumed the pending update; the device armed none
-                self._pending = False
-                raise DimensionError("token id out of embedding range") if e & 4 else NumericError("non-finite logits")
+        errs = [int(ws.err.item()) for ws in self.ws.values()]
+        if any(errs):
+            self._pending = False          # the blocks consumed the pending update; the device armed none
+            _store_view(self).check_errors(*self.ws.values(), flags=errs)
         if self.trace:
             self.timelines.append([{"op": k, "block_id": b, "stream": k, "start": t0.elapsed_time(e),
                                     "end": t0.elapsed_time(ev[(k, b)])} for k, b, e in rec])
+            for name, e0, e1, nb in self._phase_ev:
+                st_ = self.phase_stats.setdefault(name, {"ms": 0.0, "bytes": 0, "n": 0})
+                st_["ms"] += e0.elapsed_time(e1)
+                st_["bytes"] += nb
+                st_["n"] += 1
+            for k, b, e in rec:
+                if k == COMPUTE and b in self.wids:
+                    st_ = self.phase_stats.setdefault("compute", {"ms": 0.0, "bytes": 0, "n": 0})
+                    st_["ms"] += e.elapsed_time(ev[(k, b)])
+                    st_["n"] += 1
+            self._phase_ev = []
         self.uploaded_params += sum(self.layouts[i].elem_count for i in self.wids)
         self.offloaded_params += sum(self.layouts[i].elem_count for i in self.wids)
         st = ZoStep(self.iteration, seed, float(r[0]), float(r[1]), float(r[2]))
@@ -868,7 +919,7 @@ class OffloadedZo:
                 with torch.cuda.stream(cs):
                     stage[:ln].copy_(self._hi[bid], non_blocking=True)
                     ops.planes_join(stage[:ln], self._lo[bid], tmp[:ln])
-                    self.host.block_buf(bid)[off:off + ln].copy_(tmp[:ln], non_blocking=True)
+                    self._host_part(bid).copy_(tmp[:ln], non_blocking=True)
                 cs.synchronize()
         for bid, slot in self.persistent.items():
             if getattr(self.host, "is_sharded", False):
@@ -948,6 +999,7 @@ class _StoreView:
         self.scal = rt.scal
         self.precision = rt.precision
         self._fc = DeviceStore.forward_calls.__get__(self)
+        self.check_errors = DeviceStore.check_errors.__get__(self)
         self._fc32 = DeviceStore.forward_calls_f32.__get__(self)
 
     def forward_calls(self, *a, **k):

@@ -1,4 +1,6 @@
-"""HBM-sharded fp32 master (ZeRO-3 style).
+"""Sharded fp32 master: in HBM (ZeRO-3 style)
+or in per-rank, NUMA-local pinned host memory (the sliced offload of configs
+#4 / #5).
 
 Instead of the pinned host master of the ZO2 offload runtime, the fp32 master
 is split over the N ranks' HBM with the reference's slice layout
@@ -16,6 +18,15 @@ so every rank computes the identical fused update+perturb on the whole block
 slices of the resident master -- sharded == resident bit for bit, like the
 sliced offload path.  Per-GPU HBM at the OPT-175B shape on 8 ranks: 87.6 GB
 of shards + the resident embedding / head + 3 block slots.
+
+``where="host"`` keeps the same slices in pinned host memory instead: each
+rank owns ONLY its 1/N of every block (87.6 GB per rank at 175B / 8, not the
+701 GB master on every rank), allocated after the process is bound to the
+CPUs of its GPU's NUMA node (``bind_to_gpu_numa``), so the pages are local to
+the socket whose PCIe root serves that GPU.  upload(b) is then the own slice
+over this rank's PCIe link (comm.py:314-328 phase 1) and offload(b) the own
+slice back (comm.py:331-342); the full master exists only when gathered for
+flush checks / checkpoints (``gather_master``).
 """
 
 from __future__ import annotations
@@ -40,8 +51,12 @@ class ShardStore:
 
     is_sharded = True
 
-    def __init__(self, config: ModelConfig, fabric=None, init_seed: int = 7, init: str = "host", device=None):
+    def __init__(self, config: ModelConfig, fabric=None, init_seed: int = 7, init: str = "host", device=None,
+                 where: str = "hbm", numa: bool = True):
         config.validate()
+        if where not in ("hbm", "host"):
+            raise ConfigurationError(f"where must be 'hbm' or 'host', got {where!r}")
+        self.on_host = where == "host"
         self.config, self.init_seed, self.fabric = config, init_seed, fabric
         self.device = torch.device(device or f"cuda:{torch.cuda.current_device()}")
         L.lib()
@@ -55,7 +70,11 @@ class ShardStore:
         for bl in self.layouts:
             self.offsets[bl.block_id] = off
             off += self.slice_plan["layouts"][bl.block_id].width
-        self.shard = torch.zeros(max(off, 1), dtype=torch.float32, device=self.device)
+        self.numa = bind_to_gpu_numa(self.device) if (self.on_host and numa) else None
+        if self.on_host:          # first touch by this (NUMA-bound) process -> node-local pages
+            self.shard = torch.zeros(max(off, 1), dtype=torch.float32, pin_memory=True)
+        else:
+            self.shard = torch.zeros(max(off, 1), dtype=torch.float32, device=self.device)
         if init == "host":
             for bl in self.layouts:
                 _, lo, ln = self.own(bl.block_id)
@@ -82,6 +101,10 @@ class ShardStore:
     def shard_bytes(self) -> int:
         return self.shard.numel() * 4
 
+    def host_part(self, bid: int) -> torch.Tensor:
+        """The part of block ``bid`` this rank moves over PCIe (its slice)."""
+        return self.slice_of(bid)
+
     def _init_philox(self, init_seed: int):
         """DeviceStore._init_philox restricted to this rank's slices: the same
         values the resident store draws (z keyed by the global element)."""
@@ -100,8 +123,14 @@ class ShardStore:
                 elif name.startswith("b") or name.endswith("_b"):
                     seg.zero_()
                 else:
-                    L.call("zo_philox_normals", seed, bl.key0 + i0, i1 - i0, seg.data_ptr(), L.stream_ptr())
-                    seg.mul_(0.02)
+                    for c0 in range(i0, i1, 1 << 26):
+                        c1 = min(i1, c0 + (1 << 26))
+                        tmp = seg[c0 - i0:c1 - i0] if not self.on_host else \
+                            torch.empty(c1 - c0, dtype=torch.float32, device=self.device)
+                        L.call("zo_philox_normals", seed, bl.key0 + c0, c1 - c0, tmp.data_ptr(), L.stream_ptr())
+                        tmp.mul_(0.02)
+                        if self.on_host:
+                            seg[c0 - i0:c1 - i0].copy_(tmp)
 
     # -- the two byte movements of the streaming schedule ----------------------------
     def upload_into(self, bid: int, slot_theta: torch.Tensor, stream=None, gather: bool = True) -> None:
@@ -156,3 +185,38 @@ class _Null:
 
     def __exit__(self, *a):
         return False
+
+
+def bind_to_gpu_numa(device) -> dict:
+    """Pin this process to the CPUs NVML reports as local to ``device``'s
+    PCIe root (its NUMA node), so pinned buffers allocated afterwards are
+    first-touched on that node and the H2D / D2H of the sliced schedule never
+    cross the socket interconnect.  No-op (reported) where NVML or the
+    affinity call is unavailable."""
+    import os
+
+    info = {"bound": False, "cpus": None, "node": None}
+    try:
+        import pynvml
+
+        pynvml.nvmlInit()
+        uuid = str(torch.cuda.get_device_properties(device).uuid)
+        h = pynvml.nvmlDeviceGetHandleByUUID(uuid if uuid.startswith("GPU-") else "GPU-" + uuid)
+        ncpu = os.cpu_count() or 1
+        words = pynvml.nvmlDeviceGetCpuAffinity(h, (ncpu + 63) // 64)
+        cpus = {64 * i + b for i, w in enumerate(words) for b in range(64) if (int(w) >> b) & 1 and 64 * i + b < ncpu}
+        if cpus and len(cpus) < ncpu:
+            os.sched_setaffinity(0, cpus)
+            info.update(bound=True, cpus=len(cpus))
+        elif cpus:
+            info.update(cpus=len(cpus))          # one node (or no topology): nothing to restrict
+        try:
+            bus = pynvml.nvmlDeviceGetPciInfo(h).busId
+            bus = (bus.decode() if isinstance(bus, bytes) else bus).lower()[-12:]     # dddd:bb:dd.f
+            with open(f"/sys/bus/pci/devices/{bus}/numa_node") as f:
+                info["node"] = int(f.read().strip())
+        except (OSError, ValueError, AttributeError):
+            pass
+    except Exception as e:  # noqa: BLE001  (NVML missing / no permission: keep the default placement)
+        info["error"] = type(e).__name__
+    return info

@@ -99,7 +99,11 @@ class MeshZo:
     is the launch plan the benchmark replays."""
 
     def __init__(self, store: DeviceStore, hyper: ZoHyper, fabric, strategy: str, batch: int, seq: int,
-                 mgr: RngStateManager | None = None):
+                 mgr: RngStateManager | None = None, graph: bool = True):
+        """graph: from the second step on, replay the step's launches -- the
+        fused pass, the forward(s), the NCCL loss all-gather and the ordered
+        g reduction -- from one captured CUDA graph (NCCL fabrics only: a
+        gloo collective stages through the host and cannot be captured)."""
         self.store, self.hyper, self.fabric = store, hyper.validate(), fabric
         self.mesh = MeshLayout(strategy, fabric.k, fabric.rank)
         for s in self.mesh.dirs:
@@ -112,6 +116,8 @@ class MeshZo:
         self.gathered = torch.zeros(2 * fabric.k, dtype=torch.float64, device=dev)
         self.iteration, self._pending, self._g_prev, self.last_seed = 0, False, 0.0, None
         self._zc = self._zp = None
+        self.graph = bool(graph) and not self.mgr.oracle and getattr(fabric, "backend", None) == "nccl"
+        self._graph = None
 
     @property
     def g_prev(self) -> float:
@@ -148,6 +154,18 @@ class MeshZo:
                        float(self.hyper.lr), s.scal.data_ptr(), s.record.data_ptr(), L.stream_ptr())))
         return calls
 
+    def replay(self):
+        """Capture the Philox step once (the first step ran eagerly, so the
+        NCCL communicator, kernel attributes and TMA descriptors exist), then
+        replay it; seeds / pending flag / g live on the device, so one graph
+        serves every step."""
+        if self._graph is None:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, capture_error_mode="thread_local"):
+                self.store.run(self.step_calls())
+            self._graph = g
+        self._graph.replay()
+
     def stage(self, shard: Batch):
         shard.validate(self.store.config)
         for ws in self.ws.values():
@@ -165,7 +183,10 @@ class MeshZo:
             self._zp = self._zc if self._pending else None
             self.mgr.reset(seed)
             self._zc = torch.from_numpy(self.mgr.generator(seed).standard_normal(s.total_params)).to(s.device)
-        s.run(self.step_calls(update=not self.mgr.oracle or self._zp is not None, zc=self._zc, zp=self._zp))
+        if self.graph and self.iteration > 1:
+            self.replay()
+        else:
+            s.run(self.step_calls(update=not self.mgr.oracle or self._zp is not None, zc=self._zc, zp=self._zp))
         try:
             st = _finish_record(s, list(self.ws.values()), self.iteration, seed)
         except NumericError:
@@ -307,40 +328,3 @@ def twod_step(fabric, rank, assign, store, shard, hyper, seed, ordering="pertp_i
         raise ConfigurationError(f"mesh needs {2 * assign.n_groups} ranks (= {assign.n_groups} groups x 2), "
                                  f"fabric has {fabric.k}")
     return _eager_step(fabric, rank, store, shard, hyper, seed, "2d", mgr, iteration, verify, ordering)
-
-
-class TwoDRunner:
-    """Benchmark adaptor: MeshZo('2d') with the launch-plan interface bench.py
-    replays (N=2 is PertP = the 2D mesh with one group)."""
-
-    def __init__(self, store, hyper, rank, world, batch, seq):
-        from .fabric import TorchFabric
-
-        self.fabric = TorchFabric()
-        self.mesh_zo = MeshZo(store, hyper, self.fabric, "2d", batch, seq)
-        self.ws_list = list(self.mesh_zo.ws.values())
-
-    def step_calls(self):
-        return self.mesh_zo.step_calls()
-
-    def e2e(self, batches, seeds, warmup, steps):
-        import time
-
-        n_groups = self.mesh_zo.mesh.n_groups
-        g = self.mesh_zo.mesh.group
-        for j in range(warmup):
-            self.mesh_zo.step(batches[j], seeds[j])
-        torch.cuda.synchronize()
-        self.fabric.barrier()
-        t0 = time.perf_counter()
-        for j in range(warmup, warmup + steps):
-            self.mesh_zo.step(batches[j], seeds[j])
-        torch.cuda.synchronize()
-        ms = (time.perf_counter() - t0) * 1e3 / steps
-        t = torch.tensor([ms], dtype=torch.float64, device=self.mesh_zo.store.device)
-        import torch.distributed as dist
-
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        M = batches[0].token_ids.size
-        _ = (n_groups, g)
-        return float(t.item()), 2 * M * 4, 3 * 8 + 4

@@ -154,14 +154,14 @@ class StreamingZo:
         self.store = store
         self.hyper = hyper.validate()
         self.mgr = mgr or RngStateManager()
-        # "stacked" (default): one fused pass, then both forwards as one launch
-        # per layer over stacked activations; False: the fused pass, then the
-        # two forwards on two streams; "blocks" (or True): per-block passes on a
-        # side stream gated by events; "background": one co-resident pass gated
-        # per block by device counters.  All plans give identical results.
-        plan = {False: None, True: "blocks", "blocks": "blocks", "background": "background",
-                "stacked": "stacked", "stacked_bg": "stacked_bg"}[overlap]
-        self.overlap = plan if not self.mgr.oracle else None
+        # "stacked" (default): the fused pass, then both directional forwards
+        # as one launch per layer over stacked activations; False / "none":
+        # the fused pass, then the two forwards on two streams (also the plan
+        # for shapes the stacked GEMMs cannot split and for oracle-z runs).
+        # Both plans give identical results.
+        if overlap not in (False, None, "none", "stacked"):
+            raise ProtocolError(f"unknown step plan {overlap!r} (plans: 'stacked', 'none')")
+        self.overlap = "stacked" if (overlap == "stacked" and not self.mgr.oracle) else None
         self.dual_stream = True
         # Philox steps replay one captured CUDA graph per batch shape (the
         # step's scalars are device-resident, so the launches never change)
@@ -208,68 +208,6 @@ class StreamingZo:
         calls += s.grad_call(wsp, wsn, eps, self.hyper.lr)
         return calls
 
-    def overlapped_step_calls(self, wsp, wsn, side_stream=None):
-        """Same step, pipelined across two streams: the per-block fused
-        update+perturb passes (HBM-bound) run on a side stream one block ahead
-        of the +eps forward (tensor-core-bound) on the current stream, which
-        waits per block on an event.  The -eps forward follows on the main
-        stream.  Numerically identical to step_calls (same kernels, same
-        per-element arithmetic; only the launch granularity changes)."""
-        if self.mgr.oracle:
-            raise ProtocolError("the overlapped plan runs the Philox direction only")
-        s, eps = self.store, self.hyper.epsilon
-        main = torch.cuda.current_stream()
-        side = side_stream or _side_stream(s)
-        nb = len(s.layouts)
-        evs = _block_events(s, nb)
-        start = evs[-1]
-        flags = L.ZO_PU_UPDATE | L.ZO_PU_SHADOW_A | L.ZO_PU_SHADOW_B
-        calls = [(_record_and_wait, (start, main, side))]
-        for b in range(nb):
-            calls += s.perturb_call(s.block_tables[b], flags, +eps, -eps, stream=side)
-            calls.append((_record, (evs[b], side)))
-        for b in range(nb):
-            calls.append((_wait, (main, evs[b])))
-            calls += s.forward_calls(PLUS, wsp, +eps, blocks=[b])
-        calls += s.forward_calls(MINUS, wsn, -eps)
-        calls += s.grad_call(wsp, wsn, eps, self.hyper.lr)
-        return calls
-
-    def background_step_calls(self, wsp, wsn):
-        """Same step with the fused update+perturb pass as a co-resident
-        background kernel: block 0 (the embedding, needed first) runs as a
-        full-width pass, the rest as zo_perturb_update_bg on a third stream,
-        and both directional forwards wait per block on its completion
-        counter (zo_wait_counter) instead of on the whole pass.  Same kernels'
-        per-element arithmetic as step_calls, so results are identical."""
-        if self.mgr.oracle:
-            raise ProtocolError("the background plan runs the Philox direction only")
-        s, eps = self.store, self.hyper.epsilon
-        nb = len(s.layouts)
-        main, side, pstream = torch.cuda.current_stream(), _side_stream(s), _perturb_stream(s)
-        if not hasattr(s, "_bg_events"):
-            s._bg_events = [torch.cuda.Event() for _ in range(4)]
-        ev = s._bg_events
-        if not hasattr(s, "_bg_tables"):
-            s._bg_tables = (s.range_table(0, 1), s.range_table(1, nb))
-        head, rest = s._bg_tables
-        flags = L.ZO_PU_UPDATE | L.ZO_PU_SHADOW_A | L.ZO_PU_SHADOW_B
-        calls = [(_record_and_wait, (ev[0], main, pstream)),
-                 (_zero_on, (s.block_done, pstream))]
-        calls += s.perturb_call(head, flags, +eps, -eps, stream=pstream)
-        calls.append((_record, (ev[1], pstream)))            # block 0 done, counters reset
-        calls += s.perturb_bg_call(rest, flags, +eps, -eps, stream=pstream)
-        calls.append((_record, (ev[2], pstream)))
-        calls += [(_wait, (main, ev[1])), (_wait, (side, ev[1]))]
-        for b in range(nb):
-            for sgn, ws, st in ((PLUS, wsp, None), (MINUS, wsn, side)):
-                if b > 0:
-                    calls += s.wait_block_call(b, rest.block_tiles[b], stream=st)
-                calls += s.forward_calls(sgn, ws, eps if sgn == PLUS else -eps, blocks=[b], stream=st)
-        calls += [(_record_and_wait, (ev[3], side, main)), (_wait, (main, ev[2]))]
-        calls += s.grad_call(wsp, wsn, eps, self.hyper.lr)
-        return calls
-
     def stacked_step_calls(self, wsp, wsn):
         """Same step with both directional forwards as ONE launch per layer
         over stacked [+eps; -eps] activations (DeviceStore.forward_calls_stacked):
@@ -286,59 +224,12 @@ class StreamingZo:
         calls += s.grad_call_stacked(ws, eps, self.hyper.lr)
         return calls
 
-    def stacked_bg_step_calls(self, wsp, wsn):
-        """The stacked step with the perturb pass split per block onto a
-        LOW-priority stream while the forward runs on a HIGH-priority one:
-        blocks 0-1 are perturbed up front (the forward starts at once), every
-        later block's pass is queued behind at low priority and the forward of
-        block b waits on its event.  The short perturb CTAs fill the SMs the
-        forward leaves idle (partial GEMM waves, LayerNorm / attention
-        tails, kernel boundaries) and the block scheduler hands freed SMs to the
-        forward's pending CTAs first.  Same kernels and per-element arithmetic
-        as stacked_step_calls, so results are bit-identical."""
-        if self.mgr.oracle:
-            raise ProtocolError("the stacked background plan runs the Philox direction only")
-        s, eps = self.store, self.hyper.epsilon
-        ws = s.stacked_workspace(wsp.batch, wsp.seq)
-        nb = len(s.layouts)
-        if not hasattr(s, "_prio_streams"):
-            lo, hi = torch.cuda.Stream.priority_range() if hasattr(torch.cuda.Stream, "priority_range") else (0, -1)
-            s._prio_streams = (torch.cuda.Stream(device=s.device, priority=hi),
-                               torch.cuda.Stream(device=s.device, priority=lo))
-            s._prio_events = [torch.cuda.Event() for _ in range(nb + 2)]
-        hi_s, lo_s = s._prio_streams
-        ev = s._prio_events
-        main = torch.cuda.current_stream()
-        flags = L.ZO_PU_UPDATE | L.ZO_PU_SHADOW_A | L.ZO_PU_SHADOW_B
-        calls = [(_record_and_wait, (ev[nb], main, hi_s)), (_wait, (lo_s, ev[nb]))]
-        head = min(2, nb)
-        for b in range(head):
-            calls += s.perturb_call(s.block_tables[b], flags, +eps, -eps, stream=hi_s)
-        calls.append((_record, (ev[0], hi_s)))
-        calls.append((_wait, (lo_s, ev[0])))        # the background pass starts behind the head blocks
-        for b in range(head, nb):
-            calls += s.perturb_call(s.block_tables[b], flags, +eps, -eps, stream=lo_s)
-            calls.append((_record, (ev[b], lo_s)))
-        for b in range(nb):
-            if b >= head:
-                calls.append((_wait, (hi_s, ev[b])))
-            calls += s.forward_calls_stacked(ws, eps, stream=hi_s, blocks=[b])
-        calls += s.grad_call_stacked(ws, eps, self.hyper.lr, stream=hi_s)
-        calls.append((_record_and_wait, (ev[nb + 1], hi_s, main)))
-        return calls
-
     def _stacked_ok(self, wsp):
-        return self.overlap in ("stacked", "stacked_bg") and self.store.stackable(wsp.batch, wsp.seq)
+        return self.overlap == "stacked" and self.store.stackable(wsp.batch, wsp.seq)
 
     def _plan(self, wsp, wsn, zc=None, zp=None, update=True):
         if self._stacked_ok(wsp):
-            if self.overlap == "stacked_bg":
-                return self.stacked_bg_step_calls(wsp, wsn)
             return self.stacked_step_calls(wsp, wsn)
-        if self.overlap == "blocks":
-            return self.overlapped_step_calls(wsp, wsn)
-        if self.overlap == "background":
-            return self.background_step_calls(wsp, wsn)
         return self.step_calls(wsp, wsn, zc, zp, update=update)
 
     def _replay(self, wsp, wsn):
@@ -409,18 +300,6 @@ def _side_stream(store: DeviceStore):
     return store._side
 
 
-def _perturb_stream(store: DeviceStore):
-    if not hasattr(store, "_pstream"):
-        store._pstream = torch.cuda.Stream(device=store.device)
-    return store._pstream
-
-
-def _zero_on(t: torch.Tensor, stream):
-    with torch.cuda.stream(stream):
-        t.zero_()
-    return 0
-
-
 def _block_events(store: DeviceStore, n: int):
     if getattr(store, "_evs", None) is None or len(store._evs) != n + 1:
         store._evs = [torch.cuda.Event() for _ in range(n + 1)]
@@ -430,16 +309,6 @@ def _block_events(store: DeviceStore, n: int):
 def _record_and_wait(ev, main, side):
     ev.record(main)
     side.wait_event(ev)
-    return 0
-
-
-def _record(ev, stream):
-    ev.record(stream)
-    return 0
-
-
-def _wait(stream, ev):
-    stream.wait_event(ev)
     return 0
 
 

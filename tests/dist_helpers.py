@@ -479,3 +479,56 @@ def mesh_golden_worker(rank, world, port, strategy, precision, teacher, golden_p
     theta = store.theta.cpu().numpy()
     dist.destroy_process_group()
     q.put((rank, recs, [tuple(map(float, x)) for x in ref_mine], sha, str(gd[key + "_sha"]), theta))
+
+
+def nccl_world1_worker(rank, world, port, q):
+    """(test_gpu_nccl) NCCL at world size 1: the captured mesh step and the
+    sliced offload runtime over an NCCL fabric vs the single-GPU paths."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2507_03211_b200 import zo
+    from paper_2507_03211_b200.engine import DeviceStore
+    from paper_2507_03211_b200.fabric import TorchFabric
+    from paper_2507_03211_b200.model import ModelConfig, make_batch
+    from paper_2507_03211_b200.rng import iteration_seeds
+    from paper_2507_03211_b200.scheduler import OffloadedZo
+    from paper_2507_03211_b200.sharded import ShardStore
+    from paper_2507_03211_b200.strategies import MeshZo
+
+    torch.cuda.set_device(0)
+    init(rank, world, port, backend="nccl")
+    fab = TorchFabric()
+    out = {"backend": fab.backend}
+    cfg = ModelConfig(64, 32, 4, 3, 16, "f32")
+    h = zo.ZoHyper(1e-3, 1e-2)
+    seeds = iteration_seeds(71, 5)
+    ref, mesh = DeviceStore(cfg, 7), DeviceStore(cfg, 7)
+    sz = zo.StreamingZo(ref, h, overlap=False, graph=False)
+    mz = MeshZo(mesh, h, fab, "ddp", 2, 16, graph=True)
+    same = True
+    for j, s in enumerate(seeds, 1):
+        b = make_batch(cfg, 2, 900 + j)
+        a, c = sz.step(b, s), mz.step(b, s)
+        same &= (a.loss_pos, a.loss_neg, a.g) == (c.loss_pos, c.loss_neg, c.g)
+    sz.flush()
+    mz.flush()
+    out["mesh_graph"] = mz._graph is not None
+    out["mesh_same"] = bool(same and torch.equal(ref.theta, mesh.theta))
+    # sliced offload over the NCCL fabric, host-pinned per-rank slices (N = 1: the whole block)
+    host = ShardStore(cfg, fab, 7, where="host")
+    rt = OffloadedZo(host, h, batch=2, fabric=fab, strategy="mezo", trace=True)
+    ref2 = DeviceStore(cfg, 7)
+    sz2 = zo.StreamingZo(ref2, h, overlap=False, graph=False)
+    same = True
+    for j, s in enumerate(seeds, 1):
+        b = make_batch(cfg, 2, 900 + j)
+        a, c = sz2.step(b, s), rt.step(b, s)
+        same &= (a.loss_pos, a.loss_neg, a.g) == (c.loss_pos, c.loss_neg, c.g)
+    sz2.flush()
+    rt.flush()
+    out["offload_same"] = bool(same and np.array_equal(host.gather_master(), ref2.theta.cpu().numpy()))
+    out["phases"] = sorted(rt.phase_stats)
+    dist.destroy_process_group()
+    q.put((rank, out))

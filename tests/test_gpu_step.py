@@ -290,46 +290,7 @@ def test_error_behaviour_matches_reference():
         sz.flush()
 
 
-@pytest.mark.parametrize("plan", ["blocks", "background"])
-def test_overlapped_step_is_bit_identical(plan):
-    """Per-block perturb passes on a side stream overlapping the +eps forward
-    ("blocks"), or one co-resident pass gating each block's forwards through
-    device counters ("background"), give exactly the serial plan's records
-    and weights."""
-    cfg, bsz, _ = _cfg("mid32")
-    a, b = DeviceStore(cfg, 7), DeviceStore(cfg, 7)
-    h = zo.ZoHyper(EPS, LR)
-    sa, sb = zo.StreamingZo(a, h), zo.StreamingZo(b, h, overlap=plan)
-    for j, s in enumerate(iteration_seeds(13, 4), 1):
-        batch = _batch(cfg, bsz, 300 + j)
-        ra, rb = sa.step(batch, s), sb.step(batch, s)
-        assert (ra.loss_pos, ra.loss_neg, ra.g) == (rb.loss_pos, rb.loss_neg, rb.g)
-    sa.flush()
-    sb.flush()
-    assert torch.equal(a.theta, b.theta)
-
-
-def test_background_plan_at_width_matches_serial():
-    """The background plan on a wider model (many tiles per block, unaligned
-    vocab rows through the generic path) equals the serial plan; the block
-    counters end at each block's tile count."""
-    cfg = ModelConfig(1000, 256, 4, 3, 64, "f32")
-    a, b = DeviceStore(cfg, 7), DeviceStore(cfg, 7)
-    h = zo.ZoHyper(EPS, LR)
-    sa, sb = zo.StreamingZo(a, h), zo.StreamingZo(b, h, overlap="background")
-    for j, s in enumerate(iteration_seeds(21, 3), 1):
-        batch = make_batch(cfg, 2, 500 + j)
-        ra, rb = sa.step(batch, s), sb.step(batch, s)
-        assert (ra.loss_pos, ra.loss_neg, ra.g) == (rb.loss_pos, rb.loss_neg, rb.g)
-    done = b.block_done.cpu().tolist()
-    rest = b._bg_tables[1]
-    assert done[1:] == [rest.block_tiles[i] for i in range(1, len(b.layouts))]
-    sa.flush()
-    sb.flush()
-    assert torch.equal(a.theta, b.theta)
-
-
-@pytest.mark.parametrize("plan", [False, "background"])
+@pytest.mark.parametrize("plan", [False, "stacked"])
 def test_graph_replay_equals_eager(plan):
     """Philox steps replayed from a captured CUDA graph give exactly the eager
     launches' records and weights (seeds / pending flag / g live on the
@@ -349,10 +310,9 @@ def test_graph_replay_equals_eager(plan):
     assert torch.equal(a.theta, b.theta)
 
 
-@pytest.mark.parametrize("plan", ["stacked", "stacked_bg"])
 @pytest.mark.parametrize("arch", ["zosim", "opt"])
 @pytest.mark.parametrize("graph", [False, True])
-def test_stacked_plan_is_bit_identical(arch, graph, plan):
+def test_stacked_plan_is_bit_identical(arch, graph):
     """Both directions as one launch per layer over stacked [+eps; -eps]
     activations (zo_gemm_bf16_split / zo_layernorm_fwd_split, attention over
     2B sequences) give exactly the two-stream plan's records and weights --
@@ -367,7 +327,7 @@ def test_stacked_plan_is_bit_identical(arch, graph, plan):
     assert a.stackable(2, 128)
     h = zo.ZoHyper(EPS, LR)
     sa = zo.StreamingZo(a, h, overlap=False, graph=graph)
-    sb = zo.StreamingZo(b, h, overlap=plan, graph=graph)
+    sb = zo.StreamingZo(b, h, overlap="stacked", graph=graph)
     for j, s in enumerate(iteration_seeds(29, 4), 1):
         batch = make_batch(cfg, 2, 900 + j)
         ra, rb = sa.step(batch, s), sb.step(batch, s)

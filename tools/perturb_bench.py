@@ -31,18 +31,3 @@ for name, (flags, bpp) in cases.items():
     torch.cuda.synchronize()
     ms = s.elapsed_time(e) / 10
     print(f"{name:36s} {ms:7.3f} ms  {P * bpp / ms / 1e6:7.0f} GB/s", flush=True)
-
-# background variant (one 4-warp CTA per SM), alone on the GPU
-flags = L.ZO_PU_UPDATE | L.ZO_PU_SHADOW_A | L.ZO_PU_SHADOW_B
-calls = st.perturb_bg_call(st.model_table, flags, 1e-3, -1e-3)
-for k in range(11):
-    if k == 1:
-        torch.cuda.synchronize()
-        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        s.record()
-    st.block_done.zero_()
-    st.run(calls)
-e.record()
-torch.cuda.synchronize()
-ms = s.elapsed_time(e) / 10
-print(f"{'background pass (1 CTA/SM), 12 B/param':36s} {ms:7.3f} ms  {P * 12 / ms / 1e6:7.0f} GB/s", flush=True)
