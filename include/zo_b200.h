@@ -109,19 +109,6 @@ int zo_perturb_update(float* theta, int64_t theta_key0, const ZoSegment* segs,
                       const ZoStepScalars* scal, int32_t zmode,
                       const double* z_cur, const double* z_prev, int64_t z_key0,
                       void* stream);
-/* Same pass as a "background" kernel: one 4-warp CTA per SM sized to run
- * beside the forward's GEMM / attention CTAs, Philox direction only.  After
- * each tile it adds 1 to block_done[segment.reserved] (gpu-scope release), so
- * a forward stream can start block b as soon as its tiles are done
- * (zo_wait_counter) while the pass continues on later blocks. */
-int zo_perturb_update_bg(float* theta, int64_t theta_key0, const ZoSegment* segs,
-                         const int64_t* tile_prefix, int32_t n_segs, int64_t n_tiles,
-                         void* wsh_a, float* vsh_a, void* wsh_b, float* vsh_b,
-                         double scale_a, double scale_b, uint32_t flags,
-                         const ZoStepScalars* scal, int32_t* block_done, void* stream);
-/* Enqueue a one-thread kernel that returns once *counter >= target. */
-int zo_wait_counter(const int32_t* counter, int32_t target, void* stream);
-
 /* Tile granularity (elements) the host must use to build tile_prefix. */
 int64_t zo_perturb_tile_elems(void);
 
@@ -178,19 +165,6 @@ int zo_gemm_bf16_split(const void* A, int64_t lda, const void* B, const void* B2
                        const int32_t* targets, float* ce_part, float* ce_tgt,
                        int32_t* err_flag, void* stream);
 /* number of N tiles the ZO_EPI_CE epilogue writes per row for a given N */
-/* Same GEMM with a caller-owned workspace (zero-initialised once, reusable
- * by later calls on the same stream; not shared by concurrent calls): the
- * CTA-pair kernel then splits its last waves along K ("stream-K") so every
- * SM stays busy, with a fixed, deterministic reduction order.  A null or
- * too-small workspace gives the plain data-parallel schedule. */
-int zo_gemm_bf16_ws(const void* A, int64_t lda, const void* B, int64_t ldb,
-                    int64_t M, int64_t N, int64_t K, int32_t epilogue,
-                    const float* bias, void* out, int64_t ldo,
-                    const int32_t* targets, float* ce_part, float* ce_tgt,
-                    int32_t* err_flag, void* workspace, int64_t workspace_bytes,
-                    void* stream);
-/* Workspace bytes zo_gemm_bf16_ws needs for an M x N x K problem (0: none). */
-int64_t zo_gemm_workspace_bytes(int64_t M, int64_t N, int64_t K);
 int64_t zo_gemm_ce_tiles(int64_t N);
 
 /*

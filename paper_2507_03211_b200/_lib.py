@@ -48,16 +48,12 @@ SIGNATURES = {
     "zo_last_error": (C.c_char_p, []),
     "zo_device_check": (C.c_int, [C.c_int]),
     "zo_perturb_update": (C.c_int, [P, I64, P, P, I32, I64, P, P, P, P, D, D, U32, P, I32, P, P, I64, P]),
-    "zo_perturb_update_bg": (C.c_int, [P, I64, P, P, I32, I64, P, P, P, P, D, D, U32, P, P, P]),
-    "zo_wait_counter": (C.c_int, [P, I32, P]),
     "zo_perturb_tile_elems": (I64, []),
     "zo_embed_fwd": (C.c_int, [P, I64, P, I64, P, I64, I64, I64, I64, D, P, I32, P, I64, P, I64, P, P]),
     "zo_layernorm_fwd": (C.c_int, [P, I64, P, P, I64, I64, P, I64, P]),
     "zo_layernorm_fwd_split": (C.c_int, [P, I64, P, P, P, P, I64, I64, I64, P, I64, P]),
     "zo_gemm_bf16_split": (C.c_int, [P, I64, P, P, I64, I64, I64, I64, I64, I32, P, P, P, I64, P, P, P, P, P]),
     "zo_gemm_bf16": (C.c_int, [P, I64, P, I64, I64, I64, I64, I32, P, P, I64, P, P, P, P, P]),
-    "zo_gemm_bf16_ws": (C.c_int, [P, I64, P, I64, I64, I64, I64, I32, P, P, I64, P, P, P, P, P, I64, P]),
-    "zo_gemm_workspace_bytes": (I64, [I64, I64, I64]),
     "zo_gemm_ce_tiles": (I64, [I64]),
     "zo_attn_causal_fwd": (C.c_int, [P, I64, I64, I64, I64, I64, P, I64, P]),
     "zo_gemm_f32": (C.c_int, [P, I64, P, I64, I64, I64, I64, I32, P, P, I64, P]),

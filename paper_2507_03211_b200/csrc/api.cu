@@ -21,13 +21,9 @@ void set_error(const char* fmt, ...) {
   va_end(ap);
 }
 
-bool pdl_enabled() {
-  static const bool on = [] {
-    const char* e = getenv("ZO_PDL");   // 1 enables programmatic dependent launch (measured: no gain yet)
-    return e && e[0] == '1';
-  }();
-  return on;
-}
+// Programmatic dependent launch measured no gain on the step's launch chain
+// (profiles/r01_*): kernels keep the griddepcontrol hooks, launches do not set it.
+bool pdl_enabled() { return false; }
 
 int num_sms() {
   static int cached[64] = {0};
@@ -42,8 +38,7 @@ int num_sms() {
   return cached[dev];
 }
 
-int perturb_update_launch(const PuParams& p, int zmode, cudaStream_t stream, bool background);
-int wait_counter_launch(const int32_t* counter, int32_t target, cudaStream_t stream);
+int perturb_update_launch(const PuParams& p, int zmode, cudaStream_t stream);
 int philox_normals_launch(uint64_t seed, int64_t e0, int64_t n, float* out, cudaStream_t stream);
 int embed_launch(const float*, int64_t, const float*, int64_t, const int32_t*, int64_t, int64_t, int64_t, int64_t,
                  double, const ZoStepScalars*, int32_t, const double*, int64_t, float*, int64_t, int32_t*,
@@ -60,9 +55,7 @@ int hash_launch(const void*, int64_t, uint64_t*, uint64_t*, int, cudaStream_t);
 int planes_join_launch(const uint16_t*, const uint16_t*, float*, int64_t, cudaStream_t);
 int planes_split_launch(const float*, uint16_t*, uint16_t*, int64_t, cudaStream_t);
 int gemm_launch(const void*, int64_t, const void*, int64_t, int64_t, int64_t, int64_t, int, const float*, void*,
-                int64_t, const int32_t*, float*, float*, int32_t*, void*, int64_t, cudaStream_t, const void*,
-                const float*, int64_t);
-int64_t gemm_workspace_bytes(int64_t M, int64_t N, int64_t K);
+                int64_t, const int32_t*, float*, float*, int32_t*, cudaStream_t, const void*, const float*, int64_t);
 int64_t perturb_tile_elems();
 int64_t gemm_ce_tiles(int64_t N);
 int gemm_f32_launch(const float*, int64_t, const float*, int64_t, int64_t, int64_t, int64_t, int, const float*,
@@ -129,40 +122,7 @@ int zo_perturb_update(float* theta, int64_t theta_key0, const ZoSegment* segs, c
   p.z_cur = z_cur;
   p.z_prev = z_prev;
   p.z_key0 = z_key0;
-  p.block_done = nullptr;
-  return zo::perturb_update_launch(p, zmode, ZO_STREAM(stream), false);
-}
-
-int zo_perturb_update_bg(float* theta, int64_t theta_key0, const ZoSegment* segs, const int64_t* tile_prefix,
-                         int32_t n_segs, int64_t n_tiles, void* wsh_a, float* vsh_a, void* wsh_b, float* vsh_b,
-                         double scale_a, double scale_b, uint32_t flags, const ZoStepScalars* scal,
-                         int32_t* block_done, void* stream) {
-  ZO_CHECK_ARG(theta && segs && tile_prefix && scal && block_done, ZO_ERR_CONFIG, "zo_perturb_update_bg: null argument");
-  zo::PuParams p;
-  p.theta = theta;
-  p.theta_key0 = theta_key0;
-  p.segs = segs;
-  p.prefix = tile_prefix;
-  p.n_segs = n_segs;
-  p.n_tiles = n_tiles;
-  p.wsh[0] = static_cast<__nv_bfloat16*>(wsh_a);
-  p.wsh[1] = static_cast<__nv_bfloat16*>(wsh_b);
-  p.vsh[0] = vsh_a;
-  p.vsh[1] = vsh_b;
-  p.scale[0] = scale_a;
-  p.scale[1] = scale_b;
-  p.flags = flags;
-  p.scal = scal;
-  p.z_cur = nullptr;
-  p.z_prev = nullptr;
-  p.z_key0 = 0;
-  p.block_done = block_done;
-  return zo::perturb_update_launch(p, ZO_Z_PHILOX, ZO_STREAM(stream), true);
-}
-
-int zo_wait_counter(const int32_t* counter, int32_t target, void* stream) {
-  ZO_CHECK_ARG(counter, ZO_ERR_CONFIG, "zo_wait_counter: null counter");
-  return zo::wait_counter_launch(counter, target, ZO_STREAM(stream));
+  return zo::perturb_update_launch(p, zmode, ZO_STREAM(stream));
 }
 
 int zo_embed_fwd(const float* tok, int64_t tok_key0, const float* pos, int64_t pos_key0, const int32_t* ids,
@@ -205,7 +165,7 @@ int zo_gemm_bf16(const void* A, int64_t lda, const void* B, int64_t ldb, int64_t
                ZO_ERR_CONFIG, "zo_gemm_bf16: missing epilogue buffers");
   ZO_CHECK_ARG(epi == ZO_EPI_F32 || epi == ZO_EPI_CE || bias, ZO_ERR_CONFIG, "zo_gemm_bf16: bias required");
   return zo::gemm_launch(A, lda, B, ldb, M, N, K, epilogue, bias, out, ldo, targets, ce_part, ce_tgt, err_flag,
-                         nullptr, 0, ZO_STREAM(stream), nullptr, nullptr, 0);
+                         ZO_STREAM(stream), nullptr, nullptr, 0);
 }
 
 int zo_gemm_bf16_split(const void* A, int64_t lda, const void* B, const void* B2, int64_t ldb, int64_t M, int64_t N,
@@ -220,24 +180,8 @@ int zo_gemm_bf16_split(const void* A, int64_t lda, const void* B, const void* B2
                "zo_gemm_bf16_split: bias required");
   ZO_CHECK_ARG(m_split > 0, ZO_ERR_CONFIG, "zo_gemm_bf16_split: m_split must be positive");
   return zo::gemm_launch(A, lda, B, ldb, M, N, K, epilogue, bias, out, ldo, targets, ce_part, ce_tgt, err_flag,
-                         nullptr, 0, ZO_STREAM(stream), B2, bias2, m_split);
+                         ZO_STREAM(stream), B2, bias2, m_split);
 }
-
-int zo_gemm_bf16_ws(const void* A, int64_t lda, const void* B, int64_t ldb, int64_t M, int64_t N, int64_t K,
-                    int32_t epilogue, const float* bias, void* out, int64_t ldo, const int32_t* targets,
-                    float* ce_part, float* ce_tgt, int32_t* err_flag, void* workspace, int64_t workspace_bytes,
-                    void* stream) {
-  ZO_CHECK_ARG(A && B, ZO_ERR_CONFIG, "zo_gemm_bf16_ws: null operand");
-  const int32_t epi = epilogue & ~ZO_GEMM_B_KMAJOR;
-  ZO_CHECK_ARG(epi == ZO_EPI_CE ? (targets && ce_part && ce_tgt && err_flag) : (out != nullptr),
-               ZO_ERR_CONFIG, "zo_gemm_bf16_ws: missing epilogue buffers");
-  ZO_CHECK_ARG(epi == ZO_EPI_F32 || epi == ZO_EPI_CE || bias, ZO_ERR_CONFIG,
-               "zo_gemm_bf16_ws: bias required");
-  return zo::gemm_launch(A, lda, B, ldb, M, N, K, epilogue, bias, out, ldo, targets, ce_part, ce_tgt, err_flag,
-                         workspace, workspace_bytes, ZO_STREAM(stream), nullptr, nullptr, 0);
-}
-
-int64_t zo_gemm_workspace_bytes(int64_t M, int64_t N, int64_t K) { return zo::gemm_workspace_bytes(M, N, K); }
 
 int zo_gemm_f32(const float* A, int64_t lda, const float* B, int64_t ldb, int64_t M, int64_t N, int64_t K,
                 int32_t epilogue, const float* bias, float* out, int64_t ldo, void* stream) {

@@ -417,6 +417,422 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   }
 }
 
+// ----------------------------------------------------------------------------
+// hd 64: two query tiles in flight per CTA ("ping-pong").  A work item is the
+// same query tile qt of two (batch, head) pairs -- tiles A and B have the same
+// causal length, so their pipelines stay in step.  Each tile has its own four
+// softmax warps (one thread per query row, the whole 128-key row of S in
+// registers: no cross-warp row exchange), so while one tile's warps run the
+// exponentials the other tile's S / PV MMAs run on the tensor core, and one
+// tile's per-item tail (last PV wait, output store) hides under the other's
+// softmax.  O accumulates in TMEM (PV with accumulate = 1); a row's running
+// max is only raised -- and O, l rescaled -- when it grows by more than 2^8,
+// so the rescale (a TMEM read-modify-write by the row's own thread) is rare.
+//   warp 0     TMA: Q_A, Q_B once per item; K/V blocks (A0, B0, A1, B1, ...)
+//              through a 4-stage ring
+//   warp 1     TMEM alloc + MMA issue: per block j and tile t:
+//                S_t,j+1 = Q_t K_t,j+1^T  (issued as soon as S_t,j is in registers)
+//                PV:  O_t += P_t,j V_t,j  (after the softmax wrote P_t,j)
+//   warps 2-5  softmax + output of tile A, warps 6-9 of tile B
+// TMEM: S_A [0,128) S_B [128,256) O_A[2] [256,384) O_B[2] [384,512)  (O
+// double-buffered across items so the next item's first PV never waits for
+// the previous item's output read).
+// ----------------------------------------------------------------------------
+namespace pp {
+constexpr int kThreads = 320;
+constexpr int kQB = 128 * 64 * 2;          // 16 KB Q tile
+constexpr int kKVB = 2 * kQB;              // K + V of one block: 32 KB
+constexpr int kStages = 4;
+constexpr int kPB = 128 * 128 * 2;         // 32 KB P tile (two 64-key SW128 chunks)
+constexpr int kOffQ = 0;
+constexpr int kOffKV = kOffQ + 2 * kQB;
+constexpr int kOffP = kOffKV + kStages * kKVB;
+constexpr int kOffBar = kOffP + 2 * kPB;
+constexpr int kNBar = 26;
+constexpr int kSmem = kOffBar + 8 * kNBar + 16 + 1024;
+static_assert(kSmem <= 232448, "attention pp smem");
+// barrier indices
+constexpr int QF = 0, QE = 2, KVF = 4, KVE = 8, SF = 12, SE = 14, PF = 16, PVD = 18, OE = 20;  // OE: [t][2]
+}  // namespace pp
+
+__device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};\n" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
+}
+// sm_100 packed-fp32 and 3-input ops (FFMA2 / FADD2 / FMNMX3)
+__device__ __forceinline__ uint64_t pack_f32x2(float lo, float hi) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ uint64_t pack_u32x2(uint32_t lo, uint32_t hi) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "r"(lo), "r"(hi));
+  return r;
+}
+__device__ __forceinline__ void unpack_f32x2(uint64_t v, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ uint64_t ffma_f32x2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ uint64_t add_f32x2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+  float d;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+
+__global__ void __launch_bounds__(pp::kThreads, 1)
+    attn_pp_kernel(const __grid_constant__ CUtensorMap tm, const AttnArgs a) {
+  using namespace pp;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  const uint32_t base = (raw + 1023u) & ~1023u;
+  uint8_t* gbase = smem_raw + (base - raw);
+  const uint32_t sQ = base + kOffQ, sKV = base + kOffKV, sP = base + kOffP;
+  const uint32_t bars = base + kOffBar;
+  auto bar = [&](int i) { return bars + 8u * i; };
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + kOffBar + 8 * kNBar);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&tm);
+    for (int t = 0; t < 2; ++t) {
+      mbar_init(bar(QF + t), 1); mbar_init(bar(QE + t), 1);
+      mbar_init(bar(SF + t), 1); mbar_init(bar(SE + t), 4);
+      mbar_init(bar(PF + t), 4); mbar_init(bar(PVD + t), 1);
+      mbar_init(bar(OE + 2 * t), 4); mbar_init(bar(OE + 2 * t + 1), 4);
+    }
+    for (int s = 0; s < kStages; ++s) { mbar_init(bar(KVF + s), 1); mbar_init(bar(KVE + s), 1); }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tmem_slot)),
+                 "r"(512u));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  pdl_trigger();
+  pdl_wait();
+
+  const int n_bh = a.batch * a.heads;
+  const int n_pairs = (n_bh + 1) >> 1;
+  // item -> (query tile, first (b,h) of the pair); heaviest (latest) tiles first
+  auto coords = [&](int it, int& qt, int& bh0) {
+    qt = a.n_qt - 1 - it / n_pairs;
+    bh0 = 2 * (it % n_pairs);
+  };
+
+  if (warp == 0) {
+    // ============================ TMA producer ============================
+    if (lane == 0) {
+      uint32_t kvc = 0, qc[2] = {0u, 0u};
+      for (int it = blockIdx.x; it < a.items; it += gridDim.x) {
+        int qt, bh0;
+        coords(it, qt, bh0);
+        const int T = bh0 + 1 < n_bh ? 2 : 1;
+        for (int t = 0; t < T; ++t) {
+          const int bh = bh0 + t, b = bh / a.heads, h = bh % a.heads;
+          mbar_wait(bar(QE + t), (qc[t]++ & 1u) ^ 1u);
+          mbar_expect_tx(bar(QF + t), kQB);
+          tma_load_2d(sQ + t * kQB, &tm, bar(QF + t), h * 64, b * a.seq + qt * 128);
+        }
+        for (int j = 0; j <= qt; ++j) {
+          for (int t = 0; t < T; ++t, ++kvc) {
+            const int bh = bh0 + t, b = bh / a.heads, h = bh % a.heads;
+            const uint32_t st = kvc % kStages, ph = (kvc / kStages) & 1u;
+            TRP(2048 + 2 * (int)kvc);
+            mbar_wait(bar(KVE + st), ph ^ 1u);
+            TRP(2048 + 2 * (int)kvc + 1);
+            mbar_expect_tx(bar(KVF + st), kKVB);
+            tma_load_2d(sKV + st * kKVB, &tm, bar(KVF + st), (int)(a.d + h * 64), b * a.seq + j * 128);
+            tma_load_2d(sKV + st * kKVB + kQB, &tm, bar(KVF + st), (int)(2 * a.d + h * 64), b * a.seq + j * 128);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ============================ MMA issuer =============================
+    const uint32_t idesc_s = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(128 >> 3) << 17) |
+                             ((uint32_t)(128 >> 4) << 24);
+    const uint32_t idesc_pv = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) | ((uint32_t)(64 >> 3) << 17) |
+                              ((uint32_t)(128 >> 4) << 24);
+    uint32_t kvc = 0;
+    uint32_t qc[2] = {0u, 0u}, sc[2] = {0u, 0u}, pc[2] = {0u, 0u}, ic[2] = {0u, 0u};
+    int trm = 0;
+    auto issue_s = [&](int t, uint32_t kv, bool last) {
+      TRW(1024 + 4 * trm);
+      mbar_wait(bar(KVF + kv % kStages), (kv / kStages) & 1u);     // K, V landed
+      TRW(1024 + 4 * trm + 1);
+      mbar_wait(bar(SE + t), (sc[t] & 1u) ^ 1u);                   // S_t drained into registers
+      TRW(1024 + 4 * trm + 2);
+      ++trm;
+      tc_fence_after();
+      if (lane == 0) {
+        const uint32_t k0 = sKV + (kv % kStages) * kKVB;
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          tc_mma_f16(tmem + t * 128, desc_sw128(sQ + t * kQB + kk * 32, 16, 1024), desc_sw128(k0 + kk * 32, 16, 1024),
+                     idesc_s, kk != 0 ? 1u : 0u);
+        tc_commit(bar(SF + t));
+        if (last) tc_commit(bar(QE + t));                          // Q_t no longer read
+      }
+      __syncwarp();
+      ++sc[t];
+    };
+    auto issue_pv = [&](int t, uint32_t kv, bool first) {
+      TRW(1024 + 4 * trm);
+      mbar_wait(bar(PF + t), pc[t] & 1u);                          // P_t written (and O_t rescaled)
+      TRW(1024 + 4 * trm + 1);
+      ++trm;
+      const uint32_t ob = ic[t] & 1u;
+      if (first) mbar_wait(bar(OE + 2 * t + ob), ((ic[t] >> 1) & 1u) ^ 1u);   // O buffer read out
+      tc_fence_after();
+      if (lane == 0) {
+        const uint32_t v0 = sKV + (kv % kStages) * kKVB + kQB;
+        const uint32_t p0 = sP + t * kPB;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)                              // 128 keys = 8 x K16
+          tc_mma_f16(tmem + 256 + t * 128 + ob * 64, desc_sw128(p0 + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024),
+                     desc_sw128(v0 + kk * 2048, 16384, 1024), idesc_pv, (!first || kk != 0) ? 1u : 0u);
+        tc_commit(bar(PVD + t));                                     // PV done: O_t final / P_t free
+        tc_commit(bar(KVE + kv % kStages));                          // K/V stage free
+      }
+      __syncwarp();
+      ++pc[t];
+    };
+    for (int it = blockIdx.x; it < a.items; it += gridDim.x) {
+      int qt, bh0;
+      coords(it, qt, bh0);
+      const int T = bh0 + 1 < n_bh ? 2 : 1;
+      const int nkb = qt + 1;
+      for (int t = 0; t < T; ++t) mbar_wait(bar(QF + t), qc[t]++ & 1u);
+      for (int t = 0; t < T; ++t) issue_s(t, kvc + t, nkb == 1);
+      for (int j = 0; j < nkb; ++j) {
+        // the next block's S of both tiles first: a tile's softmax finds S_j+1
+        // ready when it finishes block j whatever the other tile is doing
+        if (j + 1 < nkb)
+          for (int t = 0; t < T; ++t) issue_s(t, kvc + (j + 1) * T + t, j + 2 == nkb);
+        for (int t = 0; t < T; ++t) issue_pv(t, kvc + j * T + t, j == 0);
+      }
+      kvc += nkb * T;
+      for (int t = 0; t < T; ++t) ++ic[t];
+    }
+  } else {
+    // ====================== softmax + output (tile t) =====================
+    // Warp (t, quarter) owns query rows 32*quarter .. +31 of tile t; tile A's
+    // and tile B's warps of a quarter share one SM sub-partition (and its MUFU
+    // pipe: two warps issuing exponentials together keep it busy, one alone
+    // reaches about half its rate -- measured with an alternating hand-off).
+    const int t = (warp - 2) >> 2;
+    const int quarter = warp & 3;               // TMEM lane quarter this warp may access
+    const int r = quarter * 32 + lane;          // query row within the tile
+    const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+    const uint32_t s_tm = tmem + t * 128 + lane_off;
+    const uint32_t prow = sP + t * kPB + r * 128;   // row r of chunk 0 (keys 0-63); chunk 1 at +16 KB
+    const uint64_t sl2x2 = pack_f32x2(a.sl2, a.sl2);
+    uint32_t sc = 0, pw = 0, ic = 0;
+    int trn = 0;
+    (void)trn;
+    for (int it = blockIdx.x; it < a.items; it += gridDim.x) {
+      int qt, bh0;
+      coords(it, qt, bh0);
+      if (bh0 + t >= n_bh) continue;            // odd (b,h) count: no tile B in the last pair
+      const int bh = bh0 + t, b = bh / a.heads, h = bh % a.heads;
+      const int qi = qt * 128 + r;
+      const int q_lo = qt * 128 + quarter * 32, q_hi = q_lo + 31;   // this warp's query rows
+      const uint32_t ob = ic & 1u;
+      const uint32_t o_tm = tmem + 256 + t * 128 + ob * 64 + lane_off;
+      float m = -INFINITY, l = 0.f;
+      for (int j = 0; j <= qt; ++j) {
+        const int tr = (trn++) * 8;
+        (void)tr;
+        TR(tr + 0);
+        mbar_wait(bar(SF + t), sc & 1u);
+        ++sc;
+        TR(tr + 1);
+        tc_fence_after();
+        uint32_t s[4][32];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) tmem_ld_32x32b_x32_nw(s_tm + c * 32, s[c]);
+        tmem_wait_ld();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(bar(SE + t));  // S_t may be overwritten by S_t,j+1
+        // 32-key chunk c: dead (no row of the warp sees a key of it), full (every
+        // row sees every key) or ragged (element mask: causal diagonal / seq end)
+        const int k0 = j * 128;
+        bool live[4], full[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const int kc = k0 + c * 32;
+          live[c] = kc <= q_hi && kc < a.seq;
+          full[c] = kc + 31 <= q_lo && kc + 32 <= a.seq;
+        }
+        float mc[3] = {-INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          if (!live[c]) continue;
+          if (!full[c]) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              const int ki = k0 + c * 32 + i;
+              if (!(ki <= qi && ki < a.seq)) s[c][i] = __float_as_uint(-INFINITY);
+            }
+          }
+#pragma unroll
+          for (int i = 0; i < 30; i += 6) {
+            mc[0] = fmax3(mc[0], __uint_as_float(s[c][i]), __uint_as_float(s[c][i + 1]));
+            mc[1] = fmax3(mc[1], __uint_as_float(s[c][i + 2]), __uint_as_float(s[c][i + 3]));
+            mc[2] = fmax3(mc[2], __uint_as_float(s[c][i + 4]), __uint_as_float(s[c][i + 5]));
+          }
+          mc[0] = fmax3(mc[0], __uint_as_float(s[c][30]), __uint_as_float(s[c][31]));
+        }
+        const float mx = fmax3(mc[0], mc[1], mc[2]);
+        // lazy max: raise the scaling max only when the row max grew by > 2^8
+        const float m_new = fmaxf(m, mx);
+        float m_use = m, alpha = 1.f;
+        bool rescale = false;
+        if (m == -INFINITY) {
+          m_use = m_new;
+        } else if ((m_new - m) * a.sl2 > 8.f) {
+          m_use = m_new;
+          alpha = ex2_approx((m - m_new) * a.sl2);
+          rescale = true;
+        }
+        const float mb = m_use == -INFINITY ? 0.f : m_use * a.sl2;
+        const uint64_t nmb2 = pack_f32x2(-mb, -mb);
+        TR(tr + 2);
+        if (j > 0) {                               // PV_t,j-1 done: P_t free, O_t stable
+          mbar_wait(bar(PVD + t), pw & 1u);
+          ++pw;
+        }
+        TR(tr + 3);
+        // P = exp2(s * log2e / sqrt(hd) - mb) -> bf16, straight into the K-major SW128 P tile
+        uint64_t sum2[2] = {0ull, 0ull};
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const uint32_t rowc = prow + (c >> 1) * 16384;
+          const int u0 = (c & 1) * 4;              // 16-B units of this 32-key chunk within the 128-B row
+          if (!live[c]) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) st_shared_v4(rowc + (((u0 + q) ^ (r & 7)) << 4), 0u, 0u, 0u, 0u);
+            continue;
+          }
+          uint32_t pk[16];
+#pragma unroll
+          for (int i = 0; i < 32; i += 2) {
+            const uint64_t x2 = ffma_f32x2(pack_u32x2(s[c][i], s[c][i + 1]), sl2x2, nmb2);
+            float x0, x1;
+            unpack_f32x2(x2, x0, x1);
+            const float p0 = ex2_approx(x0), p1 = ex2_approx(x1);
+            sum2[(i >> 1) & 1] = add_f32x2(sum2[(i >> 1) & 1], pack_f32x2(p0, p1));
+            __nv_bfloat162 h2 = __floats2bfloat162_rn(p0, p1);
+            pk[i >> 1] = *reinterpret_cast<uint32_t*>(&h2);
+          }
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            st_shared_v4(rowc + (((u0 + q) ^ (r & 7)) << 4), pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+        }
+        TR(tr + 4);
+        float s0, s1, s2, s3;
+        unpack_f32x2(sum2[0], s0, s1);
+        unpack_f32x2(sum2[1], s2, s3);
+        l = fmaf(l, alpha, (s0 + s1) + (s2 + s3));
+        m = m_use;
+        if (__any_sync(0xffffffffu, rescale)) {   // O_t *= alpha (rows that did not rescale: alpha = 1)
+          tc_fence_after();
+#pragma unroll
+          for (int c = 0; c < 2; ++c) {
+            uint32_t o[32];
+            tmem_ld_32x32b_x32_nw(o_tm + c * 32, o);
+            tmem_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+            tmem_st_32x32b_x32(o_tm + c * 32, o);
+          }
+          tmem_wait_st();
+        }
+        fence_proxy_async_smem();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(bar(PF + t));
+        TR(tr + 5);
+      }
+      // item end: O_t = sum_j P_t,j V_t,j (up to the lazy scale), out = O / l
+      mbar_wait(bar(PVD + t), pw & 1u);
+      ++pw;
+      TR(trn * 8 - 2);
+      tc_fence_after();
+      uint32_t o[2][32];
+      tmem_ld_32x32b_x32_nw(o_tm, o[0]);
+      tmem_ld_32x32b_x32_nw(o_tm + 32, o[1]);
+      tmem_wait_ld();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bar(OE + 2 * t + ob));
+      ++ic;
+      if (qi < a.seq) {
+        const float inv = l > 0.f ? 1.f / l : 0.f;
+        __nv_bfloat16* out = a.ctx + ((int64_t)b * a.seq + qi) * a.ldc + (int64_t)h * 64;
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+#pragma unroll
+          for (int i = 0; i < 32; i += 8) {
+            uint32_t pk[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              __nv_bfloat162 h2 = __floats2bfloat162_rn(__uint_as_float(o[c][i + 2 * k]) * inv,
+                                                        __uint_as_float(o[c][i + 2 * k + 1]) * inv);
+              pk[k] = *reinterpret_cast<uint32_t*>(&h2);
+            }
+            *reinterpret_cast<uint4*>(out + c * 32 + i) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+          }
+      }
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(512u));
+  }
+}
+
+int attention_pp_launch(const __nv_bfloat16* qkv, int64_t ldq, int64_t batch, int64_t seq, int64_t heads,
+                        __nv_bfloat16* ctx, int64_t ldc, cudaStream_t st) {
+  CUtensorMap tm;
+  int rc = tma_map_bf16(qkv, 3 * heads * 64, batch * seq, ldq, 64, 128, &tm);
+  if (rc) return rc;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(attn_pp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, pp::kSmem);
+    if (e != cudaSuccess) { set_error("attn_pp smem attribute: %s", cudaGetErrorString(e)); return ZO_ERR_CUDA; }
+    attr = true;
+  }
+  AttnArgs a;
+  a.batch = (int)batch;
+  a.seq = (int)seq;
+  a.heads = (int)heads;
+  a.ldc = (int)ldc;
+  a.d = heads * 64;
+  a.n_qt = (int)((seq + 127) / 128);
+  a.items = a.n_qt * (int)((batch * heads + 1) / 2);
+  a.sl2 = 1.4426950408889634f / 8.0f;   // log2(e) / sqrt(64)
+  a.ctx = ctx;
+  const int grid = a.items < num_sms() ? a.items : num_sms();
+  launch_k(attn_pp_kernel, dim3(grid), dim3(pp::kThreads), pp::kSmem, st, tm, a);
+  return launch_status("attn_pp_kernel");
+}
+
 template <int HD>
 int attention_tc_launch_t(const __nv_bfloat16* qkv, int64_t ldq, int64_t batch, int64_t seq, int64_t heads,
                           __nv_bfloat16* ctx, int64_t ldc, cudaStream_t st) {
@@ -452,7 +868,7 @@ int attention_tc_launch_t(const __nv_bfloat16* qkv, int64_t ldq, int64_t batch, 
 int attention_tc_launch(const __nv_bfloat16* qkv, int64_t ldq, int64_t batch, int64_t seq, int64_t heads,
                         int64_t hd, __nv_bfloat16* ctx, int64_t ldc, cudaStream_t st) {
   if (hd == 128) return attention_tc_launch_t<128>(qkv, ldq, batch, seq, heads, ctx, ldc, st);
-  return attention_tc_launch_t<64>(qkv, ldq, batch, seq, heads, ctx, ldc, st);
+  return attention_pp_launch(qkv, ldq, batch, seq, heads, ctx, ldc, st);
 }
 
 }  // namespace zo

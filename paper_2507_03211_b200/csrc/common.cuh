@@ -211,7 +211,6 @@ struct PuParams {
   const double* z_cur;
   const double* z_prev;
   int64_t z_key0;
-  int32_t* block_done;   // optional: per-block tile-completion counters (segment.reserved = block)
 };
 
 // ---------------------------------------------------------------------------

@@ -68,65 +68,12 @@ struct GemmArgs {
   float* ce_tgt;
   int32_t* err;
   int64_t ce_tiles;
-  // stream-K tail (pair kernel): tiles [0, dp_tiles) data-parallel, the rest
-  // split into sk_units k-blocks spread evenly over the pairs (0 = off)
-  int64_t dp_tiles;
-  int64_t sk_units;
-  int32_t sk_pieces;    // max pieces per split tile
-  int32_t* sk_flags;    // [slot][16 epilogue warps], self-clearing
-  float* sk_part;       // [slot][16][32 rows x 128 cols] fp32 partial accumulators
   // row-split ("stacked") problem: rows >= m_split use the second B operand
   // (tmB2) and bias2 -- the +eps / -eps forwards of one ZO step as ONE launch
   // over [x+; x-] (0 = off; a multiple of 256 so every pair tile is one side)
   int64_t m_split;
   const float* bias2;
 };
-
-constexpr int kSkWarpFloats = 32 * 128;   // one epilogue warp's share of a pair tile
-
-// One work item of a pair: a whole tile, or a k-range piece of a split tile.
-//   kind 0: whole tile; 1: partial (stored to `slot`, not finished here);
-//   kind 2: finisher (adds partials slot .. slot+npart-1 in k order, then the epilogue)
-struct SkItem {
-  int64_t tile, slot;
-  int kb0, kb1, kind, npart;
-};
-
-// Item i of pair c out of W.  Data-parallel tiles come first; the pair's
-// stream-K range is walked in DESCENDING tile order, so a pair's only
-// partial piece is its first item and a finisher (always a later item of
-// another pair) only ever waits on pieces that other pairs produce first.
-__device__ __forceinline__ bool sk_item(const GemmArgs& a, int64_t c, int64_t W, int nk, int64_t i, SkItem& it) {
-  const int64_t ndp = c < a.dp_tiles ? (a.dp_tiles - c + W - 1) / W : 0;
-  if (i < ndp) {
-    it.tile = c + i * W; it.kb0 = 0; it.kb1 = nk; it.kind = 0; it.slot = 0; it.npart = 0;
-    return true;
-  }
-  const int64_t U = a.sk_units;
-  if (U == 0) return false;
-  const int64_t u0 = c * U / W, u1 = (c + 1) * U / W;
-  if (u0 >= u1) return false;
-  const int64_t t = (u1 - 1) / nk - (i - ndp);
-  if (t < u0 / nk) return false;
-  const int64_t tb = t * nk;
-  it.tile = a.dp_tiles + t;
-  it.kb0 = (int)((u0 > tb ? u0 : tb) - tb);
-  it.kb1 = (int)((u1 < tb + nk ? u1 : tb + nk) - tb);
-  const int64_t first = ((tb + 1) * W - 1) / U;     // pair owning the tile's first k-block
-  const int64_t p1 = a.sk_pieces - 1;
-  it.slot = t * p1;
-  it.npart = 0;
-  if (it.kb1 < nk) { it.kind = 1; it.slot += c - first; }
-  else if (it.kb0 == 0) { it.kind = 0; }
-  else { it.kind = 2; it.npart = (int)(c - first); }
-  return true;
-}
-
-__device__ __forceinline__ int ld_acquire_s32(const int32_t* p) {
-  int v;
-  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
 
 template <int BN, bool BKM = false>
 __device__ __forceinline__ uint32_t make_idesc() {
@@ -171,54 +118,9 @@ __device__ __forceinline__ void st_v8(float* p, const float* v) {
                : "memory");
 }
 
-// stream-K partial piece: this warp's 32 rows x 128 columns of the fp32
-// accumulator to the workspace (1 KB contiguous per warp store), then publish
-__device__ __forceinline__ void store_partial(uint32_t tmem_base, int acc, int quarter, int half, int lane,
-                                              float* dst, int32_t* flag) {
-#pragma unroll 1
-  for (int cc = 0; cc < 4; ++cc) {
-    const int c = half * 4 + cc;
-    const uint32_t taddr = tmem_base + (uint32_t)(acc * 256 + c * 32) + ((uint32_t)(quarter * 32) << 16);
-    float v[32];
-    tmem_ld_32x32b_x32(taddr, v);
-#pragma unroll
-    for (int j = 0; j < 4; ++j) st_v8(dst + ((cc * 4 + j) * 32 + lane) * 8, v + 8 * j);
-  }
-  __threadfence();
-  __syncwarp();
-  if (lane == 0) asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(flag), "r"(1) : "memory");
-}
-
 template <int BN, int EPI>
 __device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t tmem_base, int acc, int quarter,
-                                              int half, int lane, int64_t m0, int64_t n0, int64_t tn,
-                                              const float* __restrict__ part = nullptr, int npart = 0,
-                                              int32_t* part_flags = nullptr) {
-  // stream-K finisher: wait for the earlier pieces of this warp's sub-tile
-  if (npart > 0) {
-    for (int p = 0; p < npart; ++p) {
-      const int32_t* f = part_flags + (int64_t)p * 16;
-      int64_t spins = 0;
-      while (ld_acquire_s32(f) == 0) {
-        __nanosleep(64);
-        if (++spins > (1ll << 26)) __trap();      // a lost producer would hang the GPU
-      }
-    }
-  }
-  // adds the partials of chunk c (this warp's half: local chunk cc) in k order
-  auto add_parts = [&](int c, float (&v)[32]) {
-    const int cc = c - half * (BN / 64);
-    for (int p = 0; p < npart; ++p) {
-      const float* src = part + (int64_t)p * 16 * kSkWarpFloats;
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        float pv[8];
-        ld_v8_na(src + ((cc * 4 + j) * 32 + lane) * 8, pv);
-#pragma unroll
-        for (int e = 0; e < 8; ++e) v[8 * j + e] += pv[e];
-      }
-    }
-  };
+                                              int half, int lane, int64_t m0, int64_t n0, int64_t tn) {
   const int64_t row_base = m0 + quarter * 32;
   const int64_t row = row_base + lane;
   const bool second = args.m_split && row_base >= args.m_split;
@@ -239,7 +141,6 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t tme
       // thread-per-row: online (max, sum exp) over this row's columns, target logit
       float v[32];
       tmem_ld_32x32b_x32(taddr, v);
-      if (npart > 0) add_parts(c, v);
       if (!row_ok || col0 >= args.N) continue;
       const int lim = col0 + 32 <= args.N ? 32 : (int)(args.N - col0);
       const bool has_bias = bias != nullptr;   // a tied head has no bias (real OPT)
@@ -324,7 +225,6 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t tme
       }
       float v[32];
       tmem_ld_32x32b_x32(taddr, v);
-      if (npart > 0) add_parts(c, v);
       if (!row_ok || col0 >= args.N) continue;
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
@@ -378,7 +278,6 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t tme
       }
       float v[32];
       tmem_ld_32x32b_x32(taddr, v);
-      if (npart > 0) add_parts(c, v);
       if (!row_ok || col0 >= args.N) continue;
       if constexpr (EPI == ZO_EPI_BIAS_RESID_F32) {
         if (vec) {
@@ -405,11 +304,6 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t tme
           if (col0 + i < args.N) o[i] = v[i];
       }
     }
-  }
-  if (npart > 0) {            // self-clearing: the next launch finds 0
-    __syncwarp();
-    if (lane == 0)
-      for (int p = 0; p < npart; ++p) part_flags[(int64_t)p * 16] = 0;
   }
   if constexpr (EPI == ZO_EPI_CE) {
     if (row_ok) {
@@ -662,13 +556,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, kGemmM
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      SkItem it;
-      for (int64_t i = 0; sk_item(args, cluster_id, n_clusters, nk, i, it); ++i) {
-        const int64_t tile = it.tile;
+      const int64_t tiles = num_m * num_n;
+      for (int64_t tile = cluster_id; tile < tiles; tile += n_clusters) {
         const int m0 = (int)((tile % num_m) * (2 * kBM) + rank * kBM);
         const int n0 = (int)((tile / num_m) * BN + rank * 128);
         const CUtensorMap* mb = (args.m_split && (tile % num_m) * (2 * kBM) >= args.m_split) ? &tmB2 : &tmB;
-        for (int kb = it.kb0; kb < it.kb1; ++kb) {
+        for (int kb = 0; kb < nk; ++kb) {
           mbar_wait(empty_bar(stage), phase ^ 1u);
           if (leader) mbar_expect_tx(full_bar(stage), (uint32_t)(2 * k2StageBytes));
           const uint32_t fb = mapa_shared(full_bar(stage), 0);
@@ -690,14 +583,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, kGemmM
                              ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
       int stage = 0;
       uint32_t phase = 0;
-      SkItem it;
-      for (int64_t local = 0; sk_item(args, cluster_id, n_clusters, nk, local, it); ++local) {
+      const int64_t tiles = num_m * num_n;
+      int64_t local = 0;
+      for (int64_t tile = cluster_id; tile < tiles; tile += n_clusters, ++local) {
         const int acc = (int)(local & 1);
         const uint32_t acc_phase = (uint32_t)((local >> 1) & 1);
         mbar_wait(tempty_bar(acc), acc_phase ^ 1u);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
-        for (int kb = it.kb0; kb < it.kb1; ++kb) {
+        for (int kb = 0; kb < nk; ++kb) {
           mbar_wait(full_bar(stage), phase);
           tc_fence_after();
           if (lane == 0) {
@@ -708,7 +602,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, kGemmM
               const uint64_t ad = desc_sw128(a0 + kk * 32, 16, 1024);
               const uint64_t bd =
                   BKM ? desc_sw128(b0 + kk * 32, 16, 1024) : desc_sw128(b0 + kk * 2048, kBK * 128, 1024);
-              tc_mma_f16_pair(d_tmem, ad, bd, idesc, (kb != it.kb0 || kk != 0) ? 1u : 0u);
+              tc_mma_f16_pair(d_tmem, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
             }
             tc_commit_pair(empty_bar(stage));
           }
@@ -722,9 +616,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, kGemmM
   } else {
     // ====== epilogue (both CTAs): this CTA's 128 rows x 256 columns ======
     const int quarter = warp & 3;
-    SkItem it;
-    for (int64_t local = 0; sk_item(args, cluster_id, n_clusters, nk, local, it); ++local) {
-      const int64_t tile = it.tile;
+    const int64_t tiles = num_m * num_n;
+    int64_t local = 0;
+    for (int64_t tile = cluster_id; tile < tiles; tile += n_clusters, ++local) {
       const int acc = (int)(local & 1);
       const uint32_t acc_phase = (uint32_t)((local >> 1) & 1);
       const int64_t m0 = (tile % num_m) * (2 * kBM) + rank * kBM;
@@ -732,18 +626,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, kGemmM
       mbar_wait(tfull_bar(acc), acc_phase);
       tc_fence_after();
 #pragma unroll 1
-      for (int e = warp - 2; e < 8; e += kEpiWarps) {      // logical slot e: lane quarter, column half e / 4
-        const int half = e >> 2;
-        const int64_t wslot = (int64_t)rank * 8 + e;        // this slot's share of a pair tile (16 per pair)
-        if (it.kind == 1) {
-          store_partial(tmem_base, acc, quarter, half, lane, args.sk_part + (it.slot * 16 + wslot) * kSkWarpFloats,
-                        args.sk_flags + it.slot * 16 + wslot);
-        } else {
-          epilogue_tile<BN, EPI>(args, tmem_base, acc, quarter, half, lane, m0, tn * BN, tn,
-                                 args.sk_part + (it.slot * 16 + wslot) * kSkWarpFloats, it.npart,
-                                 args.sk_flags + it.slot * 16 + wslot);
-        }
-      }
+      for (int e = warp - 2; e < 8; e += kEpiWarps)        // logical slot e: lane quarter, column half e / 4
+        epilogue_tile<BN, EPI>(args, tmem_base, acc, quarter, e >> 2, lane, m0, tn * BN, tn);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(mapa_shared(tempty_bar(acc), 0));
@@ -872,7 +756,7 @@ int launch_pair_t(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMa
   }
   const int64_t tiles = ((a.M + 255) / 256) * ((a.N + 255) / 256);
   const int64_t pairs = num_sms() / 2;
-  const int grid = 2 * (int)(a.sk_units ? pairs : (tiles < pairs ? tiles : pairs));
+  const int grid = 2 * (int)(tiles < pairs ? tiles : pairs);
   launch_k(gemm_tcgen05_pair_kernel<EPI, BKM>, dim3(grid), dim3(kGemmThreads), k2Smem, st, ma, mb, mb2, a);
   return launch_status("gemm_tcgen05_pair_kernel");
 }
@@ -909,47 +793,9 @@ int tma_map_bf16(const void* ptr, int64_t inner, int64_t outer, int64_t ld, int 
 
 int64_t gemm_ce_tiles(int64_t N) { return 2 * ((N + 255) / 256); }   // one partial per 128-column half
 
-// Stream-K tail of the pair kernel.  With W pairs and T tiles, the last full
-// wave plus the partial one ((T mod W) + W tiles, or all T when T < W) are cut
-// into k-blocks spread evenly over all W pairs, so no pair idles in the last
-// wave.  Returns the workspace bytes it needs (0: not worthwhile).
-struct SkPlan {
-  int64_t dp_tiles, units, slots, bytes, flag_bytes;
-  int pieces;
-};
-
-SkPlan sk_plan(int64_t M, int64_t N, int64_t K) {
-  SkPlan pl{0, 0, 0, 0, 0, 1};
-  const int64_t W = num_sms() / 2;
-  const int64_t tiles = ((M + 255) / 256) * ((N + 255) / 256);
-  const int64_t nk = (K + kBK - 1) / kBK;
-  pl.dp_tiles = tiles;
-  if (M <= kBM || tiles % W == 0 || tiles * nk < 8 * W) return pl;
-  static const int tail_only = [] {
-    const char* e = getenv("ZO_SK_POLICY");   // "tail": split only the partial last wave
-    return e && e[0] == 't' ? 1 : 0;
-  }();
-  const int64_t full = tiles / W;
-  const int64_t dp = tail_only ? full * W : (full >= 1 ? (full - 1) * W : 0);
-  const int64_t units = (tiles - dp) * nk;
-  const int64_t lmin = units / W;
-  if (lmin < 4) return pl;                     // pieces too small to pay for the fixup
-  pl.pieces = (int)((nk + lmin - 1) / lmin + 1);
-  pl.dp_tiles = dp;
-  pl.units = units;
-  pl.slots = (tiles - dp) * (pl.pieces - 1);
-  pl.flag_bytes = (pl.slots * 16 * 4 + 4095) / 4096 * 4096;
-  pl.bytes = pl.flag_bytes + pl.slots * 16 * (int64_t)kSkWarpFloats * 4;
-  return pl;
-}
-
-int64_t gemm_workspace_bytes(int64_t M, int64_t N, int64_t K) { return sk_plan(M, N, K).bytes; }
-
-
 int gemm_launch(const void* A, int64_t lda, const void* B, int64_t ldb, int64_t M, int64_t N, int64_t K, int epi,
                 const float* bias, void* out, int64_t ldo, const int32_t* targets, float* ce_part, float* ce_tgt,
-                int32_t* err, void* ws, int64_t ws_bytes, cudaStream_t st, const void* B2, const float* bias2,
-                int64_t m_split) {
+                int32_t* err, cudaStream_t st, const void* B2, const float* bias2, int64_t m_split) {
   const bool bkm = (epi & ZO_GEMM_B_KMAJOR) != 0;
   epi &= ~ZO_GEMM_B_KMAJOR;
   if (M == 0 || N == 0) return ZO_OK;
@@ -965,23 +811,13 @@ int gemm_launch(const void* A, int64_t lda, const void* B, int64_t ldb, int64_t 
     set_error("zo_gemm_bf16: operands must be 16-byte aligned");
     return ZO_ERR_CONFIG;
   }
-  int bn = 128;
-  const int64_t tiles256 = ((M + kBM - 1) / kBM) * ((N + 255) / 256);
-  (void)tiles256;
-  bn = 256;   // measured: BN=256 beats BN=128 even below one wave (tools/gemm_bench.py)
-  static const int force_bn = [] {
-    const char* e = getenv("ZO_GEMM_BN");   // tuning override (128 | 256)
-    return e ? atoi(e) : 0;
-  }();
-  if (epi != ZO_EPI_CE && (force_bn == 128 || force_bn == 256)) bn = force_bn;
+  // 128 x 256 tiles (measured: BN=256 beats BN=128 even below one wave), CTA
+  // pairs with 256 x 256 tiles once M spans more than one 128-row tile
+  constexpr int bn = 256;
   CUtensorMap ma, mb;
   int rc = get_map(A, K, M, lda, kBK, kBM, &ma);
   if (rc) return rc;
-  static const int pair_mode = [] {
-    const char* e = getenv("ZO_GEMM_PAIR");   // 0: single-CTA only, 1: CTA pairs when M > 128 (default)
-    return e ? atoi(e) : 1;
-  }();
-  const bool pair = pair_mode && M > kBM && bn == 256;
+  const bool pair = M > kBM;
   // B tile: MN-major 64-column boxes, or K-major (rows = N) boxes of 128 (pair half) / BN rows
   rc = bkm ? get_map(B, K, N, ldb, kBK, pair ? 128 : bn, &mb) : get_map(B, N, K, ldb, 64, kBK, &mb);
   if (rc) return rc;
@@ -995,21 +831,9 @@ int gemm_launch(const void* A, int64_t lda, const void* B, int64_t ldb, int64_t 
     rc = bkm ? get_map(B2, K, N, ldb, kBK, 128, &mb2) : get_map(B2, N, K, ldb, 64, kBK, &mb2);
     if (rc) return rc;
   }
-  GemmArgs a{M, N, K, bias, out, ldo, targets, ce_part, ce_tgt, err, gemm_ce_tiles(N), 0, 0, 1, nullptr, nullptr,
-             m_split, bias2};
-  a.dp_tiles = ((M + 255) / 256) * ((N + 255) / 256);
-  if (ws && (reinterpret_cast<uintptr_t>(ws) & 255) == 0) {
-    const SkPlan pl = sk_plan(M, N, K);
-    if (pl.units && pl.bytes <= ws_bytes) {
-      a.dp_tiles = pl.dp_tiles;
-      a.sk_units = pl.units;
-      a.sk_pieces = pl.pieces;
-      a.sk_flags = static_cast<int32_t*>(ws);
-      a.sk_part = reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + pl.flag_bytes);
-    }
-  }
+  GemmArgs a{M, N, K, bias, out, ldo, targets, ce_part, ce_tgt, err, gemm_ce_tiles(N), m_split, bias2};
   if (pair) return launch_pair(epi, bkm, ma, mb, mb2, a, st);
-  return bn == 256 ? launch_bn<256>(epi, bkm, ma, mb, a, st) : launch_bn<128>(epi, bkm, ma, mb, a, st);
+  return launch_bn<bn>(epi, bkm, ma, mb, a, st);
 }
 
 }  // namespace zo

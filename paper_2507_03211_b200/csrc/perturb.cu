@@ -16,7 +16,7 @@
 
 namespace zo {
 
-constexpr int kPuThreads = 128;   // small CTAs: one co-resides with a GEMM CTA per SM
+constexpr int kPuThreads = 128;
 #ifndef ZO_PU_G
 #define ZO_PU_G 4
 #endif
@@ -174,54 +174,6 @@ __device__ __forceinline__ void pu_compute_fast(const PuParams& p, int64_t e0, i
   }
 }
 
-// Background tile body: all four theta groups are loaded up front (the
-// memory parallelism a 4-warp CTA needs), then one Philox chain at a time
-// (registers stay under the 80 that let the CTA sit beside a GEMM CTA).
-template <bool PEND, bool BF16>
-__device__ __forceinline__ void pu_tile_bg_t(const PuParams& p, int64_t e0, int ngroups, int64_t dbase,
-                                             bool SA, bool SB, float sa, float sb, uint64_t seed_cur,
-                                             uint64_t seed_prev, float lrg32, int lane) {
-  constexpr int G = kPuGroupsPerThread;
-  float4* tp = reinterpret_cast<float4*>(p.theta + (e0 - p.theta_key0)) + lane;
-  const uint64_t qa = (uint64_t)(e0 >> 2) + (uint64_t)lane;
-  const bool full = ngroups == 32 * G;
-  float4 th[G];
-#pragma unroll
-  for (int g = 0; g < G; ++g)
-    if (full || lane + 32 * g < ngroups) th[g] = tp[32 * g];
-#pragma unroll
-  for (int g = 0; g < G; ++g) {
-    if (!full && lane + 32 * g >= ngroups) break;
-    const uint64_t q = qa + (uint64_t)(32 * g);
-    float4 t = th[g];
-    if constexpr (PEND) {
-      const f32x4 zp = philox_normal4(seed_prev, q);
-      t.x = fmaf(-lrg32, zp.x, t.x); t.y = fmaf(-lrg32, zp.y, t.y);
-      t.z = fmaf(-lrg32, zp.z, t.z); t.w = fmaf(-lrg32, zp.w, t.w);
-      tp[32 * g] = t;
-    }
-    if (SA || SB) {
-      const f32x4 z = philox_normal4(seed_cur, q);
-#pragma unroll
-      for (int d = 0; d < 2; ++d) {
-        if ((d == 0 && !SA) || (d == 1 && !SB)) continue;
-        const float sc = d == 0 ? sa : sb;
-        const float a = fmaf(sc, z.x, t.x), b = fmaf(sc, z.y, t.y);
-        const float c = fmaf(sc, z.z, t.z), e = fmaf(sc, z.w, t.w);
-        if constexpr (BF16) {
-          __nv_bfloat162 lo2 = __floats2bfloat162_rn(a, b), hi2 = __floats2bfloat162_rn(c, e);
-          uint2 pk;
-          pk.x = *reinterpret_cast<uint32_t*>(&lo2);
-          pk.y = *reinterpret_cast<uint32_t*>(&hi2);
-          (reinterpret_cast<uint2*>(p.wsh[d] + dbase) + lane)[32 * g] = pk;
-        } else {
-          (reinterpret_cast<float4*>(p.vsh[d] + dbase) + lane)[32 * g] = make_float4(a, b, c, e);
-        }
-      }
-    }
-  }
-}
-
 __device__ __forceinline__ void pu_tile_fast(const PuParams& p, int64_t e0, int ngroups, int64_t dbase,
                                              bool pending, bool want_sh, const bool (&sh)[2],
                                              const float (&sc32)[2], uint64_t seed_cur, uint64_t seed_prev,
@@ -252,28 +204,6 @@ __device__ __forceinline__ void pu_tile_fast(const PuParams& p, int64_t e0, int 
     if (pending) pu_compute_fast<true, false, G>(p, e0, ngroups, dbase, sa, sb, sc32[0], sc32[1], seed_cur, seed_prev, lrg32, lane, th);
     else pu_compute_fast<false, false, G>(p, e0, ngroups, dbase, sa, sb, sc32[0], sc32[1], seed_cur, seed_prev, lrg32, lane, th);
   }
-}
-
-__device__ __forceinline__ void pu_tile_bg(const PuParams& p, int64_t e0, int ngroups, int64_t dbase,
-                                           bool pending, bool want_sh, const bool (&sh)[2],
-                                           const float (&sc32)[2], uint64_t seed_cur, uint64_t seed_prev,
-                                           float lrg32, int kind, int lane) {
-  const bool sa = want_sh && sh[0], sb = want_sh && sh[1];
-  if (kind == ZO_SHADOW_BF16) {
-    if (pending) pu_tile_bg_t<true, true>(p, e0, ngroups, dbase, sa, sb, sc32[0], sc32[1], seed_cur, seed_prev, lrg32, lane);
-    else pu_tile_bg_t<false, true>(p, e0, ngroups, dbase, sa, sb, sc32[0], sc32[1], seed_cur, seed_prev, lrg32, lane);
-  } else {
-    if (pending) pu_tile_bg_t<true, false>(p, e0, ngroups, dbase, sa, sb, sc32[0], sc32[1], seed_cur, seed_prev, lrg32, lane);
-    else pu_tile_bg_t<false, false>(p, e0, ngroups, dbase, sa, sb, sc32[0], sc32[1], seed_cur, seed_prev, lrg32, lane);
-  }
-}
-
-// publish one finished tile of a block: every lane fences its own stores at
-// gpu scope, then one lane bumps the block counter
-__device__ __forceinline__ void tile_done(const PuParams& p, int32_t block) {
-  __threadfence();
-  __syncwarp();
-  if ((threadIdx.x & 31) == 0) atomicAdd(p.block_done + block, 1);
 }
 
 // Generic tile (unaligned groups, oracle z, shadow-less segments): one group
@@ -353,7 +283,7 @@ struct PuCursor {
 // current tile's Philox/Box-Muller math, so the loads overlap the compute.
 constexpr int kPuChunk = 8;
 
-template <int ZMODE, bool BG>
+template <int ZMODE>
 __device__ __forceinline__ void perturb_update_body(const PuParams& p) {
   extern __shared__ int64_t s_prefix[];
   pdl_trigger();
@@ -390,7 +320,7 @@ __device__ __forceinline__ void perturb_update_body(const PuParams& p) {
     };
     bool fast = is_fast(cur.s, e0, e1, drow);
     float4 th[kPuGroupsPerThread];
-    if (!BG && fast) pu_load_fast<kPuGroupsPerThread>(p, e0, (int)((e1 - e0) >> 2), lane, th);
+    if (fast) pu_load_fast<kPuGroupsPerThread>(p, e0, (int)((e1 - e0) >> 2), lane, th);
     while (true) {
       const ZoSegment s = cur.s;
       const int64_t ce0 = e0, ce1 = e1, cdrow = drow;
@@ -403,93 +333,39 @@ __device__ __forceinline__ void perturb_update_body(const PuParams& p) {
         cur.next(p, pref);
         cur.geo(e0, e1, drow);
         fast = is_fast(cur.s, e0, e1, drow);
-        if (!BG && fast) pu_load_fast<kPuGroupsPerThread>(p, e0, (int)((e1 - e0) >> 2), lane, th);
+        if (fast) pu_load_fast<kPuGroupsPerThread>(p, e0, (int)((e1 - e0) >> 2), lane, th);
       }
       if (cfast) {
-        if constexpr (BG)
-          pu_tile_bg(p, ce0, (int)((ce1 - ce0) >> 2), ce0 + cdrow, pending, s.kind != ZO_SHADOW_NONE, sh, sc32,
-                     seed_cur, seed_prev, lrg32, s.kind, lane);
-        else
-          pu_tile_fast(p, ce0, (int)((ce1 - ce0) >> 2), ce0 + cdrow, pending, s.kind != ZO_SHADOW_NONE, sh, sc32,
-                       seed_cur, seed_prev, lrg32, s.kind, lane, thc);
+        pu_tile_fast(p, ce0, (int)((ce1 - ce0) >> 2), ce0 + cdrow, pending, s.kind != ZO_SHADOW_NONE, sh, sc32,
+                     seed_cur, seed_prev, lrg32, s.kind, lane, thc);
       } else {
         pu_tile_generic<ZMODE>(p, s, ce0, ce1, cdrow, theta_vec, pending, need_z, sh, sc32, seed_cur, seed_prev,
                                lrg64, lrg32, lane);
       }
-      if (p.block_done) tile_done(p, s.reserved);
       if (!more) break;
     }
   }
 }
 
-template <int ZMODE, int MINB = 4>
-__global__ void __launch_bounds__(kPuThreads, MINB) perturb_update_kernel(const PuParams p) {
-  perturb_update_body<ZMODE, false>(p);
-}
-
-// 88 registers x 4 warps fit in what a 168-register 10-warp GEMM CTA leaves
+// 126 registers x 4 CTAs of 4 warps per SM; a grid of 4 resident waves of
+// chunks (measured best of 1 / 2 / 4: late-starting CTAs even out the tail)
 template <int ZMODE>
-__global__ void __maxnreg__(88) perturb_update_bg_kernel(const PuParams p) {
-  perturb_update_body<ZMODE, true>(p);
+__global__ void __launch_bounds__(kPuThreads, 4) perturb_update_kernel(const PuParams p) {
+  perturb_update_body<ZMODE>(p);
 }
 
 int64_t perturb_tile_elems() { return kPuTile; }   // the host builds its tile prefixes with this
 
-int perturb_update_launch(const PuParams& p, int zmode, cudaStream_t stream, bool background) {
+int perturb_update_launch(const PuParams& p, int zmode, cudaStream_t stream) {
   if (p.n_tiles <= 0) return ZO_OK;
-  static const int occ = [] { const char* e = getenv("ZO_PU_OCC"); return e ? atoi(e) : 4; }();
-  static const int waves = [] { const char* e = getenv("ZO_PU_WAVES"); return e ? atoi(e) : 4; }();
-  static const int bg_ctas = [] { const char* e = getenv("ZO_PU_BG_CTAS"); return e ? atoi(e) : 1; }();
-  // four resident waves of chunks (measured best of 1/2/4): late-starting CTAs even out the tail;
-  // the background pass keeps bg_ctas CTAs per SM beside the forward's kernels
-  const int64_t want = (int64_t)num_sms() * (background ? bg_ctas : occ * waves);
+  const int64_t want = (int64_t)num_sms() * 4 * 4;
   const int grid = (int)(p.n_tiles < want ? p.n_tiles : want);
   const size_t smem = p.n_segs + 1 <= kPuMaxSmemSegs ? (size_t)(p.n_segs + 1) * sizeof(int64_t) : 0;
-  if (background) {
-    static bool carve = false;
-    if (!carve) {
-      // configure the SM for maximum shared memory when these CTAs land first,
-      // so the forward's GEMM / attention CTAs (~200 KB of smem) can still be
-      // placed beside them (an SM's L1/smem split changes only when it is idle)
-      cudaFuncSetAttribute(perturb_update_bg_kernel<ZO_Z_PHILOX>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                           (int)cudaSharedmemCarveoutMaxShared);
-      cudaFuncSetAttribute(perturb_update_bg_kernel<ZO_Z_ORACLE>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                           (int)cudaSharedmemCarveoutMaxShared);
-      carve = true;
-    }
-    if (zmode == ZO_Z_PHILOX)
-      launch_k(perturb_update_bg_kernel<ZO_Z_PHILOX>, dim3(grid), dim3(kPuThreads), smem, stream, p);
-    else
-      launch_k(perturb_update_bg_kernel<ZO_Z_ORACLE>, dim3(grid), dim3(kPuThreads), smem, stream, p);
-  } else {
-    if (zmode == ZO_Z_PHILOX && occ == 5)
-      launch_k(perturb_update_kernel<ZO_Z_PHILOX, 5>, dim3(grid), dim3(kPuThreads), smem, stream, p);
-    else if (zmode == ZO_Z_PHILOX && occ == 6)
-      launch_k(perturb_update_kernel<ZO_Z_PHILOX, 6>, dim3(grid), dim3(kPuThreads), smem, stream, p);
-    else if (zmode == ZO_Z_PHILOX && occ == 8)
-      launch_k(perturb_update_kernel<ZO_Z_PHILOX, 8>, dim3(grid), dim3(kPuThreads), smem, stream, p);
-    else if (zmode == ZO_Z_PHILOX)
-      launch_k(perturb_update_kernel<ZO_Z_PHILOX>, dim3(grid), dim3(kPuThreads), smem, stream, p);
-    else
-      launch_k(perturb_update_kernel<ZO_Z_ORACLE>, dim3(grid), dim3(kPuThreads), smem, stream, p);
-  }
+  if (zmode == ZO_Z_PHILOX)
+    launch_k(perturb_update_kernel<ZO_Z_PHILOX>, dim3(grid), dim3(kPuThreads), smem, stream, p);
+  else
+    launch_k(perturb_update_kernel<ZO_Z_ORACLE>, dim3(grid), dim3(kPuThreads), smem, stream, p);
   return launch_status("perturb_update_kernel");
-}
-
-// spin until *counter >= target (one thread); gates a forward stream on the
-// background perturb pass having finished a block
-__global__ void wait_counter_kernel(const int32_t* counter, int32_t target) {
-  int32_t v;
-  while (true) {
-    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(counter) : "memory");
-    if (v >= target) break;
-    __nanosleep(256);
-  }
-}
-
-int wait_counter_launch(const int32_t* counter, int32_t target, cudaStream_t stream) {
-  wait_counter_kernel<<<1, 1, 0, stream>>>(counter, target);
-  return launch_status("wait_counter_kernel");
 }
 
 // ---------------------------------------------------------------------------

@@ -152,12 +152,10 @@ class SegTable:
         arr = (L.ZoSegment * max(1, len(segs)))()
         prefix = np.zeros(len(segs) + 1, dtype=np.int64)
         block_ids = block_ids or [0] * len(segs)
-        self.block_tiles = {}     # block id -> tiles (the completion target of zo_perturb_update_bg)
         for i, ((src, rows, cols, dst, ld, kind), bid) in enumerate(zip(segs, block_ids)):
             arr[i] = L.ZoSegment(src, rows, cols, dst, ld, kind, bid)
             n = rows * ((cols + tile - 1) // tile)
             prefix[i + 1] = prefix[i] + n
-            self.block_tiles[bid] = self.block_tiles.get(bid, 0) + n
         raw = np.frombuffer(bytes(arr), dtype=np.uint8).copy()
         self.segs = torch.from_numpy(raw).to(device)
         self.prefix = torch.from_numpy(prefix).to(device)

@@ -22,11 +22,10 @@ def _ld(t):
 
 
 def gemm(a: torch.Tensor, b: torch.Tensor, epilogue: int, out=None, bias=None, m=None, n=None, k=None,
-         targets=None, ce_part=None, ce_tgt=None, err=None, stream=None, workspace=None):
+         targets=None, ce_part=None, ce_tgt=None, err=None, stream=None):
     """out (+)= epilogue(a[M,K] @ b[K,N]) on tcgen05.  a, b bf16 2-D with unit
     inner stride (b as [N, K] when ``epilogue`` carries ZO_GEMM_B_KMAJOR);
-    bias fp32 [N].  ``workspace`` (uint8, zero-initialised,
-    gemm_workspace_bytes(M, N, K) long) enables the stream-K tail."""
+    bias fp32 [N]."""
     if a.dtype != torch.bfloat16 or b.dtype != torch.bfloat16:
         raise DimensionError("gemm operands must be bf16")
     M = m if m is not None else a.shape[0]
@@ -36,20 +35,9 @@ def gemm(a: torch.Tensor, b: torch.Tensor, epilogue: int, out=None, bias=None, m
     if b.shape[1 if bkm else 0] < K or a.stride(-1) != 1 or b.stride(-1) != 1:
         raise DimensionError("gemm: operand shapes/strides do not match")
     ldo = 0 if out is None else _ld(out)
-    if workspace is not None:
-        L.call("zo_gemm_bf16_ws", _p(a), _ld(a), _p(b), _ld(b), M, N, K, epilogue, _p(bias), _p(out), ldo,
-               _p(targets), _p(ce_part), _p(ce_tgt), _p(err), _p(workspace), workspace.numel(),
-               L.stream_ptr(stream))
-    else:
-        L.call("zo_gemm_bf16", _p(a), _ld(a), _p(b), _ld(b), M, N, K, epilogue, _p(bias), _p(out), ldo,
-               _p(targets), _p(ce_part), _p(ce_tgt), _p(err), L.stream_ptr(stream))
+    L.call("zo_gemm_bf16", _p(a), _ld(a), _p(b), _ld(b), M, N, K, epilogue, _p(bias), _p(out), ldo,
+           _p(targets), _p(ce_part), _p(ce_tgt), _p(err), L.stream_ptr(stream))
     return out
-
-
-def gemm_workspace(m: int, n: int, k: int, device="cuda") -> torch.Tensor:
-    """Zero-initialised stream-K workspace for an m x n x k GEMM."""
-    nbytes = int(L.lib().zo_gemm_workspace_bytes(m, n, k))
-    return torch.zeros(max(nbytes, 256), dtype=torch.uint8, device=device)
 
 
 def ce_tiles(n: int) -> int:

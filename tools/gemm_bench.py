@@ -17,12 +17,9 @@ for M, N, K in shapes:
     bias = torch.randn(N, device="cuda")
     o32 = torch.zeros(M, N, device="cuda")
     o16 = torch.zeros(M, N, device="cuda", dtype=torch.bfloat16)
-    wsp = ops.gemm_workspace(M, N, K)
-    for (en, e), ws in [(x, None) for x in epis.items()] + [((x[0] + "+sk", x[1]), wsp) for x in epis.items()]:
-        if ws is not None and ws.numel() <= 256:
-            continue
+    for en, e in epis.items():
         out = o32 if e in (L.ZO_EPI_F32, L.ZO_EPI_BIAS_RESID_F32) else o16
-        f = lambda: ops.gemm(a, b, e, out=out, bias=bias, workspace=ws)  # noqa: E731
+        f = lambda: ops.gemm(a, b, e, out=out, bias=bias)  # noqa: E731
         f()
         torch.cuda.synchronize()
         s, t = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

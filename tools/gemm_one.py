@@ -1,6 +1,6 @@
 """Run one GEMM shape/epilogue a few times (for ncu captures).
 
-    python tools/gemm_one.py M N K epi [reps] [sk]      epi in f32|bias|gelu|resid
+    python tools/gemm_one.py M N K epi [reps]      epi in f32|bias|gelu|resid
 """
 import sys
 
@@ -19,8 +19,7 @@ b = torch.randn(K, N, device="cuda").bfloat16()
 bias = torch.randn(N, device="cuda")
 out = torch.zeros(M, N, device="cuda", dtype=torch.float32 if epi in (L.ZO_EPI_F32, L.ZO_EPI_BIAS_RESID_F32)
                   else torch.bfloat16)
-ws = ops.gemm_workspace(M, N, K) if "sk" in sys.argv[6:] else None
 for _ in range(reps):
-    ops.gemm(a, b, epi, out=out, bias=bias, workspace=ws)
+    ops.gemm(a, b, epi, out=out, bias=bias)
 torch.cuda.synchronize()
 print("ok")
