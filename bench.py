@@ -63,8 +63,9 @@ def _args():
     ap.add_argument("--seq", type=int, default=SEQ)
     ap.add_argument("--batch", type=int, default=BATCH,
                     help="sequences per directional forward (N=1); a 2-rank PertP group runs 2x this")
-    ap.add_argument("--plan", default="stacked", choices=["stacked", "none"],
-                    help="N=1 step plan: both directions as one launch per layer (stacked) or two streams")
+    ap.add_argument("--plan", default="fill", choices=["stacked", "fill", "none"],
+                    help="N=1 step plan: both directions as one launch per layer (stacked), the same with the "
+                         "perturb pass filling idle SMs from a low-priority stream (fill), or two streams")
     ap.add_argument("--no-graph", action="store_true", help="launch the step eagerly instead of replaying a CUDA graph")
     ap.add_argument("--no-e2e", action="store_true", help="skip the public-API pass (profiling runs)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -328,7 +329,7 @@ def ours(args, rank, world, local_rank):
                for j in range(1, args.warmup + args.steps + 1)]
 
     if world == 1:
-        runner = zo.StreamingZo(store, hyper, overlap=args.plan if args.plan == "stacked" else False,
+        runner = zo.StreamingZo(store, hyper, overlap=args.plan if args.plan in ("stacked", "fill") else False,
                                 graph=not args.no_graph)
         wss = [store.workspace(PLUS, B, T), store.workspace(MINUS, B, T)]
         step_calls = runner._plan(wss[0], wss[1])
@@ -346,6 +347,8 @@ def ours(args, rank, world, local_rank):
     streams = {int(torch.cuda.current_stream().cuda_stream): torch.cuda.current_stream()}
     if hasattr(store, "_side"):
         streams[int(store._side.cuda_stream)] = store._side
+    for st_ in getattr(store, "_prio", None) or ():
+        streams[int(st_.cuda_stream)] = st_
 
     use_graph = not args.no_graph and (world == 1 or runner.graph)     # (a gloo mesh cannot be captured)
 
@@ -410,6 +413,8 @@ def ours(args, rank, world, local_rank):
     # never overlap): per-kernel CUDA-event durations for the roofline rows
     if world == 1 and args.plan != "stacked":
         runner.dual_stream = False
+        if args.plan == "fill":
+            runner.overlap = "stacked"          # per-kernel windows: the same launches, serialised
         step_calls = runner._plan(wss[0], wss[1])
     events = []
     for j in range(args.warmup, args.warmup + args.steps):
@@ -444,7 +449,7 @@ def ours(args, rank, world, local_rank):
     api = None
     if not args.no_e2e:
         if world == 1:
-            api = zo.StreamingZo(store, hyper, overlap=args.plan if args.plan == "stacked" else False,
+            api = zo.StreamingZo(store, hyper, overlap=args.plan if args.plan in ("stacked", "fill") else False,
                                  graph=not args.no_graph)
         else:
             api = MeshZo(store, hyper, fabric, "2d", B, T, graph=not args.no_graph)
@@ -501,7 +506,8 @@ def ours(args, rank, world, local_rank):
     pert_ms = d["ms"] / args.steps
     r_pert = {"bound": "hbm", "kernel": "perturb_update_kernel", "achieved": pert_bytes / (pert_ms * 1e-3) / 1e9,
               "peak": hbm, "unit": "GB/s", "frac": pert_bytes / (pert_ms * 1e-3) / 1e9 / hbm,
-              "traffic": traffic.get("perturb_bytes_per_launch"), "traffic_algorithmic": pert_bytes,
+              "traffic": traffic.get("perturb_bytes_per_step", traffic.get("perturb_bytes_per_launch")),
+              "traffic_algorithmic": pert_bytes,
               "peak_kind": f"{peak_kind} HBM copy", "share_of_step": pert_ms / ms,
               "algorithmic": (f"R+W fp32 master (8 B) + the bf16 / fp32 shadows this rank writes, per parameter "
                               f"(embedding: no shadow, 8 B): {pert_bytes} B over {P} params, one launch per step")}

@@ -51,6 +51,9 @@ extern "C" {
 #define ZO_PU_UPDATE 1u  /* apply the pending update theta -= (lr g_prev) z_prev  */
 #define ZO_PU_SHADOW_A 2u /* write shadow A = theta' + scale_a z_cur             */
 #define ZO_PU_SHADOW_B 4u /* write shadow B = theta' + scale_b z_cur             */
+#define ZO_PU_FILL 8u     /* launch as short-lived CTAs (one chunk per warp) so a
+                             pass on a low-priority stream only fills SMs that the
+                             forward leaves idle and never holds one for long    */
 
 /* zo_gemm_bf16 epilogues */
 #define ZO_EPI_F32 0          /* out f32  = acc                                   */
@@ -109,6 +112,22 @@ int zo_perturb_update(float* theta, int64_t theta_key0, const ZoSegment* segs,
                       const ZoStepScalars* scal, int32_t zmode,
                       const double* z_cur, const double* z_prev, int64_t z_key0,
                       void* stream);
+/*
+ * CUDA-graph capture of a step that honours per-launch priorities (torch's
+ * graphs instantiate without cudaGraphInstantiateFlagUseNodePriority): every
+ * kernel this library launches carries its stream's priority as a launch
+ * attribute, and a graph instantiated here replays with those priorities, so
+ * a low-priority ZO_PU_FILL pass keeps yielding SMs to the forward.
+ *   zo_graph_begin(stream)            cudaStreamBeginCapture (thread-local mode)
+ *   zo_graph_end(stream, &exec)       end capture, instantiate with node priorities
+ *   zo_graph_launch(exec, stream)     replay
+ *   zo_graph_destroy(exec)
+ */
+int zo_graph_begin(void* stream);
+int zo_graph_end(void* stream, void** exec_out);
+int zo_graph_launch(void* exec, void* stream);
+int zo_graph_destroy(void* exec);
+
 /* Tile granularity (elements) the host must use to build tile_prefix. */
 int64_t zo_perturb_tile_elems(void);
 

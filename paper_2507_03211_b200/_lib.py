@@ -19,7 +19,7 @@ LIB_PATH = os.environ.get("ZO_B200_LIB", os.path.join(_HERE, "lib", "libzo_b200.
 ZO_OK = 0
 ZO_Z_PHILOX, ZO_Z_ORACLE = 0, 1
 ZO_SHADOW_BF16, ZO_SHADOW_F32, ZO_SHADOW_NONE = 0, 1, 2
-ZO_PU_UPDATE, ZO_PU_SHADOW_A, ZO_PU_SHADOW_B = 1, 2, 4
+ZO_PU_UPDATE, ZO_PU_SHADOW_A, ZO_PU_SHADOW_B, ZO_PU_FILL = 1, 2, 4, 8
 ZO_EPI_F32, ZO_EPI_BIAS_BF16, ZO_EPI_BIAS_GELU_BF16, ZO_EPI_BIAS_RESID_F32, ZO_EPI_CE = 0, 1, 2, 3, 4
 ZO_EPI_BIAS_RELU_BF16 = 5
 ZO_GEMM_B_KMAJOR = 0x100
@@ -64,6 +64,10 @@ SIGNATURES = {
     "zo_grad_finalize": (C.c_int, [P, P, D, D, P, P, P]),
     "zo_grad_finalize_groups": (C.c_int, [P, I32, I32, I32, I32, I32, I32, D, D, P, P, P]),
     "zo_hash_u64": (C.c_int, [P, I64, P, P, P]),
+    "zo_graph_begin": (C.c_int, [P]),
+    "zo_graph_end": (C.c_int, [P, P]),
+    "zo_graph_launch": (C.c_int, [P, P]),
+    "zo_graph_destroy": (C.c_int, [P]),
     "zo_planes_join": (C.c_int, [P, P, P, I64, P]),
     "zo_planes_split": (C.c_int, [P, P, P, I64, P]),
     "zo_philox_normals": (C.c_int, [U64, I64, I64, P, P]),

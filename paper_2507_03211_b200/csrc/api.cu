@@ -268,4 +268,32 @@ int zo_philox_normals(uint64_t seed, int64_t e0, int64_t n, float* out, void* st
   return zo::philox_normals_launch(seed, e0, n, out, ZO_STREAM(stream));
 }
 
+int zo_graph_begin(void* stream) {
+  ZO_CUDA_TRY(cudaStreamBeginCapture(ZO_STREAM(stream), cudaStreamCaptureModeThreadLocal));
+  return ZO_OK;
+}
+
+int zo_graph_end(void* stream, void** exec_out) {
+  ZO_CHECK_ARG(exec_out, ZO_ERR_CONFIG, "zo_graph_end: null output");
+  cudaGraph_t g = nullptr;
+  ZO_CUDA_TRY(cudaStreamEndCapture(ZO_STREAM(stream), &g));
+  cudaGraphExec_t ex = nullptr;
+  const cudaError_t e = cudaGraphInstantiateWithFlags(&ex, g, cudaGraphInstantiateFlagUseNodePriority);
+  cudaGraphDestroy(g);
+  ZO_CUDA_TRY(e);
+  *exec_out = ex;
+  return ZO_OK;
+}
+
+int zo_graph_launch(void* exec, void* stream) {
+  ZO_CHECK_ARG(exec, ZO_ERR_CONFIG, "zo_graph_launch: null graph");
+  ZO_CUDA_TRY(cudaGraphLaunch(static_cast<cudaGraphExec_t>(exec), ZO_STREAM(stream)));
+  return ZO_OK;
+}
+
+int zo_graph_destroy(void* exec) {
+  if (exec) ZO_CUDA_TRY(cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(exec)));
+  return ZO_OK;
+}
+
 }  // extern "C"

@@ -358,7 +358,10 @@ int64_t perturb_tile_elems() { return kPuTile; }   // the host builds its tile p
 
 int perturb_update_launch(const PuParams& p, int zmode, cudaStream_t stream) {
   if (p.n_tiles <= 0) return ZO_OK;
-  const int64_t want = (int64_t)num_sms() * 4 * 4;
+  const int64_t n_chunks = (p.n_tiles + kPuChunk - 1) / kPuChunk;
+  // ZO_PU_FILL: one chunk per warp, CTAs live a few microseconds; otherwise a
+  // persistent grid of four resident waves
+  const int64_t want = (p.flags & ZO_PU_FILL) ? (n_chunks + 3) / 4 : (int64_t)num_sms() * 4 * 4;
   const int grid = (int)(p.n_tiles < want ? p.n_tiles : want);
   const size_t smem = p.n_segs + 1 <= kPuMaxSmemSegs ? (size_t)(p.n_segs + 1) * sizeof(int64_t) : 0;
   if (zmode == ZO_Z_PHILOX)

@@ -150,7 +150,7 @@ class StreamingZo:
     one.  Numerically identical to repeated ``mezo_step`` after flush."""
 
     def __init__(self, store: DeviceStore, hyper: ZoHyper, mgr: RngStateManager | None = None,
-                 overlap: bool | str = "stacked", graph: bool = True):
+                 overlap: bool | str = "fill", graph: bool = True):
         self.store = store
         self.hyper = hyper.validate()
         self.mgr = mgr or RngStateManager()
@@ -159,9 +159,14 @@ class StreamingZo:
         # the fused pass, then the two forwards on two streams (also the plan
         # for shapes the stacked GEMMs cannot split and for oracle-z runs).
         # Both plans give identical results.
-        if overlap not in (False, None, "none", "stacked"):
-            raise ProtocolError(f"unknown step plan {overlap!r} (plans: 'stacked', 'none')")
-        self.overlap = "stacked" if (overlap == "stacked" and not self.mgr.oracle) else None
+        # "fill": the stacked forward on a high-priority stream while the
+        # perturb pass of blocks 2.. runs block by block as short-lived CTAs on
+        # a low-priority stream, each block's forward waiting only for its own
+        # block's pass -- the pass fills the SMs the forward's kernels leave
+        # idle (partial waves, launch gaps) instead of running before it.
+        if overlap not in (False, None, "none", "stacked", "fill"):
+            raise ProtocolError(f"unknown step plan {overlap!r} (plans: 'stacked', 'fill', 'none')")
+        self.overlap = overlap if (overlap in ("stacked", "fill") and not self.mgr.oracle) else None
         self.dual_stream = True
         # Philox steps replay one captured CUDA graph per batch shape (the
         # step's scalars are device-resident, so the launches never change)
@@ -224,11 +229,44 @@ class StreamingZo:
         calls += s.grad_call_stacked(ws, eps, self.hyper.lr)
         return calls
 
+    def fill_step_calls(self, wsp, wsn):
+        """The stacked step with the perturb pass split by block: embedding +
+        block 1 at full speed on the forward's (high-priority) stream, blocks
+        2.. and the head as ZO_PU_FILL launches on a low-priority stream, one
+        event per block; block b's forward waits for block b's event only.
+        Same per-element arithmetic as stacked_step_calls (bit-identical)."""
+        if self.mgr.oracle:
+            raise ProtocolError("the fill plan runs the Philox direction only")
+        s, eps = self.store, self.hyper.epsilon
+        ws = s.stacked_workspace(wsp.batch, wsp.seq)
+        nl = len(s.layouts)
+        main = torch.cuda.current_stream()
+        hi, lo = _priority_streams(s)
+        ev = _block_events(s, nl + 3)          # [b] block b's pass done; [nl] start; [nl+1], [nl+2] joins
+        flags = L.ZO_PU_UPDATE | L.ZO_PU_SHADOW_A | L.ZO_PU_SHADOW_B
+        calls = [(_record_and_wait, (ev[nl], main, hi)), (_wait, (lo, ev[nl]))]
+        if getattr(s, "_fill_head", None) is None:
+            s._fill_head = s.range_table(0, 2)          # built once, outside any graph capture
+        calls += s.perturb_call(s._fill_head, flags, +eps, -eps, stream=hi)
+        for b in range(2, nl):
+            calls += s.perturb_call(s.block_tables[b], flags | L.ZO_PU_FILL, +eps, -eps, stream=lo)
+            calls.append((_record, (ev[b], lo)))
+        calls += s.forward_calls_stacked(ws, eps, stream=hi, blocks=[0, 1])
+        for b in range(2, nl):
+            calls.append((_wait, (hi, ev[b])))
+            calls += s.forward_calls_stacked(ws, eps, stream=hi, blocks=[b])
+        calls += s.grad_call_stacked(ws, eps, self.hyper.lr, stream=hi)
+        calls.append((_record_and_wait, (ev[nl + 1], hi, main)))
+        calls.append((_record_and_wait, (ev[nl + 2], lo, main)))
+        return calls
+
     def _stacked_ok(self, wsp):
-        return self.overlap == "stacked" and self.store.stackable(wsp.batch, wsp.seq)
+        return self.overlap in ("stacked", "fill") and self.store.stackable(wsp.batch, wsp.seq)
 
     def _plan(self, wsp, wsn, zc=None, zp=None, update=True):
         if self._stacked_ok(wsp):
+            if self.overlap == "fill":
+                return self.fill_step_calls(wsp, wsn)
             return self.stacked_step_calls(wsp, wsn)
         return self.step_calls(wsp, wsn, zc, zp, update=update)
 
@@ -240,9 +278,12 @@ class StreamingZo:
         key = (wsp.batch, wsp.seq, self.overlap, self.dual_stream)
         g = self._graphs.get(key)
         if g is None:
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g, capture_error_mode="thread_local"):
-                self.store.run(self._plan(wsp, wsn))      # stream handles bound inside the capture
+            if self.overlap == "fill" and self._stacked_ok(wsp):
+                g = NativeGraph(self.store.run, lambda: self._plan(wsp, wsn))   # replays with launch priorities
+            else:
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, capture_error_mode="thread_local"):
+                    self.store.run(self._plan(wsp, wsn))      # stream handles bound inside the capture
             self._graphs[key] = g
         g.replay()
 
@@ -310,6 +351,57 @@ def _record_and_wait(ev, main, side):
     ev.record(main)
     side.wait_event(ev)
     return 0
+
+
+def _record(ev, stream):
+    ev.record(stream)
+    return 0
+
+
+def _wait(stream, ev):
+    stream.wait_event(ev)
+    return 0
+
+
+def _priority_streams(store: DeviceStore):
+    """(high, low) priority streams of the fill plan (lower number = higher)."""
+    if getattr(store, "_prio", None) is None:
+        store._prio = (torch.cuda.Stream(device=store.device, priority=-5),
+                       torch.cuda.Stream(device=store.device, priority=0))
+    return store._prio
+
+
+class NativeGraph:
+    """A step captured with the library's own graph API (zo_graph_*): unlike
+    torch.cuda.CUDAGraph it instantiates with per-node priorities, so the
+    fill plan's low-priority pass keeps yielding SMs on replay.  Capture runs
+    on a private stream forked from the caller's; replay on the current one."""
+
+    def __init__(self, run, build):
+        import ctypes
+        self._lib = L.lib()
+        cur = torch.cuda.current_stream()
+        cap = torch.cuda.Stream(device=cur.device)
+        cap.wait_stream(cur)
+        self.exec = ctypes.c_void_p()
+        with torch.cuda.stream(cap):
+            L.check(self._lib.zo_graph_begin(L.stream_ptr(cap)))
+            try:
+                run(build())          # the plan binds the capture stream as its "current" stream
+            finally:
+                rc = self._lib.zo_graph_end(L.stream_ptr(cap), ctypes.byref(self.exec))
+            L.check(rc)
+        cur.wait_stream(cap)
+
+    def replay(self):
+        L.check(self._lib.zo_graph_launch(self.exec, L.stream_ptr(torch.cuda.current_stream())))
+
+    def __del__(self):
+        try:
+            if self.exec:
+                self._lib.zo_graph_destroy(self.exec)
+        except Exception:
+            pass
 
 
 def flush_pending_update(store: DeviceStore, g_last: float, seed: int, mgr: RngStateManager, lr: float) -> None:

@@ -310,6 +310,28 @@ def test_graph_replay_equals_eager(plan):
     assert torch.equal(a.theta, b.theta)
 
 
+@pytest.mark.parametrize("graph", [False, True])
+def test_fill_plan_is_bit_identical(graph):
+    """The fill plan (embedding + block 1 perturbed up front, later blocks as
+    ZO_PU_FILL launches on a low-priority stream with per-block events; graph
+    replay through zo_graph_* with node priorities) gives exactly the stacked
+    plan's records and weights -- 4 blocks, so three blocks ride the filler."""
+    cfg = ModelConfig(500, 128, 2, 4, 128, "f32")
+    a, b = DeviceStore(cfg, 7), DeviceStore(cfg, 7)
+    h = zo.ZoHyper(EPS, LR)
+    sa = zo.StreamingZo(a, h, overlap="stacked", graph=graph)
+    sb = zo.StreamingZo(b, h, overlap="fill", graph=graph)
+    for j, s in enumerate(iteration_seeds(41, 5), 1):
+        batch = make_batch(cfg, 2, 950 + j)
+        ra, rb = sa.step(batch, s), sb.step(batch, s)
+        assert (ra.loss_pos, ra.loss_neg, ra.g) == (rb.loss_pos, rb.loss_neg, rb.g)
+    if graph:
+        assert isinstance(next(iter(sb._graphs.values())), zo.NativeGraph)
+    sa.flush()
+    sb.flush()
+    assert torch.equal(a.theta, b.theta)
+
+
 @pytest.mark.parametrize("arch", ["zosim", "opt"])
 @pytest.mark.parametrize("graph", [False, True])
 def test_stacked_plan_is_bit_identical(arch, graph):

@@ -44,6 +44,9 @@ def main(path):
         "source": path,
         "launches": len(launches),
         "perturb_bytes_per_launch": (sum(v["bytes"] for v in pert) / max(1, sum(v["n"] for v in pert))) if pert else None,
+        # the fill plan splits the pass into one launch per block: the step's total is the comparable figure
+        "perturb_bytes_per_step": sum(v["bytes"] for v in pert) if pert else None,
+        "perturb_launches_per_step": sum(v["n"] for v in pert),
         "gemm_bytes_per_step": sum(v["bytes"] for v in gemm) if gemm else None,
         "gemm_launches_per_step": sum(v["n"] for v in gemm),
         "kernels": {k: {"n": v["n"], "dram_bytes": v["bytes"], "ncu_time_ms": v["s"] * 1e3}
