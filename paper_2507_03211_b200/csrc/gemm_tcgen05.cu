@@ -546,7 +546,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, kGemmM
   }
   tc_fence_before();
   cluster_sync_all();
-  __syncthreads();   // also a CTA barrier: orders the alloc's smem write for tools that model only CTA barriers
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   pdl_trigger();
