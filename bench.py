@@ -467,7 +467,7 @@ def ours(args, rank, world, local_rank):
             t = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e2e_ms = float(t.item())
-        h2d = 2 * M * 4                      # ids + targets (int32), shared by the rank's workspaces
+        h2d = 2 * M * 4 + (16 if world == 1 else 0)   # ids + targets (int32, shared by the workspaces) + seed / pending
         d2h = 3 * 8 + len(wss) * 4           # ZoStep record (f64 x3) + error flags (int32)
     P = store.total_params
     pert_bytes = store.perturb_bytes(dirs)

@@ -124,6 +124,10 @@ int zo_perturb_update(float* theta, int64_t theta_key0, const ZoSegment* segs,
  *   zo_graph_destroy(exec)
  */
 int zo_graph_begin(void* stream);
+/* Asynchronous copy on `stream` (pinned host <-> device, device <-> device);
+ * captured as a graph node, so a replayed step carries its own batch upload
+ * and record read-back and the host only fills / reads pinned memory. */
+int zo_copy_async(void* dst, const void* src, int64_t bytes, void* stream);
 int zo_graph_end(void* stream, void** exec_out);
 int zo_graph_launch(void* exec, void* stream);
 int zo_graph_destroy(void* exec);

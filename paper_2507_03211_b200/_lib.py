@@ -65,6 +65,7 @@ SIGNATURES = {
     "zo_grad_finalize_groups": (C.c_int, [P, I32, I32, I32, I32, I32, I32, D, D, P, P, P]),
     "zo_hash_u64": (C.c_int, [P, I64, P, P, P]),
     "zo_graph_begin": (C.c_int, [P]),
+    "zo_copy_async": (C.c_int, [P, P, I64, P]),
     "zo_graph_end": (C.c_int, [P, P]),
     "zo_graph_launch": (C.c_int, [P, P]),
     "zo_graph_destroy": (C.c_int, [P]),

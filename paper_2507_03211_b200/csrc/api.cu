@@ -268,6 +268,12 @@ int zo_philox_normals(uint64_t seed, int64_t e0, int64_t n, float* out, void* st
   return zo::philox_normals_launch(seed, e0, n, out, ZO_STREAM(stream));
 }
 
+int zo_copy_async(void* dst, const void* src, int64_t bytes, void* stream) {
+  ZO_CHECK_ARG(bytes >= 0 && (bytes == 0 || (dst && src)), ZO_ERR_CONFIG, "zo_copy_async: bad argument");
+  if (bytes) ZO_CUDA_TRY(cudaMemcpyAsync(dst, src, (size_t)bytes, cudaMemcpyDefault, ZO_STREAM(stream)));
+  return ZO_OK;
+}
+
 int zo_graph_begin(void* stream) {
   ZO_CUDA_TRY(cudaStreamBeginCapture(ZO_STREAM(stream), cudaStreamCaptureModeThreadLocal));
   return ZO_OK;

@@ -270,22 +270,91 @@ class StreamingZo:
             return self.stacked_step_calls(wsp, wsn)
         return self.step_calls(wsp, wsn, zc, zp, update=update)
 
-    def _replay(self, wsp, wsn):
+    def _replay(self, wsp, wsn, io: bool = False):
         """Capture the step's launches once per (batch shape, plan) -- the
         first step ran eagerly, so one-time kernel attributes and TMA
         descriptors already exist -- then replay the graph on the current
-        stream, after this step's batch upload and seed write."""
-        key = (wsp.batch, wsp.seq, self.overlap, self.dual_stream)
+        stream.  io=False: the caller uploaded the batch and seed; io=True
+        (the public step): the graph itself copies the batch / seed / pending
+        flag in from pinned staging and the record / error flags back out."""
+        key = (wsp.batch, wsp.seq, self.overlap, self.dual_stream, io)
         g = self._graphs.get(key)
         if g is None:
+            def build():
+                calls = self._plan(wsp, wsn)
+                if io:
+                    cin, cout = self._io_calls(wsp)
+                    calls = cin + calls + cout
+                return calls
+
             if self.overlap == "fill" and self._stacked_ok(wsp):
-                g = NativeGraph(self.store.run, lambda: self._plan(wsp, wsn))   # replays with launch priorities
+                g = NativeGraph(self.store.run, build)          # replays with launch priorities
             else:
                 g = torch.cuda.CUDAGraph()
                 with torch.cuda.graph(g, capture_error_mode="thread_local"):
-                    self.store.run(self._plan(wsp, wsn))      # stream handles bound inside the capture
+                    self.store.run(build())                     # stream handles bound inside the capture
             self._graphs[key] = g
         g.replay()
+
+    def _io_bufs(self, wsp):
+        """Pinned staging of the graph-carried step I/O for M = B*T rows:
+        ids / targets in, (seed, pending) in, the ZoStep record and the
+        workspaces' error flags out."""
+        io = getattr(self, "_io", None)
+        if io is None or io["M"] != wsp.M:
+            io = self._io = {"M": wsp.M,
+                             "ids": torch.empty(2, wsp.M, dtype=torch.int32, pin_memory=True),
+                             "scal": torch.zeros(2, dtype=torch.int64, pin_memory=True),
+                             "rec": torch.zeros(3, dtype=torch.float64, pin_memory=True),
+                             "err": torch.zeros(4, dtype=torch.int32, pin_memory=True)}
+        return io
+
+    def _io_wss(self, wsp, wsn):
+        wss = [wsp, wsn]
+        if self._stacked_ok(wsp):
+            wss.append(self.store.stacked_workspace(wsp.batch, wsp.seq))
+        return wss
+
+    def _io_calls(self, wsp):
+        """(in, out) copy launches of the I/O-carrying graph, on the capture stream."""
+        s, lib, st = self.store, L.lib(), L.stream_ptr()
+        io = self._io_bufs(wsp)
+        B, T = wsp.batch, wsp.seq
+        wsn = s.workspace(MINUS, B, T)
+        nb = 4 * wsp.M
+        cin = [(lib.zo_copy_async, (wsp.ids.data_ptr(), io["ids"].data_ptr(), nb, st)),
+               (lib.zo_copy_async, (wsp.tgt.data_ptr(), io["ids"].data_ptr() + nb, nb, st)),
+               (lib.zo_copy_async, (s.scal.data_ptr(), io["scal"].data_ptr(), 8, st)),           # seed_cur
+               (lib.zo_copy_async, (s.scal.data_ptr() + 24, io["scal"].data_ptr() + 8, 8, st))]  # pending
+        cout = [(lib.zo_copy_async, (io["rec"].data_ptr(), s.record.data_ptr(), 24, st))]
+        for i, ws in enumerate(self._io_wss(wsp, wsn)):
+            cout.append((lib.zo_copy_async, (io["err"].data_ptr() + 4 * i, ws.err.data_ptr(), 4, st)))
+        return cin, cout
+
+    def _step_graph_io(self, batch: Batch, seed: int, pending: bool) -> ZoStep:
+        """A replayed step whose graph carries its own I/O: the host fills
+        pinned memory, launches once, synchronises once and reads pinned memory."""
+        s = self.store
+        batch.validate(s.config)
+        ids, tg = np.asarray(batch.token_ids), np.asarray(batch.targets)
+        B, T = ids.shape
+        wsp, wsn = s.workspace(PLUS, B, T), s.workspace(MINUS, B, T)
+        if tg.shape != ids.shape:
+            raise DimensionError(f"targets shape {tg.shape} does not match ids {ids.shape}")
+        if ids.size and (ids.min() < 0 or ids.max() >= s.config.vocab_size):
+            raise DimensionError("token id out of embedding range")
+        io = self._io_bufs(wsp)
+        h = io["ids"].numpy()
+        h[0] = ids.reshape(-1)
+        h[1] = tg.reshape(-1)
+        io["scal"].numpy()[:] = (_u64_as_i64(seed), 1 if pending else 0)
+        self._replay(wsp, wsn, io=True)
+        torch.cuda.current_stream().synchronize()
+        wss = self._io_wss(wsp, wsn)
+        errs = [int(v) for v in io["err"].numpy()[:len(wss)]]
+        s.check_errors(*wss, flags=errs)
+        r = io["rec"].numpy()
+        return ZoStep(self.iteration, seed, float(r[0]), float(r[1]), float(r[2]))
 
     def step(self, batch: Batch, seed: int) -> ZoStep:
         self.iteration += 1
@@ -294,19 +363,17 @@ class StreamingZo:
         apply_pending = self.iteration > 1 and self._pending
         if apply_pending:
             self.mgr.pop_state()
-        wsp, wsn = _stage_batch(self.store, batch)
-        zc = _oracle_z(self.mgr, seed, self.store.total_params, self.store.device) if self.mgr.oracle else None
-        _write_scal(self.store, seed, pending=apply_pending)
-        if self.graph and self.iteration > 1:
-            self._replay(wsp, wsn)
-        else:
-            self.store.run(self._plan(wsp, wsn, zc, self._z_prev if apply_pending else None,
-                                      update=apply_pending or not self.mgr.oracle))
-        wss = [wsp, wsn]
-        if self._stacked_ok(wsp):
-            wss.append(self.store.stacked_workspace(wsp.batch, wsp.seq))
         try:
-            st = _finish_record(self.store, wss, self.iteration, seed)
+            if self.graph and self.iteration > 1:
+                st = self._step_graph_io(batch, seed, apply_pending)
+                zc = None
+            else:
+                wsp, wsn = _stage_batch(self.store, batch)
+                zc = _oracle_z(self.mgr, seed, self.store.total_params, self.store.device) if self.mgr.oracle else None
+                _write_scal(self.store, seed, pending=apply_pending)
+                self.store.run(self._plan(wsp, wsn, zc, self._z_prev if apply_pending else None,
+                                          update=apply_pending or not self.mgr.oracle))
+                st = _finish_record(self.store, self._io_wss(wsp, wsn), self.iteration, seed)
         except NumericError:
             # the step's pass consumed the pending update and the device did
             # not arm a new one (zo_grad_finalize gates on a finite g), so
