@@ -30,7 +30,7 @@ import torch
 
 from . import _lib as L
 from .engine import MINUS, PLUS, DeviceStore
-from .errors import ConfigurationError, ConsistencyError, NumericError, ProtocolError
+from .errors import ConfigurationError, ConsistencyError, DimensionError, NumericError, ProtocolError
 from .model import Batch
 from .rng import RngStateManager
 from .zo import ZoHyper, ZoStep, _finish_record, _u64_as_i64
@@ -117,7 +117,8 @@ class MeshZo:
         self.iteration, self._pending, self._g_prev, self.last_seed = 0, False, 0.0, None
         self._zc = self._zp = None
         self.graph = bool(graph) and not self.mgr.oracle and getattr(fabric, "backend", None) == "nccl"
-        self._graph = None
+        self._graphs = {}          # io flag -> captured step
+        self._io = None
 
     @property
     def g_prev(self) -> float:
@@ -154,17 +155,74 @@ class MeshZo:
                        float(self.hyper.lr), s.scal.data_ptr(), s.record.data_ptr(), L.stream_ptr())))
         return calls
 
-    def replay(self):
+    def replay(self, io: bool = False):
         """Capture the Philox step once (the first step ran eagerly, so the
         NCCL communicator, kernel attributes and TMA descriptors exist), then
         replay it; seeds / pending flag / g live on the device, so one graph
-        serves every step."""
-        if self._graph is None:
+        serves every step.  io=True (the public step): the graph also copies
+        the shard / seed / pending flag in from pinned staging and the record /
+        error flags out (zo_copy_async nodes)."""
+        g = self._graphs.get(io)
+        if g is None:
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g, capture_error_mode="thread_local"):
-                self.store.run(self.step_calls())
-            self._graph = g
-        self._graph.replay()
+                calls = self.step_calls()
+                if io:
+                    cin, cout = self._io_calls()
+                    calls = cin + calls + cout
+                self.store.run(calls)
+            self._graphs[io] = g
+        g.replay()
+
+    def _io_bufs(self):
+        ws0 = next(iter(self.ws.values()))
+        io = self._io
+        if io is None or io["M"] != ws0.M:
+            io = self._io = {"M": ws0.M,
+                             "ids": torch.empty(2, ws0.M, dtype=torch.int32, pin_memory=True),
+                             "scal": torch.zeros(2, dtype=torch.int64, pin_memory=True),
+                             "rec": torch.zeros(3, dtype=torch.float64, pin_memory=True),
+                             "err": torch.zeros(4, dtype=torch.int32, pin_memory=True)}
+        return io
+
+    def _io_calls(self):
+        s, lib, st = self.store, L.lib(), L.stream_ptr()
+        io = self._io_bufs()
+        nb = 4 * io["M"]
+        cin, seen = [], set()
+        for ws in self.ws.values():                # the directions' workspaces may share ids / targets
+            if ws.ids.data_ptr() in seen:
+                continue
+            seen.add(ws.ids.data_ptr())
+            cin += [(lib.zo_copy_async, (ws.ids.data_ptr(), io["ids"].data_ptr(), nb, st)),
+                    (lib.zo_copy_async, (ws.tgt.data_ptr(), io["ids"].data_ptr() + nb, nb, st))]
+        cin += [(lib.zo_copy_async, (s.scal.data_ptr(), io["scal"].data_ptr(), 8, st)),
+                (lib.zo_copy_async, (s.scal.data_ptr() + 24, io["scal"].data_ptr() + 8, 8, st))]
+        cout = [(lib.zo_copy_async, (io["rec"].data_ptr(), s.record.data_ptr(), 24, st))]
+        for i, ws in enumerate(self.ws.values()):
+            cout.append((lib.zo_copy_async, (io["err"].data_ptr() + 4 * i, ws.err.data_ptr(), 4, st)))
+        return cin, cout
+
+    def _step_graph_io(self, shard: Batch, seed: int) -> ZoStep:
+        s = self.store
+        shard.validate(s.config)
+        ids, tg = np.asarray(shard.token_ids), np.asarray(shard.targets)
+        ws0 = next(iter(self.ws.values()))
+        if ids.shape != (ws0.batch, ws0.seq) or tg.shape != ids.shape:
+            raise DimensionError(f"batch shape {ids.shape} does not match workspace ({ws0.batch}, {ws0.seq})")
+        if ids.size and (ids.min() < 0 or ids.max() >= s.config.vocab_size):
+            raise DimensionError("token id out of embedding range")
+        io = self._io_bufs()
+        h = io["ids"].numpy()
+        h[0] = ids.reshape(-1)
+        h[1] = tg.reshape(-1)
+        io["scal"].numpy()[:] = (_u64_as_i64(seed), 1 if self._pending else 0)
+        self.replay(io=True)
+        torch.cuda.current_stream().synchronize()
+        wss = list(self.ws.values())
+        s.check_errors(*wss, flags=[int(v) for v in io["err"].numpy()[:len(wss)]])
+        r = io["rec"].numpy()
+        return ZoStep(self.iteration, seed, float(r[0]), float(r[1]), float(r[2]))
 
     def stage(self, shard: Batch):
         shard.validate(self.store.config)
@@ -175,20 +233,20 @@ class MeshZo:
         """Lazy step: applies the previous iteration's update (folded), then
         this iteration's directional forward(s), loss exchange and g."""
         self.iteration += 1
-        self.stage(shard)
         s = self.store
-        s.scal[0:1].fill_(_u64_as_i64(seed))
-        s.scal[3:4].fill_(1 if self._pending else 0)
-        if self.mgr.oracle:
-            self._zp = self._zc if self._pending else None
-            self.mgr.reset(seed)
-            self._zc = torch.from_numpy(self.mgr.generator(seed).standard_normal(s.total_params)).to(s.device)
-        if self.graph and self.iteration > 1:
-            self.replay()
-        else:
-            s.run(self.step_calls(update=not self.mgr.oracle or self._zp is not None, zc=self._zc, zp=self._zp))
         try:
-            st = _finish_record(s, list(self.ws.values()), self.iteration, seed)
+            if self.graph and self.iteration > 1:
+                st = self._step_graph_io(shard, seed)
+            else:
+                self.stage(shard)
+                s.scal[0:1].fill_(_u64_as_i64(seed))
+                s.scal[3:4].fill_(1 if self._pending else 0)
+                if self.mgr.oracle:
+                    self._zp = self._zc if self._pending else None
+                    self.mgr.reset(seed)
+                    self._zc = torch.from_numpy(self.mgr.generator(seed).standard_normal(s.total_params)).to(s.device)
+                s.run(self.step_calls(update=not self.mgr.oracle or self._zp is not None, zc=self._zc, zp=self._zp))
+                st = _finish_record(s, list(self.ws.values()), self.iteration, seed)
         except NumericError:
             self._pending, s.unflushed = False, False     # nothing armed (see StreamingZo.step)
             raise
