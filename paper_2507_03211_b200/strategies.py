@@ -33,7 +33,8 @@ from .engine import MINUS, PLUS, DeviceStore
 from .errors import ConfigurationError, ConsistencyError, DimensionError, NumericError, ProtocolError
 from .model import Batch
 from .rng import RngStateManager
-from .zo import ZoHyper, ZoStep, _finish_record, _u64_as_i64
+from .zo import (NativeGraph, ZoHyper, ZoStep, _block_events, _finish_record, _priority_streams, _record,
+                 _record_and_wait, _u64_as_i64, _wait)
 
 PLUS_DIR, MINUS_DIR = +1, -1
 
@@ -99,11 +100,17 @@ class MeshZo:
     is the launch plan the benchmark replays."""
 
     def __init__(self, store: DeviceStore, hyper: ZoHyper, fabric, strategy: str, batch: int, seq: int,
-                 mgr: RngStateManager | None = None, graph: bool = True):
+                 mgr: RngStateManager | None = None, graph: bool = True, overlap: str = "fill"):
         """graph: from the second step on, replay the step's launches -- the
         fused pass, the forward(s), the NCCL loss all-gather and the ordered
         g reduction -- from one captured CUDA graph (NCCL fabrics only: a
-        gloo collective stages through the host and cannot be captured)."""
+        gloo collective stages through the host and cannot be captured).
+        overlap: "fill" (Philox runs) perturbs blocks 2.. as short-CTA
+        launches on a low-priority stream under the high-priority forward,
+        as StreamingZo's fill plan; "none": the whole pass, then the forward.
+        Same arithmetic either way."""
+        if overlap not in ("fill", "none"):
+            raise ConfigurationError(f"unknown step plan {overlap!r} (plans: 'fill', 'none')")
         self.store, self.hyper, self.fabric = store, hyper.validate(), fabric
         self.mesh = MeshLayout(strategy, fabric.k, fabric.rank)
         for s in self.mesh.dirs:
@@ -116,6 +123,7 @@ class MeshZo:
         self.gathered = torch.zeros(2 * fabric.k, dtype=torch.float64, device=dev)
         self.iteration, self._pending, self._g_prev, self.last_seed = 0, False, 0.0, None
         self._zc = self._zp = None
+        self.overlap = overlap if not self.mgr.oracle else "none"
         self.graph = bool(graph) and not self.mgr.oracle and getattr(fabric, "backend", None) == "nccl"
         self._graphs = {}          # io flag -> captured step
         self._io = None
@@ -143,16 +151,49 @@ class MeshZo:
         if MINUS in m.dirs:
             flags |= L.ZO_PU_SHADOW_B
             sb, sc_b = MINUS, -eps
-        calls = s.perturb_call(s.model_table, flags, sc_a, sc_b, sa=sa, sb=sb, zmode=zmode, z_cur=zc, z_prev=zp)
-        for d in m.dirs:
-            loss_out = self.local.data_ptr() + 8 * d
-            calls += s.forward_calls(d, self.ws[d], +eps if d == PLUS else -eps, zmode=zmode, z_cur=zc,
-                                     loss_out=loss_out)
+        if self.overlap == "fill" and zmode == L.ZO_Z_PHILOX:
+            calls = self._fill_calls(flags, sa, sb, sc_a, sc_b)
+        else:
+            calls = s.perturb_call(s.model_table, flags, sc_a, sc_b, sa=sa, sb=sb, zmode=zmode, z_cur=zc,
+                                   z_prev=zp)
+            for d in m.dirs:
+                loss_out = self.local.data_ptr() + 8 * d
+                calls += s.forward_calls(d, self.ws[d], +eps if d == PLUS else -eps, zmode=zmode, z_cur=zc,
+                                         loss_out=loss_out)
         calls.append((_gather, (self.fabric, self.gathered, self.local)))
         sp, op, sm, om = m.layout
         calls.append((L.lib().zo_grad_finalize_groups,
                       (self.gathered.data_ptr(), m.n_groups, sp, op, sm, om, m.group, float(eps),
                        float(self.hyper.lr), s.scal.data_ptr(), s.record.data_ptr(), L.stream_ptr())))
+        return calls
+
+    def _fill_calls(self, flags, sa, sb, sc_a, sc_b):
+        """The fused pass of the embedding + block 1 on the high-priority
+        stream, blocks 2.. as ZO_PU_FILL launches on the low-priority stream
+        (one event per block), this rank's forward(s) on the high-priority
+        stream waiting for each block's event; both streams join the caller's
+        stream before the loss exchange (StreamingZo.fill_step_calls)."""
+        s, eps = self.store, self.hyper.epsilon
+        nl = len(s.layouts)
+        main = torch.cuda.current_stream()
+        hi, lo = _priority_streams(s)
+        ev = _block_events(s, nl + 3)
+        calls = [(_record_and_wait, (ev[nl], main, hi)), (_wait, (lo, ev[nl]))]
+        if getattr(s, "_fill_head", None) is None:
+            s._fill_head = s.range_table(0, 2)          # built once, outside any graph capture
+        calls += s.perturb_call(s._fill_head, flags, sc_a, sc_b, sa=sa, sb=sb, stream=hi)
+        for b in range(2, nl):
+            calls += s.perturb_call(s.block_tables[b], flags | L.ZO_PU_FILL, sc_a, sc_b, sa=sa, sb=sb, stream=lo)
+            calls.append((_record, (ev[b], lo)))
+        for i, d in enumerate(self.mesh.dirs):
+            sc, loss_out = (+eps if d == PLUS else -eps), self.local.data_ptr() + 8 * d
+            calls += s.forward_calls(d, self.ws[d], sc, stream=hi, blocks=[0, 1], loss_out=loss_out)
+            for b in range(2, nl):
+                if i == 0:
+                    calls.append((_wait, (hi, ev[b])))
+                calls += s.forward_calls(d, self.ws[d], sc, stream=hi, blocks=[b], loss_out=loss_out)
+        calls.append((_record_and_wait, (ev[nl + 1], hi, main)))
+        calls.append((_record_and_wait, (ev[nl + 2], lo, main)))
         return calls
 
     def replay(self, io: bool = False):
@@ -164,13 +205,19 @@ class MeshZo:
         error flags out (zo_copy_async nodes)."""
         g = self._graphs.get(io)
         if g is None:
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g, capture_error_mode="thread_local"):
+            def build():
                 calls = self.step_calls()
                 if io:
                     cin, cout = self._io_calls()
                     calls = cin + calls + cout
-                self.store.run(calls)
+                return calls
+
+            if self.overlap == "fill":
+                g = NativeGraph(self.store.run, build)          # replays with launch priorities
+            else:
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, capture_error_mode="thread_local"):
+                    self.store.run(build())
             self._graphs[io] = g
         g.replay()
 
