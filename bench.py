@@ -71,6 +71,8 @@ def _args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-cpu-full", action="store_true", help="skip the one full (unsampled) CPU reference step")
     ap.add_argument("--offload", default="on", choices=["on", "off"])
+    ap.add_argument("--offload-timeout", type=float, default=900.0,
+                    help="seconds after which a still-running offload leg is reported as an error")
     ap.add_argument("--offload-model", default="opt-13b")
     ap.add_argument("--offload-seq", type=int, default=2048)
     ap.add_argument("--offload-steps", type=int, default=3)
@@ -476,11 +478,9 @@ def ours(args, rank, world, local_rank):
     torch.cuda.synchronize()
     torch.cuda.empty_cache()
 
-    offload = None
-    if args.offload == "on":
-        offload = offload_leg(args, rank, world, local_rank)
-
     if rank != 0:
+        if args.offload == "on":
+            _guarded_offload(args, rank, world, local_rank, None)
         return
     hbm, tf_sus, tf_burst, peak_kind = _peaks()
     headline = (args.model, T, args.batch, args.arch, world) == (MODEL, SEQ, BATCH, "zosim", 1)
@@ -537,8 +537,8 @@ def ours(args, rank, world, local_rank):
                 "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
         "last_step": {"loss_pos": float(rec[0]), "loss_neg": float(rec[1]), "g": float(rec[2])},
     }
-    if offload is not None:
-        line["offload"] = offload
+    if args.offload == "on":
+        line["offload"] = _guarded_offload(args, rank, world, local_rank, line)
     if world == 1 and not args.no_cpu_baseline and args.arch == "zosim":
         s = cpu_reference_sample(cfg, B)
         line["cpu_baseline"] = {"value": s["tokens_per_s"], "unit": "tokens/s", "cores": s["cores"], "kind": "port",
@@ -555,6 +555,30 @@ def ours(args, rank, world, local_rank):
 # ----------------------------------------------------------------------------
 # our arm: the offload leg (configs #4 / #5 at a shape every box can hold)
 # ----------------------------------------------------------------------------
+def _guarded_offload(args, rank, world, local_rank, line) -> dict:
+    """The offload leg must not cost the headline line: an exception becomes
+    {"error": ...}, and a leg still running after --offload-timeout seconds
+    (e.g. a collective that never completes) makes rank 0 print the line with
+    {"error": "timeout"} and every rank exit."""
+    import threading
+
+    def expire():
+        if line is not None:
+            line["offload"] = {"error": f"offload leg did not finish within {args.offload_timeout} s"}
+            print(json.dumps(line), flush=True)
+        os._exit(0)
+
+    t = threading.Timer(args.offload_timeout, expire)
+    t.daemon = True
+    t.start()
+    try:
+        return offload_leg(args, rank, world, local_rank)
+    except Exception as e:                       # noqa: BLE001 (reported in the line)
+        return {"error": f"{type(e).__name__}: {e}"[:400]}
+    finally:
+        t.cancel()
+
+
 def offload_leg(args, rank, world, local_rank) -> dict | None:
     affinity = os.sched_getaffinity(0)          # the NUMA binding below is undone on return
     try:
