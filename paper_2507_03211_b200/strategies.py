@@ -212,9 +212,16 @@ class MeshZo:
                     calls = cin + calls + cout
                 return calls
 
+            g = None
             if self.overlap == "fill":
-                g = NativeGraph(self.store.run, build)          # replays with launch priorities
-            else:
+                try:
+                    g = NativeGraph(self.store.run, build)      # replays with launch priorities
+                except Exception:                               # noqa: BLE001
+                    # a communicator that refuses a raw stream capture: torch's
+                    # capture (node priorities dropped, same launches)
+                    torch.cuda.synchronize()
+                    g = None
+            if g is None:
                 g = torch.cuda.CUDAGraph()
                 with torch.cuda.graph(g, capture_error_mode="thread_local"):
                     self.store.run(build())
