@@ -512,7 +512,7 @@ def ours(args, rank, world, local_rank):
               "algorithmic": (f"R+W fp32 master (8 B) + the bf16 / fp32 shadows this rank writes, per parameter "
                               f"(embedding: no shadow, 8 B): {pert_bytes} B over {P} params, one launch per step")}
     r_attn = roof("attention", "tensor", "TFLOP/s", tf_sus, 1e12, "2*B*T^2*d per launch (causal halves of QK^T, PV)",
-                  "attn_tc_kernel (tcgen05)")
+                  "attn_pp_kernel (tcgen05, hd 64; attn_tc_kernel<128> at hd 128)")
     r_ln = roof("layernorm", "hbm", "GB/s", hbm, 1e9, "4 B read + 2 B write per element", "layernorm_warp_kernel")
     dominant = max([r for r in (r_gemm, r_pert) if r], key=lambda r: r["share_of_step"])
     line = {
