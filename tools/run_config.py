@@ -5,6 +5,7 @@ for configs #3-#5; the bench line is config #2).
     python tools/run_config.py offload  opt-66b 2048 1      # ZO2 schedule, host master, 3 slots
     python tools/run_config.py sharded  opt-13b 2048 1      # same schedule, fp32 master in HBM (1 rank)
     python tools/run_config.py offload:20 opt-13b 2048 1    # 20 of 40 blocks resident, the rest streamed
+    python tools/run_config.py resident opt-175b/4 2048 1   # 4 decoder blocks of the OPT-175B shape
 """
 import json
 import sys
@@ -22,7 +23,13 @@ from paper_2507_03211_b200.rng import iteration_seeds  # noqa: E402
 def main():
     mode, name, T, B = sys.argv[1], sys.argv[2], int(sys.argv[3]), int(sys.argv[4])
     steps = int(sys.argv[5]) if len(sys.argv) > 5 else 4
-    cfg = opt_config(name, T)
+    if "/" in name:          # "<shape>/<n>": n decoder blocks of that shape (per-block rates of 66B / 175B)
+        import dataclasses
+
+        base, nb = name.split("/")
+        cfg = dataclasses.replace(opt_config(base, T), n_blocks=int(nb)).validate()
+    else:
+        cfg = opt_config(name, T)
     hyper = zo.ZoHyper(1e-3, 1e-7)
     t0 = time.time()
     if mode == "resident":
