@@ -532,3 +532,36 @@ def nccl_world1_worker(rank, world, port, q):
     out["phases"] = sorted(rt.phase_stats)
     dist.destroy_process_group()
     q.put((rank, out))
+
+
+def mesh_plan_worker(rank, world, port, strategy, overlap, steps, q):
+    """MeshZo lazy steps (gloo, ranks sharing cuda:0) under one step plan:
+    records and the flushed master, for the fill == serial check."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2507_03211_b200 import ops
+    from paper_2507_03211_b200.engine import DeviceStore
+    from paper_2507_03211_b200.fabric import TorchFabric
+    from paper_2507_03211_b200.model import ModelConfig, make_batch
+    from paper_2507_03211_b200.rng import iteration_seeds
+    from paper_2507_03211_b200.strategies import MeshZo
+    from paper_2507_03211_b200.zo import ZoHyper
+
+    torch.cuda.set_device(0)
+    init(rank, world, port)
+    fab = TorchFabric()
+    cfg = ModelConfig(*DEEP, "f32")
+    store = DeviceStore(cfg, 7)
+    n_groups = world // 2 if strategy == "2d" else (1 if strategy == "pertp" else world)
+    B = 2
+    mz = MeshZo(store, ZoHyper(1e-3, 1e-2), fab, strategy, B, cfg.seq_len, overlap=overlap)
+    recs = []
+    for j, s in enumerate(iteration_seeds(13, steps), 1):
+        b = make_batch(cfg, B * n_groups, 70 + j).shard(n_groups, mz.mesh.group)
+        r = mz.step(b, s)
+        recs.append((r.loss_pos, r.loss_neg, r.g))
+    mz.flush()
+    h = int(ops.hash_u64(store.theta).item())
+    dist.destroy_process_group()
+    q.put((rank, recs, h))

@@ -153,3 +153,15 @@ def test_mesh_teacher_forced_reproduces_reference_checksum(strategy, world):
     res = H.run(H.mesh_golden_worker, world, strategy, "f32", True, _golden_path())
     for r in res:
         assert r[3] == r[4], (strategy, r[0])
+
+
+@pytest.mark.parametrize("strategy,world", [("pertp", 2), ("2d", 4)])
+def test_mesh_fill_plan_equals_serial_plan(strategy, world):
+    """MeshZo's fill plan (blocks 2.. perturbed on a low-priority stream under
+    the forward) gives the serial plan's records and
+    flushed master bit for bit on every rank."""
+    fill = H.run(H.mesh_plan_worker, world, strategy, "fill", 3)
+    ser = H.run(H.mesh_plan_worker, world, strategy, "none", 3)
+    for a, b in zip(sorted(fill), sorted(ser)):
+        assert a[1] == b[1] and a[2] == b[2], (a, b)
+    assert len({r[2] for r in fill}) == 1          # identical replicas
