@@ -292,6 +292,9 @@ def reference_arm(args, rank, world):
 # ----------------------------------------------------------------------------
 # our arm: the resident headline step
 # ----------------------------------------------------------------------------
+MIX_CEILING_GBS = 5652.0   # read 4 B + write 4 + 2 + 2 B per element, no arithmetic (profiles/r02/mix_probe/)
+
+
 def _kernel_kind(name: str) -> str:
     if name.startswith("zo_gemm"):
         return "gemm"
@@ -509,6 +512,10 @@ def ours(args, rank, world, local_rank):
               "traffic": traffic.get("perturb_bytes_per_step", traffic.get("perturb_bytes_per_launch")),
               "traffic_algorithmic": pert_bytes,
               "peak_kind": f"{peak_kind} HBM copy", "share_of_step": pert_ms / ms,
+              # the pure-memory ceiling of this exact R4/W4/W2/W2 mix, measured on this pool's B200s
+              # (tools/mix_probe.cu, profiles/r02/mix_probe/): the pass's own bandwidth roof
+              "mix_ceiling_gbs": MIX_CEILING_GBS,
+              "frac_of_mix_ceiling": pert_bytes / (pert_ms * 1e-3) / 1e9 / MIX_CEILING_GBS,
               "algorithmic": (f"R+W fp32 master (8 B) + the bf16 / fp32 shadows this rank writes, per parameter "
                               f"(embedding: no shadow, 8 B): {pert_bytes} B over {P} params, one launch per step")}
     r_attn = roof("attention", "tensor", "TFLOP/s", tf_sus, 1e12, "2*B*T^2*d per launch (causal halves of QK^T, PV)",
