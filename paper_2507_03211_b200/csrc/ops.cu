@@ -128,6 +128,62 @@ __global__ void layernorm_kernel(const float* __restrict__ x, int64_t ldx, const
     orow[c] = __float2bfloat16_rn(fmaf((srow[c] - mu) * rstd, g[c], b[c]));
 }
 
+// Wide rows (4096 < d <= 1024 NV: the 13B / 66B / 175B widths): one CTA of 256
+// threads per row, NV float4 per thread kept in registers (one pass over
+// memory), the two statistics by warp shuffles + a fixed-order sum of the 8
+// warp partials.  (The smem kernel above re-reads the row from shared memory
+// and ran at ~0.2 of HBM at d = 5120.)
+template <int NV>
+__global__ void __launch_bounds__(256) layernorm_row_kernel(const float* __restrict__ x, int64_t ldx,
+                                                            const float* __restrict__ g,
+                                                            const float* __restrict__ b, int d,
+                                                            __nv_bfloat16* __restrict__ out, int64_t ldo,
+                                                            const float* __restrict__ g2,
+                                                            const float* __restrict__ b2, int64_t row_split) {
+  __shared__ float red[8];
+  pdl_trigger();
+  pdl_wait();
+  const int64_t r = blockIdx.x;
+  if (row_split && r >= row_split) { g = g2; b = b2; }   // stacked +eps / -eps rows
+  const float4* xr = reinterpret_cast<const float4*>(x + r * ldx);
+  float4 v[NV];
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const int c = (i * 256 + threadIdx.x) * 4;
+    v[i] = c < d ? xr[i * 256 + threadIdx.x] : make_float4(0.f, 0.f, 0.f, 0.f);
+    s += (v[i].x + v[i].y) + (v[i].z + v[i].w);
+  }
+  const float mu = block_sum(s, red) / (float)d;
+  float q = 0.f;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const int c = (i * 256 + threadIdx.x) * 4;
+    if (c < d) {
+      const float a0 = v[i].x - mu, a1 = v[i].y - mu, a2 = v[i].z - mu, a3 = v[i].w - mu;
+      q += (a0 * a0 + a1 * a1) + (a2 * a2 + a3 * a3);
+    }
+  }
+  const float rstd = 1.0f / sqrtf(block_sum(q, red) / (float)d + 1e-5f);
+  __nv_bfloat16* orow = out + r * ldo;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const int c = (i * 256 + threadIdx.x) * 4;
+    if (c < d) {
+      const float4 gg = *reinterpret_cast<const float4*>(g + c);
+      const float4 bb = *reinterpret_cast<const float4*>(b + c);
+      __nv_bfloat162 lo = __floats2bfloat162_rn(fmaf((v[i].x - mu) * rstd, gg.x, bb.x),
+                                                fmaf((v[i].y - mu) * rstd, gg.y, bb.y));
+      __nv_bfloat162 hi = __floats2bfloat162_rn(fmaf((v[i].z - mu) * rstd, gg.z, bb.z),
+                                                fmaf((v[i].w - mu) * rstd, gg.w, bb.w));
+      uint2 pk;
+      pk.x = *reinterpret_cast<uint32_t*>(&lo);
+      pk.y = *reinterpret_cast<uint32_t*>(&hi);
+      *reinterpret_cast<uint2*>(orow + c) = pk;
+    }
+  }
+}
+
 // Warp-per-row variant for d <= 32*4*NV: the row lives in registers as float4,
 // statistics via warp shuffles only (no block barriers); 8 rows per CTA.
 template <int NV>
@@ -211,6 +267,17 @@ int layernorm_launch(const float* x, int64_t ldx, const float* g, const float* b
   }
     ZO_LN_CASE(1) ZO_LN_CASE(2) ZO_LN_CASE(4) ZO_LN_CASE(8) ZO_LN_CASE(16) ZO_LN_CASE(32)
 #undef ZO_LN_CASE
+  }
+  if (vec && d <= 12288) {
+    const int nv = (int)((d + 1023) / 1024);
+#define ZO_LN_ROW(N)                                                                                  \
+  if (nv <= N) {                                                                                      \
+    launch_k(layernorm_row_kernel<N>, dim3((unsigned)rows), dim3(256), 0, st, x, ldx, g, b, (int)d, out, ldo, \
+             g2, b2, row_split);                                                                      \
+    return launch_status("layernorm_row_kernel");                                                     \
+  }
+    ZO_LN_ROW(5) ZO_LN_ROW(6) ZO_LN_ROW(8) ZO_LN_ROW(9) ZO_LN_ROW(10) ZO_LN_ROW(12)
+#undef ZO_LN_ROW
   }
   const size_t smem = (size_t)d * sizeof(float);
   static bool big_smem = false;

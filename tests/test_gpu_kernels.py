@@ -157,8 +157,9 @@ def test_gemm_split_equals_two_gemms(M, N, K):
                                        0, 0, 0, 0, L.stream_ptr()))
 
 
-def test_layernorm_split_equals_two_layernorms():
-    rows, d = 512, 2048
+@pytest.mark.parametrize("d", [2048, 5120])
+def test_layernorm_split_equals_two_layernorms(d):
+    rows = 512
     x = _rand(rows, d, dtype=torch.float32, seed=47)
     g1, b1, g2, b2 = (_rand(d, dtype=torch.float32, seed=s) for s in (48, 49, 50, 51))
     got = torch.empty(rows, d, device=DEV, dtype=torch.bfloat16)
@@ -209,7 +210,7 @@ def test_gemm_multiwave_epilogues(M, N, K):
     assert err.item() == 0 and abs(loss.item() - cref.item()) < 1e-3
 
 
-@pytest.mark.parametrize("rows,d", [(64, 768), (513, 2048), (7, 6), (3, 12288)])
+@pytest.mark.parametrize("rows,d", [(64, 768), (513, 2048), (7, 6), (3, 12288), (65, 5120), (9, 9216), (4, 7168)])
 def test_layernorm(rows, d):
     x = _rand(rows, d, dtype=torch.float32, seed=13) * 3 + 1
     g = _rand(d, dtype=torch.float32, seed=14)
