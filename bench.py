@@ -83,9 +83,15 @@ def _args():
 
 
 def _config(args):
+    """--model <shape> or <shape>/<n>: n decoder blocks of that shape (per-block
+    rates of shapes whose full model does not fit one GPU, e.g. opt-175b/4)."""
+    import dataclasses
+
     from paper_2507_03211_b200.model import opt_config, real_opt_config
 
-    return real_opt_config(args.model, args.seq) if args.arch == "opt" else opt_config(args.model, args.seq)
+    name, _, nb = args.model.partition("/")
+    cfg = real_opt_config(name, args.seq) if args.arch == "opt" else opt_config(name, args.seq)
+    return dataclasses.replace(cfg, n_blocks=int(nb)).validate() if nb else cfg
 
 
 # ----------------------------------------------------------------------------
