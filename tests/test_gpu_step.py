@@ -487,3 +487,24 @@ def test_bf16_production_g_relative_bound_at_eps_1e2(name):
         assert abs(got.loss_pos - lp) <= 2e-3 and abs(got.loss_neg - ln) <= 2e-3
     print(f"eps=1e-2 {name}: worst relative g error {worst:.3%}")
     assert worst <= 0.10, worst
+
+
+def test_hd128_production_path_matches_oracle():
+    """Head dim 128 -- the attention kernel of the 13B / 66B / 175B shapes
+    (attn_tc_kernel<128>) -- through the shipped bf16 step with the
+    reference's z, against the oracle: losses within the bf16 bound and g
+    within 10% relative with the oracle's sign at eps = 1e-2, each step started
+    from the reference's weights (teacher forcing)."""
+    cfg = ModelConfig(256, 256, 2, 2, 128, "f32")
+    assert cfg.head_dim == 128
+    store = DeviceStore(cfg, init_seed=7)
+    om = _oracle_model(cfg)
+    eps = 1e-2
+    for j, s in enumerate(iteration_seeds(53, 3), 1):
+        ids, tg = O.synthetic_batch(cfg.vocab_size, cfg.seq_len, 2, 500 + j)
+        lp, ln, g = O.mezo_step(om, ids, tg, eps, LR, s)
+        got = zo.mezo_step(store, Batch(ids, tg), zo.ZoHyper(eps, LR), s, mgr=RngStateManager("oracle"))
+        assert abs(got.loss_pos - lp) <= 2e-3 and abs(got.loss_neg - ln) <= 2e-3, (j, got, lp, ln)
+        assert np.sign(got.g) == np.sign(g) and abs(got.g - g) <= 0.10 * abs(g), (j, got.g, g)
+        # teacher forcing: the next step starts from the reference's weights
+        store.theta.copy_(torch.from_numpy(np.concatenate(om.blocks)).to(store.theta.device))
