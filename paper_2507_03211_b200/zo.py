@@ -172,6 +172,7 @@ class StreamingZo:
         # step's scalars are device-resident, so the launches never change)
         self.graph = graph and not self.mgr.oracle
         self._graphs = {}
+        self._ios = {}             # batch rows -> pinned staging of the I/O-carrying graph
         self.iteration = 0
         self._g_prev = 0.0
         self.last_seed = None
@@ -300,13 +301,14 @@ class StreamingZo:
         """Pinned staging of the graph-carried step I/O for M = B*T rows:
         ids / targets in, (seed, pending) in, the ZoStep record and the
         workspaces' error flags out."""
-        io = getattr(self, "_io", None)
-        if io is None or io["M"] != wsp.M:
-            io = self._io = {"M": wsp.M,
-                             "ids": torch.empty(2, wsp.M, dtype=torch.int32, pin_memory=True),
-                             "scal": torch.zeros(2, dtype=torch.int64, pin_memory=True),
-                             "rec": torch.zeros(3, dtype=torch.float64, pin_memory=True),
-                             "err": torch.zeros(4, dtype=torch.int32, pin_memory=True)}
+        # one staging set per batch shape, alive as long as the graphs that captured its pointers
+        io = self._ios.get(wsp.M)
+        if io is None:
+            io = self._ios[wsp.M] = {"M": wsp.M,
+                                     "ids": torch.empty(2, wsp.M, dtype=torch.int32, pin_memory=True),
+                                     "scal": torch.zeros(2, dtype=torch.int64, pin_memory=True),
+                                     "rec": torch.zeros(3, dtype=torch.float64, pin_memory=True),
+                                     "err": torch.zeros(4, dtype=torch.int32, pin_memory=True)}
         return io
 
     def _io_wss(self, wsp, wsn):

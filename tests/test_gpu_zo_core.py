@@ -412,3 +412,26 @@ def test_estimator_second_order_in_epsilon_f32_mode():
     assert drift < 1e-25, drift          # updates below an ulp of the weights (zero-init biases move by ~1e-30)
     order = math.log2(np.mean(e_full) / np.mean(e_half))
     assert 1.8 <= order <= 2.2, (order, e_full, e_half)
+
+
+def test_graph_replay_with_changing_batch_shapes_matches_eager():
+    """The public step replays one I/O-carrying graph per batch shape (its own
+    pinned staging): alternating shapes, and coming back to an earlier one,
+    gives the eager executor's records and master bit for bit."""
+    cfg = ModelConfig(32, 32, 4, 2, 16, "f32")
+    shapes = [(2, 16), (1, 8), (2, 16), (4, 8), (1, 8), (2, 16)]
+    seeds = iteration_seeds(61, len(shapes))
+    runs = []
+    for graph in (True, False):
+        store = _store(cfg)
+        sz = zo.StreamingZo(store, HYPER, graph=graph)
+        recs = []
+        for j, ((b, t), s) in enumerate(zip(shapes, seeds), 1):
+            full = make_batch(cfg, b, 80 + j)
+            batch = type(full)(full.token_ids[:, :t], full.targets[:, :t])
+            r = sz.step(batch, s)
+            recs.append((r.loss_pos, r.loss_neg, r.g))
+        sz.flush()
+        runs.append((recs, _theta(store)))
+    assert runs[0][0] == runs[1][0]
+    assert np.array_equal(runs[0][1], runs[1][1])
