@@ -73,6 +73,8 @@ def _args():
     ap.add_argument("--offload", default="on", choices=["on", "off"])
     ap.add_argument("--offload-timeout", type=float, default=900.0,
                     help="seconds after which a still-running offload leg is reported as an error")
+    ap.add_argument("--offload-data-plane", default="collective", choices=["collective", "copy_engine"],
+                    help="N>1 offload leg: block slices over NCCL collectives or pulled by the copy engines (CUDA IPC)")
     ap.add_argument("--offload-model", default="opt-13b")
     ap.add_argument("--offload-seq", type=int, default=2048)
     ap.add_argument("--offload-steps", type=int, default=3)
@@ -637,13 +639,14 @@ def _offload_leg(args, rank, world, local_rank) -> dict | None:
         from paper_2507_03211_b200.sharded import ShardStore
 
         compress = "split16" if args.offload_compress == "auto" else args.offload_compress
-        fabric = TorchFabric()
+        fabric = TorchFabric(data_plane=args.offload_data_plane)
         host = ShardStore(cfg, fabric, init_seed=7, init="philox", device=dev, where="host")
         rt = OffloadedZo(host, hyper, batch=1, device=dev, fabric=fabric, strategy="2d", redistribute="bf16",
                          compress=compress, trace=True)
         schedule = (f"2D mesh ({world // 2} groups x 2 directions) + sliced offload: per-rank NUMA-local pinned "
                     f"slices (1/{world} of every block over each rank's PCIe link, comm.py:314-342), "
-                    f"direction-aware bf16 exchange over NVLink, compress={compress}")
+                    f"direction-aware bf16 exchange over NVLink ({args.offload_data_plane} data plane), "
+                    f"compress={compress}")
         n_groups, group, numa = world // 2, rank // 2, host.numa
     t_setup = time.perf_counter() - t_setup
     batches = [make_batch(cfg, n_groups, DATA_SEED * 1_000_003 + j).shard(n_groups, group)

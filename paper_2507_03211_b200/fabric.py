@@ -23,7 +23,7 @@ import numpy as np
 import torch
 import torch.distributed as dist
 
-from .errors import FabricFault
+from .errors import ConfigurationError, FabricFault
 
 
 def _payload_bytes(value) -> int:
@@ -41,11 +41,25 @@ def _payload_bytes(value) -> int:
 
 
 class TorchFabric:
-    """K processes with ordered, deterministic collectives."""
+    """K processes with ordered, deterministic collectives.
 
-    def __init__(self, group=None):
+    data_plane: "collective" moves the offload's block slices with NCCL
+    (all_gather_into_tensor / batched send-recv: SM-driven kernels);
+    "copy_engine" maps the peers' buffers once through CUDA IPC and has every
+    rank PULL the slices it needs with cudaMemcpyAsync -- the DMA copy engines,
+    so the transfer takes no SMs from the GEMMs it overlaps (option
+    b) -- between two host barriers per exchange.  Same bytes, same results."""
+
+    CE_MIN_BYTES = 64 << 10        # smaller payloads (the loss exchange) stay collective
+
+    def __init__(self, group=None, data_plane: str = "collective"):
         if not dist.is_initialized():
             raise FabricFault("torch.distributed is not initialised")
+        if data_plane not in ("collective", "copy_engine"):
+            raise ConfigurationError(f"data_plane must be 'collective' or 'copy_engine', got {data_plane!r}")
+        self.data_plane = data_plane
+        self._peer_storages: dict = {}
+        self.ce_exchanges = 0          # exchanges that went through the copy engines
         self.group = group
         self.rank = dist.get_rank(group)
         self.k = dist.get_world_size(group)
@@ -115,11 +129,59 @@ class TorchFabric:
             total += v
         return total / len(vals)
 
+    # -- copy-engine data plane -------------------------------------------------
+    def _use_ce(self, t: torch.Tensor) -> bool:
+        return (self.data_plane == "copy_engine" and self.k > 1 and t.is_cuda
+                and t.numel() * t.element_size() >= self.CE_MIN_BYTES
+                and not torch.cuda.is_current_stream_capturing())
+
+    def _peers_of(self, t: torch.Tensor) -> list:
+        """Every rank's storage corresponding to ``t``'s, as flat tensors of
+        t's dtype (rank order).  Collective on first use: the storages' CUDA
+        IPC handles are all-gathered; corresponding buffers are allocated in
+        the same order on every rank, so their views share storage offsets."""
+        st = t.untyped_storage()
+        key = st.data_ptr()
+        peers = self._peer_storages.get(key)
+        if peers is None:
+            from torch.multiprocessing.reductions import reduce_tensor
+
+            flat = torch.empty(0, dtype=t.dtype, device=t.device).set_(st)
+            fn, args = reduce_tensor(flat)
+            objs = [None] * self.k
+            dist.all_gather_object(objs, args, group=self.group)
+            peers = [flat if q == self.rank else fn(*objs[q]) for q in range(self.k)]
+            self._peer_storages[key] = peers
+        return peers
+
+    def _ce_pull(self, dst: torch.Tensor, pulls) -> None:
+        """pulls: (element range in dst, rank, source tensor) -- every rank has
+        written its part before the first barrier, and nobody reuses its buffer
+        before every rank has finished reading (second barrier)."""
+        self.ce_exchanges += 1
+        cur = torch.cuda.current_stream()
+        cur.synchronize()
+        dist.barrier(group=self.group)
+        for (a, b), src in pulls:
+            dst[a:b].copy_(src, non_blocking=True)        # cudaMemcpyAsync: a DMA copy engine
+        cur.synchronize()
+        dist.barrier(group=self.group)
+
     # -- device tensor gather (the step's loss exchange) ------------------------
     def all_gather_tensor(self, out: torch.Tensor, inp: torch.Tensor, tag: str) -> None:
         """out[k*n:(k+1)*n] = inp of rank k.  NCCL: in place on the GPU (no host
-        round trip, graph-capturable); gloo: staged through host memory."""
+        round trip, graph-capturable); gloo: staged through host memory;
+        copy-engine plane: pulled from the peers' buffers."""
         self._account("all_gather", tag, self.k, _payload_bytes(inp))
+        if self._use_ce(out):
+            n, r = inp.numel(), self.rank
+            mine = out[r * n:(r + 1) * n]
+            if inp.data_ptr() != mine.data_ptr():
+                mine.copy_(inp)
+            peers, off = self._peers_of(out), out.storage_offset()
+            self._ce_pull(out, [((q * n, (q + 1) * n), peers[q][off + q * n:off + (q + 1) * n])
+                                for q in range(self.k) if q != r])
+            return
         if self.backend == "nccl":
             dist.all_gather_into_tensor(out, inp, group=self.group)
             return
@@ -139,6 +201,12 @@ class TorchFabric:
         r, w, mine = self.rank, width, bufs[my_dir]
         self._account("exchange", tag, self.k, w * mine.element_size())   # own slice, as all_gather_tensor counts
         if self.k == 1:
+            return
+        if self._use_ce(mine):
+            peer_bufs = {d: self._peers_of(bufs[d]) for d in sorted(bufs)}    # symmetric registration
+            src, off = peer_bufs[my_dir], mine.storage_offset()
+            self._ce_pull(mine, [((q * w, (q + 1) * w), src[q][off + q * w:off + (q + 1) * w])
+                                 for q in range(self.k) if q != r])
             return
         if self.backend == "nccl":
             peer = (lambda q: q) if self.group is None else (lambda q: dist.get_global_rank(self.group, q))

@@ -256,6 +256,15 @@ def sliced_dir_worker(rank, world, port, redistribute, steps, sharded, compress,
     """OffloadedZo on the 2D mesh (one direction per rank) with the fp32
     all-gather or the direction-aware bf16 exchange, over a
     shared host master or an HBM-sharded one (gloo, one GPU)."""
+    _sliced_dir(rank, world, port, redistribute, steps, sharded, compress, strategy, q, "collective")
+
+
+def sliced_dir_ce_worker(rank, world, port, redistribute, steps, sharded, strategy, q):
+    """The same over the copy-engine data plane (CUDA IPC pulls)."""
+    _sliced_dir(rank, world, port, redistribute, steps, sharded, "none", strategy, q, "copy_engine")
+
+
+def _sliced_dir(rank, world, port, redistribute, steps, sharded, compress, strategy, q, data_plane):
     import torch
     import torch.distributed as dist
 
@@ -268,7 +277,8 @@ def sliced_dir_worker(rank, world, port, redistribute, steps, sharded, compress,
 
     torch.cuda.set_device(0)
     init(rank, world, port)
-    fab = TorchFabric()
+    fab = TorchFabric(data_plane=data_plane)
+    fab.CE_MIN_BYTES = 0           # the test model's slices are small: exercise the copy engines anyway
     cfg = ModelConfig(*DEEP, "f32")
     path = f"/dev/shm/zo_b200_test_{port}"
     if sharded:
@@ -289,6 +299,7 @@ def sliced_dir_worker(rank, world, port, redistribute, steps, sharded, compress,
         recs.append((r.loss_pos, r.loss_neg, r.g))
     nbytes = dict(fab.bytes_by_tag)
     nbytes["pcie"] = rt.pcie_bytes_per_step()
+    nbytes["ce_exchanges"] = fab.ce_exchanges
     rt.flush()
     torch.cuda.synchronize()
     fab.barrier()

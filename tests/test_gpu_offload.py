@@ -451,3 +451,20 @@ def test_no_slots_when_every_block_is_resident():
     P = 12 * 32 * 32 + 13 * 32                    # one DEEP transformer block
     with pytest.raises(MemoryCapacityError):
         plan_residency(DEEP, int(1.5 * P * 8))
+
+
+@pytest.mark.parametrize("redistribute,world,sharded", [("fp32", 2, False), ("bf16", 2, False), ("bf16", 4, True),
+                                                        ("fp32", 4, True)])
+def test_copy_engine_data_plane_equals_collective(redistribute, world, sharded):
+    """The copy-engine data plane (peers' slot / staging buffers mapped once
+    through CUDA IPC, slices pulled with cudaMemcpyAsync between two host
+    barriers) moves the same bytes as the collective plane: records and the
+    flushed master bit for bit, fp32 all-gather and bf16 exchange, host or
+    HBM-sharded master (gloo ranks sharing one GPU)."""
+    a = H.run(H.sliced_dir_worker, world, redistribute, 3, sharded, "none", "2d")
+    b = H.run(H.sliced_dir_ce_worker, world, redistribute, 3, sharded, "2d")
+    for x, y in zip(a, b):
+        assert x[1] == y[1]
+        assert np.array_equal(x[2], y[2])
+        assert x[3]["param"] == y[3]["param"]          # same accounted bytes
+        assert x[3]["ce_exchanges"] == 0 and y[3]["ce_exchanges"] > 0
