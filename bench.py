@@ -368,9 +368,7 @@ def ours(args, rank, world, local_rank):
     tgt_dev = torch.stack([torch.from_numpy(b.targets.reshape(-1).astype(np.int32)) for b in batches]).to(dev)
     n_launch = sum(2 if fn.__name__ == "zo_ce_finalize" else 1 for fn, _ in step_calls if fn.__name__.startswith("zo_"))
     streams = {int(torch.cuda.current_stream().cuda_stream): torch.cuda.current_stream()}
-    if hasattr(store, "_side"):
-        streams[int(store._side.cuda_stream)] = store._side
-    for st_ in getattr(store, "_prio", None) or ():
+    for st_ in store.plan_streams():
         streams[int(st_.cuda_stream)] = st_
 
     use_graph = not args.no_graph and (world == 1 or runner.graph)     # (a gloo mesh cannot be captured)

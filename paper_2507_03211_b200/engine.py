@@ -244,6 +244,8 @@ class DeviceStore:
         self.scal = torch.zeros(4, dtype=torch.int64, device=self.device)   # ZoStepScalars
         self.record = torch.zeros(3, dtype=torch.float64, device=self.device)
         self._ws = {}
+        # launch resources of the step plans, created on first use (outside graph captures)
+        self._side = self._prio = self._events = self._head_table = None
 
     # -- initialisation at scale -----------------------------------------------
     def _init_philox(self, init_seed: int):
@@ -364,6 +366,37 @@ class DeviceStore:
             ws.loss2 = torch.zeros(2, dtype=torch.float64, device=self.device)
             self._ws[key] = ws
         return self._ws[key]
+
+    # -- launch resources of the step plans -------------------------------------
+    def side_stream(self) -> torch.cuda.Stream:
+        """The second stream of the two-stream plan."""
+        if self._side is None:
+            self._side = torch.cuda.Stream(device=self.device)
+        return self._side
+
+    def priority_streams(self):
+        """(high, low) priority streams of the fill plan (lower number = higher)."""
+        if self._prio is None:
+            self._prio = (torch.cuda.Stream(device=self.device, priority=-5),
+                          torch.cuda.Stream(device=self.device, priority=0))
+        return self._prio
+
+    def plan_streams(self) -> list:
+        """Every stream a step plan of this store has launched on so far."""
+        return [x for x in (self._side, *(self._prio or ())) if x is not None]
+
+    def block_events(self, n: int) -> list:
+        """n reusable events (per-block ordering inside a step plan)."""
+        if self._events is None or len(self._events) < n:
+            self._events = [torch.cuda.Event() for _ in range(n)]
+        return self._events
+
+    def head_table(self) -> "SegTable":
+        """Segment table of the embedding + first decoder block (the fill plan's
+        full-speed part of the perturb pass)."""
+        if self._head_table is None:
+            self._head_table = self.range_table(0, 2)
+        return self._head_table
 
     def stackable(self, batch: int, seq: int) -> bool:
         """The stacked GEMMs split rows on a CTA-pair tile boundary (bf16 path)."""

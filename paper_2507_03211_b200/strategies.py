@@ -179,9 +179,7 @@ class MeshZo:
         hi, lo = _priority_streams(s)
         ev = _block_events(s, nl + 3)
         calls = [(_record_and_wait, (ev[nl], main, hi)), (_wait, (lo, ev[nl]))]
-        if getattr(s, "_fill_head", None) is None:
-            s._fill_head = s.range_table(0, 2)          # built once, outside any graph capture
-        calls += s.perturb_call(s._fill_head, flags, sc_a, sc_b, sa=sa, sb=sb, stream=hi)
+        calls += s.perturb_call(s.head_table(), flags, sc_a, sc_b, sa=sa, sb=sb, stream=hi)
         for b in range(2, nl):
             calls += s.perturb_call(s.block_tables[b], flags | L.ZO_PU_FILL, sc_a, sc_b, sa=sa, sb=sb, stream=lo)
             calls.append((_record, (ev[b], lo)))

@@ -246,9 +246,7 @@ class StreamingZo:
         ev = _block_events(s, nl + 3)          # [b] block b's pass done; [nl] start; [nl+1], [nl+2] joins
         flags = L.ZO_PU_UPDATE | L.ZO_PU_SHADOW_A | L.ZO_PU_SHADOW_B
         calls = [(_record_and_wait, (ev[nl], main, hi)), (_wait, (lo, ev[nl]))]
-        if getattr(s, "_fill_head", None) is None:
-            s._fill_head = s.range_table(0, 2)          # built once, outside any graph capture
-        calls += s.perturb_call(s._fill_head, flags, +eps, -eps, stream=hi)
+        calls += s.perturb_call(s.head_table(), flags, +eps, -eps, stream=hi)
         for b in range(2, nl):
             calls += s.perturb_call(s.block_tables[b], flags | L.ZO_PU_FILL, +eps, -eps, stream=lo)
             calls.append((_record, (ev[b], lo)))
@@ -405,15 +403,11 @@ class StreamingZo:
 
 
 def _side_stream(store: DeviceStore):
-    if not hasattr(store, "_side"):
-        store._side = torch.cuda.Stream(device=store.device)
-    return store._side
+    return store.side_stream()
 
 
 def _block_events(store: DeviceStore, n: int):
-    if getattr(store, "_evs", None) is None or len(store._evs) != n + 1:
-        store._evs = [torch.cuda.Event() for _ in range(n + 1)]
-    return store._evs
+    return store.block_events(n)
 
 
 def _record_and_wait(ev, main, side):
@@ -434,10 +428,7 @@ def _wait(stream, ev):
 
 def _priority_streams(store: DeviceStore):
     """(high, low) priority streams of the fill plan (lower number = higher)."""
-    if getattr(store, "_prio", None) is None:
-        store._prio = (torch.cuda.Stream(device=store.device, priority=-5),
-                       torch.cuda.Stream(device=store.device, priority=0))
-    return store._prio
+    return store.priority_streams()
 
 
 class NativeGraph:
